@@ -1,0 +1,333 @@
+/*
+ * fbgpu.h -- C ABI of the B200-native FairBatching per-iteration scheduling
+ * hot path (drop-in for the fbsim reference, /root/reference/proj).
+ *
+ * Plain C: pointers, sizes and POD structs only.  No torch types, no C++
+ * exceptions cross this boundary; every entry point returns an FB_* status and
+ * fb_last_error() holds a message for the calling thread.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   - Pure scheduler surface  sched.h:81-115
+ *       init_time_budget / form_batch / pab           -> fb_init_time_budget,
+ *                                                        fb_form_batch, fb_pab
+ *   - Stateful step machine   engine.h:111-176  (class Node)
+ *       Node::enqueue / begin_step / complete_step     -> fb_arena_* (batched
+ *       over thousands of independent Node instances resident in HBM)
+ *   - Drivers                 engine.h:180  run_node
+ *                             cluster.h:107-109 run_cluster
+ *                                                      -> fb_arena_run,
+ *                                                         fb_run_batch,
+ *                                                         fb_cluster_*
+ *   - Per-request records     metrics.h:29-49 RequestReport (built online)
+ *   - Host trace generation   workload.h:88-94 generate_bursty / scale_trace /
+ *                             truncate_trace      -> fb_generate_bursty, ...
+ *
+ * Time is int64 microseconds (time.h:23-34); cost arithmetic is fp64 in the
+ * reference's operation order (sched.cpp:129-166), so batch decisions are
+ * bit-identical to the CPU reference.
+ */
+#ifndef FBGPU_H_
+#define FBGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBGPU_ABI_VERSION 1
+
+/* Status codes; the host C++ wrapper maps them onto the fbsim exception
+ * taxonomy (errors.h:24-53) and the CLI exit codes (commands.h:30-33). */
+enum {
+  FB_OK = 0,
+  FB_ERR_VALIDATION = 1, /* ValidationError: domain invariant violated   */
+  FB_ERR_USAGE = 2,      /* UsageError: API misuse / precondition       */
+  FB_ERR_CONFIG = 3,     /* ConfigError: bad scenario or command config */
+  FB_ERR_PARSE = 4,      /* ParseError                                  */
+  FB_ERR_CUDA = 5,       /* device missing / CUDA runtime failure       */
+  FB_ERR_CAPACITY = 6    /* caller buffer too small; *_needed reported  */
+};
+
+/* Scheduling policies, sched.h:60 (same numbering as the enum order). */
+enum {
+  FB_POLICY_PREFILL_FIRST = 0,
+  FB_POLICY_SARATHI = 1,
+  FB_POLICY_FAIRBATCH = 2,
+  FB_POLICY_FAIRBATCH_PAB = 3
+};
+
+/* Task phase, sched.h:28. */
+enum { FB_PHASE_PREFILL = 0, FB_PHASE_DECODE = 1 };
+
+/* Cluster load-balancer policies, cluster.h:31. */
+enum { FB_LB_COUNT = 0, FB_LB_PAB = 1 };
+
+/* Linear step-time model a + b*new + c*context (costmodel.h:29-33). */
+typedef struct fb_cost_model {
+  double a_ms;
+  double b_ms;
+  double c_ms;
+} fb_cost_model;
+
+/* SchedulerConfig, sched.h:65-74. */
+typedef struct fb_scheduler_config {
+  int32_t policy;       /* FB_POLICY_* */
+  int32_t max_chunk;    /* per-chunk ceiling */
+  int64_t token_budget; /* per-step token ceiling */
+  fb_cost_model model;  /* the scheduler's own estimator */
+} fb_scheduler_config;
+
+/* EngineConfig, engine.h:76-82 (NoiseSpec costmodel.h:62-65 inlined,
+ * global SloTargets slo.h:34-37 inlined). */
+typedef struct fb_engine_config {
+  fb_scheduler_config scheduler;
+  fb_cost_model truth_model;
+  double noise_amplitude; /* multiplicative truth noise, factor 1 + amp*u */
+  uint64_t noise_seed;    /* keyed per (seed, step ordinal), rng.h:88-94  */
+  int64_t global_ttft_us; /* global SLOs used by PAB admission            */
+  int64_t global_tpot_us;
+  int32_t max_active; /* 0 = unbounded (engine.h:81)                  */
+  int32_t reserved;
+} fb_engine_config;
+
+/* Trace rows, structure of arrays (Request, workload.h:28-35).  Rows of one
+ * instance are contiguous and sorted by arrival (workload.h:40-43).  The row
+ * index inside an instance is the request's id for every output below. */
+typedef struct fb_trace {
+  const int64_t* arrival_us;
+  const int32_t* prompt_len;
+  const int32_t* output_len;
+  const int64_t* ttft_us;
+  const int64_t* tpot_us;
+  int64_t n_rows;
+} fb_trace;
+
+/* One simulated node (one independent run_node) inside an arena. */
+typedef struct fb_instance {
+  fb_engine_config cfg;
+  int64_t trace_off;  /* first row of this instance's trace               */
+  int64_t n_req;      /* rows; several instances may share the same rows  */
+  int64_t horizon_us; /* run_node horizon (engine.h:180)                  */
+} fb_instance;
+
+/* Per-request outcome, RequestReport (metrics.h:29-49) computed online. */
+typedef struct fb_record {
+  int64_t first_emit_us;  /* absolute time of token 0; -1 when none       */
+  double max_tpot_ms;     /* metrics.cpp:42-49 (0 for < 2 tokens)         */
+  double max_tpot_alt_ms; /* metrics.cpp:53-60 (denominator j-1)          */
+  int32_t tokens_emitted;
+  uint32_t flags; /* FB_REC_* */
+} fb_record;
+
+enum {
+  FB_REC_ARRIVED = 1u,   /* an arrival event was logged (report exists)    */
+  FB_REC_REJECTED = 2u,  /* PAB admission reject and never served          */
+  FB_REC_FINISHED = 4u,  /* request_done                                   */
+  FB_REC_MET_TTFT = 8u,  /* emits[0] <= ttft_slo (metrics.cpp:105)         */
+  FB_REC_MET_TPOT = 16u, /* finished and (e_j-e_0) <= tpot*j for all j     */
+  FB_REC_ENV_MISS = 32u  /* some token j>=1 past arrival+ttft+tpot*j       */
+};
+
+/* Per-instance summary. */
+typedef struct fb_instance_result {
+  uint64_t steps;       /* begin_step launches incl. spin steps = Node::steps_completed */
+  uint64_t plan_digest; /* rolling digest of every plan + reject (fbgpu_digest.h) */
+  int64_t end_time_us;  /* clock when the run stopped */
+  int64_t n_arrived;    /* requests enqueued (== reports) */
+  int64_t n_rejected;   /* PAB admission rejects */
+  int64_t sum_visible;  /* sum over steps of visible tasks A */
+  int64_t sum_entries;  /* sum over steps of plan entries E */
+  int64_t sum_new_tokens;
+  int32_t incomplete; /* EventLog::incomplete (engine.cpp:286) */
+  int32_t status;     /* FB_OK or an FB_ERR_* for this instance */
+} fb_instance_result;
+
+/* Optional per-step plan log (parity tooling), one row per begin_step. */
+typedef struct fb_step_log {
+  int64_t t_us;         /* batch_start time */
+  int64_t duration_us;  /* max(1, llround(actual_ms*1000)) */
+  double predicted_ms;  /* BatchPlan::predicted_ms */
+  double actual_ms;     /* ground-truth step time */
+  int64_t total_new;    /* batch_start.new_tokens */
+  int64_t total_ctx;    /* batch_start.context_tokens */
+  double init_budget_ms;/* BatchPlan::init_time_budget_ms (fair batching) */
+  int32_t entry_off;    /* first entry in the instance's entry log */
+  int32_t n_entries;
+} fb_step_log;
+
+/* BatchPlanEntry (sched.h:44-47) with the trace row as request id. */
+typedef struct fb_plan_entry {
+  int32_t req;
+  int32_t new_tokens;
+} fb_plan_entry;
+
+/* admission_reject event (engine.cpp:134-142). */
+typedef struct fb_reject_log {
+  int64_t t_us;
+  int64_t pab_tokens;
+  int32_t req;
+  int32_t reserved;
+} fb_reject_log;
+
+/* Plan-log capacities per instance; 0 disables logging. */
+typedef struct fb_log_opts {
+  int32_t step_cap;
+  int32_t entry_cap;
+  int32_t reject_cap;
+  int32_t reserved;
+} fb_log_opts;
+
+/* Log occupancy per instance after a run. */
+typedef struct fb_log_counts {
+  int32_t steps;
+  int32_t entries;
+  int32_t rejects;
+  int32_t truncated;
+} fb_log_counts;
+
+/* ---------------------------------------------------------------------- */
+/* Library                                                                */
+/* ---------------------------------------------------------------------- */
+
+int fb_abi_version(void);
+const char* fb_last_error(void);
+/* Number of CUDA devices visible (0 on a host without GPU). */
+int fb_device_count(int* n_out);
+
+/* ---------------------------------------------------------------------- */
+/* Host-side trace generation (stays on the host: libm log/exp/cos/sqrt). */
+/* ---------------------------------------------------------------------- */
+
+/* BurstProfile, workload.h:55-66, plus the generation horizon. */
+typedef struct fb_burst_profile {
+  double base_rate;  /* req/s in idle phases  */
+  double burst_rate; /* req/s in burst phases */
+  int64_t burst_duration_us;
+  int64_t idle_duration_us;
+  double prompt_mean, prompt_p90;
+  double output_mean, output_p90;
+  int64_t ttft_us, tpot_us; /* stamped on every request */
+  uint64_t seed;
+} fb_burst_profile;
+
+/* generate_bursty (workload.cpp:244-298).  Writes up to `cap` rows; *n_out
+ * receives the row count.  FB_ERR_CAPACITY when cap < *n_out (call again).
+ * Any output pointer may be NULL when cap == 0. */
+int fb_generate_bursty(const fb_burst_profile* profile, int64_t horizon_us,
+                       int64_t cap, int64_t* arrival_us, int32_t* prompt_len,
+                       int32_t* output_len, int64_t* ttft_us, int64_t* tpot_us,
+                       int64_t* n_out);
+
+/* scale_trace (workload.cpp:211-221), in place. */
+int fb_scale_trace(int64_t* arrival_us, int64_t n, double factor);
+
+/* offered_rps (workload.cpp:315-321). */
+int fb_offered_rps(const int64_t* arrival_us, int64_t n, double* rps_out);
+
+/* ---------------------------------------------------------------------- */
+/* Pure scheduler surface (sched.h:81-115), batched over task sets.        */
+/* ---------------------------------------------------------------------- */
+
+/* TaskView, sched.h:34-42. */
+typedef struct fb_task_view {
+  int64_t request_id;
+  int64_t slack_us;
+  int64_t context;
+  int64_t arrival_seq;
+  int64_t tpot_us;
+  int32_t new_tokens;
+  int32_t phase; /* FB_PHASE_* */
+} fb_task_view;
+
+/* BatchPlan scalars, sched.h:49-58. */
+typedef struct fb_batch_plan {
+  double predicted_ms;
+  double time_budget_used_ms;
+  int64_t token_budget_used;
+  double init_time_budget_ms;
+  int64_t entry_off; /* into the entries output */
+  int64_t n_entries;
+} fb_batch_plan;
+
+/* Plan entry keyed by the caller's request_id. */
+typedef struct fb_plan_entry_id {
+  int64_t request_id;
+  int32_t new_tokens;
+  int32_t reserved;
+} fb_plan_entry_id;
+
+/* form_batch (sched.cpp:234-246) for n_sets independent task sets on the
+ * device.  Set s owns tasks[set_off[s] .. set_off[s+1]).  Entries of set s are
+ * written at entries[set_off[s] ...] (a plan never has more entries than
+ * tasks) and plans[s].entry_off/n_entries describe them.  Empty sets are a
+ * UsageError for the fair-batching policies (sched.cpp:91-93). */
+int fb_form_batch(int device, const fb_task_view* tasks, const int64_t* set_off,
+                  const fb_scheduler_config* cfgs, int64_t n_sets,
+                  fb_plan_entry_id* entries, fb_batch_plan* plans);
+
+/* init_time_budget (sched.cpp:90-106) per set. */
+int fb_init_time_budget(int device, const fb_task_view* tasks,
+                        const int64_t* set_off, int64_t n_sets,
+                        int64_t* budget_us_out);
+
+/* pab (sched.cpp:248-278) per set; models[s], slos (ttft,tpot us) per set. */
+int fb_pab(int device, const fb_task_view* tasks, const int64_t* set_off,
+           const fb_cost_model* models, const int64_t* ttft_us,
+           const int64_t* tpot_us, int64_t n_sets, int64_t* pab_out);
+
+/* ---------------------------------------------------------------------- */
+/* Arena: request-state SoA for thousands of Node instances in HBM.        */
+/* ---------------------------------------------------------------------- */
+
+typedef struct fb_arena fb_arena;
+
+/* stream: a cudaStream_t to issue all work on, or NULL for a private one. */
+int fb_arena_create(int device, void* stream, fb_arena** out);
+int fb_arena_destroy(fb_arena* arena);
+
+/* Uploads trace rows and instances (validated as Node/validate_request do,
+ * engine.cpp:83-90, workload.cpp:114-124) and allocates all device state.
+ * log may be NULL. */
+int fb_arena_load(fb_arena* arena, const fb_trace* rows,
+                  const fb_instance* instances, int64_t n_instances,
+                  const fb_log_opts* log);
+
+/* Rewinds every instance to t = 0 (device-side, no host traffic). */
+int fb_arena_reset(fb_arena* arena);
+
+/* Advances every unfinished instance by at most max_events iterations of the
+ * run_node event loop (engine.cpp:271-283); max_events <= 0 runs to
+ * quiescence.  Asynchronous on the arena stream.  *n_active_out (may be NULL)
+ * receives the number of instances still running after the call, which
+ * forces a synchronisation. */
+int fb_arena_run(fb_arena* arena, int64_t max_events, int64_t* n_active_out);
+
+int fb_arena_synchronize(fb_arena* arena);
+
+/* Device time of the last fb_arena_run (CUDA events on the arena stream). */
+int fb_arena_last_run_ms(fb_arena* arena, float* ms_out);
+
+int fb_arena_fetch_results(fb_arena* arena, fb_instance_result* out);
+/* Records for instance rows: out has sum over instances of n_req rows, in
+ * instance order. */
+int fb_arena_fetch_records(fb_arena* arena, fb_record* out);
+int64_t fb_arena_record_rows(const fb_arena* arena);
+int fb_arena_fetch_log_counts(fb_arena* arena, fb_log_counts* out);
+/* Copies instance i's logs; buffers sized by the log caps (NULL skips). */
+int fb_arena_fetch_log(fb_arena* arena, int64_t instance, fb_step_log* steps,
+                       fb_plan_entry* entries, fb_reject_log* rejects);
+
+/* One-shot end-to-end run from host buffers: upload, run to quiescence,
+ * download results and records (records may be NULL).  elapsed_ms_out (may be
+ * NULL) receives the host wall time of the whole call. */
+int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
+                 int64_t n_instances, fb_instance_result* results,
+                 fb_record* records, double* elapsed_ms_out);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* FBGPU_H_ */

@@ -1,0 +1,213 @@
+"""Test-side loaders for the CPU checkers (TEST INFRASTRUCTURE ONLY).
+
+  * OracleLib -- oracle/liboracle.so, the C restatement of the reference path
+  * RefLib    -- oracle/_ref/libfbsim_ref.so, the unmodified reference library
+                compiled from /root/reference plus a C-ABI shim
+
+Both expose the same calls as the product's C ABI (include/fbgpu.h) with an
+orc_ / ref_ prefix, so a parity test runs one Batch through every backend and
+compares outputs field by field.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_2510_14392_b200 import _abi
+from paper_2510_14392_b200.batch import Batch, Rows
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libfbsim_ref.so")
+
+
+def ensure_oracle_built() -> None:
+    """The C restatement is rebuilt on demand (gcc is on every box)."""
+    src = os.path.join(ROOT, "oracle", "fbsim_oracle.c")
+    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True)
+
+
+@dataclass
+class RunOutput:
+    results: np.ndarray  # RESULT_DTYPE per instance
+    records: np.ndarray  # RECORD_DTYPE per row (instance order)
+    counts: np.ndarray | None = None  # LOGCOUNT_DTYPE per instance
+    steps: np.ndarray | None = None  # STEPLOG_DTYPE [n_inst, step_cap]
+    entries: np.ndarray | None = None  # ENTRY_DTYPE [n_inst, entry_cap]
+    rejects: np.ndarray | None = None  # REJECT_DTYPE [n_inst, reject_cap]
+
+
+def alloc_logs(n_inst: int, log: _abi.LogOpts | None):
+    if log is None:
+        return None, None, None, None
+    counts = np.zeros(n_inst, _abi.LOGCOUNT_DTYPE)
+    steps = np.zeros((n_inst, max(1, log.step_cap)), _abi.STEPLOG_DTYPE)
+    entries = np.zeros((n_inst, max(1, log.entry_cap)), _abi.ENTRY_DTYPE)
+    rejects = np.zeros((n_inst, max(1, log.reject_cap)), _abi.REJECT_DTYPE)
+    return counts, steps, entries, rejects
+
+
+class _CpuLib:
+    prefix = ""
+
+    def __init__(self, path: str):
+        self.lib = C.CDLL(path)
+        p = self.prefix
+        self._gen = getattr(self.lib, p + "generate_bursty")
+        self._gen.restype = C.c_int
+        self._gen.argtypes = [C.POINTER(_abi.BurstProfile), C.c_int64, C.c_int64,
+                              C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                              C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        self._scale = getattr(self.lib, p + "scale_trace")
+        self._scale.restype = C.c_int
+        self._scale.argtypes = [C.POINTER(C.c_int64), C.c_int64, C.c_double]
+        self._ku = getattr(self.lib, p + "keyed_uniform")
+        self._ku.restype = C.c_double
+        self._ku.argtypes = [C.c_uint64, C.c_uint64]
+        self._itb = getattr(self.lib, p + "init_time_budget")
+        self._itb.restype = C.c_int
+        self._itb.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        self._fb = getattr(self.lib, p + "form_batch")
+        self._fb.restype = C.c_int
+        self._fb.argtypes = [C.c_void_p, C.c_int64, C.POINTER(_abi.SchedulerConfig), C.c_void_p,
+                             C.c_void_p]
+        self._pab = getattr(self.lib, p + "pab")
+        self._pab.restype = C.c_int
+        self._pab.argtypes = [C.c_void_p, C.c_int64, C.POINTER(_abi.CostModel), C.c_int64,
+                              C.c_int64, C.POINTER(C.c_int64)]
+
+    # -- trace generation -------------------------------------------------
+    def generate_bursty(self, prof: _abi.BurstProfile, horizon_us: int) -> Rows:
+        n = C.c_int64(0)
+        st = self._gen(C.byref(prof), horizon_us, 0, None, None, None, None, None, C.byref(n))
+        if st not in (_abi.FB_OK, _abi.FB_ERR_CAPACITY):
+            raise RuntimeError(f"{self.prefix}generate_bursty failed: {st}")
+        k = n.value
+        arr = np.zeros(k, np.int64)
+        pr = np.zeros(k, np.int32)
+        ou = np.zeros(k, np.int32)
+        tt = np.zeros(k, np.int64)
+        tp = np.zeros(k, np.int64)
+        st = self._gen(C.byref(prof), horizon_us, k, _abi.ptr(arr, C.c_int64),
+                       _abi.ptr(pr, C.c_int32), _abi.ptr(ou, C.c_int32), _abi.ptr(tt, C.c_int64),
+                       _abi.ptr(tp, C.c_int64), C.byref(n))
+        assert st == _abi.FB_OK and n.value == k
+        return Rows(arr, pr, ou, tt, tp)
+
+    def scale_trace(self, arrival: np.ndarray, factor: float) -> np.ndarray:
+        a = np.ascontiguousarray(arrival, np.int64).copy()
+        st = self._scale(_abi.ptr(a, C.c_int64), len(a), factor)
+        if st:
+            raise ValueError("scale_trace rejected the factor")
+        return a
+
+    def keyed_uniform(self, seed: int, ordinal: int) -> float:
+        return self._ku(seed, ordinal)
+
+    # -- pure scheduler ----------------------------------------------------
+    def init_time_budget(self, tasks: np.ndarray) -> int:
+        out = C.c_int64(0)
+        st = self._itb(_abi.vptr(tasks), len(tasks), C.byref(out))
+        if st:
+            raise RuntimeError(f"init_time_budget status {st}")
+        return out.value
+
+    def form_batch(self, tasks: np.ndarray, cfg: _abi.SchedulerConfig):
+        entries = np.zeros(max(1, len(tasks)), _abi.PLANENTRYID_DTYPE)
+        plan = np.zeros(1, _abi.BATCHPLAN_DTYPE)
+        st = self._fb(_abi.vptr(tasks), len(tasks), C.byref(cfg), _abi.vptr(entries),
+                      _abi.vptr(plan))
+        if st:
+            raise RuntimeError(f"form_batch status {st}")
+        return plan[0], entries[: int(plan[0]["n_entries"])]
+
+    def pab(self, tasks: np.ndarray, model: _abi.CostModel, ttft_us: int, tpot_us: int) -> int:
+        out = C.c_int64(0)
+        st = self._pab(_abi.vptr(tasks), len(tasks), C.byref(model), ttft_us, tpot_us,
+                       C.byref(out))
+        if st:
+            raise RuntimeError(f"pab status {st}")
+        return out.value
+
+
+class OracleLib(_CpuLib):
+    prefix = "orc_"
+
+    def __init__(self):
+        ensure_oracle_built()
+        super().__init__(ORACLE_SO)
+        self._run = self.lib.orc_run_instances
+        self._run.restype = C.c_int
+        self._run.argtypes = [C.POINTER(_abi.Trace), C.c_void_p, C.c_int64,
+                              C.POINTER(_abi.LogOpts), C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+
+    def run(self, batch: Batch, log: _abi.LogOpts | None = None, nthreads: int = 1) -> RunOutput:
+        n = batch.n_instances
+        rows = batch.rows
+        tr = rows.to_c()
+        inst = batch.instances_c()
+        results = np.zeros(n, _abi.RESULT_DTYPE)
+        records = np.zeros(int(batch.record_offsets()[-1]), _abi.RECORD_DTYPE)
+        counts, steps, entries, rejects = alloc_logs(n, log)
+        st = self._run(C.byref(tr), C.cast(inst, C.c_void_p), n,
+                       C.byref(log) if log is not None else None, _abi.vptr(results),
+                       _abi.vptr(records), _abi.vptr(counts), _abi.vptr(steps),
+                       _abi.vptr(entries), _abi.vptr(rejects), nthreads)
+        if st:
+            raise RuntimeError(f"orc_run_instances status {st}")
+        return RunOutput(results, records, counts, steps, entries, rejects)
+
+
+class RefLib(_CpuLib):
+    prefix = "ref_"
+
+    @staticmethod
+    def available() -> bool:
+        return os.path.exists(REF_SO)
+
+    def __init__(self):
+        super().__init__(REF_SO)
+        self.lib.ref_last_error.restype = C.c_char_p
+        self._run = self.lib.ref_run_instances
+        self._run.restype = C.c_int
+        self._run.argtypes = [C.POINTER(_abi.Trace), C.c_void_p, C.c_int64,
+                              C.POINTER(_abi.LogOpts), C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        self._batch = self.lib.ref_run_node_batch
+        self._batch.restype = C.c_int
+        self._batch.argtypes = [C.POINTER(_abi.Trace), C.c_void_p, C.c_int64, C.c_void_p,
+                                C.c_void_p, C.c_int]
+
+    def run(self, batch: Batch, log: _abi.LogOpts | None = None, nthreads: int = 1,
+            check: bool = False) -> RunOutput:
+        n = batch.n_instances
+        tr = batch.rows.to_c()
+        inst = batch.instances_c()
+        results = np.zeros(n, _abi.RESULT_DTYPE)
+        records = np.zeros(int(batch.record_offsets()[-1]), _abi.RECORD_DTYPE)
+        counts, steps, entries, rejects = alloc_logs(n, log)
+        st = self._run(C.byref(tr), C.cast(inst, C.c_void_p), n,
+                       C.byref(log) if log is not None else None, _abi.vptr(results),
+                       _abi.vptr(records), _abi.vptr(counts), _abi.vptr(steps),
+                       _abi.vptr(entries), _abi.vptr(rejects), nthreads, 1 if check else 0)
+        if st:
+            raise RuntimeError(f"ref_run_instances status {st}: {self.lib.ref_last_error()}")
+        return RunOutput(results, records, counts, steps, entries, rejects)
+
+    def run_node_batch(self, batch: Batch, nthreads: int = 1, records: bool = True) -> RunOutput:
+        n = batch.n_instances
+        tr = batch.rows.to_c()
+        inst = batch.instances_c()
+        results = np.zeros(n, _abi.RESULT_DTYPE)
+        rec = np.zeros(int(batch.record_offsets()[-1]), _abi.RECORD_DTYPE) if records else None
+        st = self._batch(C.byref(tr), C.cast(inst, C.c_void_p), n, _abi.vptr(results),
+                         _abi.vptr(rec), nthreads)
+        if st:
+            raise RuntimeError(f"ref_run_node_batch status {st}")
+        return RunOutput(results, rec)
