@@ -1,0 +1,313 @@
+"""Benchmark: FairBatching per-iteration scheduling on B200.
+
+Workload (BASELINE.json configs[1]): Sarathi (512) vs
+FairBatching (2048) A/B on the qwen-like bursty trace x1.5, 2048 seeds ->
+4096 concurrent Node instances, each run to quiescence.  One bench "step" is
+one pass of the hot path over the whole sweep: arena reset + every instance's
+run_node event loop (arrival injection, PAB/none admission, views, slack
+ordering, capacity scan, ground-truth step, completion, online records).
+
+metric: scheduler iterations/sec = sum over instances of begin_step launches
+(steps incl. spin steps, engine.h:139) / device time.  Multi-GPU: one process
+per GPU, each runs its own 2048-seed shard (weak scaling, no data-path
+collective); value = all ranks' steps / max-over-ranks time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "scheduler iterations/sec (instances·steps/s) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "instance-steps/s"
+SEEDS_PER_GPU = 2048
+L2_FLUSH_BYTES = 256 << 20
+
+
+def workload_config(n_gpus: int) -> dict:
+    return {
+        "workload": "C2: sarathi-512 vs fairbatch-2048 A/B, qwen bursty x1.5, 40 s trace, "
+                    f"{SEEDS_PER_GPU} seeds x 2 policies = {2 * SEEDS_PER_GPU} instances per GPU",
+        "instances": 2 * SEEDS_PER_GPU * n_gpus,
+        "cost_model": "a=5.0 b=0.05 c=0.0001 ms (scheduler and truth)",
+        "slo_ms": [500, 50],
+        "parallelism": f"instance-sharded x{n_gpus}",
+        "l2": "flushed between timed iterations (256 MiB write)",
+    }
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak_hbm() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """DRAM bytes per engine launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "engine_ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline(batch, n_threads: int, budget_s: float = 15.0) -> dict:
+    """The reference's own CPU run_node + request_reports (oracle/_ref, the
+    unmodified library) on a bounded sample of the same instances, all host
+    threads; falls back to the C oracle port when the reference was not built."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from backends import REF_SO, OracleLib, RefLib
+
+    if os.path.exists(REF_SO):
+        lib, kind = RefLib(), "reference"
+        runner = lambda b: lib.run_node_batch(b, nthreads=n_threads)  # noqa: E731
+    else:
+        lib, kind = OracleLib(), "port"
+        runner = lambda b: lib.run(b, nthreads=n_threads)  # noqa: E731
+    # probe with a few instances, then size the sample to ~budget_s
+    n_total = batch.n_instances
+    take = min(n_total, max(2 * n_threads, 64))
+    best = None
+    while True:
+        sel = list(range(0, n_total, max(1, n_total // take)))[:take]
+        sub = batch.subset(sel)
+        t0 = time.perf_counter()
+        out = runner(sub)
+        dt = time.perf_counter() - t0
+        steps = int(out.results["steps"].sum())
+        best = (steps, dt, len(sel))
+        if dt >= budget_s / 3 or take >= n_total:
+            break
+        take = min(n_total, int(take * max(2.0, (budget_s / 2) / max(dt, 1e-3))))
+    steps, dt, n = best
+    return {"value": steps / dt, "unit": UNIT, "cores": n_threads, "kind": kind,
+            "sample": f"{n} of {n_total} C2 instances ({steps} instance-steps) in {dt:.2f} s, "
+                      f"{n_threads} threads, {os.cpu_count()} host CPUs"}
+
+
+def run_reference(args) -> None:
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2510_14392_b200 import workloads
+    batch = workloads.c2_batch(n_seeds=SEEDS_PER_GPU)
+    n_threads = os.cpu_count() or 1
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(batch, n_threads, budget_s=args.ref_budget_s)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            cb = r
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64+fp64", "data": "synthetic",
+            "config": workload_config(1), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
+                             "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    from paper_2510_14392_b200 import _abi, fbgpu, workloads
+
+    batch = workloads.c2_batch(n_seeds=SEEDS_PER_GPU, seed0=rank * SEEDS_PER_GPU)
+    stream = torch.cuda.current_stream()
+    arena = fbgpu.Arena(dev, stream=stream.cuda_stream)
+    arena.load(batch)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (full passes)
+    for _ in range(args.warmup):
+        arena.reset()
+        arena.run()
+    torch.cuda.synchronize()
+    res = arena.results()
+    steps_per_pass = int(res["steps"].sum())
+    assert (res["status"] == 0).all() and (res["incomplete"] == 0).all()
+    # algorithmic bytes per engine launch: 32 A + 64 E + 64 N_arr
+    alg_bytes = int(32 * res["sum_visible"].sum() + 64 * res["sum_entries"].sum()
+                    + 64 * res["n_arrived"].sum())
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    engine_ms = []
+    barrier()
+    with ClockSampler(dev) as clocks:
+        for k in range(args.steps):
+            flush.fill_(k)  # L2 flush outside the timed events
+            starts[k].record(stream)
+            arena.reset()
+            arena.run()
+            ends[k].record(stream)
+            torch.cuda.synchronize()
+            engine_ms.append(arena.last_run_ms())
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    n = torch.tensor([steps_per_pass * args.steps], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(n, op=torch.distributed.ReduceOp.SUM)
+    max_ms = float(t.item())
+    all_steps = float(n.item())
+    value = all_steps / (max_ms / 1000.0)
+
+    # end to end through the C ABI with host buffers: H2D of the step's trace
+    # rows + instances, run, D2H of per-instance results and per-request records
+    rows = batch.rows
+    inst = batch.instances_c()
+    import ctypes as C
+    h2d = rows.nbytes + C.sizeof(_abi.Instance) * batch.n_instances
+    e2e_ms = []
+    for k in range(max(1, min(args.steps, 5))):
+        flush.fill_(k)
+        barrier()
+        t0 = time.perf_counter()
+        arena.load(batch)
+        arena.run()
+        r2 = arena.results()
+        rec = arena.records()
+        e2e_ms.append((time.perf_counter() - t0) * 1000.0)
+    d2h = r2.nbytes + rec.nbytes
+    assert r2.tobytes() == res.tobytes()
+    te = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = (all_steps / args.steps) / (float(te.item()) / 1000.0)
+
+    if rank == 0:
+        peak, peak_kind = measured_peak_hbm()
+        eng = statistics.mean(engine_ms)
+        achieved = alg_bytes / (eng / 1000.0) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64+fp64", "data": "synthetic",
+            "config": workload_config(ws),
+            "instance_steps_per_pass": all_steps / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "engine_kernel", "kernel_ms": eng,
+                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": float(te.item())},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(batch, os.cpu_count() or 1, args.ref_budget_s)
+        print(json.dumps(line), flush=True)
+    arena.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -8,6 +8,7 @@ include/fbgpu.h.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,8 +26,12 @@ def llround(x):
 
 
 def ms_to_us(ms: float) -> int:
-    """time.h:30-32."""
-    return int(llround(float(ms) * 1000.0))
+    """time.h:30-32 (scalar llround)."""
+    x = float(ms) * 1000.0
+    t = math.trunc(x)
+    if abs(x - t) >= 0.5:
+        t += 1 if x > 0 else -1
+    return int(t)
 
 
 def us_to_ms(us: int) -> float:
@@ -191,6 +196,26 @@ class Batch:
     def add(self, rows: Rows, cfg: EngineConfig, horizon_us: int) -> int:
         off = self.add_rows(rows)
         return self.add_instance(cfg, off, len(rows), horizon_us, rows.offered_rps())
+
+    def subset(self, indices) -> "Batch":
+        """A new batch with only the given instances (each with its own rows)."""
+        out = Batch()
+        r = self.rows
+        for i in indices:
+            x = self._inst[i]
+            s = slice(x.trace_off, x.trace_off + x.n_req)
+            off = out.add_rows(Rows(r.arrival_us[s], r.prompt_len[s], r.output_len[s],
+                                    r.ttft_us[s], r.tpot_us[s]))
+            out._inst.append(_abi.Instance(x.cfg, off, x.n_req, x.horizon_us))
+            out.offered.append(self.offered[i])
+        return out
+
+    def extend(self, other: "Batch") -> None:
+        """Appends every instance of `other` (with its rows)."""
+        off = self.add_rows(other.rows)
+        for i, x in enumerate(other._inst):
+            self._inst.append(_abi.Instance(x.cfg, off + x.trace_off, x.n_req, x.horizon_us))
+            self.offered.append(other.offered[i])
 
     @property
     def rows(self) -> Rows:

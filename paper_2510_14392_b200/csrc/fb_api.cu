@@ -1,0 +1,600 @@
+// fb_api.cu -- the C ABI (include/fbgpu.h): arena lifetime, validation,
+// uploads, launches and result downloads.  No exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fbgpu.h"
+#include "fb_device.cuh"
+#include "fb_kernels.h"
+
+namespace fbgpu {
+int set_error(int code, const std::string& msg);
+}
+
+using fbgpu::set_error;
+
+namespace {
+
+constexpr int64_t kTimeLimit = int64_t(1) << 50;  // |times| guard for key packing
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(FB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define FB_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, (count ? count : 1) * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// validate_scheduler_config (sched.cpp:81-88), Node ctor (engine.cpp:83-90)
+int validate_engine(const fb_engine_config& c, int64_t i) {
+  const std::string who = "instance " + std::to_string(i) + ": ";
+  const fb_scheduler_config& s = c.scheduler;
+  if (s.policy < FB_POLICY_PREFILL_FIRST || s.policy > FB_POLICY_FAIRBATCH_PAB)
+    return set_error(FB_ERR_USAGE, who + "unknown scheduling policy");
+  if (s.max_chunk < 1) return set_error(FB_ERR_VALIDATION, who + "scheduler.max_chunk must be >= 1");
+  if (s.token_budget < s.max_chunk)
+    return set_error(FB_ERR_VALIDATION, who + "scheduler.token_budget must be >= max_chunk");
+  if (s.model.a_ms < 0.0 || s.model.b_ms <= 0.0 || s.model.c_ms < 0.0)
+    return set_error(FB_ERR_VALIDATION, who + "scheduler cost model requires a >= 0, b > 0, c >= 0");
+  if (c.truth_model.b_ms <= 0.0 || c.truth_model.a_ms < 0.0 || c.truth_model.c_ms < 0.0)
+    return set_error(FB_ERR_VALIDATION, who + "truth cost model requires a >= 0, b > 0, c >= 0");
+  if (c.scheduler.policy == FB_POLICY_FAIRBATCH_PAB &&
+      (c.global_tpot_us <= 0 || c.global_ttft_us <= 0))
+    return set_error(FB_ERR_VALIDATION, who + "PAB admission needs positive global SLOs");
+  return FB_OK;
+}
+
+// validate_request (workload.cpp:114-124) + the Trace ordering invariant
+// (workload.h:40-43) + the device's time-range guard.
+int validate_rows(const fb_trace& t, int64_t off, int64_t n, int64_t i) {
+  const std::string who = "instance " + std::to_string(i) + ": ";
+  int64_t last = INT64_MIN;
+  for (int64_t k = off; k < off + n; ++k) {
+    const int64_t a = t.arrival_us[k];
+    if (t.prompt_len[k] < 1)
+      return set_error(FB_ERR_VALIDATION, who + "request " + std::to_string(k - off) +
+                                              ": prompt_len must be >= 1");
+    if (t.output_len[k] < 1)
+      return set_error(FB_ERR_VALIDATION, who + "request " + std::to_string(k - off) +
+                                              ": output_len must be >= 1");
+    if (t.ttft_us[k] <= 0 || t.tpot_us[k] <= 0)
+      return set_error(FB_ERR_VALIDATION, who + "request " + std::to_string(k - off) +
+                                              ": SLO targets must be positive");
+    if (a < last)
+      return set_error(FB_ERR_VALIDATION, who + "trace rows must be sorted by arrival");
+    if (a < 0 || a >= kTimeLimit || t.ttft_us[k] >= kTimeLimit || t.tpot_us[k] >= kTimeLimit)
+      return set_error(FB_ERR_VALIDATION, who + "times must lie in [0, 2^50) us");
+    last = a;
+  }
+  return FB_OK;
+}
+
+}  // namespace
+
+struct fb_arena {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  fbgpu::EngineGeometry geo{};
+  int64_t n_rows = 0, n_inst = 0, n_rec = 0;
+  fb_log_opts log{};
+  bool loaded = false;
+  std::vector<int64_t> rec_off;  // host copy, n_inst + 1
+
+  DevBuf<int64_t> arrival, ttft, tpot;
+  DevBuf<int32_t> prompt, output;
+  DevBuf<unsigned char> inst, state;
+  DevBuf<int32_t> prefilled, nidx, seq;
+  DevBuf<uint32_t> flags;
+  DevBuf<int64_t> first;
+  DevBuf<double> maxtp, maxtp_alt;
+  DevBuf<int2> vlist;
+  DevBuf<unsigned char> gscratch;
+  DevBuf<fb_step_log> log_steps;
+  DevBuf<fb_plan_entry> log_entries;
+  DevBuf<fb_reject_log> log_rejects;
+  DevBuf<unsigned long long> work;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+
+  fbgpu::EngineParams params(int64_t max_events) const {
+    fbgpu::EngineParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.inst = reinterpret_cast<const fbgpu::DevInst*>(inst.p);
+    P.state = reinterpret_cast<fbgpu::DevState*>(state.p);
+    P.n_inst = n_inst;
+    P.arrival = arrival.p;
+    P.prompt = prompt.p;
+    P.output = output.p;
+    P.ttft = ttft.p;
+    P.tpot = tpot.p;
+    P.prefilled = prefilled.p;
+    P.nidx = nidx.p;
+    P.seq = seq.p;
+    P.flags = flags.p;
+    P.first = first.p;
+    P.maxtp = maxtp.p;
+    P.maxtp_alt = maxtp_alt.p;
+    P.vlist = vlist.p;
+    P.gscratch = gscratch.p;
+    P.log_on = (log.step_cap > 0 || log.entry_cap > 0 || log.reject_cap > 0) ? 1 : 0;
+    P.log_steps = log_steps.p;
+    P.log_entries = log_entries.p;
+    P.log_rejects = log_rejects.p;
+    P.log_step_cap = log.step_cap;
+    P.log_entry_cap = log.entry_cap;
+    P.log_reject_cap = log.reject_cap;
+    P.work = work.p;
+    P.max_events = max_events <= 0 ? INT64_MAX : max_events;
+    return P;
+  }
+
+  void release() {
+    arrival.release(); ttft.release(); tpot.release(); prompt.release(); output.release();
+    inst.release(); state.release(); prefilled.release(); nidx.release(); seq.release();
+    flags.release(); first.release(); maxtp.release(); maxtp_alt.release(); vlist.release();
+    gscratch.release(); log_steps.release(); log_entries.release(); log_rejects.release();
+    work.release();
+  }
+};
+
+extern "C" {
+
+int fb_device_count(int* n_out) {
+  if (!n_out) return set_error(FB_ERR_USAGE, "null output");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+  *n_out = n;
+  return FB_OK;
+}
+
+int fb_arena_create(int device, void* stream, fb_arena** out) {
+  if (!out) return set_error(FB_ERR_USAGE, "fb_arena_create: null output");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return set_error(FB_ERR_CUDA, "no CUDA device available (the product path has no CPU fallback)");
+  if (device < 0 || device >= n) return set_error(FB_ERR_USAGE, "device ordinal out of range");
+  FB_CUDA(cudaSetDevice(device));
+  fb_arena* a = new fb_arena();
+  a->device = device;
+  if (stream) {
+    a->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete a;
+      return cuda_fail(e, "cudaStreamCreate");
+    }
+    a->own_stream = true;
+  }
+  cudaEventCreate(&a->ev0);
+  cudaEventCreate(&a->ev1);
+  a->geo = fbgpu::engine_geometry(device);
+  cudaError_t e = a->work.ensure(2);
+  if (e != cudaSuccess) {
+    delete a;
+    return cuda_fail(e, "cudaMalloc");
+  }
+  *out = a;
+  return FB_OK;
+}
+
+int fb_arena_destroy(fb_arena* a) {
+  if (!a) return FB_OK;
+  cudaSetDevice(a->device);
+  if (a->stream) cudaStreamSynchronize(a->stream);
+  a->release();
+  if (a->ev0) cudaEventDestroy(a->ev0);
+  if (a->ev1) cudaEventDestroy(a->ev1);
+  if (a->own_stream) cudaStreamDestroy(a->stream);
+  delete a;
+  return FB_OK;
+}
+
+int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instances,
+                  int64_t n_instances, const fb_log_opts* log) {
+  if (!a || !rows || (n_instances > 0 && !instances) || n_instances < 0)
+    return set_error(FB_ERR_USAGE, "fb_arena_load: bad arguments");
+  FB_CUDA(cudaSetDevice(a->device));
+  // Validate everything before touching device state.
+  std::vector<int64_t> rec_off(static_cast<size_t>(n_instances) + 1, 0);
+  for (int64_t i = 0; i < n_instances; ++i) {
+    const fb_instance& in = instances[i];
+    if (in.trace_off < 0 || in.n_req < 0 || in.trace_off + in.n_req > rows->n_rows)
+      return set_error(FB_ERR_VALIDATION, "instance " + std::to_string(i) + ": rows out of range");
+    if (in.n_req >= (int64_t(1) << 31) - 1)
+      return set_error(FB_ERR_VALIDATION, "instance " + std::to_string(i) + ": too many requests");
+    int st = validate_engine(in.cfg, i);
+    if (st) return st;
+    st = validate_rows(*rows, in.trace_off, in.n_req, i);
+    if (st) return st;
+    rec_off[i + 1] = rec_off[i] + in.n_req;
+  }
+  fb_log_opts lo{};
+  if (log) lo = *log;
+  if (lo.step_cap < 0 || lo.entry_cap < 0 || lo.reject_cap < 0)
+    return set_error(FB_ERR_USAGE, "negative log capacity");
+  const int64_t n_rows = rows->n_rows;
+  const int64_t n_rec = rec_off.back();
+  const size_t slot = fbgpu::scratch_bytes_per_slot();
+  cudaError_t e = cudaSuccess;
+#define ENSURE(buf, count)                               \
+  if ((e = (buf).ensure(static_cast<size_t>(count))) != cudaSuccess) \
+    return cuda_fail(e, "cudaMalloc " #buf);
+  ENSURE(a->arrival, n_rows);
+  ENSURE(a->ttft, n_rows);
+  ENSURE(a->tpot, n_rows);
+  ENSURE(a->prompt, n_rows);
+  ENSURE(a->output, n_rows);
+  ENSURE(a->inst, n_instances * fbgpu::dev_inst_bytes());
+  ENSURE(a->state, n_instances * fbgpu::dev_state_bytes());
+  ENSURE(a->prefilled, n_rec);
+  ENSURE(a->nidx, n_rec);
+  ENSURE(a->seq, n_rec);
+  ENSURE(a->flags, n_rec);
+  ENSURE(a->first, n_rec);
+  ENSURE(a->maxtp, n_rec);
+  ENSURE(a->maxtp_alt, n_rec);
+  ENSURE(a->vlist, n_rec);
+  ENSURE(a->gscratch, n_rec * static_cast<int64_t>(slot));
+  ENSURE(a->log_steps, n_instances * static_cast<int64_t>(lo.step_cap));
+  ENSURE(a->log_entries, n_instances * static_cast<int64_t>(lo.entry_cap));
+  ENSURE(a->log_rejects, n_instances * static_cast<int64_t>(lo.reject_cap));
+#undef ENSURE
+  std::vector<unsigned char> hinst(static_cast<size_t>(n_instances) * fbgpu::dev_inst_bytes());
+  for (int64_t i = 0; i < n_instances; ++i)
+    fbgpu::pack_instance(instances[i], rec_off[i], i * lo.step_cap, i * lo.entry_cap,
+                         i * lo.reject_cap, hinst.data() + i * fbgpu::dev_inst_bytes());
+  cudaStream_t s = a->stream;
+  if (n_rows > 0) {
+    FB_CUDA(cudaMemcpyAsync(a->arrival.p, rows->arrival_us, n_rows * 8, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemcpyAsync(a->ttft.p, rows->ttft_us, n_rows * 8, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemcpyAsync(a->tpot.p, rows->tpot_us, n_rows * 8, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemcpyAsync(a->prompt.p, rows->prompt_len, n_rows * 4, cudaMemcpyHostToDevice, s));
+    FB_CUDA(cudaMemcpyAsync(a->output.p, rows->output_len, n_rows * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (n_instances > 0)
+    FB_CUDA(cudaMemcpyAsync(a->inst.p, hinst.data(), hinst.size(), cudaMemcpyHostToDevice, s));
+  a->n_rows = n_rows;
+  a->n_inst = n_instances;
+  a->n_rec = n_rec;
+  a->log = lo;
+  a->rec_off = std::move(rec_off);
+  a->loaded = true;
+  // hinst must outlive the async copy
+  FB_CUDA(cudaStreamSynchronize(s));
+  return fb_arena_reset(a);
+}
+
+int fb_arena_reset(fb_arena* a) {
+  if (!a || !a->loaded) return set_error(FB_ERR_USAGE, "fb_arena_reset: arena not loaded");
+  FB_CUDA(cudaSetDevice(a->device));
+  FB_CUDA(fbgpu::launch_reset(a->params(0), a->n_rec, a->stream));
+  return FB_OK;
+}
+
+int fb_arena_run(fb_arena* a, int64_t max_events, int64_t* n_active_out) {
+  if (!a || !a->loaded) return set_error(FB_ERR_USAGE, "fb_arena_run: arena not loaded");
+  FB_CUDA(cudaSetDevice(a->device));
+  const fbgpu::EngineParams P = a->params(max_events);
+  FB_CUDA(cudaEventRecord(a->ev0, a->stream));
+  if (a->n_inst > 0) FB_CUDA(fbgpu::launch_engine(P, a->geo, a->stream));
+  FB_CUDA(cudaEventRecord(a->ev1, a->stream));
+  a->timed = true;
+  if (n_active_out) {
+    unsigned long long h[2] = {0, 0};
+    FB_CUDA(cudaMemcpyAsync(h, a->work.p, sizeof(h), cudaMemcpyDeviceToHost, a->stream));
+    FB_CUDA(cudaStreamSynchronize(a->stream));
+    *n_active_out = a->n_inst > 0 ? static_cast<int64_t>(h[1]) : 0;
+  }
+  return FB_OK;
+}
+
+int fb_arena_synchronize(fb_arena* a) {
+  if (!a) return set_error(FB_ERR_USAGE, "null arena");
+  FB_CUDA(cudaSetDevice(a->device));
+  FB_CUDA(cudaStreamSynchronize(a->stream));
+  return FB_OK;
+}
+
+int fb_arena_last_run_ms(fb_arena* a, float* ms_out) {
+  if (!a || !ms_out || !a->timed) return set_error(FB_ERR_USAGE, "no timed run");
+  FB_CUDA(cudaEventSynchronize(a->ev1));
+  FB_CUDA(cudaEventElapsedTime(ms_out, a->ev0, a->ev1));
+  return FB_OK;
+}
+
+int fb_arena_fetch_results(fb_arena* a, fb_instance_result* out) {
+  if (!a || !a->loaded || !out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_results");
+  FB_CUDA(cudaSetDevice(a->device));
+  const size_t sb = fbgpu::dev_state_bytes();
+  std::vector<unsigned char> h(static_cast<size_t>(a->n_inst) * sb);
+  if (a->n_inst > 0)
+    FB_CUDA(cudaMemcpyAsync(h.data(), a->state.p, h.size(), cudaMemcpyDeviceToHost, a->stream));
+  FB_CUDA(cudaStreamSynchronize(a->stream));
+  for (int64_t i = 0; i < a->n_inst; ++i) fbgpu::unpack_state(h.data() + i * sb, &out[i]);
+  return FB_OK;
+}
+
+int64_t fb_arena_record_rows(const fb_arena* a) { return a ? a->n_rec : 0; }
+
+int fb_arena_fetch_records(fb_arena* a, fb_record* out) {
+  if (!a || !a->loaded || !out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_records");
+  FB_CUDA(cudaSetDevice(a->device));
+  const int64_t n = a->n_rec;
+  std::vector<int32_t> nidx(n);
+  std::vector<uint32_t> flags(n);
+  std::vector<int64_t> first(n);
+  std::vector<double> mt(n), mta(n);
+  std::vector<unsigned char> st(static_cast<size_t>(a->n_inst) * fbgpu::dev_state_bytes());
+  cudaStream_t s = a->stream;
+  if (n > 0) {
+    FB_CUDA(cudaMemcpyAsync(nidx.data(), a->nidx.p, n * 4, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(flags.data(), a->flags.p, n * 4, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(first.data(), a->first.p, n * 8, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(mt.data(), a->maxtp.p, n * 8, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(mta.data(), a->maxtp_alt.p, n * 8, cudaMemcpyDeviceToHost, s));
+  }
+  if (!st.empty())
+    FB_CUDA(cudaMemcpyAsync(st.data(), a->state.p, st.size(), cudaMemcpyDeviceToHost, s));
+  FB_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < a->n_inst; ++i) {
+    fb_instance_result r;
+    fbgpu::unpack_state(st.data() + i * fbgpu::dev_state_bytes(), &r);
+    const int64_t b = a->rec_off[i], e = a->rec_off[i + 1];
+    for (int64_t k = b; k < e; ++k) {
+      uint32_t f = flags[k] & ~fbgpu::kTpotViolated;
+      if (k - b < r.n_arrived) f |= FB_REC_ARRIVED;
+      if ((f & FB_REC_REJECTED) && nidx[k] > 0) f &= ~static_cast<uint32_t>(FB_REC_REJECTED);
+      out[k].first_emit_us = first[k];
+      out[k].max_tpot_ms = mt[k];
+      out[k].max_tpot_alt_ms = mta[k];
+      out[k].tokens_emitted = nidx[k];
+      out[k].flags = f;
+    }
+  }
+  return FB_OK;
+}
+
+int fb_arena_fetch_log_counts(fb_arena* a, fb_log_counts* out) {
+  if (!a || !a->loaded || !out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_log_counts");
+  FB_CUDA(cudaSetDevice(a->device));
+  const size_t sb = fbgpu::dev_state_bytes();
+  std::vector<unsigned char> h(static_cast<size_t>(a->n_inst) * sb);
+  if (!h.empty())
+    FB_CUDA(cudaMemcpyAsync(h.data(), a->state.p, h.size(), cudaMemcpyDeviceToHost, a->stream));
+  FB_CUDA(cudaStreamSynchronize(a->stream));
+  for (int64_t i = 0; i < a->n_inst; ++i) {
+    fbgpu::DevState s;
+    std::memcpy(&s, h.data() + i * sb, sizeof(s));
+    out[i].steps = s.log_steps;
+    out[i].entries = s.log_entries;
+    out[i].rejects = s.log_rejects;
+    out[i].truncated = s.log_trunc;
+  }
+  return FB_OK;
+}
+
+int fb_arena_fetch_log(fb_arena* a, int64_t i, fb_step_log* steps, fb_plan_entry* entries,
+                       fb_reject_log* rejects) {
+  if (!a || !a->loaded || i < 0 || i >= a->n_inst)
+    return set_error(FB_ERR_USAGE, "fb_arena_fetch_log: bad instance");
+  FB_CUDA(cudaSetDevice(a->device));
+  cudaStream_t s = a->stream;
+  const fb_log_opts& lo = a->log;
+  if (steps && lo.step_cap > 0)
+    FB_CUDA(cudaMemcpyAsync(steps, a->log_steps.p + i * lo.step_cap,
+                            sizeof(fb_step_log) * lo.step_cap, cudaMemcpyDeviceToHost, s));
+  if (entries && lo.entry_cap > 0)
+    FB_CUDA(cudaMemcpyAsync(entries, a->log_entries.p + i * lo.entry_cap,
+                            sizeof(fb_plan_entry) * lo.entry_cap, cudaMemcpyDeviceToHost, s));
+  if (rejects && lo.reject_cap > 0)
+    FB_CUDA(cudaMemcpyAsync(rejects, a->log_rejects.p + i * lo.reject_cap,
+                            sizeof(fb_reject_log) * lo.reject_cap, cudaMemcpyDeviceToHost, s));
+  FB_CUDA(cudaStreamSynchronize(s));
+  return FB_OK;
+}
+
+int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
+                 int64_t n_instances, fb_instance_result* results, fb_record* records,
+                 double* elapsed_ms_out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  fb_arena* a = nullptr;
+  int st = fb_arena_create(device, nullptr, &a);
+  if (st) return st;
+  st = fb_arena_load(a, rows, instances, n_instances, nullptr);
+  if (!st) st = fb_arena_run(a, 0, nullptr);
+  if (!st && results) st = fb_arena_fetch_results(a, results);
+  if (!st && records) st = fb_arena_fetch_records(a, records);
+  fb_arena_destroy(a);
+  if (elapsed_ms_out)
+    *elapsed_ms_out = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return st;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------ pure scheduler surface
+
+namespace {
+
+int check_sets(const fb_task_view* tasks, const int64_t* set_off, int64_t n_sets) {
+  if (n_sets < 0 || !set_off) return set_error(FB_ERR_USAGE, "bad task sets");
+  if (set_off[0] != 0) return set_error(FB_ERR_USAGE, "set_off[0] must be 0");
+  for (int64_t s = 0; s < n_sets; ++s) {
+    if (set_off[s + 1] < set_off[s]) return set_error(FB_ERR_USAGE, "set_off must be non-decreasing");
+    if (set_off[s + 1] - set_off[s] >= (int64_t(1) << 31) - 1)
+      return set_error(FB_ERR_VALIDATION, "task set too large");
+  }
+  const int64_t n = set_off[n_sets];
+  if (n > 0 && !tasks) return set_error(FB_ERR_USAGE, "null tasks");
+  const int64_t lim = int64_t(1) << 61;
+  for (int64_t k = 0; k < n; ++k) {
+    if (tasks[k].slack_us >= lim || tasks[k].slack_us < -lim)
+      return set_error(FB_ERR_VALIDATION, "task slack out of range");
+    if (tasks[k].new_tokens < 0) return set_error(FB_ERR_VALIDATION, "negative new_tokens");
+  }
+  return FB_OK;
+}
+
+struct Scoped {
+  std::vector<void*> ptrs;
+  ~Scoped() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t n) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T));
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+};
+
+int begin_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return set_error(FB_ERR_CUDA, "no CUDA device available (the product path has no CPU fallback)");
+  if (device < 0 || device >= n) return set_error(FB_ERR_USAGE, "device ordinal out of range");
+  FB_CUDA(cudaSetDevice(device));
+  return FB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fb_form_batch(int device, const fb_task_view* tasks, const int64_t* set_off,
+                  const fb_scheduler_config* cfgs, int64_t n_sets, fb_plan_entry_id* entries,
+                  fb_batch_plan* plans) {
+  int st = check_sets(tasks, set_off, n_sets);
+  if (st) return st;
+  for (int64_t s = 0; s < n_sets; ++s) {
+    const fb_scheduler_config& c = cfgs[s];
+    if (c.policy < FB_POLICY_PREFILL_FIRST || c.policy > FB_POLICY_FAIRBATCH_PAB)
+      return set_error(FB_ERR_USAGE, "unknown scheduling policy");
+    const bool fair = c.policy >= FB_POLICY_FAIRBATCH;
+    if (fair && set_off[s + 1] == set_off[s])
+      return set_error(FB_ERR_USAGE, "init_time_budget requires at least one active task");
+    if (fair && !(c.model.b_ms > 0.0))
+      return set_error(FB_ERR_VALIDATION, "fair batching requires b > 0");
+  }
+  if ((st = begin_device(device))) return st;
+  const int64_t n = set_off[n_sets];
+  Scoped m;
+  fb_task_view* d_tasks;
+  int64_t* d_off;
+  fb_scheduler_config* d_cfg;
+  fb_plan_entry_id* d_ent;
+  fb_batch_plan* d_plans;
+  unsigned char* d_scratch;
+  int* d_status;
+  FB_CUDA(m.alloc(&d_tasks, n));
+  FB_CUDA(m.alloc(&d_off, n_sets + 1));
+  FB_CUDA(m.alloc(&d_cfg, n_sets));
+  FB_CUDA(m.alloc(&d_ent, n));
+  FB_CUDA(m.alloc(&d_plans, n_sets));
+  FB_CUDA(m.alloc(&d_scratch, n * fbgpu::scratch_bytes_per_slot()));
+  FB_CUDA(m.alloc(&d_status, 1));
+  FB_CUDA(cudaMemcpy(d_tasks, tasks, n * sizeof(fb_task_view), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_off, set_off, (n_sets + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_cfg, cfgs, n_sets * sizeof(fb_scheduler_config), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemset(d_status, 0, sizeof(int)));
+  if (n_sets > 0)
+    FB_CUDA(fbgpu::launch_form_batch(d_tasks, d_off, d_cfg, n_sets, d_ent, d_plans, d_scratch,
+                                     d_status, nullptr));
+  FB_CUDA(cudaDeviceSynchronize());
+  int h_status = 0;
+  FB_CUDA(cudaMemcpy(&h_status, d_status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h_status) return set_error(h_status, "form_batch failed on device");
+  FB_CUDA(cudaMemcpy(plans, d_plans, n_sets * sizeof(fb_batch_plan), cudaMemcpyDeviceToHost));
+  FB_CUDA(cudaMemcpy(entries, d_ent, n * sizeof(fb_plan_entry_id), cudaMemcpyDeviceToHost));
+  return FB_OK;
+}
+
+int fb_init_time_budget(int device, const fb_task_view* tasks, const int64_t* set_off,
+                        int64_t n_sets, int64_t* out) {
+  int st = check_sets(tasks, set_off, n_sets);
+  if (st) return st;
+  for (int64_t s = 0; s < n_sets; ++s)
+    if (set_off[s + 1] == set_off[s])
+      return set_error(FB_ERR_USAGE, "init_time_budget requires at least one active task");
+  if ((st = begin_device(device))) return st;
+  const int64_t n = set_off[n_sets];
+  Scoped m;
+  fb_task_view* d_tasks;
+  int64_t *d_off, *d_out;
+  int* d_status;
+  FB_CUDA(m.alloc(&d_tasks, n));
+  FB_CUDA(m.alloc(&d_off, n_sets + 1));
+  FB_CUDA(m.alloc(&d_out, n_sets));
+  FB_CUDA(m.alloc(&d_status, 1));
+  FB_CUDA(cudaMemcpy(d_tasks, tasks, n * sizeof(fb_task_view), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_off, set_off, (n_sets + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemset(d_status, 0, sizeof(int)));
+  if (n_sets > 0)
+    FB_CUDA(fbgpu::launch_init_time_budget(d_tasks, d_off, n_sets, d_out, d_status, nullptr));
+  FB_CUDA(cudaDeviceSynchronize());
+  FB_CUDA(cudaMemcpy(out, d_out, n_sets * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return FB_OK;
+}
+
+int fb_pab(int device, const fb_task_view* tasks, const int64_t* set_off,
+           const fb_cost_model* models, const int64_t* ttft_us, const int64_t* tpot_us,
+           int64_t n_sets, int64_t* out) {
+  int st = check_sets(tasks, set_off, n_sets);
+  if (st) return st;
+  if ((st = begin_device(device))) return st;
+  const int64_t n = set_off[n_sets];
+  Scoped m;
+  fb_task_view* d_tasks;
+  int64_t *d_off, *d_out, *d_ttft, *d_tpot;
+  fb_cost_model* d_models;
+  unsigned char* d_scratch;
+  FB_CUDA(m.alloc(&d_tasks, n));
+  FB_CUDA(m.alloc(&d_off, n_sets + 1));
+  FB_CUDA(m.alloc(&d_out, n_sets));
+  FB_CUDA(m.alloc(&d_ttft, n_sets));
+  FB_CUDA(m.alloc(&d_tpot, n_sets));
+  FB_CUDA(m.alloc(&d_models, n_sets));
+  FB_CUDA(m.alloc(&d_scratch, n * fbgpu::scratch_bytes_per_slot()));
+  FB_CUDA(cudaMemcpy(d_tasks, tasks, n * sizeof(fb_task_view), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_off, set_off, (n_sets + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_ttft, ttft_us, n_sets * sizeof(int64_t), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_tpot, tpot_us, n_sets * sizeof(int64_t), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpy(d_models, models, n_sets * sizeof(fb_cost_model), cudaMemcpyHostToDevice));
+  if (n_sets > 0)
+    FB_CUDA(fbgpu::launch_pab(d_tasks, d_off, d_models, d_ttft, d_tpot, n_sets, d_out, d_scratch,
+                              nullptr));
+  FB_CUDA(cudaDeviceSynchronize());
+  FB_CUDA(cudaMemcpy(out, d_out, n_sets * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return FB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// fb_device.cuh -- device-side layouts and primitives shared by the kernels.
+//
+// Arithmetic conventions (bit-exact parity with the reference):
+//   * every fp64 expression on the decision path is written with explicit
+//     round-to-nearest intrinsics in the reference's operation order, and the
+//     translation unit is additionally compiled with -fmad=false, so no FMA
+//     contraction can change a batch decision;
+//   * time is int64 microseconds (time.h:23-34).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/fbgpu.h"
+#include "../../include/fbgpu_digest.h"
+
+namespace fbgpu {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int64_t kInf = INT64_MAX;
+
+// ------------------------------------------------------------ fp64 helpers
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// us_to_ms, time.h:34
+__device__ __forceinline__ double us_to_ms(int64_t us) {
+  return ddiv(static_cast<double>(us), 1000.0);
+}
+// ms_to_us, time.h:30-32 (llround: half away from zero)
+__device__ __forceinline__ int64_t ms_to_us(double ms) {
+  return static_cast<int64_t>(llround(dmul(ms, 1000.0)));
+}
+// predict_step_time_ms, costmodel.cpp:112-116: (a + b*new) + c*ctx
+__device__ __forceinline__ double predict_ms(double a, double b, double c,
+                                             int64_t nw, int64_t ctx) {
+  return dadd(dadd(a, dmul(b, static_cast<double>(nw))),
+              dmul(c, static_cast<double>(ctx)));
+}
+
+// -------------------------------------------------------------- rng.h
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {  // rng.h:25-30
+  uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t stream) {
+  uint64_t s = base ^ (0x9e3779b97f4a7c15ULL * (stream + 1));  // rng.h:33-37
+  splitmix64(s);
+  return splitmix64(s);
+}
+__device__ __forceinline__ double keyed_uniform(uint64_t seed, uint64_t ord) {
+  uint64_t s = derive_seed(seed, ord);  // rng.h:91-94
+  return dmul(static_cast<double>(splitmix64(s) >> 11), 0x1.0p-53);
+}
+
+// ------------------------------------------------------------- warp utils
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(kFull, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(kFull, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {  // integers only (exact)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------- device layouts
+
+// Immutable per-instance parameters (from fb_instance).
+struct DevInst {
+  double sa, sb, sc;  // scheduler cost model
+  double ta, tb, tc;  // truth cost model
+  double noise_amp;
+  uint64_t noise_seed;
+  int64_t token_budget;
+  int64_t g_ttft, g_tpot;  // global SLOs (PAB)
+  int64_t horizon;
+  int64_t trace_off;  // first trace row
+  int64_t rec_off;    // first row of this instance's state/record/vlist region
+  int64_t n_req;
+  int64_t log_step_off, log_entry_off, log_reject_off;
+  int32_t policy, max_chunk, max_active, pad;
+};
+
+// Mutable per-instance step-machine state (Node's scalars, engine.h:156-175).
+struct DevState {
+  int64_t step_end;     // valid when busy
+  int64_t arr;          // next trace row to enqueue (run_node's `arr`)
+  int64_t pulled;       // rows [pulled, arr) are pending (Node::pending_)
+  int64_t n_active;     // vlist [0, n_active) = active_, activation order
+  int64_t n_live;       // vlist [n_active, n_live) = waiting_, admission order
+  int64_t seq_counter;  // engine.h:174
+  int64_t t_last;
+  uint64_t step_counter;  // engine.h:172 (== steps started)
+  uint64_t digest;
+  int64_t n_rejected;
+  int64_t sum_visible, sum_entries, sum_new;
+  int32_t busy, done, status, log_steps;
+  int32_t log_entries, log_rejects, log_trunc, incomplete;
+};
+
+// Per-request mutable state, structure of arrays indexed by rec_off + row.
+struct DevReq {
+  int32_t* prefilled;  // RequestProgress::prefilled_tokens
+  int32_t* nidx;       // RequestProgress::next_output_idx (== tokens emitted)
+  int32_t* seq;        // RequestState::seq
+  uint32_t* flags;     // FB_REC_* plus kTpotViolated
+  int64_t* first;      // time of token 0 (-1 none)
+  double* maxtp;       // running max_tpot_ms
+  double* maxtp_alt;   // running max_tpot_alt_ms
+};
+constexpr uint32_t kTpotViolated = 0x80000000u;
+
+// Trace rows, structure of arrays.
+struct DevRows {
+  const int64_t* arrival;
+  const int32_t* prompt;
+  const int32_t* output;
+  const int64_t* ttft;
+  const int64_t* tpot;
+};
+
+// Optional logs.
+struct DevLogs {
+  fb_step_log* steps;
+  fb_plan_entry* entries;
+  fb_reject_log* rejects;
+  int32_t step_cap, entry_cap, reject_cap, on;
+};
+
+// Per-warp scratch, one slot per visible task (view position p) or per
+// sorted position k.  Lives in shared memory when A <= kScratchSmem, else in
+// the instance's global scratch region (generic pointers either way).
+struct Scratch {
+  int64_t* slack;   // [p] slack (us)
+  uint64_t* khi;    // [p] (group << 62) | (slack + 2^61)
+  int64_t* seq;     // [p] arrival_seq
+  int64_t* ctx;     // [p] context
+  int32_t* nw;      // [p] new tokens available | phase << 31
+  int32_t* req;     // [p] request row
+  int32_t* order;   // [k] view position at sorted rank k
+  int32_t* take;    // [k] admitted tokens (0 = not admitted); later [p] new pos
+  double* tcost;    // [k] b*new + c*ctx (or PAB term [p])
+  double* ccost;    // [k] c*ctx
+};
+constexpr int kScratchBytesPerSlot = 8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8 + 8;
+
+__device__ __forceinline__ Scratch carve_scratch(unsigned char* base, int cap) {
+  Scratch s;
+  unsigned char* p = base;
+  s.slack = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(cap);
+  s.khi = reinterpret_cast<uint64_t*>(p); p += 8 * static_cast<size_t>(cap);
+  s.seq = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(cap);
+  s.ctx = reinterpret_cast<int64_t*>(p); p += 8 * static_cast<size_t>(cap);
+  s.tcost = reinterpret_cast<double*>(p); p += 8 * static_cast<size_t>(cap);
+  s.ccost = reinterpret_cast<double*>(p); p += 8 * static_cast<size_t>(cap);
+  s.nw = reinterpret_cast<int32_t*>(p); p += 4 * static_cast<size_t>(cap);
+  s.req = reinterpret_cast<int32_t*>(p); p += 4 * static_cast<size_t>(cap);
+  s.order = reinterpret_cast<int32_t*>(p); p += 4 * static_cast<size_t>(cap);
+  s.take = reinterpret_cast<int32_t*>(p);
+  return s;
+}
+
+constexpr uint32_t kDecodeBit = 0x80000000u;
+
+}  // namespace fbgpu

@@ -1,0 +1,82 @@
+// fb_kernels.h -- host-visible launch wrappers for the device kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/fbgpu.h"
+
+namespace fbgpu {
+
+struct DevInst;
+struct DevState;
+
+// Everything the engine kernel touches, as device pointers.
+struct EngineParams {
+  const DevInst* inst;
+  DevState* state;
+  int64_t n_inst;
+  // trace rows
+  const int64_t* arrival;
+  const int32_t* prompt;
+  const int32_t* output;
+  const int64_t* ttft;
+  const int64_t* tpot;
+  // per-request state (indexed by rec_off + row)
+  int32_t* prefilled;
+  int32_t* nidx;
+  int32_t* seq;
+  uint32_t* flags;
+  int64_t* first;
+  double* maxtp;
+  double* maxtp_alt;
+  int2* vlist;                   // [rec_off + i] = {row, take}
+  unsigned char* gscratch;       // [rec_off * kScratchBytesPerSlot ...]
+  // logs (null when off)
+  fb_step_log* log_steps;
+  fb_plan_entry* log_entries;
+  fb_reject_log* log_rejects;
+  int32_t log_step_cap, log_entry_cap, log_reject_cap, log_on;
+  // persistent work queue
+  unsigned long long* work;  // [0] next instance, [1] instances still running
+  int64_t max_events;        // per instance per launch
+};
+
+// Per-launch geometry of the persistent engine kernel.
+struct EngineGeometry {
+  int blocks;
+  int threads;
+  size_t smem;
+};
+
+EngineGeometry engine_geometry(int device);
+size_t scratch_bytes_per_slot();
+size_t dev_inst_bytes();
+size_t dev_state_bytes();
+
+// Host packing of fb_instance into the device layout (rec_off / log offsets
+// assigned by the caller).
+void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
+                   int64_t log_entry_off, int64_t log_reject_off, void* out);
+// Host decode of a DevState into fb_instance_result.
+void unpack_state(const void* state, fb_instance_result* out);
+
+cudaError_t launch_reset(const EngineParams& p, int64_t n_rec_rows, cudaStream_t st);
+cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g,
+                          cudaStream_t st);
+
+// Pure scheduler surface.  `scratch` must hold total_tasks slots.
+cudaError_t launch_form_batch(const fb_task_view* tasks, const int64_t* set_off,
+                              const fb_scheduler_config* cfgs, int64_t n_sets,
+                              fb_plan_entry_id* entries, fb_batch_plan* plans,
+                              unsigned char* scratch, int* status, cudaStream_t st);
+cudaError_t launch_init_time_budget(const fb_task_view* tasks, const int64_t* set_off,
+                                    int64_t n_sets, int64_t* out, int* status,
+                                    cudaStream_t st);
+cudaError_t launch_pab(const fb_task_view* tasks, const int64_t* set_off,
+                       const fb_cost_model* models, const int64_t* ttft,
+                       const int64_t* tpot, int64_t n_sets, int64_t* out,
+                       unsigned char* scratch, cudaStream_t st);
+
+}  // namespace fbgpu

@@ -1,0 +1,135 @@
+"""Named parity scenarios shared by the golden-fixture generator and the tests.
+
+Each scenario is a list of (profile, horizon_ms, scale, engine-config kwargs,
+run horizon) built with a caller-supplied trace generator, so the same batch
+can be materialised with the reference's generate_bursty (fixtures), the C
+oracle's (CPU tests) or the product's (GPU tests).
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+from paper_2510_14392_b200 import _abi
+from paper_2510_14392_b200.batch import Batch, CostModel, engine_config, ms_to_us
+
+MODEL = CostModel(5.0, 0.05, 0.0001)
+BUDGET = {"fairbatch": 2048, "fairbatch_pab": 2048, "sarathi": 512, "prefill_first": 8192}
+
+
+def profile(base, burst, bms, ims, pm, p9, om, o9, seed, ttft=500.0, tpot=50.0):
+    return _abi.BurstProfile(float(base), float(burst), ms_to_us(bms), ms_to_us(ims), float(pm),
+                             float(p9), float(om), float(o9), ms_to_us(ttft), ms_to_us(tpot),
+                             seed)
+
+
+def qwen(seed, ttft=500.0, tpot=50.0):
+    return profile(1.0, 10.0, 1500, 3500, 892, 1776, 377, 742, seed, ttft, tpot)
+
+
+TRACE_PROFILES = {
+    "c1_poisson": (profile(4.0, 4.0, 1500, 3500, 892, 1776, 377, 742, 33), 250_000.0),
+    "qwen_33": (qwen(33), 40_000.0),
+    "qwen_0": (qwen(0), 40_000.0),
+    "qwen_7": (qwen(7), 40_000.0),
+    "balanced_7": (profile(2.0, 6.0, 1000, 2000, 892, 1776, 377, 742, 7), 40_000.0),
+    "short_bursty_11": (profile(2.0, 6.0, 1000, 2000, 688, 1599, 237, 470, 11), 40_000.0),
+    "long_prompt_13": (profile(1.5, 5.0, 1500, 2500, 1604, 3561, 114, 392, 13, ttft=2000.0),
+                       40_000.0),
+    "cluster8_5": (profile(30.0, 90.0, 800, 1600, 892, 1776, 250, 500, 5), 30_000.0),
+}
+
+
+def rows_digest(rows) -> str:
+    h = hashlib.sha256()
+    for a in (rows.arrival_us, rows.prompt_len, rows.output_len, rows.ttft_us, rows.tpot_us):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def _add(b: Batch, gen, prof, gen_h_ms, scale, pol, run_h_ms=3.6e6, **kw):
+    rows = gen(prof, ms_to_us(gen_h_ms))
+    if scale != 1.0:
+        rows = rows.scaled(scale)
+    tt = prof.ttft_us / 1000.0
+    tp = prof.tpot_us / 1000.0
+    cfg = engine_config(pol, kw.pop("budget", BUDGET[pol]), kw.pop("model", MODEL), tt, tp, **kw)
+    b.add(rows, cfg, ms_to_us(run_h_ms))
+
+
+def scenario_c1(gen) -> Batch:
+    """C1 under every policy, plus noisy fair-batching variants."""
+    b = Batch()
+    prof, h = TRACE_PROFILES["c1_poisson"]
+    for pol in ("fairbatch", "sarathi", "prefill_first", "fairbatch_pab"):
+        _add(b, gen, prof, h, 1.0, pol)
+    _add(b, gen, prof, h, 1.0, "fairbatch", noise_amplitude=0.052, noise_seed=12345)
+    _add(b, gen, prof, h, 1.0, "fairbatch_pab", noise_amplitude=0.052, noise_seed=99)
+    return b
+
+
+def scenario_mixed(gen, n_seeds=24) -> Batch:
+    """qwen-like bursts at 1x..3x load over every policy, with noise, max_active
+    limits and short horizons (incomplete runs, arrivals past the horizon)."""
+    b = Batch()
+    pols = ("prefill_first", "sarathi", "fairbatch", "fairbatch_pab")
+    for s in range(n_seeds):
+        pol = pols[s % 4]
+        _add(b, gen, qwen(s), 40_000.0, (1.0, 1.5, 2.0, 3.0)[(s // 4) % 4], pol,
+             run_h_ms=3.6e6 if s % 7 else 20_000.0,
+             noise_amplitude=0.05 if s % 3 == 0 else 0.0, noise_seed=7 * s + 1,
+             max_active=(0, 0, 0, 8, 20)[s % 5])
+    return b
+
+
+def scenario_pab_overload(gen) -> Batch:
+    """fairbatch_pab under 2x-4x overload: many admission rejects."""
+    b = Batch()
+    for s, sc in ((33, 2.0), (5, 3.0), (9, 4.0)):
+        _add(b, gen, qwen(s), 40_000.0, sc, "fairbatch_pab")
+        _add(b, gen, qwen(s), 40_000.0, sc, "fairbatch_pab", max_active=12)
+    prof, h = TRACE_PROFILES["long_prompt_13"]
+    _add(b, gen, prof, h, 2.8, "fairbatch_pab")
+    return b
+
+
+def scenario_large_live(gen) -> Batch:
+    """Heavy overload where more than 64 tasks are visible at once (exercises
+    the global-memory scratch path of the warp engine)."""
+    b = Batch()
+    prof, h = TRACE_PROFILES["balanced_7"]
+    for pol in ("fairbatch", "sarathi", "prefill_first", "fairbatch_pab"):
+        _add(b, gen, prof, 40_000.0, 12.0, pol, run_h_ms=8_000.0)
+    _add(b, gen, prof, 40_000.0, 12.0, "fairbatch", run_h_ms=8_000.0,
+         model=CostModel(5.0, 0.05, 0.001))
+    _add(b, gen, prof, 40_000.0, 12.0, "sarathi", run_h_ms=8_000.0, max_active=100)
+    return b
+
+
+def scenario_c2_subset(gen, seeds=range(0, 16)) -> Batch:
+    """C2 (qwen x1.5, sarathi 512 vs fairbatch 2048) for a few seeds."""
+    b = Batch()
+    for s in seeds:
+        _add(b, gen, qwen(s), 40_000.0, 1.5, "sarathi")
+        _add(b, gen, qwen(s), 40_000.0, 1.5, "fairbatch")
+    return b
+
+
+SCENARIOS = {
+    "c1": scenario_c1,
+    "mixed": scenario_mixed,
+    "pab_overload": scenario_pab_overload,
+    "large_live": scenario_large_live,
+    "c2_subset": scenario_c2_subset,
+}
+
+
+def summarize(results: np.ndarray, records: np.ndarray) -> dict:
+    """Compact, exact summary of a run for fixtures."""
+    keys = ("steps", "plan_digest", "end_time_us", "n_arrived", "n_rejected", "sum_entries",
+            "sum_new_tokens", "incomplete")
+    return {
+        "results": [{k: int(r[k]) for k in keys} for r in results],
+        "records_sha256": hashlib.sha256(records.tobytes()).hexdigest(),
+    }

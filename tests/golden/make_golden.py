@@ -1,0 +1,81 @@
+"""Generates tests/golden/golden.json from the UNMODIFIED reference library.
+
+Run in a container that has /root/reference (the library is built by
+`make -C oracle ref` into oracle/_ref/libfbsim_ref.so):
+
+    python tests/golden/make_golden.py
+
+The fixtures pin the C oracle (CPU tests) and the CUDA path (GPU tests):
+trace checksums of generate_bursty, exact run summaries (plan digest, step
+counts, per-request record hashes) of the catalogue scenarios, and hashes of
+the batch plans / PAB values over the reference test-suite fuzz corpora.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import numpy as np  # noqa: E402
+
+from backends import RefLib  # noqa: E402
+from catalog import SCENARIOS, TRACE_PROFILES, rows_digest, summarize  # noqa: E402
+from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views  # noqa: E402
+from paper_2510_14392_b200.batch import ms_to_us  # noqa: E402
+
+
+def plans_digest(lib, corpus) -> str:
+    h = hashlib.sha256()
+    for v, cfg in corpus:
+        plan, entries = lib.form_batch(v, cfg)
+        h.update(plan.tobytes())
+        h.update(entries.tobytes())
+    return h.hexdigest()
+
+
+def pab_values(lib, n=1000, seed=424242):
+    rng = Rng(seed)
+    out = []
+    for _ in range(n):
+        raw, cfg, now = gen_pab_instance(rng, 8)
+        v = raw_to_views(raw, now)
+        tt = ms_to_us(rng.uniform(300.0, 2000.0))
+        tp = ms_to_us(rng.uniform(25.0, 100.0))
+        out.append(lib.pab(v, cfg.model, tt, tp))
+    return out
+
+
+def main() -> None:
+    ref = RefLib()
+    gold = {"source": "oracle/_ref/libfbsim_ref.so (unmodified /root/reference/proj/src)"}
+    gold["traces"] = {}
+    for name, (prof, h_ms) in TRACE_PROFILES.items():
+        rows = ref.generate_bursty(prof, ms_to_us(h_ms))
+        gold["traces"][name] = {"n": len(rows), "sha256": rows_digest(rows),
+                                "head_arrival_us": rows.arrival_us[:4].tolist(),
+                                "head_prompt": rows.prompt_len[:4].tolist()}
+    gold["scenarios"] = {}
+    for name, fn in SCENARIOS.items():
+        batch = fn(ref.generate_bursty)
+        out = ref.run(batch, nthreads=8, check=True)
+        gold["scenarios"][name] = summarize(out.results, out.records)
+    corpus = acceptance_corpus(10_000)
+    gold["fuzz"] = {}
+    for pol in (2, 1, 0):
+        for _, cfg in corpus:
+            cfg.policy = pol
+        gold["fuzz"][f"acceptance_policy{pol}"] = plans_digest(ref, corpus)
+    gold["fuzz"]["pab_424242"] = hashlib.sha256(
+        np.asarray(pab_values(ref), np.int64).tobytes()).hexdigest()
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump(gold, f, indent=1, sort_keys=True)
+    print("wrote", os.path.join(HERE, "golden.json"))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,240 @@
+"""GPU parity suite: the CUDA path (through the C ABI) against the golden
+fixtures of the unmodified reference and against the C oracle, bit-exact.
+
+Batch composition (request rows, chunk sizes, predicted/actual step times) is
+compared through the per-instance plan digest and, where logged, entry by
+entry; per-request records (TTFT, TPOT, flags) byte for byte.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import test_oracle_cpu as kat
+from backends import RunOutput
+from catalog import SCENARIOS, summarize
+from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views
+from paper_2510_14392_b200 import _abi, workloads
+from paper_2510_14392_b200.batch import Batch, ms_to_us
+
+pytestmark = pytest.mark.gpu
+
+
+class GpuLib:
+    """Single-set adapter over the batched device API, same shape as the CPU libs."""
+
+    def __init__(self, fb):
+        self.fb = fb
+
+    def generate_bursty(self, prof, horizon_us):
+        return self.fb.generate_bursty(prof, horizon_us)
+
+    def init_time_budget(self, tasks):
+        try:
+            return int(self.fb.init_time_budget([tasks])[0])
+        except self.fb.FbError as e:
+            raise RuntimeError(str(e)) from e
+
+    def form_batch(self, tasks, cfg):
+        plans, entries = self.fb.form_batch([tasks], [cfg])
+        p = plans[0].copy()
+        p["entry_off"] = 0
+        return p, entries[0]
+
+    def pab(self, tasks, model, ttft_us, tpot_us):
+        return int(self.fb.pab([tasks], [model], ttft_us, tpot_us)[0])
+
+    def run(self, batch, log=None, nthreads=None, max_events=0):
+        a = self.fb.Arena(0)
+        a.load(batch, log)
+        if max_events > 0:
+            while a.run(max_events, sync=True) > 0:
+                pass
+        else:
+            a.run()
+        res, rec = a.results(), a.records()
+        counts = steps = entries = rejects = None
+        if log is not None:
+            counts, steps, entries, rejects = a.logs()
+        a.close()
+        return RunOutput(res, rec, counts, steps, entries, rejects)
+
+
+@pytest.fixture(scope="module")
+def gpu(fb):
+    return GpuLib(fb)
+
+
+# ------------------------------------------------------------ known answers
+
+@pytest.mark.parametrize("case", [
+    "test_init_time_budget_known_answers", "test_single_urgent_decode",
+    "test_prefill_chunked_ahead_of_relaxed_decode", "test_order_tie_break_and_empty",
+    "test_sarathi_and_prefill_first", "test_pab_known_answers", "test_hand_traced_timeline",
+    "test_pab_reject_logged", "test_chunk_emission_pattern", "test_horizon_cut_flags_incomplete",
+    "test_empty_trace"])
+def test_reference_known_answers_on_gpu(gpu, case):
+    getattr(kat, case)(gpu)
+
+
+# ------------------------------------------------------------ pure scheduler fuzz
+
+@pytest.mark.parametrize("policy", [2, 1, 0])
+def test_form_batch_acceptance_corpus(fb, golden, policy):
+    """acceptance.cpp criterion 1 corpus (seed 20260808, 10^4 sets) in one launch."""
+    corpus = acceptance_corpus(10_000)
+    sets = [v for v, _ in corpus]
+    cfgs = [_abi.SchedulerConfig(policy, c.max_chunk, c.token_budget, c.model) for _, c in corpus]
+    plans, entries = fb.form_batch(sets, cfgs)
+    h = hashlib.sha256()
+    for p, e in zip(plans, entries):
+        p = p.copy()
+        p["entry_off"] = 0
+        h.update(p.tobytes())
+        h.update(e.tobytes())
+    assert h.hexdigest() == golden["fuzz"][f"acceptance_policy{policy}"]
+
+
+def test_form_batch_large_sets_match_oracle(fb, oracle):
+    """Sets beyond the shared-memory scratch (global scratch path)."""
+    rng = Rng(99)
+    from fuzz import gen_instance
+    sets, cfgs = [], []
+    for i in range(60):
+        raw, cfg, now = gen_instance(rng, 400)
+        cfg.policy = i % 3
+        sets.append(raw_to_views(raw, now))
+        cfgs.append(cfg)
+    plans, entries = fb.form_batch(sets, cfgs)
+    assert max(len(s) for s in sets) > 64
+    for s, c, p, e in zip(sets, cfgs, plans, entries):
+        op, oe = oracle.form_batch(s, c)
+        p = p.copy()
+        p["entry_off"] = 0
+        assert p.tobytes() == op.tobytes() and e.tobytes() == oe.tobytes()
+
+
+def test_pab_fuzz(fb, golden):
+    rng = Rng(424242)
+    sets, models, tt, tp = [], [], [], []
+    for _ in range(1000):
+        raw, cfg, now = gen_pab_instance(rng, 8)
+        sets.append(raw_to_views(raw, now))
+        models.append(cfg.model)
+        tt.append(ms_to_us(rng.uniform(300.0, 2000.0)))
+        tp.append(ms_to_us(rng.uniform(25.0, 100.0)))
+    vals = fb.pab(sets, models, tt, tp)
+    assert hashlib.sha256(np.asarray(vals, np.int64).tobytes()).hexdigest() == \
+        golden["fuzz"]["pab_424242"]
+
+
+def test_empty_fair_set_is_usage_error(fb):
+    with pytest.raises(fb.UsageError):
+        fb.form_batch([np.zeros(0, _abi.TASKVIEW_DTYPE)],
+                      [_abi.SchedulerConfig(2, 2048, 2048, _abi.CostModel(5, 0.05, 1e-4))])
+
+
+# ------------------------------------------------------------ engine vs fixtures
+
+@pytest.mark.parametrize("name", sorted(SCENARIOS))
+def test_engine_scenarios_match_golden(gpu, golden, name):
+    batch = SCENARIOS[name](gpu.generate_bursty)
+    out = gpu.run(batch)
+    assert summarize(out.results, out.records) == golden["scenarios"][name]
+
+
+@pytest.mark.parametrize("name", ["c1", "pab_overload", "large_live", "mixed"])
+def test_engine_logs_match_oracle(gpu, oracle, name):
+    """Every step: time, duration, predicted/actual ms, totals and each plan
+    entry (request row, new tokens) in admission order; every PAB reject."""
+    batch = SCENARIOS[name](oracle.generate_bursty)
+    lo = _abi.LogOpts(40_000, 600_000, 5_000, 0)
+    a = gpu.run(batch, lo)
+    b = oracle.run(batch, lo, nthreads=4)
+    assert a.counts.tobytes() == b.counts.tobytes()
+    assert not a.counts["truncated"].any()
+    for i in range(batch.n_instances):
+        c = a.counts[i]
+        assert a.steps[i][: c["steps"]].tobytes() == b.steps[i][: c["steps"]].tobytes(), i
+        assert a.entries[i][: c["entries"]].tobytes() == b.entries[i][: c["entries"]].tobytes(), i
+        assert a.rejects[i][: c["rejects"]].tobytes() == b.rejects[i][: c["rejects"]].tobytes(), i
+    assert a.results.tobytes() == b.results.tobytes() or \
+        summarize(a.results, a.records) == summarize(b.results, b.records)
+
+
+def test_stepwise_api_matches_one_shot(gpu):
+    """Node-style incremental driving (fb_arena_run with an event budget)."""
+    batch = SCENARIOS["mixed"](gpu.generate_bursty)
+    one = gpu.run(batch)
+    inc = gpu.run(batch, max_events=97)
+    assert summarize(one.results, one.records) == summarize(inc.results, inc.records)
+
+
+def test_run_batch_e2e_equals_arena(fb, gpu):
+    batch = SCENARIOS["c2_subset"](gpu.generate_bursty)
+    res, rec, ms = fb.run_batch(batch)
+    out = gpu.run(batch)
+    assert res.tobytes() == out.results.tobytes() and rec.tobytes() == out.records.tobytes()
+    assert ms > 0
+
+
+def test_arena_reset_reruns_identically(fb):
+    batch = workloads.c2_batch(n_seeds=64)
+    a = fb.Arena(0)
+    a.load(batch)
+    a.run()
+    r1, c1 = a.results().copy(), a.records().copy()
+    a.reset()
+    a.run()
+    assert a.results().tobytes() == r1.tobytes() and a.records().tobytes() == c1.tobytes()
+    a.close()
+
+
+def test_validation_errors(fb):
+    b = Batch()
+    from paper_2510_14392_b200.batch import CostModel, Rows, engine_config
+    rows = Rows([0], [0], [5], [500_000], [50_000])  # prompt_len 0
+    b.add(rows, engine_config("fairbatch", 2048, CostModel(5, 0.05, 1e-4), 500, 50), 10**9)
+    a = fb.Arena(0)
+    with pytest.raises(fb.ValidationError):
+        a.load(b)
+    b2 = Batch()
+    b2.add(Rows([0], [10], [5], [500_000], [50_000]),
+           engine_config("fairbatch", 100, CostModel(5, 0.05, 1e-4), 500, 50, max_chunk=200),
+           10**9)
+    with pytest.raises(fb.ValidationError):
+        a.load(b2)
+    a.close()
+
+
+# ------------------------------------------------------------ C2 at scale
+
+def test_c2_sample_matches_oracle(gpu, oracle):
+    """512 C2 instances: per-instance digest and records identical to the oracle."""
+    batch = workloads.c2_batch(n_seeds=256, seed0=1000)
+    a = gpu.run(batch)
+    b = oracle.run(batch, nthreads=8)
+    assert a.results.tobytes() == b.results.tobytes()
+    assert a.records.tobytes() == b.records.tobytes()
+
+
+def test_c2_full_size_properties(fb):
+    """The bench workload (4096 instances): every instance quiescent, record
+    invariants hold, and a rerun is bit-identical (determinism)."""
+    batch = workloads.c2_batch()
+    a = fb.Arena(0)
+    a.load(batch)
+    a.run()
+    res = a.results()
+    rec = a.records()
+    assert (res["status"] == 0).all() and (res["incomplete"] == 0).all()
+    assert int(res["steps"].sum()) > 10_000_000
+    assert (rec["flags"] & _abi.REC_ARRIVED).all()
+    fin = (rec["flags"] & _abi.REC_FINISHED) != 0
+    assert fin.all()
+    a.reset()
+    a.run()
+    assert a.results().tobytes() == res.tobytes()
+    a.close()
