@@ -196,7 +196,10 @@ def run_ours(args) -> None:
     from paper_2510_14392_b200 import _abi, fbgpu, workloads
 
     batch = workloads.c2_batch(n_seeds=SEEDS_PER_GPU, seed0=rank * SEEDS_PER_GPU)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by torch events and the arena
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     arena = fbgpu.Arena(dev, stream=stream.cuda_stream)
     arena.load(batch)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
