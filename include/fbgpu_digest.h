@@ -8,8 +8,9 @@
  * and the ground-truth step times (exact fp64 bit patterns).  Per PAB reject
  * (engine.cpp:134-142) it absorbs the time, the request row and the budget.
  *
- * The entry part is a position-tagged sum so it can be reduced in any order
- * (integer addition mod 2^64 is associative) while staying order-sensitive.
+ * The entry part is a position-tagged XOR so it can be reduced in any order
+ * (one redux.sync per 32-bit half on the device) while staying
+ * order-sensitive through the admission position k.
  */
 #ifndef FBGPU_DIGEST_H_
 #define FBGPU_DIGEST_H_
@@ -48,7 +49,7 @@ FB_HD uint64_t fb_digest_bits(double x) {
   return u;
 }
 
-/* entry_sum = sum over k of fb_digest_entry(k, req_k, new_k). */
+/* entry_sum = XOR over k of fb_digest_entry(k, req_k, new_k). */
 FB_HD uint64_t fb_digest_step(uint64_t h, int64_t t_us, uint32_t n_entries,
                               uint64_t entry_sum, double predicted_ms,
                               double actual_ms) {

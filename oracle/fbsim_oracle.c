@@ -547,7 +547,7 @@ static int orc_begin_step(orc_node* nd, int64_t now) {
   uint64_t esum = 0;
   for (int64_t k = 0; k < nd->inflight.n_entries; ++k) {
     total_new += nd->plan_e[k].new_tokens;
-    esum += fb_digest_entry((uint32_t)k, (uint32_t)nd->plan_e[k].request_id,
+    esum ^= fb_digest_entry((uint32_t)k, (uint32_t)nd->plan_e[k].request_id,
                             (uint32_t)nd->plan_e[k].new_tokens);
   }
   /* ground_truth_step_time_ms, costmodel.cpp:138-146 */

@@ -210,7 +210,7 @@ int run_mirror(const fb_trace* rows, const fb_instance& inst,
       const BatchPlan& p = plans.at(step);
       uint64_t esum = 0;
       for (size_t k = 0; k < p.entries.size(); ++k)
-        esum += fb_digest_entry(static_cast<uint32_t>(k),
+        esum ^= fb_digest_entry(static_cast<uint32_t>(k),
                                 static_cast<uint32_t>(p.entries[k].request_id),
                                 static_cast<uint32_t>(p.entries[k].new_tokens));
       const double actual = actuals.at(step);

@@ -88,6 +88,32 @@ __device__ __forceinline__ T warp_sum(T v) {  // integers only (exact)
   return v;
 }
 
+// Single-instruction (redux.sync) reductions with exact fallbacks.
+
+// min over int64 values; kInf marks "no value".  One REDUX when every value
+// fits in int32, else the 5-level shuffle tree.
+__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
+  const bool none = v == kInf;
+  const bool fits = none || (v >= INT32_MIN && v < INT32_MAX);
+  if (__all_sync(kFull, fits)) {
+    const int m = __reduce_min_sync(kFull, none ? INT32_MAX : static_cast<int>(v));
+    return m == INT32_MAX ? kInf : static_cast<int64_t>(m);
+  }
+  return warp_min(v);
+}
+// sum of non-negative values below 2^50 (two 32-bit REDUX on 24-bit splits)
+__device__ __forceinline__ int64_t warp_sum_small(int64_t v) {
+  const uint32_t lo = static_cast<uint32_t>(v) & 0xffffffu;
+  const uint32_t hi = static_cast<uint32_t>(static_cast<uint64_t>(v) >> 24);
+  return (static_cast<int64_t>(__reduce_add_sync(kFull, hi)) << 24) +
+         static_cast<int64_t>(__reduce_add_sync(kFull, lo));
+}
+__device__ __forceinline__ uint64_t warp_xor_u64(uint64_t v) {
+  const uint32_t lo = __reduce_xor_sync(kFull, static_cast<uint32_t>(v));
+  const uint32_t hi = __reduce_xor_sync(kFull, static_cast<uint32_t>(v >> 32));
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
 // ---------------------------------------------------------- device layouts
 
 // Immutable per-instance parameters (from fb_instance).

@@ -22,6 +22,10 @@ namespace fbgpu {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kSmemSlots = 64;  // visible tasks held in shared-memory scratch
+#ifndef FB_ENGINE_BLOCKS_PER_SM
+#define FB_ENGINE_BLOCKS_PER_SM 2
+#endif
+constexpr int kEngineBlocksPerSm = FB_ENGINE_BLOCKS_PER_SM;  // register cap for occupancy
 
 size_t scratch_bytes_per_slot() { return kScratchBytesPerSlot; }
 size_t dev_inst_bytes() { return sizeof(DevInst); }
@@ -218,8 +222,8 @@ __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
     if (!v.decode) lpf += v.nw;
   }
   __syncwarp();
-  int64_t min_slack = warp_min(lmin);
-  int64_t pf_tok = warp_sum(lpf);
+  int64_t min_slack = warp_min_i64(lmin);
+  int64_t pf_tok = warp_sum_small(lpf);
   double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
   for (int64_t r = w.S.pulled; r < w.S.arr; ++r) {
     const int64_t row = w.toff + r;
@@ -311,7 +315,7 @@ __device__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
   f.b = I->sb;
   f.c = I->sc;
   const int Ai = static_cast<int>(A);
-  const FormOut o = form_batch_warp(s, Ai, acc, f);
+  const FormOut o = form_batch_warp(s, Ai, acc, f, /*seq_unique=*/true);
 
   // ground_truth_step_time_ms, costmodel.cpp:138-146
   double actual = predict_ms(I->ta, I->tb, I->tc, o.total_new, o.total_ctx);
@@ -345,7 +349,7 @@ __device__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
     if (adm) {
       const int idx = run_all + __popc(m & lanemask_lt());
       const int r = s.req[p];
-      esum += fb_digest_entry(static_cast<uint32_t>(idx), static_cast<uint32_t>(r),
+      esum ^= fb_digest_entry(static_cast<uint32_t>(idx), static_cast<uint32_t>(r),
                               static_cast<uint32_t>(tk));
       if (log_ok) P.log_entries[entry_base + idx] = fb_plan_entry{r, tk};
     }
@@ -357,7 +361,7 @@ __device__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
     run_w += __popc(mw);
   }
   __syncwarp();
-  esum = warp_sum(esum);
+  esum = warp_xor_u64(esum);
   // unadmitted visible waiting keep their relative order after the movers
   int run_u = 0;
   const int64_t base_u = n_act + run_w;
@@ -408,27 +412,67 @@ __device__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
   return true;
 }
 
+}  // namespace fbgpu
+
+#include "fb_engine_rr.cuh"
+
+namespace fbgpu {
+
 // run_node's event loop (engine.cpp:266-288) for up to max_events times t.
+// Steps run on the register-resident path while at most 32 requests are live
+// and on the memory path otherwise; the switch happens at step boundaries.
 __device__ void run_instance(const EngineParams& P, Inst& w) {
   const int64_t* arrival = P.arrival + w.toff;
+  const Scratch s = carve_scratch(w.smem, kSmemSlots);
+  TaskReg tk = {};
+  bool rr = false;
+  int64_t next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
   for (int64_t ev = 0; ev < P.max_events; ++ev) {
     const int64_t t_step = w.S.busy ? w.S.step_end : kInf;
-    const int64_t t_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
-    const int64_t t = t_step < t_arr ? t_step : t_arr;
+    const int64_t t = t_step < next_arr ? t_step : next_arr;
     if (t == kInf || (!w.S.busy && t >= w.horizon)) {
+      if (rr) rr_spill(P, w, tk);
       w.S.done = 1;
       w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0 ||
                         w.S.arr < w.nreq) ? 1 : 0;
       return;
     }
     w.S.t_last = t;
-    if (w.S.busy && t_step == t) complete_step(P, w);
-    while (w.S.arr < w.nreq && arrival[w.S.arr] == t) w.S.arr++;  // Node::enqueue
-    if (!w.S.busy && t < w.horizon) begin_step(P, w, t);
+    if (w.S.busy && t_step == t) {
+      if (rr) {
+        complete_rr(P, w, tk);
+      } else {
+        complete_step(P, w);
+      }
+    }
+    while (next_arr == t) {  // Node::enqueue (visible at its arrival time)
+      w.S.arr++;
+      next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
+    }
+    if (!w.S.busy && t < w.horizon) {
+      const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
+      if (rr && upcoming > kWarp) {
+        rr_spill(P, w, tk);
+        rr = false;
+      } else if (!rr && upcoming <= kWarp) {
+        rr_load(P, w, tk);
+        rr = true;
+      }
+      if (rr) {
+        if (begin_rr(P, w, tk, t, s) < 0) {  // keys outside the packed range
+          rr_spill(P, w, tk);
+          rr = false;
+          begin_step(P, w, t);
+        }
+      } else {
+        begin_step(P, w, t);
+      }
+    }
   }
+  if (rr) rr_spill(P, w, tk);
 }
 
-__global__ void __launch_bounds__(kWarp * kWarpsPerBlock)
+__global__ void __launch_bounds__(kWarp * kWarpsPerBlock, kEngineBlocksPerSm)
 engine_kernel(const __grid_constant__ EngineParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x / kWarp;
@@ -609,7 +653,7 @@ form_batch_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restr
     f.b = cfg.model.b_ms;
     f.c = cfg.model.c_ms;
     const int Ai = static_cast<int>(n);
-    const FormOut o = form_batch_warp(s, Ai, acc, f);
+    const FormOut o = form_batch_warp(s, Ai, acc, f, /*seq_unique=*/false);
     int run = 0;
     for (int k0 = 0; k0 < Ai; k0 += kWarp) {
       const int k = k0 + lane_id();

@@ -1,0 +1,422 @@
+// fb_engine_rr.cuh -- register-resident fast path of the warp engine.
+//
+// While a node has at most 32 live requests (the common case: C1/C2/C3 see
+// A <= 32 in ~99% of steps), lane i of the owning warp keeps
+// the state of live request i (views order: active in activation order, then
+// waiting in admission order) in registers across steps.  A step then costs
+// no global traffic except new arrivals and finished-request records, and the
+// K1-K5 stages run as register / shuffle / redux code.  Reordering (finished
+// requests leaving active_, waiting -> active moves) is a shuffle permutation
+// of the per-lane state.  Semantics are identical to the memory path in
+// fb_engine.cu (same helpers, same operation order); the engine switches
+// between the two at step boundaries (spill / load).
+#pragma once
+
+namespace fbgpu {
+
+// One live request held by one lane.
+struct TaskReg {
+  int32_t r, seq, prompt, output, prefilled, nidx, take;
+  uint32_t flags;
+  int64_t dl0;  // arrival + ttft_slo (TTFT deadline)
+  int64_t tpot;
+  int64_t first;  // time of token 0, -1 none
+  double maxtp, maxtp_alt;
+};
+
+__device__ __forceinline__ void permute_task(TaskReg& t, int src) {
+  t.r = __shfl_sync(kFull, t.r, src);
+  t.seq = __shfl_sync(kFull, t.seq, src);
+  t.prompt = __shfl_sync(kFull, t.prompt, src);
+  t.output = __shfl_sync(kFull, t.output, src);
+  t.prefilled = __shfl_sync(kFull, t.prefilled, src);
+  t.nidx = __shfl_sync(kFull, t.nidx, src);
+  t.take = __shfl_sync(kFull, t.take, src);
+  t.flags = __shfl_sync(kFull, t.flags, src);
+  t.dl0 = __shfl_sync(kFull, t.dl0, src);
+  t.tpot = __shfl_sync(kFull, t.tpot, src);
+  t.first = __shfl_sync(kFull, t.first, src);
+  t.maxtp = __shfl_sync(kFull, t.maxtp, src);
+  t.maxtp_alt = __shfl_sync(kFull, t.maxtp_alt, src);
+}
+
+// A request entering the node (Node::pull_arrivals, engine.cpp:146-149).
+__device__ __forceinline__ void fresh_task(const EngineParams& P, const Inst& w, int64_t r,
+                                           int64_t seq, TaskReg& t) {
+  const int64_t row = w.toff + r;
+  t.r = static_cast<int32_t>(r);
+  t.seq = static_cast<int32_t>(seq);
+  t.prompt = P.prompt[row];
+  t.output = P.output[row];
+  t.dl0 = P.arrival[row] + P.ttft[row];
+  t.tpot = P.tpot[row];
+  t.prefilled = 0;
+  t.nidx = 0;
+  t.take = 0;
+  t.flags = 0;
+  t.first = -1;
+  t.maxtp = 0.0;
+  t.maxtp_alt = 0.0;
+}
+
+// Writes a request's progress + record back to the arena.
+__device__ __forceinline__ void flush_task(const EngineParams& P, const Inst& w,
+                                           const TaskReg& t) {
+  const int64_t g = w.roff + t.r;
+  P.prefilled[g] = t.prefilled;
+  P.nidx[g] = t.nidx;
+  P.seq[g] = t.seq;
+  P.flags[g] = t.flags;
+  P.first[g] = t.first;
+  P.maxtp[g] = t.maxtp;
+  P.maxtp_alt[g] = t.maxtp_alt;
+}
+
+__device__ __forceinline__ void load_task(const EngineParams& P, const Inst& w, int p,
+                                          TaskReg& t) {
+  const int2 v = w.vl[p];
+  const int64_t g = w.roff + v.x;
+  const int64_t row = w.toff + v.x;
+  t.r = v.x;
+  t.take = v.y;
+  t.prompt = P.prompt[row];
+  t.output = P.output[row];
+  t.dl0 = P.arrival[row] + P.ttft[row];
+  t.tpot = P.tpot[row];
+  t.prefilled = P.prefilled[g];
+  t.nidx = P.nidx[g];
+  t.seq = P.seq[g];
+  t.flags = P.flags[g];
+  t.first = P.first[g];
+  t.maxtp = P.maxtp[g];
+  t.maxtp_alt = P.maxtp_alt[g];
+}
+
+// Memory path -> registers (at a step boundary).
+__device__ __forceinline__ void rr_load(const EngineParams& P, const Inst& w, TaskReg& t) {
+  if (lane_id() < w.S.n_live) load_task(P, w, lane_id(), t);
+}
+
+// Registers -> memory path / end of launch.
+__device__ __forceinline__ void rr_spill(const EngineParams& P, const Inst& w,
+                                         const TaskReg& t) {
+  if (lane_id() < w.S.n_live) {
+    flush_task(P, w, t);
+    w.vl[lane_id()] = make_int2(t.r, t.take);
+  }
+  __syncwarp();
+}
+
+// Token emission on registers (engine.cpp:211-232, metrics.cpp:42-60,196-214).
+__device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
+  const int32_t idx = t.nidx;
+  if (idx == 0) {
+    t.first = now;
+    if (now <= t.dl0) t.flags |= FB_REC_MET_TTFT;  // emits[0] <= ttft_slo
+  } else {
+    const int64_t d = now - t.first;
+    if (d > t.tpot * static_cast<int64_t>(idx)) t.flags |= kTpotViolated;
+    const double dm = us_to_ms(d);
+    const double x = ddiv(dm, static_cast<double>(idx));
+    if (t.maxtp < x) t.maxtp = x;
+    if (idx >= 2) {
+      const double y = ddiv(dm, static_cast<double>(idx - 1));
+      if (t.maxtp_alt < y) t.maxtp_alt = y;
+    }
+    if (now > t.dl0 + t.tpot * static_cast<int64_t>(idx)) t.flags |= FB_REC_ENV_MISS;
+  }
+  t.nidx = idx + 1;
+  const bool fin = t.nidx >= t.output;
+  if (fin) {
+    t.flags |= FB_REC_FINISHED;
+    if (!(t.flags & kTpotViolated)) t.flags |= FB_REC_MET_TPOT;
+  }
+  return fin;
+}
+
+// Node::complete_step (engine.cpp:204-254) on registers.
+__device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, TaskReg& t) {
+  const int64_t now = w.S.step_end;
+  const int lane = lane_id();
+  const bool live = lane < w.S.n_live;
+  bool fin = false;
+  if (live && t.take > 0) {
+    bool emit = true;
+    if (t.prefilled < t.prompt) {
+      t.prefilled += t.take;
+      emit = t.prefilled >= t.prompt;  // the completing chunk yields token 0
+    }
+    if (emit) fin = emit_reg(t, now);
+    if (fin) flush_task(P, w, t);
+  }
+  t.take = 0;
+  const unsigned finm = __ballot_sync(kFull, fin);
+  if (finm) {  // order-preserving removal from active_ (engine.cpp:228-229)
+    const unsigned keep = __ballot_sync(kFull, live && !fin);
+    const int nk = __popc(keep);
+    const int src = lane < nk ? static_cast<int>(__fns(keep, 0, lane + 1)) : lane;
+    permute_task(t, src);
+    w.S.n_live -= __popc(finm);
+    w.S.n_active -= __popc(finm);
+  }
+  w.S.busy = 0;
+}
+
+// Per-lane K1 view (build_task_views, engine.cpp:51-81).
+struct RView {
+  bool decode;
+  int32_t nw;  // new tokens available
+  int64_t ctx, slack;
+};
+
+__device__ __forceinline__ RView view_reg(const TaskReg& t, int64_t now) {
+  RView v;
+  v.decode = t.prefilled >= t.prompt;
+  if (!v.decode) {
+    v.nw = t.prompt - t.prefilled;
+    v.ctx = t.prefilled;
+    v.slack = t.dl0 + t.tpot * static_cast<int64_t>(t.nidx) - now;
+  } else {
+    v.nw = 1;
+    v.ctx = static_cast<int64_t>(t.prompt) + t.nidx;
+    int64_t anchor = t.dl0;
+    if (t.first >= 0 && t.first < anchor) anchor = t.first;
+    v.slack = anchor + t.tpot * static_cast<int64_t>(t.nidx) - now;
+  }
+  return v;
+}
+
+// Node::pull_arrivals (engine.cpp:127-151) on registers; the caller
+// guarantees n_live + pending <= 32.
+__device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg& t,
+                                        int64_t now, const Scratch& s) {
+  const int lane = lane_id();
+  if (w.policy != FB_POLICY_FAIRBATCH_PAB) {
+    const int64_t k = w.S.arr - w.S.pulled;
+    const int j = lane - static_cast<int>(w.S.n_live);
+    if (j >= 0 && j < k) fresh_task(P, w, w.S.pulled + j, w.S.seq_counter + j, t);
+    w.S.seq_counter += k;
+    w.S.n_live += k;
+    w.S.pulled = w.S.arr;
+    return;
+  }
+  // K5: PAB admission with the view fold in views order (sched.cpp:248-278)
+  const DevInst* I = w.I;
+  const double Wm = us_to_ms(I->g_ttft), Tm = us_to_ms(I->g_tpot);
+  const double a = I->sa, b = I->sb, c = I->sc;
+  int64_t A = visible_count(w);
+  int64_t lmin = kInf, lpf = 0;
+  if (lane < A) {
+    const RView v = view_reg(t, now);
+    s.tcost[lane] = pab_term(Wm, Tm, b, c, v.slack, v.ctx);
+    lmin = v.slack;
+    if (!v.decode) lpf = v.nw;
+  }
+  __syncwarp();
+  int64_t min_slack = warp_min_i64(lmin);
+  int64_t pf_tok = warp_sum_small(lpf);
+  double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
+  for (int64_t r = w.S.pulled; r < w.S.arr; ++r) {
+    const int64_t row = w.toff + r;
+    const int64_t prompt = P.prompt[row];
+    const int64_t budget = pab_close(Wm, Tm, a, b, c, A > 0, min_slack, r_tasks, pf_tok);
+    if (prompt <= budget) {
+      bool vis = true;
+      if (w.max_active > 0) {
+        int64_t slots = static_cast<int64_t>(w.max_active) - w.S.n_active;
+        if (slots < 0) slots = 0;
+        vis = (w.S.n_live - w.S.n_active) < slots;
+      }
+      if (lane == w.S.n_live) fresh_task(P, w, r, w.S.seq_counter, t);
+      w.S.seq_counter++;
+      w.S.n_live++;
+      if (vis) {
+        const int64_t slack = P.arrival[row] + P.ttft[row] - now;
+        r_tasks = dadd(r_tasks, pab_term(Wm, Tm, b, c, slack, 0));
+        min_slack = slack < min_slack ? slack : min_slack;
+        pf_tok += prompt;
+        A++;
+      }
+    } else {
+      if (lane == 0) {
+        P.flags[w.roff + r] |= FB_REC_REJECTED;
+        if (P.log_on && w.S.log_rejects < P.log_reject_cap) {
+          fb_reject_log& rl = P.log_rejects[I->log_reject_off + w.S.log_rejects];
+          rl.t_us = now;
+          rl.pab_tokens = budget;
+          rl.req = static_cast<int32_t>(r);
+          rl.reserved = 0;
+        }
+      }
+      if (P.log_on) {
+        if (w.S.log_rejects < P.log_reject_cap) {
+          w.S.log_rejects++;
+        } else {
+          w.S.log_trunc = 1;
+        }
+      }
+      w.S.digest = fb_digest_reject(w.S.digest, now, static_cast<uint32_t>(r), budget);
+      w.S.n_rejected++;
+    }
+  }
+  __syncwarp();
+  w.S.pulled = w.S.arr;
+}
+
+// Node::begin_step (engine.cpp:153-202) on registers.  Returns 0 when no step
+// was launched (nothing visible), 1 when a step was launched, and -1 when the
+// keys do not fit the packed form (caller spills and takes the memory path;
+// nothing has been modified except the pulled arrivals, which are spilled).
+__device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg& t,
+                                        int64_t now, const Scratch& s) {
+  const DevInst* I = w.I;
+  const int lane = lane_id();
+  if (w.S.pulled < w.S.arr) pull_rr(P, w, t, now, s);
+  const int A = static_cast<int>(visible_count(w));
+  if (A == 0) return 0;
+  const bool vis = lane < A;
+  const int policy = w.policy;
+  const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+
+  // K1: views + init_time_budget reductions (sched.cpp:90-106)
+  const RView v = view_reg(t, now);
+  const int64_t min_tpot = warp_min_i64(vis ? t.tpot : kInf);
+  const int64_t min_dec = warp_min_i64(vis && v.decode ? v.slack : kInf);
+  const int n_dec = __popc(__ballot_sync(kFull, vis && v.decode));
+  double init_ms = 0.0;
+  int64_t urgency = 0;
+  if (fair) {
+    const int64_t init = n_dec == 0 ? min_tpot : (min_dec > min_tpot ? min_dec : min_tpot);
+    urgency = init + min_tpot;
+    init_ms = us_to_ms(init);
+  }
+
+  // K2: packed key (group, slack, seq) and rank by counting
+  const bool fits = !vis || (t.seq >= 0 && t.seq < kPackSeq &&
+                             (!fair || (v.slack >= -kPackSlack && v.slack < kPackSlack)));
+  if (!__all_sync(kFull, fits)) return -1;
+  uint64_t key;
+  if (fair) {
+    const uint64_t g = (v.decode && v.slack < urgency) ? 0 : (!v.decode ? 1 : 2);
+    key = (g << 62) | (static_cast<uint64_t>(v.slack + kPackSlack) << 22) |
+          static_cast<uint64_t>(t.seq);
+  } else {
+    const uint64_t g = policy == FB_POLICY_SARATHI ? (v.decode ? 0 : 1) : 0;
+    key = (g << 62) | static_cast<uint64_t>(t.seq);
+  }
+  if (!vis) key = ~uint64_t(0);
+  int rank = 0;
+#pragma unroll 8
+  for (int q = 0; q < A; ++q) rank += __shfl_sync(kFull, key, q) < key;
+  if (!vis) rank = lane;
+  s.order[rank] = lane;
+  __syncwarp();
+  const int pk = s.order[lane];  // view position at sorted rank `lane` (k < A)
+
+  // K3: sorted costs (sched.cpp:142-144) -> shared scratch -> greedy scan
+  const FormCfg f{policy, I->max_chunk, I->token_budget, I->sa, I->sb, I->sc};
+  const double cc = dmul(f.c, static_cast<double>(v.ctx));
+  const double tc = dadd(dmul(f.b, static_cast<double>(v.nw)), cc);
+  const uint32_t nwp = static_cast<uint32_t>(v.nw) | (v.decode ? kDecodeBit : 0u);
+  const double tc_s = __shfl_sync(kFull, tc, pk);
+  const double cc_s = __shfl_sync(kFull, cc, pk);
+  const uint32_t nw_s = __shfl_sync(kFull, nwp, pk);
+  const int64_t ctx_s = __shfl_sync(kFull, v.ctx, pk);
+  const int32_t r_s = __shfl_sync(kFull, t.r, pk);
+  if (vis) {
+    s.tcost[lane] = tc_s;
+    s.ccost[lane] = cc_s;
+    s.khi[lane] = nw_s;
+    s.take[lane] = 0;
+  }
+  __syncwarp();
+  if (fair) {
+    scan_fairbatch(s, A, init_ms, f);
+  } else if (policy == FB_POLICY_SARATHI) {
+    scan_sarathi(s, A, n_dec, f);
+  } else {
+    scan_prefill_first(s, A, f);
+  }
+  const int32_t take_s = vis ? s.take[lane] : 0;
+
+  // finalize_plan (sched.cpp:37-48) + digest + log, in admission order
+  const unsigned madm = __ballot_sync(kFull, take_s > 0);
+  const int E = __popc(madm);
+  const int64_t tn = warp_sum_small(take_s);
+  const int64_t tctx = warp_sum_small(take_s > 0 ? ctx_s : 0);
+  const double predicted = E == 0 ? 0.0 : predict_ms(f.a, f.b, f.c, tn, tctx);
+  const int idx = __popc(madm & lanemask_lt());
+  const uint64_t eh = take_s > 0 ? fb_digest_entry(static_cast<uint32_t>(idx),
+                                                   static_cast<uint32_t>(r_s),
+                                                   static_cast<uint32_t>(take_s))
+                                 : 0;
+  const uint64_t esum = warp_xor_u64(eh);
+  const bool log_ok = P.log_on && w.S.log_steps < P.log_step_cap &&
+                      w.S.log_entries + E <= P.log_entry_cap;
+  if (log_ok && take_s > 0)
+    P.log_entries[I->log_entry_off + w.S.log_entries + idx] = fb_plan_entry{r_s, take_s};
+
+  // ground_truth_step_time_ms, costmodel.cpp:138-146
+  double actual = predict_ms(I->ta, I->tb, I->tc, tn, tctx);
+  const double amp = I->noise_amp;
+  if (amp != 0.0) {
+    const double u = dsub(dmul(2.0, keyed_uniform(I->noise_seed, w.S.step_counter)), 1.0);
+    actual = dmul(actual, dadd(1.0, dmul(amp, u)));
+  }
+  int64_t dur = ms_to_us(actual);
+  if (dur < 1) dur = 1;
+
+  // takes back to view positions; waiting -> active in plan order
+  // (engine.cpp:176-182) as a shuffle permutation
+  const int n_act = static_cast<int>(w.S.n_active);
+  const int32_t take_v = __shfl_sync(kFull, take_s, vis ? rank : lane);
+  t.take = vis ? take_v : 0;
+  const unsigned mw = __ballot_sync(kFull, take_s > 0 && pk >= n_act);
+  const int n_w = __popc(mw);
+  if (n_w > 0) {
+    const int widx = __popc(mw & lanemask_lt());
+    const int widx_v = __shfl_sync(kFull, widx, vis ? rank : lane);
+    const bool un = vis && lane >= n_act && t.take == 0;
+    const unsigned mu = __ballot_sync(kFull, un);
+    int dest = lane;
+    if (vis && lane >= n_act)
+      dest = t.take > 0 ? n_act + widx_v : n_act + n_w + __popc(mu & lanemask_lt());
+    __syncwarp();
+    s.order[dest] = lane;
+    __syncwarp();
+    const int src = s.order[lane];
+    permute_task(t, src);
+  }
+
+  if (P.log_on) {
+    if (log_ok) {
+      if (lane == 0) {
+        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
+        sl.t_us = now;
+        sl.duration_us = dur;
+        sl.predicted_ms = predicted;
+        sl.actual_ms = actual;
+        sl.total_new = tn;
+        sl.total_ctx = tctx;
+        sl.init_budget_ms = init_ms;
+        sl.entry_off = w.S.log_entries;
+        sl.n_entries = E;
+      }
+      w.S.log_steps++;
+      w.S.log_entries += E;
+    } else {
+      w.S.log_trunc = 1;
+    }
+  }
+  w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(E), esum, predicted, actual);
+  w.S.sum_visible += A;
+  w.S.sum_entries += E;
+  w.S.sum_new += tn;
+  w.S.n_active = n_act + n_w;
+  w.S.busy = 1;
+  w.S.step_end = now + dur;
+  w.S.step_counter++;
+  return 1;
+}
+
+}  // namespace fbgpu

@@ -42,39 +42,77 @@ struct ViewAcc {
     }
   }
   __device__ __forceinline__ void reduce() {
-    min_tpot = warp_min(min_tpot);
-    min_dec = warp_min(min_dec);
-    n_dec = warp_sum(n_dec);
+    min_tpot = warp_min_i64(min_tpot);
+    min_dec = warp_min_i64(min_dec);
+    n_dec = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(n_dec)));
   }
 };
+
+constexpr int64_t kPackSlack = int64_t(1) << 39;  // packed slack range [-2^39, 2^39)
+constexpr int64_t kPackSeq = int64_t(1) << 22;    // packed seq range [0, 2^22)
 
 // K2a: sort keys.  Fair batching: (group, slack, seq) with group 0 urgent
 // decode / 1 prefill / 2 relaxed decode (sched.cpp:110-127); sarathi:
 // (decode first, fifo) (sched.cpp:174-178); prefill-first: fifo
-// (sched.cpp:210-211).  slack must lie in [-2^61, 2^61) (validated on input).
-__device__ __forceinline__ void make_keys(const Scratch& s, int A, int policy,
-                                          int64_t urgency) {
+// (sched.cpp:210-211).
+//
+// With unique seqs inside the packing range (always, for engine nodes) the key
+// is ONE u64: (group << 62) | ((slack + 2^39) << 22) | seq.  Otherwise khi
+// holds (group << 62) | (slack + 2^61) and seq breaks ties (slack must lie in
+// [-2^61, 2^61), validated on input).  Returns the (warp-uniform) packing.
+__device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
+                                          int64_t urgency, bool seq_unique) {
+  const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+  bool ok = seq_unique;
+  if (ok) {
+    for (int p = lane_id(); p < A; p += kWarp) {
+      const int64_t sq = s.seq[p];
+      bool f = sq >= 0 && sq < kPackSeq;
+      if (fair) {
+        const int64_t slack = s.slack[p];
+        f = f && slack >= -kPackSlack && slack < kPackSlack;
+      }
+      ok = ok && f;
+    }
+  }
+  const bool packed = __all_sync(kFull, ok);
   for (int p = lane_id(); p < A; p += kWarp) {
     const bool decode = (static_cast<uint32_t>(s.nw[p]) & kDecodeBit) != 0;
     uint64_t g, sl = 0;
-    if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
+    if (fair) {
       const int64_t slack = s.slack[p];
       g = (decode && slack < urgency) ? 0 : (!decode ? 1 : 2);
-      sl = static_cast<uint64_t>(slack + (int64_t(1) << 61)) & ((uint64_t(1) << 62) - 1);
-    } else if (policy == FB_POLICY_SARATHI) {
-      g = decode ? 0 : 1;
+      sl = packed ? (static_cast<uint64_t>(slack + kPackSlack) << 22) |
+                        static_cast<uint64_t>(s.seq[p])
+                  : static_cast<uint64_t>(slack + (int64_t(1) << 61)) &
+                        ((uint64_t(1) << 62) - 1);
     } else {
-      g = 0;
+      g = policy == FB_POLICY_SARATHI ? (decode ? 0 : 1) : 0;
+      if (packed) sl = static_cast<uint64_t>(s.seq[p]);
     }
     s.khi[p] = (g << 62) | sl;
   }
   __syncwarp();
+  return packed;
 }
 
-// K2b: order[k] = view position of rank k.  Keys (khi, seq) are unique per
-// node (seq_counter_ only grows, engine.cpp:147); exact ties fall back to view
+// K2b: order[k] = view position of rank k, by counting smaller keys.  Packed
+// keys are unique (seq_counter_ only grows, engine.cpp:147), so one u64
+// compare per pair suffices; the general form breaks exact ties by view
 // position so the result is always a permutation.
-__device__ __forceinline__ void rank_order(const Scratch& s, int A) {
+__device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed) {
+  if (packed) {
+    for (int p0 = 0; p0 < A; p0 += kWarp) {
+      const int p = p0 + lane_id();
+      const uint64_t kh = p < A ? s.khi[p] : 0;
+      int rank = 0;
+#pragma unroll 4
+      for (int q = 0; q < A; ++q) rank += s.khi[q] < kh;
+      if (p < A) s.order[rank] = p;
+    }
+    __syncwarp();
+    return;
+  }
   for (int p0 = 0; p0 < A; p0 += kWarp) {
     const int p = p0 + lane_id();
     uint64_t kh = 0;
@@ -202,7 +240,7 @@ __device__ __forceinline__ void scan_prefill_first(const Scratch& s, int A,
 // s.seq (sorted context) for the caller's bookkeeping.
 __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
                                                    const ViewAcc& acc,
-                                                   const FormCfg& f) {
+                                                   const FormCfg& f, bool seq_unique) {
   FormOut out;
   out.init_ms = 0.0;
   const bool fair = f.policy == FB_POLICY_FAIRBATCH || f.policy == FB_POLICY_FAIRBATCH_PAB;
@@ -214,8 +252,8 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
     urgency = init + acc.min_tpot;
     out.init_ms = us_to_ms(init);
   }
-  make_keys(s, A, f.policy, urgency);
-  rank_order(s, A);
+  const bool packed = make_keys(s, A, f.policy, urgency, seq_unique);
+  rank_order(s, A, packed);
   gather_sorted(s, A, f.b, f.c);
   if (fair) {
     scan_fairbatch(s, A, out.init_ms, f);
@@ -235,9 +273,9 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
       tc += s.seq[k];
     }
   }
-  out.n_entries = warp_sum(e);
-  out.total_new = warp_sum(tn);
-  out.total_ctx = warp_sum(tc);
+  out.n_entries = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(e)));
+  out.total_new = warp_sum_small(tn);
+  out.total_ctx = warp_sum_small(tc);
   out.predicted_ms = out.n_entries == 0 ? 0.0 : predict_ms(f.a, f.b, f.c, out.total_new, out.total_ctx);
   return out;
 }

@@ -21,7 +21,7 @@ from . import _abi
 from .batch import Batch, Rows
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfbgpu.so")
+LIB_PATH = os.environ.get("FBGPU_LIB") or os.path.join(_HERE, "libfbgpu.so")  # FBGPU_LIB: dev A/B builds
 
 
 class FbError(RuntimeError):

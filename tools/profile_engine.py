@@ -24,3 +24,13 @@ a.run()
 a.synchronize()
 r = a.results()
 print(which, batch.n_instances, "instances", int(r["steps"].sum()), "steps", a.last_run_ms(), "ms")
+
+if which == "c2" and len(sys.argv) > 3 and sys.argv[3] == "top":
+    import numpy as np
+    order = np.argsort(-r["steps"].astype(np.int64))
+    sub = batch.subset(order[: int(sys.argv[4]) if len(sys.argv) > 4 else 1].tolist())
+    b = fbgpu.Arena(0)
+    b.load(sub)
+    b.run()
+    b.synchronize()
+    print("top subset", sub.n_instances, b.last_run_ms(), "ms")
