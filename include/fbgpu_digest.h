@@ -33,10 +33,12 @@ FB_HD uint64_t fb_mix64(uint64_t z) {
   return z;
 }
 
+FB_HD uint64_t fb_rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
 /* Hash of the k-th plan entry (k = admission position). */
 FB_HD uint64_t fb_digest_entry(uint32_t k, uint32_t req, uint32_t new_tokens) {
-  return fb_mix64(fb_mix64(((uint64_t)k << 32) | (uint64_t)req) ^
-                  (0x9e3779b97f4a7c15ULL + (uint64_t)new_tokens));
+  return fb_mix64((((uint64_t)k << 32) | (uint64_t)req) ^
+                  ((uint64_t)new_tokens * 0x9e3779b97f4a7c15ULL));
 }
 
 FB_HD uint64_t fb_digest_bits(double x) {
@@ -54,10 +56,8 @@ FB_HD uint64_t fb_digest_step(uint64_t h, int64_t t_us, uint32_t n_entries,
                               uint64_t entry_sum, double predicted_ms,
                               double actual_ms) {
   h = fb_mix64(h ^ (uint64_t)t_us);
-  h = fb_mix64(h ^ (0x5354455000000000ULL | (uint64_t)n_entries));
-  h = fb_mix64(h ^ entry_sum);
-  h = fb_mix64(h ^ fb_digest_bits(predicted_ms));
-  h = fb_mix64(h ^ fb_digest_bits(actual_ms));
+  h = fb_mix64(h ^ entry_sum ^ fb_rotl64((uint64_t)n_entries | 0x5354455000000000ULL, 19));
+  h = fb_mix64(h ^ fb_digest_bits(predicted_ms) ^ fb_rotl64(fb_digest_bits(actual_ms), 29));
   return h;
 }
 

@@ -120,6 +120,7 @@ struct fb_arena {
   DevBuf<fb_plan_entry> log_entries;
   DevBuf<fb_reject_log> log_rejects;
   DevBuf<unsigned long long> work;
+  DevBuf<int64_t> wide_list;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
 
@@ -151,6 +152,7 @@ struct fb_arena {
     P.log_entry_cap = log.entry_cap;
     P.log_reject_cap = log.reject_cap;
     P.work = work.p;
+    P.wide_list = wide_list.p;
     P.max_events = max_events <= 0 ? INT64_MAX : max_events;
     return P;
   }
@@ -161,6 +163,7 @@ struct fb_arena {
     flags.release(); first.release(); maxtp.release(); maxtp_alt.release(); vlist.release();
     gscratch.release(); log_steps.release(); log_entries.release(); log_rejects.release();
     work.release();
+    wide_list.release();
   }
 };
 
@@ -197,7 +200,7 @@ int fb_arena_create(int device, void* stream, fb_arena** out) {
   cudaEventCreate(&a->ev0);
   cudaEventCreate(&a->ev1);
   a->geo = fbgpu::engine_geometry(device);
-  cudaError_t e = a->work.ensure(2);
+  cudaError_t e = a->work.ensure(4);
   if (e != cudaSuccess) {
     delete a;
     return cuda_fail(e, "cudaMalloc");
@@ -255,6 +258,7 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   ENSURE(a->output, n_rows);
   ENSURE(a->inst, n_instances * fbgpu::dev_inst_bytes());
   ENSURE(a->state, n_instances * fbgpu::dev_state_bytes());
+  ENSURE(a->wide_list, n_instances);
   ENSURE(a->prefilled, n_rec);
   ENSURE(a->nidx, n_rec);
   ENSURE(a->seq, n_rec);
@@ -398,6 +402,22 @@ int fb_arena_fetch_log_counts(fb_arena* a, fb_log_counts* out) {
     out[i].entries = s.log_entries;
     out[i].rejects = s.log_rejects;
     out[i].truncated = s.log_trunc;
+  }
+  return FB_OK;
+}
+
+int fb_arena_fetch_paths(fb_arena* a, uint32_t* out) {
+  if (!a || !a->loaded || !out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_paths");
+  FB_CUDA(cudaSetDevice(a->device));
+  const size_t sb = fbgpu::dev_state_bytes();
+  std::vector<unsigned char> h(static_cast<size_t>(a->n_inst) * sb);
+  if (!h.empty())
+    FB_CUDA(cudaMemcpyAsync(h.data(), a->state.p, h.size(), cudaMemcpyDeviceToHost, a->stream));
+  FB_CUDA(cudaStreamSynchronize(a->stream));
+  for (int64_t i = 0; i < a->n_inst; ++i) {
+    fbgpu::DevState s;
+    std::memcpy(&s, h.data() + i * sb, sizeof(s));
+    out[i] = s.paths;
   }
   return FB_OK;
 }

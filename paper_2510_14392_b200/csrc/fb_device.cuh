@@ -108,6 +108,12 @@ __device__ __forceinline__ int64_t warp_sum_small(int64_t v) {
   return (static_cast<int64_t>(__reduce_add_sync(kFull, hi)) << 24) +
          static_cast<int64_t>(__reduce_add_sync(kFull, lo));
 }
+// Upper bound of a sum of doubles (every partial rounded toward +inf).
+__device__ __forceinline__ double warp_sum_ru(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_ru(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
 __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t v) {
   const uint32_t lo = __reduce_xor_sync(kFull, static_cast<uint32_t>(v));
   const uint32_t hi = __reduce_xor_sync(kFull, static_cast<uint32_t>(v >> 32));
@@ -147,7 +153,12 @@ struct DevState {
   int64_t sum_visible, sum_entries, sum_new;
   int32_t busy, done, status, log_steps;
   int32_t log_entries, log_rejects, log_trunc, incomplete;
+  int32_t escalated;      // handed to the CTA-wide engine (fb_wide.cuh)
+  int32_t pending_begin;  // a begin_step at t_last is owed by the wide engine
+  uint32_t paths;         // engine paths used: 1 register, 2 warp-memory, 4 CTA-wide
+  int32_t pad2;
 };
+constexpr uint32_t kPathRegister = 1u, kPathMemory = 2u, kPathWide = 4u;
 
 // Per-request mutable state, structure of arrays indexed by rec_off + row.
 struct DevReq {

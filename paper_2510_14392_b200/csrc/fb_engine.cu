@@ -26,6 +26,7 @@ constexpr int kSmemSlots = 64;  // visible tasks held in shared-memory scratch
 #define FB_ENGINE_BLOCKS_PER_SM 2
 #endif
 constexpr int kEngineBlocksPerSm = FB_ENGINE_BLOCKS_PER_SM;  // register cap for occupancy
+constexpr int64_t kEscalateLive = 512;  // live requests beyond which a node goes CTA-wide
 
 size_t scratch_bytes_per_slot() { return kScratchBytesPerSlot; }
 size_t dev_inst_bytes() { return sizeof(DevInst); }
@@ -39,6 +40,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // Warp-uniform view of one instance while a warp owns it.
 struct Inst {
+  int64_t id;
   const DevInst* I;
   DevState S;
   int64_t toff, roff, nreq, horizon;
@@ -160,7 +162,7 @@ __device__ __forceinline__ void compact_vlist(Inst& w) {
 
 // Node::complete_step, engine.cpp:204-254.  In-flight plan entries are the
 // active tasks with a nonzero take (plan order only affects the event log).
-__device__ void complete_step(const EngineParams& P, Inst& w) {
+__device__ __noinline__ void complete_step(const EngineParams& P, Inst& w) {
   const int64_t t = w.S.step_end;
   bool any_fin = false;
   for (int64_t b = 0; b < w.S.n_active; b += kWarp) {
@@ -279,7 +281,7 @@ __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
 
 // Node::begin_step, engine.cpp:153-202.  Returns false when there is nothing
 // to schedule (no step launched, no step ordinal consumed).
-__device__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
+__device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
   const DevInst* I = w.I;
   if (w.S.pulled < w.S.arr) {
     if (w.policy == FB_POLICY_FAIRBATCH_PAB) {
@@ -415,6 +417,7 @@ __device__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
 }  // namespace fbgpu
 
 #include "fb_engine_rr.cuh"
+#include "fb_wide.cuh"
 
 namespace fbgpu {
 
@@ -451,6 +454,16 @@ __device__ void run_instance(const EngineParams& P, Inst& w) {
     }
     if (!w.S.busy && t < w.horizon) {
       const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
+      if (upcoming > kEscalateLive) {  // hand over to the CTA-wide engine
+        if (rr) rr_spill(P, w, tk);
+        w.S.pending_begin = 1;
+        w.S.escalated = 1;
+        if (lane_id() == 0) {
+          const unsigned long long slot = atomicAdd(&P.work[3], 1ull);
+          P.wide_list[slot] = w.id;
+        }
+        return;
+      }
       if (rr && upcoming > kWarp) {
         rr_spill(P, w, tk);
         rr = false;
@@ -463,9 +476,13 @@ __device__ void run_instance(const EngineParams& P, Inst& w) {
           rr_spill(P, w, tk);
           rr = false;
           begin_step(P, w, t);
+          w.S.paths |= kPathMemory;
+        } else {
+          w.S.paths |= kPathRegister;
         }
       } else {
         begin_step(P, w, t);
+        w.S.paths |= kPathMemory;
       }
     }
   }
@@ -483,9 +500,10 @@ engine_kernel(const __grid_constant__ EngineParams P) {
     i = __shfl_sync(kFull, i, 0);
     if (i >= static_cast<unsigned long long>(P.n_inst)) break;
     Inst w;
+    w.id = static_cast<int64_t>(i);
     w.I = P.inst + i;
     w.S = P.state[i];
-    if (w.S.done) continue;
+    if (w.S.done || w.S.escalated) continue;
     w.toff = w.I->trace_off;
     w.roff = w.I->rec_off;
     w.nreq = w.I->n_req;
@@ -498,7 +516,7 @@ engine_kernel(const __grid_constant__ EngineParams P) {
     __syncwarp();
     if (lane_id() == 0) {
       P.state[i] = w.S;
-      if (!w.S.done) atomicAdd(&P.work[1], 1ull);
+      if (!w.S.done && !w.S.escalated) atomicAdd(&P.work[1], 1ull);
     }
   }
 }
@@ -536,6 +554,11 @@ EngineGeometry engine_geometry(int device) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, g.threads, g.smem);
   if (per_sm < 1) per_sm = 1;
   g.blocks = sms * per_sm;
+  g.wide_threads = kWideThreads;
+  g.wide_smem = sizeof(WideSmem);
+  g.wide_blocks = sms;
+  cudaFuncSetAttribute(wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(g.wide_smem));
   return g;
 }
 
@@ -588,13 +611,17 @@ cudaError_t launch_reset(const EngineParams& p, int64_t n_rec, cudaStream_t st) 
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks < 1) blocks = 1;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  cudaMemsetAsync(p.work, 0, 4 * sizeof(unsigned long long), st);
   reset_kernel<<<blocks, 256, 0, st>>>(p, n_rec);
   return cudaGetLastError();
 }
 
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaStream_t st) {
-  cudaMemsetAsync(p.work, 0, 2 * sizeof(unsigned long long), st);
+  cudaMemsetAsync(p.work, 0, 3 * sizeof(unsigned long long), st);
   engine_kernel<<<g.blocks, g.threads, g.smem, st>>>(p);
+  // Escalated instances (more than kEscalateLive live requests) continue on
+  // the CTA-wide engine; with none escalated every CTA exits at once.
+  wide_kernel<<<g.wide_blocks, g.wide_threads, g.wide_smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -323,21 +323,41 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   const uint32_t nw_s = __shfl_sync(kFull, nwp, pk);
   const int64_t ctx_s = __shfl_sync(kFull, v.ctx, pk);
   const int32_t r_s = __shfl_sync(kFull, t.r, pk);
-  if (vis) {
-    s.tcost[lane] = tc_s;
-    s.ccost[lane] = cc_s;
-    s.khi[lane] = nw_s;
-    s.take[lane] = 0;
-  }
-  __syncwarp();
+  // Fair batching, everything fits: the greedy pass admits every task whole
+  // iff each prefix fits.  Exact sufficient test without the serial pass:
+  // with tb0 = init - a, S = sum of the (already rounded) task costs and
+  // N = sum of new tokens, the reference's rounded running budget satisfies
+  // tb_k >= tb0 - S_k - k*u*tb0 (u = 2^-53, every intermediate in [0, tb0]),
+  // so tb0 - S >= A*2^-52*tb0 (checked with directed rounding on an upper
+  // bound of S) and N <= token_budget imply every `consider` admits whole.
+  bool all_fit = false;
   if (fair) {
-    scan_fairbatch(s, A, init_ms, f);
-  } else if (policy == FB_POLICY_SARATHI) {
-    scan_sarathi(s, A, n_dec, f);
-  } else {
-    scan_prefill_first(s, A, f);
+    const double tb0 = dsub(init_ms, f.a);
+    const double s_up = warp_sum_ru(vis ? tc : 0.0);
+    const int64_t n_new = warp_sum_small(vis ? static_cast<int64_t>(v.nw) : 0);
+    all_fit = tb0 >= 0.0 && n_new <= f.token_budget &&
+              __dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0);
   }
-  const int32_t take_s = vis ? s.take[lane] : 0;
+  int32_t take_s;
+  if (all_fit) {
+    take_s = vis ? static_cast<int32_t>(nw_s & 0x7fffffffu) : 0;
+  } else {
+    if (vis) {
+      s.tcost[lane] = tc_s;
+      s.ccost[lane] = cc_s;
+      s.khi[lane] = nw_s;
+      s.take[lane] = 0;
+    }
+    __syncwarp();
+    if (fair) {
+      scan_fairbatch(s, A, init_ms, f);
+    } else if (policy == FB_POLICY_SARATHI) {
+      scan_sarathi(s, A, n_dec, f);
+    } else {
+      scan_prefill_first(s, A, f);
+    }
+    take_s = vis ? s.take[lane] : 0;
+  }
 
   // finalize_plan (sched.cpp:37-48) + digest + log, in admission order
   const unsigned madm = __ballot_sync(kFull, take_s > 0);

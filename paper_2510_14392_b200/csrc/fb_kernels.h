@@ -38,9 +38,12 @@ struct EngineParams {
   fb_plan_entry* log_entries;
   fb_reject_log* log_rejects;
   int32_t log_step_cap, log_entry_cap, log_reject_cap, log_on;
-  // persistent work queue
-  unsigned long long* work;  // [0] next instance, [1] instances still running
-  int64_t max_events;        // per instance per launch
+  // persistent work queues: [0] next instance (warp engine), [1] instances
+  // still running after the launch, [2] next escalated instance (wide engine),
+  // [3] number of escalated instances (list in wide_list)
+  unsigned long long* work;
+  int64_t* wide_list;
+  int64_t max_events;  // per instance per launch
 };
 
 // Per-launch geometry of the persistent engine kernel.
@@ -48,6 +51,9 @@ struct EngineGeometry {
   int blocks;
   int threads;
   size_t smem;
+  int wide_blocks;  // CTA-wide engine: one CTA per SM
+  int wide_threads;
+  size_t wide_smem;
 };
 
 EngineGeometry engine_geometry(int device);

@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         "fb_arena_record_rows": (i64, [vp]),
         "fb_arena_fetch_log_counts": (C.c_int, [vp, vp]),
         "fb_arena_fetch_log": (C.c_int, [vp, i64, vp, vp, vp]),
+        "fb_arena_fetch_paths": (C.c_int, [vp, vp]),
         "fb_run_batch": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i64, vp, vp,
                                    C.POINTER(C.c_double)]),
     }
@@ -289,6 +290,12 @@ class Arena:
         out = np.zeros(max(1, n), _abi.RECORD_DTYPE)
         _check(self._lib.fb_arena_fetch_records(self._h, _abi.vptr(out)), "fb_arena_fetch_records")
         return out[:n]
+
+    def paths(self) -> np.ndarray:
+        """Per instance FB_PATH_* bits: 1 register-resident, 2 warp memory, 4 CTA-wide."""
+        out = np.zeros(max(1, self.n_instances), np.uint32)
+        _check(self._lib.fb_arena_fetch_paths(self._h, _abi.vptr(out)), "fb_arena_fetch_paths")
+        return out[:self.n_instances]
 
     def logs(self):
         """(counts, steps[n_inst, cap], entries[n_inst, cap], rejects[n_inst, cap])."""

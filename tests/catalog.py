@@ -12,7 +12,7 @@ import hashlib
 import numpy as np
 
 from paper_2510_14392_b200 import _abi
-from paper_2510_14392_b200.batch import Batch, CostModel, engine_config, ms_to_us
+from paper_2510_14392_b200.batch import Batch, CostModel, Rows, engine_config, ms_to_us
 
 MODEL = CostModel(5.0, 0.05, 0.0001)
 BUDGET = {"fairbatch": 2048, "fairbatch_pab": 2048, "sarathi": 512, "prefill_first": 8192}
@@ -107,6 +107,33 @@ def scenario_large_live(gen) -> Batch:
     return b
 
 
+def wide_rows(n=5000, gap_us=8, seed=0):
+    """C4-like decode-heavy burst: n arrivals every gap_us, varied lengths."""
+    rng = np.random.default_rng(seed)
+    arr = np.arange(n, dtype=np.int64) * gap_us
+    prompt = rng.integers(16, 96, n).astype(np.int32)
+    output = rng.integers(2, 40, n).astype(np.int32)
+    return Rows(arr, prompt, output, np.full(n, 500_000, np.int64), np.full(n, 50_000, np.int64))
+
+
+def scenario_wide(gen) -> Batch:
+    """More than 512 live requests (the CTA-wide engine): selection windows,
+    early scan termination, activation moves and completions at large A."""
+    b = Batch()
+    rows = wide_rows()
+    m = CostModel(5.0, 0.01, 1e-6)  # SURVEY §8d C4 model
+    for pol, budget in (("fairbatch", 1 << 20), ("sarathi", 512), ("prefill_first", 8192),
+                        ("fairbatch_pab", 1 << 20)):
+        b.add(rows, engine_config(pol, budget, m, 500, 50), ms_to_us(2_000.0))
+    b.add(rows, engine_config("fairbatch", 1 << 20, m, 500, 50, noise_amplitude=0.05,
+                              noise_seed=3, max_active=1500), ms_to_us(2_000.0))
+    b.add(wide_rows(3000, 40, 1), engine_config("fairbatch", 4096, CostModel(5.0, 0.05, 1e-4),
+                                                500, 50), ms_to_us(3_000.0))
+    prof, h = TRACE_PROFILES["balanced_7"]
+    _add(b, gen, prof, 40_000.0, 40.0, "fairbatch", run_h_ms=3_000.0)
+    return b
+
+
 def scenario_c2_subset(gen, seeds=range(0, 16)) -> Batch:
     """C2 (qwen x1.5, sarathi 512 vs fairbatch 2048) for a few seeds."""
     b = Batch()
@@ -122,6 +149,7 @@ SCENARIOS = {
     "pab_overload": scenario_pab_overload,
     "large_live": scenario_large_live,
     "c2_subset": scenario_c2_subset,
+    "wide": scenario_wide,
 }
 
 

@@ -145,7 +145,7 @@ def test_engine_scenarios_match_golden(gpu, golden, name):
     assert summarize(out.results, out.records) == golden["scenarios"][name]
 
 
-@pytest.mark.parametrize("name", ["c1", "pab_overload", "large_live", "mixed"])
+@pytest.mark.parametrize("name", ["c1", "pab_overload", "large_live", "mixed", "wide"])
 def test_engine_logs_match_oracle(gpu, oracle, name):
     """Every step: time, duration, predicted/actual ms, totals and each plan
     entry (request row, new tokens) in admission order; every PAB reject."""
@@ -162,6 +162,18 @@ def test_engine_logs_match_oracle(gpu, oracle, name):
         assert a.rejects[i][: c["rejects"]].tobytes() == b.rejects[i][: c["rejects"]].tobytes(), i
     assert a.results.tobytes() == b.results.tobytes() or \
         summarize(a.results, a.records) == summarize(b.results, b.records)
+
+
+@pytest.mark.parametrize("name,want", [("c2_subset", 1), ("large_live", 2), ("wide", 4)])
+def test_engine_paths_exercised(fb, gpu, name, want):
+    """The scenarios really drive the register, memory and CTA-wide paths."""
+    batch = SCENARIOS[name](gpu.generate_bursty)
+    a = fb.Arena(0)
+    a.load(batch)
+    a.run()
+    paths = a.paths()
+    a.close()
+    assert (paths & want).any(), paths
 
 
 def test_stepwise_api_matches_one_shot(gpu):
