@@ -431,6 +431,19 @@ __device__ void run_instance(const EngineParams& P, Inst& w) {
   bool rr = false;
   int64_t next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
   for (int64_t ev = 0; ev < P.max_events; ++ev) {
+    if (w.S.busy && next_arr < w.S.step_end) {
+      // Arrivals strictly before the in-flight step's end only enqueue
+      // (run_node's loop neither completes nor begins a step at those times):
+      // consume them 32 at a time.
+      for (;;) {
+        const int64_t q = w.S.arr + lane_id();
+        const bool early = q < w.nreq && arrival[q] < w.S.step_end;
+        const int n = __popc(__ballot_sync(kFull, early));
+        w.S.arr += n;
+        if (n < kWarp) break;
+      }
+      next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
+    }
     const int64_t t_step = w.S.busy ? w.S.step_end : kInf;
     const int64_t t = t_step < next_arr ? t_step : next_arr;
     if (t == kInf || (!w.S.busy && t >= w.horizon)) {

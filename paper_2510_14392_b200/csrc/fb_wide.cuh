@@ -178,10 +178,16 @@ __device__ int wide_select(const WideScratch& ws, int A, bool has_lo, uint64_t l
     const uint64_t dmask = (uint64_t(1) << bits) - 1;
     for (int i = threadIdx.x; i < kRadixBins; i += kWideThreads) sm.hist[i] = 0;
     __syncthreads();
-    for (int p = threadIdx.x; p < A; p += kWideThreads) {
-      const uint64_t key = wide_key(ws.klow[p], policy, urgency);
-      if ((!has_lo || key > lo) && (key & pmask) == prefix)
-        atomicAdd(&sm.hist[(key >> shift) & dmask], 1u);
+    for (int b0 = 0; b0 < A; b0 += kWideThreads) {  // warp-aggregated histogram
+      const int p = b0 + threadIdx.x;
+      int bin = -1;
+      if (p < A) {
+        const uint64_t key = wide_key(ws.klow[p], policy, urgency);
+        if ((!has_lo || key > lo) && (key & pmask) == prefix)
+          bin = static_cast<int>((key >> shift) & dmask);
+      }
+      const unsigned same = __match_any_sync(kFull, bin);
+      if (bin >= 0 && lane_id() == __ffs(same) - 1) atomicAdd(&sm.hist[bin], __popc(same));
     }
     __syncthreads();
     {  // locate the bin holding the need-th candidate: block scan over bins
@@ -716,6 +722,18 @@ __device__ void wide_run(const EngineParams& P, Inst& w, WideSmem& sm) {
     if (w.S.done) return;
   }
   for (int64_t ev = 0; ev < P.max_events; ++ev) {
+    if (w.S.busy) {
+      // Arrivals strictly before the in-flight step's end only enqueue
+      // (run_node's loop neither completes nor begins a step at those
+      // times), so they are consumed in one block-wide sweep.
+      while (w.S.arr < w.nreq) {
+        const int64_t q = w.S.arr + threadIdx.x;
+        const bool early = q < w.nreq && arrival[q] < w.S.step_end;
+        const int n = __syncthreads_count(early);
+        w.S.arr += n;
+        if (n < kWideThreads) break;
+      }
+    }
     const int64_t t_step = w.S.busy ? w.S.step_end : kInf;
     const int64_t t_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
     const int64_t t = t_step < t_arr ? t_step : t_arr;
