@@ -329,6 +329,33 @@ int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
                  int64_t n_instances, fb_instance_result* results,
                  fb_record* records, double* elapsed_ms_out);
 
+/* ---------------------------------------------------------------------- */
+/* Cluster: run_cluster (cluster.h:107-109) on the device.                 */
+/* ---------------------------------------------------------------------- */
+
+/* LbConfig, cluster.h:36-47. */
+typedef struct fb_lb_config {
+  int32_t policy;                /* FB_LB_COUNT / FB_LB_PAB */
+  int32_t report_interval_steps; /* reports every k completed steps (0 = none) */
+  int64_t report_latency_us;     /* delivery delay of a report */
+  double w_waiting;              /* count_lb weights */
+  double w_running;
+  int32_t retry_reroute; /* must be 0 (rerouting is not supported) */
+  int32_t report_cap;    /* per-node in-flight report capacity (0 = default 4096) */
+} fb_lb_config;
+
+/* Simulates one data-parallel cluster: the trace rows (sorted by arrival,
+ * row index = request id) are routed on arrival to n_nodes nodes with
+ * node_cfgs[i] by the load balancer, exactly as run_cluster
+ * (cluster.cpp:134-251).  Outputs: per-node results (plan digest, steps,
+ * routed/rejected counts), per-request records (global order; a request
+ * never routed has flags == 0), route_node[i] = node of request i or -1,
+ * *incomplete_out = ClusterResult::incomplete.  Any output may be NULL. */
+int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                   int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                   fb_instance_result* node_results, fb_record* records,
+                   int32_t* route_node, int32_t* incomplete_out, double* device_ms_out);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -815,3 +815,211 @@ int orc_run_instances(const fb_trace* rows, const fb_instance* inst,
     if (results[i].status) st = results[i].status;
   return st;
 }
+
+/* ------------------------------------------------------------- cluster.cpp */
+
+typedef struct {
+  int has;
+  int64_t t, pab, waiting, running, dec, inc;
+} orc_nview; /* NodeView, cluster.h:55-69 */
+
+typedef struct {
+  int64_t deliver_at, node, emitted_at, pab, waiting, running;
+} orc_delivery; /* MetricReport in flight, cluster.cpp:149-152 */
+
+static void orc_node_alloc(orc_node* nd, const fb_instance* inst, const fb_trace* rows,
+                           fb_instance_result* res) {
+  const int64_t n = inst->n_req;
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  memset(nd, 0, sizeof(*nd));
+  nd->inst = inst;
+  nd->rows = rows;
+  nd->base = inst->trace_off;
+  nd->prefilled = (int32_t*)calloc(nn, sizeof(int32_t));
+  nd->nidx = (int32_t*)calloc(nn, sizeof(int32_t));
+  nd->first = (int64_t*)malloc(nn * sizeof(int64_t));
+  nd->seq = (int64_t*)calloc(nn, sizeof(int64_t));
+  nd->maxtp = (double*)calloc(nn, sizeof(double));
+  nd->maxtp_alt = (double*)calloc(nn, sizeof(double));
+  nd->flags = (uint32_t*)calloc(nn, sizeof(uint32_t));
+  nd->active = (int32_t*)malloc(nn * sizeof(int32_t));
+  nd->waiting = (int32_t*)malloc(nn * sizeof(int32_t));
+  nd->pend_row = (int32_t*)malloc(nn * sizeof(int32_t));
+  nd->pend_vis = (int64_t*)malloc(nn * sizeof(int64_t));
+  nd->views = (fb_task_view*)malloc(nn * sizeof(fb_task_view));
+  nd->plan_e = (fb_plan_entry_id*)malloc(nn * sizeof(fb_plan_entry_id));
+  for (int64_t i = 0; i < n; ++i) nd->first[i] = -1;
+  memset(res, 0, sizeof(*res));
+  res->plan_digest = FB_DIGEST_INIT;
+  nd->res = res;
+}
+
+static void orc_node_free(orc_node* nd) {
+  free(nd->prefilled); free(nd->nidx); free(nd->first); free(nd->seq);
+  free(nd->maxtp); free(nd->maxtp_alt); free(nd->flags); free(nd->active);
+  free(nd->waiting); free(nd->pend_row); free(nd->pend_vis); free(nd->views);
+  free(nd->plan_e);
+}
+
+/* make_report, cluster.cpp:50-58 */
+static orc_delivery orc_make_report(const orc_node* nd, int64_t node, int64_t now,
+                                    int pab_lb, int64_t latency) {
+  orc_delivery d;
+  d.deliver_at = now + latency;
+  d.node = node;
+  d.emitted_at = now;
+  d.waiting = nd->n_waiting;
+  d.running = nd->n_active;
+  d.pab = pab_lb ? orc_current_pab(nd, now) : 0;
+  return d;
+}
+
+/* route, cluster.cpp:75-112 */
+static int orc_route(orc_nview* v, int n, int64_t prompt, const fb_lb_config* lb) {
+  int chosen = -1;
+  if (lb->policy == FB_LB_PAB) {
+    for (int i = 0; i < n; ++i) {
+      const int64_t eff = v[i].pab - v[i].dec;
+      if (eff < prompt) continue;
+      if (chosen < 0 || eff > v[chosen].pab - v[chosen].dec) chosen = i;
+    }
+    if (chosen < 0)
+      for (int i = 0; i < n; ++i)
+        if (chosen < 0 || v[i].pab - v[i].dec > v[chosen].pab - v[chosen].dec) chosen = i;
+    v[chosen].dec += prompt;
+  } else {
+    double best = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double score = lb->w_waiting * (double)(v[i].waiting + v[i].inc) +
+                           lb->w_running * (double)v[i].running;
+      if (chosen < 0 || score < best) {
+        chosen = i;
+        best = score;
+      }
+    }
+    v[chosen].inc += 1;
+  }
+  return chosen;
+}
+
+/* run_cluster, cluster.cpp:134-251 (retry_reroute unsupported). */
+int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                    const fb_lb_config* lb, int64_t horizon, fb_instance_result* node_results,
+                    fb_record* records, int32_t* route_node, int32_t* incomplete_out) {
+  if (n_nodes < 1) return FB_ERR_USAGE;
+  if (lb->report_latency_us < 0) return FB_ERR_VALIDATION;
+  if (lb->retry_reroute) return FB_ERR_USAGE;
+  const int n = n_nodes;
+  const int64_t nr = rows->n_rows;
+  fb_instance* inst = (fb_instance*)calloc((size_t)n, sizeof(fb_instance));
+  orc_node* nodes = (orc_node*)calloc((size_t)n, sizeof(orc_node));
+  fb_instance_result* res = (fb_instance_result*)calloc((size_t)n, sizeof(fb_instance_result));
+  orc_nview* view = (orc_nview*)calloc((size_t)n, sizeof(orc_nview));
+  size_t dcap = 1024, dhead = 0, dtail = 0;
+  orc_delivery* dq = (orc_delivery*)malloc(dcap * sizeof(orc_delivery));
+  const int pab_lb = lb->policy == FB_LB_PAB;
+  for (int i = 0; i < n; ++i) {
+    inst[i].cfg = cfgs[i];
+    inst[i].trace_off = 0;
+    inst[i].n_req = nr;
+    inst[i].horizon_us = horizon;
+    orc_node_alloc(&nodes[i], &inst[i], rows, &res[i]);
+  }
+  if (route_node)
+    for (int64_t k = 0; k < nr; ++k) route_node[k] = -1;
+#define ORC_PUSH(d)                                                        \
+  do {                                                                     \
+    if (dtail == dcap) {                                                   \
+      memmove(dq, dq + dhead, (dtail - dhead) * sizeof(orc_delivery));     \
+      dtail -= dhead;                                                      \
+      dhead = 0;                                                           \
+      if (dtail == dcap) {                                                 \
+        dcap *= 2;                                                         \
+        dq = (orc_delivery*)realloc(dq, dcap * sizeof(orc_delivery));      \
+      }                                                                    \
+    }                                                                      \
+    dq[dtail++] = (d);                                                     \
+  } while (0)
+  for (int i = 0; i < n; ++i) ORC_PUSH(orc_make_report(&nodes[i], i, 0, pab_lb, lb->report_latency_us));
+  int64_t arr = 0;
+  int status = FB_OK;
+  for (;;) {
+    int64_t t = ORC_INF;
+    for (int i = 0; i < n; ++i)
+      if (nodes[i].busy && nodes[i].step_end < t) t = nodes[i].step_end;
+    const int any_busy = t != ORC_INF;
+    if (arr < nr && rows->arrival_us[arr] < t) t = rows->arrival_us[arr];
+    if (dhead < dtail && dq[dhead].deliver_at < t) t = dq[dhead].deliver_at;
+    if (t == ORC_INF) break;
+    if (!any_busy && t >= horizon) break;
+    for (int i = 0; i < n; ++i) { /* completions, then reports (cluster.cpp:195-205) */
+      if (nodes[i].busy && nodes[i].step_end == t) {
+        orc_complete_step(&nodes[i]);
+        if (lb->report_interval_steps > 0 &&
+            nodes[i].step_counter % (uint64_t)lb->report_interval_steps == 0)
+          ORC_PUSH(orc_make_report(&nodes[i], i, t, pab_lb, lb->report_latency_us));
+      }
+    }
+    while (dhead < dtail && dq[dhead].deliver_at <= t) { /* apply_report, cluster.cpp:60-73 */
+      const orc_delivery* d = &dq[dhead++];
+      orc_nview* v = &view[d->node];
+      if (v->has && d->emitted_at < v->t) continue;
+      v->has = 1;
+      v->t = d->emitted_at;
+      v->pab = d->pab;
+      v->waiting = d->waiting;
+      v->running = d->running;
+      v->dec = 0;
+      v->inc = 0;
+    }
+    while (arr < nr && rows->arrival_us[arr] == t) { /* route on arrival */
+      const int target = orc_route(view, n, rows->prompt_len[arr], lb);
+      if (route_node) route_node[arr] = target;
+      orc_enqueue(&nodes[target], (int32_t)arr, t);
+      ++arr;
+    }
+    if (t < horizon) {
+      for (int i = 0; i < n && !status; ++i)
+        if (!nodes[i].busy) status = orc_begin_step(&nodes[i], t);
+    }
+    if (status) break;
+  }
+#undef ORC_PUSH
+  int live = arr < nr;
+  for (int i = 0; i < n; ++i)
+    live = live || nodes[i].busy || nodes[i].pend_head < nodes[i].pend_tail ||
+           nodes[i].n_waiting > 0 || nodes[i].n_active > 0;
+  for (int i = 0; i < n; ++i) {
+    res[i].steps = nodes[i].step_counter;
+    res[i].incomplete = live;
+    res[i].status = status;
+    res[i].end_time_us = -1;
+    if (node_results) node_results[i] = res[i];
+  }
+  if (records) {
+    for (int64_t k = 0; k < nr; ++k) {
+      records[k].first_emit_us = -1;
+      records[k].max_tpot_ms = 0.0;
+      records[k].max_tpot_alt_ms = 0.0;
+      records[k].tokens_emitted = 0;
+      records[k].flags = 0;
+    }
+    for (int i = 0; i < n; ++i) {
+      const orc_node* nd = &nodes[i];
+      for (int64_t k = 0; k < nr; ++k) {
+        if (!(nd->flags[k] & FB_REC_ARRIVED)) continue;
+        records[k].first_emit_us = nd->first[k];
+        records[k].max_tpot_ms = nd->maxtp[k];
+        records[k].max_tpot_alt_ms = nd->maxtp_alt[k];
+        records[k].tokens_emitted = nd->nidx[k];
+        uint32_t f = nd->flags[k] & 0x7fffffffu;
+        if ((f & FB_REC_REJECTED) && nd->nidx[k] > 0) f &= ~(uint32_t)FB_REC_REJECTED;
+        records[k].flags = f;
+      }
+    }
+  }
+  if (incomplete_out) *incomplete_out = live;
+  for (int i = 0; i < n; ++i) orc_node_free(&nodes[i]);
+  free(nodes); free(inst); free(res); free(view); free(dq);
+  return status;
+}

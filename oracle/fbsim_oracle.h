@@ -47,6 +47,11 @@ int orc_run_instances(const fb_trace* rows, const fb_instance* instances,
                       fb_plan_entry* entries, fb_reject_log* rejects,
                       int nthreads);
 
+/* run_cluster over the whole trace (row index = request id). */
+int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                    const fb_lb_config* lb, int64_t horizon, fb_instance_result* node_results,
+                    fb_record* records, int32_t* route_node, int32_t* incomplete_out);
+
 #ifdef __cplusplus
 }
 #endif

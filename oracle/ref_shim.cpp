@@ -12,6 +12,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <deque>
+#include <memory>
+#include <set>
 #include <exception>
 #include <limits>
 #include <string>
@@ -253,9 +256,175 @@ int run_mirror(const fb_trace* rows, const fb_instance& inst,
   return FB_OK;
 }
 
+// Plan digest + counters of one node log (same definition as run_mirror).
+void digest_node_log(const EventLog& log, const std::vector<BatchPlan>& plans,
+                     const std::vector<double>& actuals, uint64_t steps_completed,
+                     fb_instance_result* res) {
+  std::memset(res, 0, sizeof(*res));
+  uint64_t h = FB_DIGEST_INIT;
+  size_t step = 0;
+  for (const auto& e : log.events) {
+    if (e.kind == EventKind::kArrival) {
+      res->n_arrived++;
+    } else if (e.kind == EventKind::kAdmissionReject) {
+      res->n_rejected++;
+      h = fb_digest_reject(h, e.t, static_cast<uint32_t>(e.req_id), e.pab_tokens);
+    } else if (e.kind == EventKind::kBatchStart) {
+      const BatchPlan& p = plans.at(step);
+      uint64_t esum = 0;
+      for (size_t k = 0; k < p.entries.size(); ++k)
+        esum ^= fb_digest_entry(static_cast<uint32_t>(k),
+                                static_cast<uint32_t>(p.entries[k].request_id),
+                                static_cast<uint32_t>(p.entries[k].new_tokens));
+      h = fb_digest_step(h, e.t, static_cast<uint32_t>(p.entries.size()), esum,
+                         e.predicted_ms, actuals.at(step));
+      res->sum_entries += static_cast<int64_t>(p.entries.size());
+      res->sum_new_tokens += e.new_tokens;
+      ++step;
+    }
+  }
+  res->steps = steps_completed;
+  res->plan_digest = h;
+  res->incomplete = log.incomplete ? 1 : 0;
+  res->sum_visible = -1;
+  res->end_time_us = -1;
+}
+
 }  // namespace
 
 extern "C" {
+
+// run_cluster (cluster.cpp:134-251) mirrored through Node / route /
+// apply_report / make_report so that every node's plans can be captured;
+// with check != 0 the node logs and routing decisions are compared with the
+// real run_cluster.  route_node[i] = node of request i (-1: never routed).
+int ref_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                    const fb_lb_config* lbc, int64_t horizon, fb_instance_result* node_results,
+                    fb_record* records, int32_t* route_node, int32_t* incomplete_out,
+                    int check) {
+  try {
+    constexpr TimeUs kInf = std::numeric_limits<TimeUs>::max();
+    fb_instance whole{};
+    whole.trace_off = 0;
+    whole.n_req = rows->n_rows;
+    const Trace tr = instance_trace(rows, whole);
+    LbConfig lb;
+    lb.policy = lbc->policy == FB_LB_PAB ? LbPolicy::kPabLb : LbPolicy::kCountLb;
+    lb.report_interval_steps = lbc->report_interval_steps;
+    lb.report_latency = lbc->report_latency_us;
+    lb.w_waiting = lbc->w_waiting;
+    lb.w_running = lbc->w_running;
+    lb.retry_reroute = lbc->retry_reroute != 0;
+    std::vector<EngineConfig> ecfg;
+    for (int i = 0; i < n_nodes; ++i) ecfg.push_back(to_engine(cfgs[i]));
+    const int n = n_nodes;
+    std::vector<std::unique_ptr<Node>> nodes;
+    for (int i = 0; i < n; ++i) nodes.push_back(std::make_unique<Node>(i, ecfg[i]));
+    std::vector<std::vector<BatchPlan>> plans(n);
+    std::vector<std::vector<double>> actuals(n);
+    std::vector<int> route(tr.requests.size(), -1);
+    ClusterView view;
+    view.nodes.resize(n);
+    struct InFlight {
+      TimeUs deliver_at;
+      MetricReport report;
+    };
+    std::deque<InFlight> deliveries;
+    std::set<std::int64_t> retried;
+    auto emit_report = [&](const Node& node, TimeUs now) {
+      deliveries.push_back({now + lb.report_latency, make_report(node, now, lb.policy)});
+    };
+    std::vector<int> routed_nodes;  // in routing order
+    auto route_request = [&](const Request& r, TimeUs now) {
+      const int target = fbsim::route(view, r, lb);
+      route[static_cast<size_t>(r.id)] = target;
+      routed_nodes.push_back(target);
+      nodes[static_cast<size_t>(target)]->enqueue(r, now);
+    };
+    for (const auto& node : nodes) emit_report(*node, 0);
+    size_t arr = 0;
+    const auto& reqs = tr.requests;
+    for (;;) {
+      TimeUs t = kInf;
+      for (const auto& node : nodes)
+        if (node->busy()) t = std::min(t, node->step_end());
+      const bool any_busy = t != kInf;
+      if (arr < reqs.size()) t = std::min(t, reqs[arr].arrival);
+      if (!deliveries.empty()) t = std::min(t, deliveries.front().deliver_at);
+      if (t == kInf) break;
+      if (!any_busy && t >= horizon) break;
+      for (int i = 0; i < n; ++i) {
+        auto& node = nodes[static_cast<size_t>(i)];
+        if (node->busy() && node->step_end() == t) {
+          StepOutcome out = node->complete_step();
+          plans[i].push_back(std::move(out.plan));
+          actuals[i].push_back(out.actual_ms);
+          if (lb.report_interval_steps > 0 &&
+              node->steps_completed() % static_cast<std::uint64_t>(lb.report_interval_steps) == 0)
+            emit_report(*node, t);
+        }
+      }
+      while (!deliveries.empty() && deliveries.front().deliver_at <= t) {
+        apply_report(view, deliveries.front().report);
+        deliveries.pop_front();
+      }
+      while (arr < reqs.size() && reqs[arr].arrival == t) {
+        route_request(reqs[arr], t);
+        ++arr;
+      }
+      if (t < horizon) {
+        bool progress = true;
+        while (progress) {
+          progress = false;
+          for (auto& node : nodes) {
+            if (!node->busy()) node->begin_step(t);
+            for (const auto& r : node->drain_rejects()) {
+              if (lb.retry_reroute && retried.insert(r.id).second) {
+                route_request(r, t);
+                progress = true;
+              }
+            }
+          }
+        }
+      }
+    }
+    bool live = arr < reqs.size();
+    for (auto& node : nodes) live = live || node->has_live_requests();
+    std::vector<EventLog> logs;
+    for (auto& node : nodes) {
+      EventLog lg = std::move(node->log());
+      lg.incomplete = live;
+      logs.push_back(std::move(lg));
+    }
+    if (check) {
+      const ClusterResult real = run_cluster(tr, ecfg, lb, horizon);
+      if (real.incomplete != live) return fail(FB_ERR_VALIDATION, "cluster mirror: incomplete");
+      if (real.routing.size() != routed_nodes.size())
+        return fail(FB_ERR_VALIDATION, "cluster mirror: routing size");
+      for (size_t k = 0; k < routed_nodes.size(); ++k)
+        if (real.routing[k].node != routed_nodes[k])
+          return fail(FB_ERR_VALIDATION, "cluster mirror: routing differs");
+      for (int i = 0; i < n; ++i) {
+        const auto& a = real.node_logs[static_cast<size_t>(i)].events;
+        const auto& b = logs[static_cast<size_t>(i)].events;
+        if (a.size() != b.size()) return fail(FB_ERR_VALIDATION, "cluster mirror: log size");
+        for (size_t k = 0; k < a.size(); ++k)
+          if (!same_event(a[k], b[k])) return fail(FB_ERR_VALIDATION, "cluster mirror: event");
+      }
+    }
+    for (int i = 0; i < n; ++i)
+      if (node_results)
+        digest_node_log(logs[static_cast<size_t>(i)], plans[i], actuals[i],
+                        nodes[static_cast<size_t>(i)]->steps_completed(), &node_results[i]);
+    if (records) fill_records(logs, tr, records);
+    if (route_node)
+      for (size_t k = 0; k < route.size(); ++k) route_node[k] = route[k];
+    if (incomplete_out) *incomplete_out = live ? 1 : 0;
+    return FB_OK;
+  } catch (const std::exception& e) {
+    return map_exception(e);
+  }
+}
 
 const char* ref_last_error(void) { return g_err.c_str(); }
 

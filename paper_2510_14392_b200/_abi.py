@@ -176,6 +176,18 @@ class BurstProfile(C.Structure):
     ]
 
 
+class LbConfig(C.Structure):
+    _fields_ = [
+        ("policy", C.c_int32),
+        ("report_interval_steps", C.c_int32),
+        ("report_latency_us", C.c_int64),
+        ("w_waiting", C.c_double),
+        ("w_running", C.c_double),
+        ("retry_reroute", C.c_int32),
+        ("report_cap", C.c_int32),
+    ]
+
+
 class TaskView(C.Structure):
     _fields_ = [
         ("request_id", C.c_int64),

@@ -459,6 +459,144 @@ int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
   return st;
 }
 
+// run_cluster (cluster.cpp:134-251): all nodes of one cluster in one CTA
+// (fb_cluster.cuh); routing decisions and node plans are exact.
+int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                   int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                   fb_instance_result* node_results, fb_record* records, int32_t* route_node,
+                   int32_t* incomplete_out, double* device_ms_out) {
+  if (!rows || !node_cfgs || !lb) return set_error(FB_ERR_USAGE, "fb_run_cluster: null argument");
+  if (n_nodes < 1) return set_error(FB_ERR_USAGE, "run_cluster requires at least one node");
+  if (n_nodes > fbgpu::cluster_max_nodes())
+    return set_error(FB_ERR_USAGE, "fb_run_cluster: too many nodes for one CTA");
+  if (lb->report_latency_us < 0) return set_error(FB_ERR_VALIDATION, "report_latency must be >= 0");
+  if (lb->retry_reroute) return set_error(FB_ERR_USAGE, "retry_reroute is not supported");
+  if (lb->policy != FB_LB_PAB && lb->policy != FB_LB_COUNT)
+    return set_error(FB_ERR_USAGE, "unknown load-balancer policy");
+  const int64_t nr = rows->n_rows;
+  std::vector<fb_instance> inst(static_cast<size_t>(n_nodes));
+  for (int i = 0; i < n_nodes; ++i) {
+    inst[i].cfg = node_cfgs[i];
+    inst[i].trace_off = 0;
+    inst[i].n_req = nr;
+    inst[i].horizon_us = horizon_us;
+  }
+  // dispatch epochs: distinct arrival times and their request ranges
+  std::vector<int64_t> ep_t, ep_lo;
+  for (int64_t q = 0; q < nr; ++q) {
+    if (q == 0 || rows->arrival_us[q] != rows->arrival_us[q - 1]) {
+      ep_t.push_back(rows->arrival_us[q]);
+      ep_lo.push_back(q);
+    }
+  }
+  ep_lo.push_back(nr);
+  fb_arena* a = nullptr;
+  int st = fb_arena_create(device, nullptr, &a);
+  if (st) return st;
+  struct Guard {
+    fb_arena* a;
+    std::vector<void*> bufs;
+    ~Guard() {
+      for (void* p : bufs) cudaFree(p);
+      fb_arena_destroy(a);
+    }
+  } guard{a, {}};
+  if ((st = fb_arena_load(a, rows, inst.data(), n_nodes, nullptr))) return st;
+  const int cap = lb->report_cap > 0 ? lb->report_cap : 4096;
+  auto dalloc = [&](void** p, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
+    if (e == cudaSuccess) guard.bufs.push_back(*p);
+    return e;
+  };
+  int64_t *d_ept, *d_eplo, *d_rep, *d_out;
+  int32_t *d_routed, *d_route;
+  const int64_t ne = static_cast<int64_t>(ep_t.size());
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_ept), sizeof(int64_t) * (ne + 1)));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_eplo), sizeof(int64_t) * (ne + 1)));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_rep), sizeof(int64_t) * 4 * cap * n_nodes));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_out), sizeof(int64_t) * 2));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_routed), sizeof(int32_t) * n_nodes * (nr + 1)));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_route), sizeof(int32_t) * (nr + 1)));
+  cudaStream_t s = a->stream;
+  if (ne > 0) FB_CUDA(cudaMemcpyAsync(d_ept, ep_t.data(), sizeof(int64_t) * ne, cudaMemcpyHostToDevice, s));
+  FB_CUDA(cudaMemcpyAsync(d_eplo, ep_lo.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice, s));
+  FB_CUDA(cudaMemsetAsync(d_route, 0xff, sizeof(int32_t) * (nr + 1), s));
+  fbgpu::ClusterParamsHost cp;
+  cp.n_nodes = n_nodes;
+  cp.lb_policy = lb->policy;
+  cp.interval = lb->report_interval_steps;
+  cp.report_cap = cap;
+  cp.latency = lb->report_latency_us;
+  cp.horizon = horizon_us;
+  cp.n_rows = nr;
+  cp.n_epochs = ne;
+  cp.w_waiting = lb->w_waiting;
+  cp.w_running = lb->w_running;
+  cp.epoch_t = d_ept;
+  cp.epoch_lo = d_eplo;
+  cp.routed = d_routed;
+  cp.route_node = d_route;
+  cp.rep = d_rep;
+  cp.out = d_out;
+  if (fbgpu::cluster_param_bytes() != sizeof(cp))
+    return set_error(FB_ERR_USAGE, "cluster parameter layout mismatch");
+  FB_CUDA(cudaEventRecord(a->ev0, s));
+  FB_CUDA(fbgpu::launch_cluster(a->params(0), &cp, s));
+  FB_CUDA(cudaEventRecord(a->ev1, s));
+  int64_t out[2] = {0, 0};
+  FB_CUDA(cudaMemcpyAsync(out, d_out, sizeof(out), cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> route(static_cast<size_t>(nr));
+  if (nr > 0) FB_CUDA(cudaMemcpyAsync(route.data(), d_route, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, s));
+  FB_CUDA(cudaStreamSynchronize(s));
+  if (device_ms_out) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a->ev0, a->ev1);
+    *device_ms_out = ms;
+  }
+  if (out[1] != FB_OK) return set_error(static_cast<int>(out[1]), "cluster: report FIFO overflow");
+  std::vector<fb_instance_result> res(static_cast<size_t>(n_nodes));
+  if ((st = fb_arena_fetch_results(a, res.data()))) return st;
+  bool live = out[0] < nr;
+  for (auto& r : res) live = live || r.incomplete;
+  for (auto& r : res) {
+    r.incomplete = live ? 1 : 0;
+    r.end_time_us = -1;
+  }
+  if (node_results) std::memcpy(node_results, res.data(), sizeof(fb_instance_result) * n_nodes);
+  if (route_node && nr > 0) std::memcpy(route_node, route.data(), sizeof(int32_t) * nr);
+  if (incomplete_out) *incomplete_out = live ? 1 : 0;
+  if (records && nr > 0) {
+    const int64_t n = a->n_rec;
+    std::vector<int32_t> nidx(n);
+    std::vector<uint32_t> flags(n);
+    std::vector<int64_t> first(n);
+    std::vector<double> mt(n), mta(n);
+    FB_CUDA(cudaMemcpyAsync(nidx.data(), a->nidx.p, n * 4, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(flags.data(), a->flags.p, n * 4, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(first.data(), a->first.p, n * 8, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(mt.data(), a->maxtp.p, n * 8, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaMemcpyAsync(mta.data(), a->maxtp_alt.p, n * 8, cudaMemcpyDeviceToHost, s));
+    FB_CUDA(cudaStreamSynchronize(s));
+    for (int64_t q = 0; q < nr; ++q) {
+      fb_record& o = records[q];
+      const int node = route[q];
+      if (node < 0) {
+        o = fb_record{-1, 0.0, 0.0, 0, 0u};
+        continue;
+      }
+      const int64_t k = static_cast<int64_t>(node) * nr + q;
+      uint32_t f = (flags[k] & ~fbgpu::kTpotViolated) | FB_REC_ARRIVED;
+      if ((f & FB_REC_REJECTED) && nidx[k] > 0) f &= ~static_cast<uint32_t>(FB_REC_REJECTED);
+      o.first_emit_us = first[k];
+      o.max_tpot_ms = mt[k];
+      o.max_tpot_alt_ms = mta[k];
+      o.tokens_emitted = nidx[k];
+      o.flags = f;
+    }
+  }
+  return FB_OK;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------ pure scheduler surface

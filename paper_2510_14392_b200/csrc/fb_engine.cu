@@ -41,6 +41,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // Warp-uniform view of one instance while a warp owns it.
 struct Inst {
   int64_t id;
+  const int32_t* routed;  // cluster node: pending slot -> trace row (else identity)
   const DevInst* I;
   DevState S;
   int64_t toff, roff, nreq, horizon;
@@ -48,6 +49,12 @@ struct Inst {
   int2* vl;
   unsigned char* smem;  // this warp's shared scratch
 };
+
+// Trace row of the q-th request that reached this node (run_node: the trace
+// itself; cluster nodes: the router's append order).
+__device__ __forceinline__ int64_t arrival_row(const Inst& w, int64_t q) {
+  return w.routed ? static_cast<int64_t>(w.routed[q]) : q;
+}
 
 __device__ __forceinline__ int64_t visible_count(const Inst& w) {
   int64_t nw = w.S.n_live - w.S.n_active;
@@ -196,7 +203,7 @@ __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w) {
 __device__ __forceinline__ void pull_plain(const EngineParams& P, Inst& w) {
   const int64_t k = w.S.arr - w.S.pulled;
   for (int64_t j = lane_id(); j < k; j += kWarp) {
-    const int64_t r = w.S.pulled + j;
+    const int64_t r = arrival_row(w, w.S.pulled + j);
     P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter + j);
     w.vl[w.S.n_live + j] = make_int2(static_cast<int>(r), 0);
   }
@@ -227,7 +234,8 @@ __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
   int64_t min_slack = warp_min_i64(lmin);
   int64_t pf_tok = warp_sum_small(lpf);
   double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
-  for (int64_t r = w.S.pulled; r < w.S.arr; ++r) {
+  for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
+    const int64_t r = arrival_row(w, q);
     const int64_t row = w.toff + r;
     const int64_t prompt = P.prompt[row];
     const int64_t budget = pab_close(Wm, Tm, a, b, c, A > 0, min_slack, r_tasks, pf_tok);
@@ -418,6 +426,7 @@ __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t 
 
 #include "fb_engine_rr.cuh"
 #include "fb_wide.cuh"
+#include "fb_cluster.cuh"
 
 namespace fbgpu {
 
@@ -514,6 +523,7 @@ engine_kernel(const __grid_constant__ EngineParams P) {
     if (i >= static_cast<unsigned long long>(P.n_inst)) break;
     Inst w;
     w.id = static_cast<int64_t>(i);
+    w.routed = nullptr;
     w.I = P.inst + i;
     w.S = P.state[i];
     if (w.S.done || w.S.escalated) continue;
@@ -626,6 +636,20 @@ cudaError_t launch_reset(const EngineParams& p, int64_t n_rec, cudaStream_t st) 
   if (blocks > 148 * 16) blocks = 148 * 16;
   cudaMemsetAsync(p.work, 0, 4 * sizeof(unsigned long long), st);
   reset_kernel<<<blocks, 256, 0, st>>>(p, n_rec);
+  return cudaGetLastError();
+}
+
+size_t cluster_param_bytes() { return sizeof(ClusterParams); }
+int cluster_max_nodes() { return kClusterMaxNodes; }
+
+cudaError_t launch_cluster(const EngineParams& p, const void* cluster_params, cudaStream_t st) {
+  ClusterParams c;
+  std::memcpy(&c, cluster_params, sizeof(c));
+  const size_t smem = ((sizeof(ClusterSmem) + 15) / 16) * 16 +
+                      static_cast<size_t>(kClusterWarps) * kSmemSlots * kScratchBytesPerSlot;
+  cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  cluster_kernel<<<1, kWarp * kClusterWarps, smem, st>>>(p, c);
   return cudaGetLastError();
 }
 

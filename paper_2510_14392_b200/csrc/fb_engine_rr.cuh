@@ -194,7 +194,7 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
   if (w.policy != FB_POLICY_FAIRBATCH_PAB) {
     const int64_t k = w.S.arr - w.S.pulled;
     const int j = lane - static_cast<int>(w.S.n_live);
-    if (j >= 0 && j < k) fresh_task(P, w, w.S.pulled + j, w.S.seq_counter + j, t);
+    if (j >= 0 && j < k) fresh_task(P, w, arrival_row(w, w.S.pulled + j), w.S.seq_counter + j, t);
     w.S.seq_counter += k;
     w.S.n_live += k;
     w.S.pulled = w.S.arr;
@@ -216,7 +216,8 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
   int64_t min_slack = warp_min_i64(lmin);
   int64_t pf_tok = warp_sum_small(lpf);
   double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
-  for (int64_t r = w.S.pulled; r < w.S.arr; ++r) {
+  for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
+    const int64_t r = arrival_row(w, q);
     const int64_t row = w.toff + r;
     const int64_t prompt = P.prompt[row];
     const int64_t budget = pab_close(Wm, Tm, a, b, c, A > 0, min_slack, r_tasks, pf_tok);

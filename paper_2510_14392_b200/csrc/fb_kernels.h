@@ -69,6 +69,22 @@ void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
 void unpack_state(const void* state, fb_instance_result* out);
 
 cudaError_t launch_reset(const EngineParams& p, int64_t n_rec_rows, cudaStream_t st);
+
+// Cluster (fb_cluster.cuh): ClusterParams is opaque to the host code here.
+struct ClusterParamsHost {
+  int32_t n_nodes, lb_policy, interval, report_cap;
+  int64_t latency, horizon, n_rows, n_epochs;
+  double w_waiting, w_running;
+  const int64_t* epoch_t;
+  const int64_t* epoch_lo;
+  int32_t* routed;
+  int32_t* route_node;
+  int64_t* rep;
+  int64_t* out;
+};
+size_t cluster_param_bytes();
+int cluster_max_nodes();
+cudaError_t launch_cluster(const EngineParams& p, const void* cluster_params, cudaStream_t st);
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g,
                           cudaStream_t st);
 

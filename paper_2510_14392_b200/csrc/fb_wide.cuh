@@ -419,7 +419,7 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
   if (w.policy != FB_POLICY_FAIRBATCH_PAB) {
     const int64_t k = w.S.arr - w.S.pulled;
     for (int64_t j = threadIdx.x; j < k; j += kWideThreads) {
-      const int64_t r = w.S.pulled + j;
+      const int64_t r = arrival_row(w, w.S.pulled + j);
       P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter + j);
       w.vl[w.S.n_live + j] = make_int2(static_cast<int>(r), 0);
     }
@@ -447,7 +447,8 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
   if (threadIdx.x == 0) {
     double r_tasks = 0.0;
     for (int64_t p = 0; p < A; ++p) r_tasks = dadd(r_tasks, terms[p]);
-    for (int64_t r = w.S.pulled; r < w.S.arr; ++r) {
+    for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
+      const int64_t r = arrival_row(w, q);
       const int64_t row = w.toff + r;
       const int64_t prompt = P.prompt[row];
       const int64_t budget = pab_close(Wm, Tm, a, b, c, A > 0, min_slack, r_tasks, pf_tok);
@@ -766,6 +767,8 @@ wide_kernel(const __grid_constant__ EngineParams P) {
     if (j >= P.work[3]) break;
     const int64_t i = P.wide_list[j];
     Inst w;
+    w.id = i;
+    w.routed = nullptr;
     w.I = P.inst + i;
     w.S = P.state[i];
     if (w.S.done) continue;

@@ -100,6 +100,9 @@ def lib() -> C.CDLL:
         "fb_arena_fetch_paths": (C.c_int, [vp, vp]),
         "fb_run_batch": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i64, vp, vp,
                                    C.POINTER(C.c_double)]),
+        "fb_run_cluster": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,
+                                     C.POINTER(_abi.LbConfig), i64, vp, vp, vp,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

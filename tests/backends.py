@@ -147,6 +147,14 @@ class OracleLib(_CpuLib):
                               C.POINTER(_abi.LogOpts), C.c_void_p, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
 
+    def run_cluster(self, rows: Rows, cfgs, lb, horizon_us: int):
+        fn = self.lib.orc_run_cluster
+        fn.restype = C.c_int
+        st, out = _cluster_call(fn, rows, cfgs, lb, horizon_us)
+        if st:
+            raise RuntimeError(f"orc_run_cluster status {st}")
+        return out
+
     def run(self, batch: Batch, log: _abi.LogOpts | None = None, nthreads: int = 1) -> RunOutput:
         n = batch.n_instances
         rows = batch.rows
@@ -162,6 +170,36 @@ class OracleLib(_CpuLib):
         if st:
             raise RuntimeError(f"orc_run_instances status {st}")
         return RunOutput(results, records, counts, steps, entries, rejects)
+
+
+def _cluster_call(fn, rows, cfgs, lb, horizon_us, *extra):
+    from paper_2510_14392_b200.cluster import ClusterOutput, node_configs_c
+    n = len(cfgs)
+    tr = rows.to_c()
+    nc = node_configs_c(cfgs)
+    lbc = lb.to_c()
+    res = np.zeros(max(1, n), _abi.RESULT_DTYPE)
+    rec = np.zeros(max(1, len(rows)), _abi.RECORD_DTYPE)
+    route = np.zeros(max(1, len(rows)), np.int32)
+    inc = C.c_int32(0)
+    st = fn(C.byref(tr), C.cast(nc, C.c_void_p), C.c_int32(n), C.byref(lbc), C.c_int64(horizon_us),
+            _abi.vptr(res), _abi.vptr(rec), _abi.vptr(route), C.byref(inc), *extra)
+    return st, ClusterOutput(res[:n], rec[:len(rows)], route[:len(rows)], inc.value)
+
+
+CLUSTER_KEYS = ("steps", "plan_digest", "n_arrived", "n_rejected", "sum_entries",
+                "sum_new_tokens", "incomplete")
+
+
+def cluster_summary(out) -> dict:
+    """Exact, comparable part of a cluster run."""
+    import hashlib
+    return {
+        "nodes": [{k: int(r[k]) for k in CLUSTER_KEYS} for r in out.node_results],
+        "records_sha256": hashlib.sha256(out.records.tobytes()).hexdigest(),
+        "route_sha256": hashlib.sha256(out.route_node.astype(np.int32).tobytes()).hexdigest(),
+        "incomplete": int(out.incomplete),
+    }
 
 
 class RefLib(_CpuLib):
@@ -199,6 +237,26 @@ class RefLib(_CpuLib):
         if st:
             raise RuntimeError(f"ref_run_instances status {st}: {self.lib.ref_last_error()}")
         return RunOutput(results, records, counts, steps, entries, rejects)
+
+    def run_cluster(self, rows: Rows, cfgs, lb, horizon_us: int, check: bool = False):
+        """The reference's run_cluster (mirrored through Node/route/apply_report)."""
+        from paper_2510_14392_b200.cluster import ClusterOutput, node_configs_c
+        fn = self.lib.ref_run_cluster
+        fn.restype = C.c_int
+        n = len(cfgs)
+        tr = rows.to_c()
+        nc = node_configs_c(cfgs)
+        lbc = lb.to_c()
+        res = np.zeros(max(1, n), _abi.RESULT_DTYPE)
+        rec = np.zeros(max(1, len(rows)), _abi.RECORD_DTYPE)
+        route = np.zeros(max(1, len(rows)), np.int32)
+        inc = C.c_int32(0)
+        st = fn(C.byref(tr), C.cast(nc, C.c_void_p), C.c_int32(n), C.byref(lbc),
+                C.c_int64(horizon_us), _abi.vptr(res), _abi.vptr(rec), _abi.vptr(route),
+                C.byref(inc), C.c_int(1 if check else 0))
+        if st:
+            raise RuntimeError(f"ref_run_cluster status {st}: {self.lib.ref_last_error()}")
+        return ClusterOutput(res[:n], rec[:len(rows)], route[:len(rows)], inc.value)
 
     def run_node_batch(self, batch: Batch, nthreads: int = 1, records: bool = True) -> RunOutput:
         n = batch.n_instances

@@ -153,6 +153,30 @@ SCENARIOS = {
 }
 
 
+def cluster_cases(gen):
+    """run_cluster parity cases: (name, rows, node cfgs, LbConfig, horizon_us).
+    The 8-node trace is cluster8.json's (acceptance.cpp:403-414); the last
+    case is BASELINE config 5 (64 nodes)."""
+    from paper_2510_14392_b200.cluster import LbConfig
+    prof, h = TRACE_PROFILES["cluster8_5"]
+    rows = gen(prof, ms_to_us(h))
+    out = []
+    for name, pol, lat, nn, hz in (("pab0_8", "pab_lb", 0.0, 8, 3.6e6),
+                                   ("count0_8", "count_lb", 0.0, 8, 3.6e6),
+                                   ("pab5000_8", "pab_lb", 5000.0, 8, 3.6e6),
+                                   ("count37_3", "count_lb", 37.0, 3, 3.6e6),
+                                   ("pab_hz10s_8", "pab_lb", 0.0, 8, 10_000.0),
+                                   ("pab20_2", "pab_lb", 20.0, 2, 3.6e6)):
+        node_pol = "fairbatch_pab" if pol == "pab_lb" else "fairbatch"
+        cfgs = [engine_config(node_pol, 2048, MODEL, 500, 50) for _ in range(nn)]
+        out.append((name, rows, cfgs, LbConfig(pol, 1, lat), ms_to_us(hz)))
+    p5 = profile(240.0, 720.0, 800, 1600, 892, 1776, 250, 500, 5)
+    rows5 = gen(p5, ms_to_us(30_000.0))
+    cfgs5 = [engine_config("fairbatch_pab", 2048, MODEL, 500, 50) for _ in range(64)]
+    out.append(("c5_pab0_64", rows5, cfgs5, LbConfig("pab_lb", 1, 0.0), ms_to_us(3.6e6)))
+    return out
+
+
 def summarize(results: np.ndarray, records: np.ndarray) -> dict:
     """Compact, exact summary of a run for fixtures."""
     keys = ("steps", "plan_digest", "end_time_us", "n_arrived", "n_rejected", "sum_entries",

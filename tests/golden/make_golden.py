@@ -23,8 +23,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 import numpy as np  # noqa: E402
 
-from backends import RefLib  # noqa: E402
-from catalog import SCENARIOS, TRACE_PROFILES, rows_digest, summarize  # noqa: E402
+from backends import RefLib, cluster_summary  # noqa: E402
+from catalog import (SCENARIOS, TRACE_PROFILES, cluster_cases, rows_digest,  # noqa: E402
+                     summarize)
 from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views  # noqa: E402
 from paper_2510_14392_b200.batch import ms_to_us  # noqa: E402
 
@@ -64,6 +65,9 @@ def main() -> None:
         batch = fn(ref.generate_bursty)
         out = ref.run(batch, nthreads=8, check=True)
         gold["scenarios"][name] = summarize(out.results, out.records)
+    gold["clusters"] = {}
+    for name, rows, cfgs, lb, hz in cluster_cases(ref.generate_bursty):
+        gold["clusters"][name] = cluster_summary(ref.run_cluster(rows, cfgs, lb, hz, check=True))
     corpus = acceptance_corpus(10_000)
     gold["fuzz"] = {}
     for pol in (2, 1, 0):

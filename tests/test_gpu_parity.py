@@ -250,3 +250,32 @@ def test_c2_full_size_properties(fb):
     a.run()
     assert a.results().tobytes() == res.tobytes()
     a.close()
+
+
+# ------------------------------------------------------------ cluster (C5)
+
+@pytest.fixture(scope="module")
+def gpu_cluster_cases(fb):
+    from catalog import cluster_cases
+    return {c[0]: c for c in cluster_cases(fb.generate_bursty)}
+
+
+@pytest.mark.parametrize("name", ["pab0_8", "count0_8", "pab5000_8", "count37_3", "pab_hz10s_8",
+                                  "pab20_2", "c5_pab0_64"])
+def test_cluster_matches_golden(golden, gpu_cluster_cases, name):
+    """fb_run_cluster: per-node plan digests, routing decisions and records
+    equal the reference run_cluster's (cluster.cpp:134-251)."""
+    from backends import cluster_summary
+    from paper_2510_14392_b200.cluster import run_cluster
+    _, rows, cfgs, lb, hz = gpu_cluster_cases[name]
+    out = run_cluster(rows, cfgs, lb, hz)
+    assert cluster_summary(out) == golden["clusters"][name]
+
+
+def test_cluster_rejects_reroute(fb):
+    from paper_2510_14392_b200.cluster import LbConfig, run_cluster
+    from paper_2510_14392_b200.batch import CostModel, Rows, engine_config
+    rows = Rows([0], [10], [5], [500_000], [50_000])
+    cfgs = [engine_config("fairbatch", 2048, CostModel(5, 0.05, 1e-4), 500, 50)]
+    with pytest.raises(fb.UsageError):
+        run_cluster(rows, cfgs, LbConfig("pab_lb", 1, 0.0, retry_reroute=True), 10**9)

@@ -243,3 +243,34 @@ def test_oracle_equals_reference_with_logs(oracle, ref):
         assert a.steps[i][: c["steps"]].tobytes() == b.steps[i][: c["steps"]].tobytes()
         assert a.entries[i][: c["entries"]].tobytes() == b.entries[i][: c["entries"]].tobytes()
         assert a.rejects[i][: c["rejects"]].tobytes() == b.rejects[i][: c["rejects"]].tobytes()
+
+
+# --------------------------------------------------------------- cluster
+
+@pytest.fixture(scope="module")
+def cluster_case_list(oracle):
+    from catalog import cluster_cases
+    return {c[0]: c for c in cluster_cases(oracle.generate_bursty)}
+
+
+@pytest.mark.parametrize("name", ["pab0_8", "count0_8", "pab5000_8", "count37_3", "pab_hz10s_8",
+                                  "pab20_2", "c5_pab0_64"])
+def test_oracle_cluster_matches_golden(oracle, golden, cluster_case_list, name):
+    """run_cluster (cluster.cpp:134-251): per-node plan digests, routing
+    decisions and per-request records equal the reference's."""
+    from backends import cluster_summary
+    _, rows, cfgs, lb, hz = cluster_case_list[name]
+    assert cluster_summary(oracle.run_cluster(rows, cfgs, lb, hz)) == golden["clusters"][name]
+
+
+def test_route_known_answers(oracle):
+    """test_cluster.cpp:76-113 through a 2-node cluster's first decisions:
+    pab_lb prefers the roomiest node that fits, ties go to the lowest id."""
+    from paper_2510_14392_b200.cluster import LbConfig
+    rows = Rows([0, 0, 0], [800, 100, 50_000], [4, 4, 4], [500_000] * 3, [50_000] * 3)
+    cfgs = [engine_config("fairbatch_pab", 8192, ENGINE_MODEL, 500, 50) for _ in range(2)]
+    out = oracle.run_cluster(rows, cfgs, LbConfig("pab_lb", 1, 0.0), ms_to_us(60_000.0))
+    # empty nodes report 49009 each: request 0 -> node 0 (tie, lowest id),
+    # request 1 -> node 1 (node 0 decremented by 800), request 2 fits nowhere ->
+    # best effort to the roomiest (node 0: 48209 vs node 1: 48909) -> node 1
+    assert out.route_node.tolist() == [0, 1, 1]
