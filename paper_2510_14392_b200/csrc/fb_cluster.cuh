@@ -47,7 +47,8 @@ struct ClusterSmem {
   int64_t f_t[kClusterMaxNodes], f_pab[kClusterMaxNodes], f_wait[kClusterMaxNodes],
       f_run[kClusterMaxNodes];
   int32_t fresh[kClusterMaxNodes];
-  int32_t bz[kClusterMaxNodes];  // busy when the global clock reaches t_a
+  int32_t bz[kClusterMaxNodes];   // busy when the global clock reaches t_a
+  int32_t cmp[kClusterMaxNodes];  // completed exactly at t_a
   int32_t status;
 };
 
@@ -159,15 +160,18 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
         Inst w = cluster_node(P, C, i, my);
         advance_node(P, C, cs, w, t_a, false);
         const bool busy_at = w.S.busy != 0;  // busy when the clock reaches t_a
+        const bool ends_at = busy_at && w.S.step_end == t_a;
         advance_node(P, C, cs, w, t_a, true);
         if (lane_id() == 0) {
           P.state[i] = w.S;
           cs.busy[i] = w.S.busy;
           cs.step_end[i] = w.S.step_end;
           cs.bz[i] = busy_at;
+          cs.cmp[i] = ends_at;  // owes a begin_step(t_a) after the routing
         }
       } else if (lane_id() == 0) {
         cs.bz[i] = cs.busy[i];
+        cs.cmp[i] = 0;
       }
       if (lane_id() == 0) {
         int64_t h = cs.rep_head[i];
@@ -281,7 +285,7 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     __syncthreads();
     // C: enqueue (visible at t_a) and begin_step(t_a) on idle nodes
     for (int i = warp; i < n; i += kClusterWarps) {
-      if (cs.got[i]) {
+      if (cs.got[i] || cs.cmp[i]) {
         Inst w = cluster_node(P, C, i, my);
         w.S.arr = cs.n_routed[i];  // Node::enqueue
         w.S.t_last = t_a;
