@@ -286,7 +286,9 @@ def run_ours(args) -> None:
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": float(te.item())},
-            "gpu_launches": 2 * args.steps,
+            # per step: reset_kernel, engine_kernel (warp engine), wide_kernel
+            # (CTA-wide engine; exits at once when no instance escalated)
+            "gpu_launches": 3 * args.steps,
             "clocks": clocks.summary(),
         }
         if ws == 1 and not args.no_cpu_baseline:
