@@ -2,6 +2,7 @@
 // uploads, launches and result downloads.  No exception crosses the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -121,6 +122,7 @@ struct fb_arena {
   DevBuf<fb_reject_log> log_rejects;
   DevBuf<unsigned long long> work;
   DevBuf<int64_t> wide_list;
+  DevBuf<int64_t> order;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
 
@@ -153,6 +155,7 @@ struct fb_arena {
     P.log_reject_cap = log.reject_cap;
     P.work = work.p;
     P.wide_list = wide_list.p;
+    P.order = order.p;
     P.max_events = max_events <= 0 ? INT64_MAX : max_events;
     return P;
   }
@@ -164,6 +167,7 @@ struct fb_arena {
     gscratch.release(); log_steps.release(); log_entries.release(); log_rejects.release();
     work.release();
     wide_list.release();
+    order.release();
   }
 };
 
@@ -259,6 +263,7 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   ENSURE(a->inst, n_instances * fbgpu::dev_inst_bytes());
   ENSURE(a->state, n_instances * fbgpu::dev_state_bytes());
   ENSURE(a->wide_list, n_instances);
+  ENSURE(a->order, n_instances);
   ENSURE(a->prefilled, n_rec);
   ENSURE(a->nidx, n_rec);
   ENSURE(a->seq, n_rec);
@@ -276,7 +281,30 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   for (int64_t i = 0; i < n_instances; ++i)
     fbgpu::pack_instance(instances[i], rec_off[i], i * lo.step_cap, i * lo.entry_cap,
                          i * lo.reject_cap, hinst.data() + i * fbgpu::dev_inst_bytes());
+  // Work-queue order: longest predicted run first, so the long-tailed
+  // instances start in the first wave (scheduling only, no semantic effect).
+  // Predicted length in steps ~ max over requests of arrival/a + output_len.
+  std::vector<int64_t> order(static_cast<size_t>(n_instances));
+  {
+    std::vector<double> key(static_cast<size_t>(n_instances), 0.0);
+    for (int64_t i = 0; i < n_instances; ++i) {
+      const fb_instance& in = instances[i];
+      const double a_us = in.cfg.truth_model.a_ms * 1000.0 > 1.0 ? in.cfg.truth_model.a_ms * 1000.0 : 1.0;
+      double k = 0.0;
+      for (int64_t r = in.trace_off; r < in.trace_off + in.n_req; ++r) {
+        const double v = static_cast<double>(rows->arrival_us[r]) / a_us + rows->output_len[r];
+        if (v > k) k = v;
+      }
+      key[i] = k;
+      order[i] = i;
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t x, int64_t y) { return key[x] > key[y]; });
+  }
   cudaStream_t s = a->stream;
+  if (n_instances > 0)
+    FB_CUDA(cudaMemcpyAsync(a->order.p, order.data(), sizeof(int64_t) * n_instances,
+                            cudaMemcpyHostToDevice, s));
   if (n_rows > 0) {
     FB_CUDA(cudaMemcpyAsync(a->arrival.p, rows->arrival_us, n_rows * 8, cudaMemcpyHostToDevice, s));
     FB_CUDA(cudaMemcpyAsync(a->ttft.p, rows->ttft_us, n_rows * 8, cudaMemcpyHostToDevice, s));

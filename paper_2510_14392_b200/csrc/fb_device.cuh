@@ -41,6 +41,20 @@ __device__ __forceinline__ double predict_ms(double a, double b, double c,
               dmul(c, static_cast<double>(ctx)));
 }
 
+// Running max of x_j = fl(fl(d/1000)/j) (RequestReport::max_tpot_ms,
+// metrics.cpp:42-49) without the two divisions when x_j cannot exceed the
+// current max m: x_j <= (d/(1000 j)) (1+2^-53)^2 < (d/(1000 j)) (1+2^-51), so
+// d*(1+2^-51) <= 1000*j*m (evaluated with upward / downward rounding) proves
+// x_j <= m and the std::max leaves m unchanged.  Otherwise x_j is computed
+// exactly in the reference's operation order.  d >= 0, 1 <= j < 2^31.
+__device__ __forceinline__ void max_ratio(double& m, int64_t d, int32_t j) {
+  const double lhs = __dmul_ru(static_cast<double>(d), 1.0 + 0x1p-51);
+  const double rhs = __dmul_rd(__dmul_rd(1000.0, static_cast<double>(j)), m);
+  if (lhs <= rhs) return;
+  const double x = ddiv(us_to_ms(d), static_cast<double>(j));
+  if (m < x) m = x;
+}
+
 // -------------------------------------------------------------- rng.h
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t& s) {  // rng.h:25-30

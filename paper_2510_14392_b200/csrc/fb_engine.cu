@@ -124,12 +124,13 @@ __device__ __forceinline__ bool emit_token(const EngineParams& P, int64_t g, int
   } else {
     const int64_t d = t - P.first[g];
     if (d > tpot * static_cast<int64_t>(idx)) fl |= kTpotViolated;
-    const double dm = us_to_ms(d);
-    const double x = ddiv(dm, static_cast<double>(idx));
-    if (P.maxtp[g] < x) P.maxtp[g] = x;  // std::max(best, x)
+    double m = P.maxtp[g];
+    max_ratio(m, d, idx);  // std::max(best, x)
+    P.maxtp[g] = m;
     if (idx >= 2) {
-      const double y = ddiv(dm, static_cast<double>(idx - 1));
-      if (P.maxtp_alt[g] < y) P.maxtp_alt[g] = y;
+      double ma = P.maxtp_alt[g];
+      max_ratio(ma, d, idx - 1);
+      P.maxtp_alt[g] = ma;
     }
     if (t - arr > ttft + tpot * static_cast<int64_t>(idx)) fl |= FB_REC_ENV_MISS;
   }
@@ -521,6 +522,7 @@ engine_kernel(const __grid_constant__ EngineParams P) {
     if (lane_id() == 0) i = atomicAdd(&P.work[0], 1ull);
     i = __shfl_sync(kFull, i, 0);
     if (i >= static_cast<unsigned long long>(P.n_inst)) break;
+    if (P.order) i = static_cast<unsigned long long>(P.order[i]);
     Inst w;
     w.id = static_cast<int64_t>(i);
     w.routed = nullptr;

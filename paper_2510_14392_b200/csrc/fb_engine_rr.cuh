@@ -116,13 +116,8 @@ __device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
   } else {
     const int64_t d = now - t.first;
     if (d > t.tpot * static_cast<int64_t>(idx)) t.flags |= kTpotViolated;
-    const double dm = us_to_ms(d);
-    const double x = ddiv(dm, static_cast<double>(idx));
-    if (t.maxtp < x) t.maxtp = x;
-    if (idx >= 2) {
-      const double y = ddiv(dm, static_cast<double>(idx - 1));
-      if (t.maxtp_alt < y) t.maxtp_alt = y;
-    }
+    max_ratio(t.maxtp, d, idx);
+    if (idx >= 2) max_ratio(t.maxtp_alt, d, idx - 1);
     if (now > t.dl0 + t.tpot * static_cast<int64_t>(idx)) t.flags |= FB_REC_ENV_MISS;
   }
   t.nidx = idx + 1;

@@ -43,6 +43,7 @@ struct EngineParams {
   // [3] number of escalated instances (list in wide_list)
   unsigned long long* work;
   int64_t* wide_list;
+  const int64_t* order;  // work-queue order (longest predicted instance first); may be null
   int64_t max_events;  // per instance per launch
 };
 
