@@ -428,6 +428,31 @@ int ref_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
 
 const char* ref_last_error(void) { return g_err.c_str(); }
 
+// The reference's own JSONL event log (run_node + save_event_log,
+// engine.cpp:395-451) of one instance, copied into buf (len_out = bytes;
+// FB_ERR_CAPACITY when cap is too small).
+int ref_event_log(const fb_trace* rows, const fb_instance* inst, const char* tmp_path, char* buf,
+                  int64_t cap, int64_t* len_out) {
+  try {
+    const Trace tr = instance_trace(rows, *inst);
+    const EventLog log = run_node(tr, to_engine(inst->cfg), inst->horizon_us);
+    save_event_log(log, tmp_path);
+    FILE* f = std::fopen(tmp_path, "rb");
+    if (!f) return fail(FB_ERR_PARSE, "cannot reopen event log");
+    std::string s;
+    char tmp[65536];
+    size_t k;
+    while ((k = std::fread(tmp, 1, sizeof(tmp), f)) > 0) s.append(tmp, k);
+    std::fclose(f);
+    *len_out = static_cast<int64_t>(s.size());
+    if (static_cast<int64_t>(s.size()) > cap) return fail(FB_ERR_CAPACITY, "buffer too small");
+    std::memcpy(buf, s.data(), s.size());
+    return FB_OK;
+  } catch (const std::exception& e) {
+    return map_exception(e);
+  }
+}
+
 int ref_generate_bursty(const fb_burst_profile* p, int64_t horizon_us, int64_t cap,
                         int64_t* arrival_us, int32_t* prompt_len,
                         int32_t* output_len, int64_t* ttft_us, int64_t* tpot_us,

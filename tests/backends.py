@@ -258,6 +258,24 @@ class RefLib(_CpuLib):
             raise RuntimeError(f"ref_run_cluster status {st}: {self.lib.ref_last_error()}")
         return ClusterOutput(res[:n], rec[:len(rows)], route[:len(rows)], inc.value)
 
+    def event_log(self, batch: Batch, i: int, tmp_path: str) -> str:
+        """The reference's save_event_log JSONL of instance i."""
+        fn = self.lib.ref_event_log
+        fn.restype = C.c_int
+        tr = batch.rows.to_c()
+        inst = batch.instance(i)
+        n = C.c_int64(0)
+        cap = 1 << 20
+        while True:
+            buf = C.create_string_buffer(cap)
+            st = fn(C.byref(tr), C.byref(inst), tmp_path.encode(), buf, C.c_int64(cap), C.byref(n))
+            if st == _abi.FB_ERR_CAPACITY:
+                cap = n.value + 1
+                continue
+            if st:
+                raise RuntimeError(f"ref_event_log status {st}")
+            return buf.raw[: n.value].decode()
+
     def run_node_batch(self, batch: Batch, nthreads: int = 1, records: bool = True) -> RunOutput:
         n = batch.n_instances
         tr = batch.rows.to_c()

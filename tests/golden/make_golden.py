@@ -65,6 +65,12 @@ def main() -> None:
         batch = fn(ref.generate_bursty)
         out = ref.run(batch, nthreads=8, check=True)
         gold["scenarios"][name] = summarize(out.results, out.records)
+    gold["event_logs"] = {}
+    for name in ("c1", "pab_overload", "wide"):
+        batch = SCENARIOS[name](ref.generate_bursty)
+        gold["event_logs"][name] = [
+            hashlib.sha256(ref.event_log(batch, i, "/tmp/_golden_ev.jsonl").encode()).hexdigest()
+            for i in range(batch.n_instances)]
     gold["clusters"] = {}
     for name, rows, cfgs, lb, hz in cluster_cases(ref.generate_bursty):
         gold["clusters"][name] = cluster_summary(ref.run_cluster(rows, cfgs, lb, hz, check=True))

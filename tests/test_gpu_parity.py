@@ -176,6 +176,21 @@ def test_engine_paths_exercised(fb, gpu, name, want):
     assert (paths & want).any(), paths
 
 
+@pytest.mark.parametrize("name", ["c1", "pab_overload", "wide"])
+def test_gpu_event_logs_match_reference_jsonl(gpu, golden, name):
+    """The reference's JSONL event log (save_event_log) rebuilt from the
+    device plan logs, byte for byte (sha256 per instance)."""
+    from paper_2510_14392_b200.events import event_log_jsonl
+    batch = SCENARIOS[name](gpu.generate_bursty)
+    lo = _abi.LogOpts(40_000, 600_000, 5_000, 0)
+    out = gpu.run(batch, lo)
+    got = [hashlib.sha256(event_log_jsonl(batch.rows, batch.instance(i), out.results[i],
+                                          out.counts[i], out.steps[i], out.entries[i],
+                                          out.rejects[i]).encode()).hexdigest()
+           for i in range(batch.n_instances)]
+    assert got == golden["event_logs"][name]
+
+
 def test_stepwise_api_matches_one_shot(gpu):
     """Node-style incremental driving (fb_arena_run with an event budget)."""
     batch = SCENARIOS["mixed"](gpu.generate_bursty)

@@ -245,6 +245,23 @@ def test_oracle_equals_reference_with_logs(oracle, ref):
         assert a.rejects[i][: c["rejects"]].tobytes() == b.rejects[i][: c["rejects"]].tobytes()
 
 
+# --------------------------------------------------------------- event logs
+
+@pytest.mark.parametrize("name", ["c1", "pab_overload", "wide"])
+def test_event_logs_from_plan_logs_match_reference_jsonl(oracle, golden, name):
+    """save_event_log JSONL (engine.cpp:395-451) rebuilt from plan logs is
+    byte-identical to the reference's own writer (hashes in golden.json)."""
+    from paper_2510_14392_b200.events import event_log_jsonl
+    batch = SCENARIOS[name](oracle.generate_bursty)
+    lo = _abi.LogOpts(40_000, 600_000, 5_000, 0)
+    out = oracle.run(batch, lo, nthreads=4)
+    got = [hashlib.sha256(event_log_jsonl(batch.rows, batch.instance(i), out.results[i],
+                                          out.counts[i], out.steps[i], out.entries[i],
+                                          out.rejects[i]).encode()).hexdigest()
+           for i in range(batch.n_instances)]
+    assert got == golden["event_logs"][name]
+
+
 # --------------------------------------------------------------- cluster
 
 @pytest.fixture(scope="module")
