@@ -71,6 +71,18 @@ def main() -> None:
         gold["event_logs"][name] = [
             hashlib.sha256(ref.event_log(batch, i, "/tmp/_golden_ev.jsonl").encode()).hexdigest()
             for i in range(batch.n_instances)]
+    import acceptance_cases as ac
+
+    def ref_runner(b):
+        o = ref.run_node_batch(b, nthreads=8)
+        return o.results, o.records
+
+    gold["acceptance"] = {
+        "crit67": ac.crit67(ref.generate_bursty, ref_runner),
+        "crit8": ac.crit8(ref.generate_bursty, ref_runner),
+        "crit9": ac.crit9(ref.generate_bursty,
+                          lambda r, c, lb, h: ref.run_cluster(r, c, lb, h).records),
+    }
     gold["clusters"] = {}
     for name, rows, cfgs, lb, hz in cluster_cases(ref.generate_bursty):
         gold["clusters"][name] = cluster_summary(ref.run_cluster(rows, cfgs, lb, hz, check=True))
