@@ -278,9 +278,17 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   ENSURE(a->log_rejects, n_instances * static_cast<int64_t>(lo.reject_cap));
 #undef ENSURE
   std::vector<unsigned char> hinst(static_cast<size_t>(n_instances) * fbgpu::dev_inst_bytes());
-  for (int64_t i = 0; i < n_instances; ++i)
+  for (int64_t i = 0; i < n_instances; ++i) {
+    // a uniform tpot_slo makes init_time_budget's min over tasks a constant
+    int64_t tpot_u = instances[i].n_req > 0 ? rows->tpot_us[instances[i].trace_off] : -1;
+    for (int64_t r = instances[i].trace_off; r < instances[i].trace_off + instances[i].n_req; ++r)
+      if (rows->tpot_us[r] != tpot_u) {
+        tpot_u = -1;
+        break;
+      }
     fbgpu::pack_instance(instances[i], rec_off[i], i * lo.step_cap, i * lo.entry_cap,
-                         i * lo.reject_cap, hinst.data() + i * fbgpu::dev_inst_bytes());
+                         i * lo.reject_cap, tpot_u, hinst.data() + i * fbgpu::dev_inst_bytes());
+  }
   // Work-queue order: longest predicted run first, so the long-tailed
   // instances start in the first wave (scheduling only, no semantic effect).
   // Predicted length in steps ~ max over requests of arrival/a + output_len.

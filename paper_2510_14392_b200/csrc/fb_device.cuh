@@ -149,6 +149,7 @@ struct DevInst {
   int64_t rec_off;    // first row of this instance's state/record/vlist region
   int64_t n_req;
   int64_t log_step_off, log_entry_off, log_reject_off;
+  int64_t tpot_uniform;  // every row's tpot_slo when they are all equal, else -1
   int32_t policy, max_chunk, max_active, pad;
 };
 

@@ -493,6 +493,7 @@ __device__ void run_instance(const EngineParams& P, Inst& w) {
       } else if (!rr && upcoming <= kWarp) {
         rr_load(P, w, tk);
         rr = true;
+        w.S.paths |= kPathRegister;
       }
       if (rr) {
         if (begin_rr(P, w, tk, t, s) < 0) {  // keys outside the packed range
@@ -500,8 +501,6 @@ __device__ void run_instance(const EngineParams& P, Inst& w) {
           rr = false;
           begin_step(P, w, t);
           w.S.paths |= kPathMemory;
-        } else {
-          w.S.paths |= kPathRegister;
         }
       } else {
         begin_step(P, w, t);
@@ -588,7 +587,8 @@ EngineGeometry engine_geometry(int device) {
 }
 
 void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
-                   int64_t log_entry_off, int64_t log_reject_off, void* out) {
+                   int64_t log_entry_off, int64_t log_reject_off, int64_t tpot_uniform,
+                   void* out) {
   DevInst d;
   std::memset(&d, 0, sizeof(d));
   const fb_engine_config& c = in.cfg;
@@ -610,6 +610,7 @@ void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
   d.log_step_off = log_step_off;
   d.log_entry_off = log_entry_off;
   d.log_reject_off = log_reject_off;
+  d.tpot_uniform = tpot_uniform;
   d.policy = c.scheduler.policy;
   d.max_chunk = c.scheduler.max_chunk;
   d.max_active = c.max_active;

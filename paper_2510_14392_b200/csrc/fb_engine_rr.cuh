@@ -276,7 +276,8 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
 
   // K1: views + init_time_budget reductions (sched.cpp:90-106)
   const RView v = view_reg(t, now);
-  const int64_t min_tpot = warp_min_i64(vis ? t.tpot : kInf);
+  const int64_t tpot_u = I->tpot_uniform;
+  const int64_t min_tpot = tpot_u >= 0 ? tpot_u : warp_min_i64(vis ? t.tpot : kInf);
   const int64_t min_dec = warp_min_i64(vis && v.decode ? v.slack : kInf);
   const int n_dec = __popc(__ballot_sync(kFull, vis && v.decode));
   double init_ms = 0.0;
@@ -291,19 +292,35 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   const bool fits = !vis || (t.seq >= 0 && t.seq < kPackSeq &&
                              (!fair || (v.slack >= -kPackSlack && v.slack < kPackSlack)));
   if (!__all_sync(kFull, fits)) return -1;
+  // Ranks are counted on 32-bit keys whenever that is exact: sarathi /
+  // prefill-first keys (group, seq) fit in 32 bits; fair-batching keys use
+  // their high half when it is distinct across the visible tasks (the order of
+  // distinct high halves is the order of the full keys).
   uint64_t key;
+  uint32_t k32;
+  bool use32;
   if (fair) {
     const uint64_t g = (v.decode && v.slack < urgency) ? 0 : (!v.decode ? 1 : 2);
     key = (g << 62) | (static_cast<uint64_t>(v.slack + kPackSlack) << 22) |
           static_cast<uint64_t>(t.seq);
+    k32 = vis ? static_cast<uint32_t>(key >> 32) : 0xffffffffu;  // visible hi <= 0xbfffffff
+    const unsigned same = __match_any_sync(kFull, k32);
+    use32 = __all_sync(kFull, !vis || same == (1u << lane));
   } else {
-    const uint64_t g = policy == FB_POLICY_SARATHI ? (v.decode ? 0 : 1) : 0;
-    key = (g << 62) | static_cast<uint64_t>(t.seq);
+    const uint32_t g = policy == FB_POLICY_SARATHI ? (v.decode ? 0u : 1u) : 0u;
+    key = (static_cast<uint64_t>(g) << 62) | static_cast<uint64_t>(t.seq);
+    k32 = vis ? ((g << 30) | static_cast<uint32_t>(t.seq)) : 0xffffffffu;
+    use32 = true;
   }
   if (!vis) key = ~uint64_t(0);
   int rank = 0;
+  if (use32) {
 #pragma unroll 8
-  for (int q = 0; q < A; ++q) rank += __shfl_sync(kFull, key, q) < key;
+    for (int q = 0; q < A; ++q) rank += __shfl_sync(kFull, k32, q) < k32;
+  } else {
+#pragma unroll 8
+    for (int q = 0; q < A; ++q) rank += __shfl_sync(kFull, key, q) < key;
+  }
   if (!vis) rank = lane;
   s.order[rank] = lane;
   __syncwarp();
