@@ -47,7 +47,8 @@ enum {
   FB_ERR_CONFIG = 3,     /* ConfigError: bad scenario or command config */
   FB_ERR_PARSE = 4,      /* ParseError                                  */
   FB_ERR_CUDA = 5,       /* device missing / CUDA runtime failure       */
-  FB_ERR_CAPACITY = 6    /* caller buffer too small; *_needed reported  */
+  FB_ERR_CAPACITY = 6,   /* caller buffer too small; *_needed reported  */
+  FB_ERR_TIMEOUT = 7     /* a peer rank never reached the epoch exchange */
 };
 
 /* Scheduling policies, sched.h:60 (same numbering as the enum order). */
@@ -355,6 +356,59 @@ int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* nod
                    int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
                    fb_instance_result* node_results, fb_record* records,
                    int32_t* route_node, int32_t* incomplete_out, double* device_ms_out);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU cluster: the nodes are partitioned over n_ranks processes (one
+ * GPU each, contiguous node ranges, fb_cluster_partition).  Every rank runs
+ * one persistent kernel over its nodes; per dispatch epoch (distinct arrival
+ * time) each node publishes an fb_node_report into every rank's exchange
+ * buffer (NVLink peer memory opened with CUDA IPC), the ranks meet at a
+ * device-side barrier, and each rank runs the same deterministic router
+ * (route, cluster.cpp:75-112) -- run_cluster's event order.
+ * Sequence on every rank:
+ *   create -> exchange_handle -> (allgather handles) -> connect -> reset ->
+ *   (host barrier across ranks) -> launch -> wait -> fetch -> destroy.
+ * Ranks of one process on one device may use exchange_ptr / connect_ptrs.
+ * The merged outputs equal fb_run_cluster's: route_node is identical on all
+ * ranks; rank r fills node_results of its own nodes and the records of the
+ * requests routed to them (the others stay "never routed"). */
+#define FB_CLUSTER_MAX_RANKS 8
+#define FB_IPC_HANDLE_BYTES 64
+
+typedef struct fb_node_report {
+  int64_t emitted_at; /* newest report delivered by the epoch time, -1 none */
+  int64_t pab_tokens;
+  int32_t waiting;
+  int32_t running;
+  int32_t fresh; /* delivered since the previous epoch */
+  int32_t busy;  /* node busy when the clock reaches the epoch time */
+} fb_node_report;
+
+typedef struct fb_cluster_shard fb_cluster_shard;
+
+/* Node range [*node_lo, *node_lo + *n_local) of `rank`. */
+int fb_cluster_partition(int32_t n_nodes, int32_t n_ranks, int32_t rank, int32_t* node_lo,
+                         int32_t* n_local);
+int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                            int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                            int32_t rank, int32_t n_ranks, fb_cluster_shard** out);
+int fb_cluster_shard_exchange_handle(fb_cluster_shard* s, void* handle_out);
+int fb_cluster_shard_exchange_ptr(fb_cluster_shard* s, void** dev_ptr_out);
+/* handles: n_ranks * FB_IPC_HANDLE_BYTES (this rank's entry is ignored). */
+int fb_cluster_shard_connect(fb_cluster_shard* s, const void* handles);
+int fb_cluster_shard_connect_ptrs(fb_cluster_shard* s, void* const* dev_ptrs);
+/* Zeroes this rank's exchange counter; all ranks must finish reset before
+ * any rank launches. */
+int fb_cluster_shard_reset(fb_cluster_shard* s);
+int fb_cluster_shard_launch(fb_cluster_shard* s);
+int fb_cluster_shard_wait(fb_cluster_shard* s, double* device_ms_out);
+/* local_results: n_local entries (incomplete = this rank's view);
+ * records / route_node: n_rows; *n_routed = requests routed before the loop
+ * stopped; *incomplete = this rank's ClusterResult::incomplete share. */
+int fb_cluster_shard_fetch(fb_cluster_shard* s, fb_instance_result* local_results,
+                           fb_record* records, int32_t* route_node, int64_t* n_routed,
+                           int32_t* incomplete);
+void fb_cluster_shard_destroy(fb_cluster_shard* s);
 
 #ifdef __cplusplus
 } /* extern "C" */

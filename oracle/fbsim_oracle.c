@@ -1023,3 +1023,252 @@ int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
   free(nodes); free(inst); free(res); free(view); free(dq);
   return status;
 }
+
+/* ---------------------------------------------------------------------------
+ * The epoch decomposition of run_cluster for one rank of a node partition
+ * (SURVEY §8e / P14), restated on the CPU so that the multi-rank protocol of
+ * fb_cluster_shard_* can be exercised between processes (gloo) in the CPU
+ * tests.  Per epoch e (distinct arrival time t_a):
+ *   advance      -- local nodes: events before t_a, the completion (+report)
+ *                   at t_a, then the newest report delivered by t_a;
+ *   route_begin  -- all reports -> view (apply_report), route the arrivals at
+ *                   t_a (route), enqueue to local nodes, begin_step(t_a).
+ * Partition: fb_cluster_partition's contiguous ranges. */
+struct orc_cluster_shard {
+  const fb_trace* rows;
+  fb_lb_config lb;
+  int32_t n_nodes, rank, n_ranks, node_lo, n_local;
+  int64_t horizon, nr, n_epochs, e_done, n_routed;
+  int64_t* ep_t;
+  int64_t* ep_lo;
+  fb_instance* inst;
+  orc_node* nodes;
+  fb_instance_result* res;
+  orc_nview* view;
+  orc_delivery** fifo; /* per local node */
+  int64_t* f_head;
+  int64_t* f_tail;
+  int64_t* f_cap;
+  int* cmp;
+  int32_t* route;
+  int stopped, finished, status;
+};
+
+int orc_cluster_partition(int32_t n_nodes, int32_t n_ranks, int32_t rank, int32_t* lo,
+                          int32_t* n_local) {
+  if (n_nodes < 1 || n_ranks < 1 || rank < 0 || rank >= n_ranks || n_ranks > n_nodes)
+    return FB_ERR_USAGE;
+  const int64_t a = (int64_t)n_nodes * rank / n_ranks;
+  const int64_t b = (int64_t)n_nodes * (rank + 1) / n_ranks;
+  *lo = (int32_t)a;
+  *n_local = (int32_t)(b - a);
+  return FB_OK;
+}
+
+static void orc_shard_push(orc_cluster_shard* s, int i, orc_delivery d) {
+  if (s->f_tail[i] == s->f_cap[i]) {
+    s->f_cap[i] *= 2;
+    s->fifo[i] = (orc_delivery*)realloc(s->fifo[i], (size_t)s->f_cap[i] * sizeof(orc_delivery));
+  }
+  s->fifo[i][s->f_tail[i]++] = d;
+}
+
+static void orc_shard_complete(orc_cluster_shard* s, int i, int report) {
+  orc_node* nd = &s->nodes[i];
+  const int64_t t = nd->step_end;
+  orc_complete_step(nd);
+  if (report && s->lb.report_interval_steps > 0 &&
+      nd->step_counter % (uint64_t)s->lb.report_interval_steps == 0)
+    orc_shard_push(s, i, orc_make_report(nd, s->node_lo + i, t, s->lb.policy == FB_LB_PAB,
+                                         s->lb.report_latency_us));
+}
+
+int orc_cluster_shard_create(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                             const fb_lb_config* lb, int64_t horizon, int32_t rank,
+                             int32_t n_ranks, orc_cluster_shard** out) {
+  int32_t lo, nl;
+  *out = NULL;
+  if (lb->report_latency_us < 0) return FB_ERR_VALIDATION;
+  if (lb->retry_reroute) return FB_ERR_USAGE;
+  if (orc_cluster_partition(n_nodes, n_ranks, rank, &lo, &nl)) return FB_ERR_USAGE;
+  orc_cluster_shard* s = (orc_cluster_shard*)calloc(1, sizeof(*s));
+  const int64_t nr = rows->n_rows;
+  s->rows = rows;
+  s->lb = *lb;
+  s->n_nodes = n_nodes;
+  s->rank = rank;
+  s->n_ranks = n_ranks;
+  s->node_lo = lo;
+  s->n_local = nl;
+  s->horizon = horizon;
+  s->nr = nr;
+  s->ep_t = (int64_t*)malloc((size_t)(nr + 1) * sizeof(int64_t));
+  s->ep_lo = (int64_t*)malloc((size_t)(nr + 2) * sizeof(int64_t));
+  for (int64_t q = 0; q < nr; ++q) {
+    if (q == 0 || rows->arrival_us[q] != rows->arrival_us[q - 1]) {
+      s->ep_t[s->n_epochs] = rows->arrival_us[q];
+      s->ep_lo[s->n_epochs++] = q;
+    }
+  }
+  s->ep_lo[s->n_epochs] = nr;
+  s->inst = (fb_instance*)calloc((size_t)nl + 1, sizeof(fb_instance));
+  s->nodes = (orc_node*)calloc((size_t)nl + 1, sizeof(orc_node));
+  s->res = (fb_instance_result*)calloc((size_t)nl + 1, sizeof(fb_instance_result));
+  s->view = (orc_nview*)calloc((size_t)n_nodes, sizeof(orc_nview));
+  s->fifo = (orc_delivery**)calloc((size_t)nl + 1, sizeof(orc_delivery*));
+  s->f_head = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
+  s->f_tail = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
+  s->f_cap = (int64_t*)calloc((size_t)nl + 1, sizeof(int64_t));
+  s->cmp = (int*)calloc((size_t)nl + 1, sizeof(int));
+  s->route = (int32_t*)malloc((size_t)(nr + 1) * sizeof(int32_t));
+  for (int64_t q = 0; q < nr; ++q) s->route[q] = -1;
+  for (int i = 0; i < nl; ++i) {
+    s->inst[i].cfg = cfgs[lo + i];
+    s->inst[i].trace_off = 0;
+    s->inst[i].n_req = nr;
+    s->inst[i].horizon_us = horizon;
+    orc_node_alloc(&s->nodes[i], &s->inst[i], rows, &s->res[i]);
+    s->f_cap[i] = 64;
+    s->fifo[i] = (orc_delivery*)malloc(64 * sizeof(orc_delivery));
+    /* initial reports (cluster.cpp:198) */
+    orc_shard_push(s, i, orc_make_report(&s->nodes[i], lo + i, 0, lb->policy == FB_LB_PAB,
+                                         lb->report_latency_us));
+  }
+  *out = s;
+  return FB_OK;
+}
+
+int64_t orc_cluster_shard_epochs(const orc_cluster_shard* s) { return s->n_epochs; }
+
+int orc_cluster_shard_advance(orc_cluster_shard* s, int64_t e, fb_node_report* local) {
+  if (e < 0 || e >= s->n_epochs || s->stopped || s->finished) return FB_ERR_USAGE;
+  const int64_t t_a = s->ep_t[e];
+  for (int i = 0; i < s->n_local; ++i) {
+    orc_node* nd = &s->nodes[i];
+    while (nd->busy && nd->step_end < t_a) {
+      const int64_t t = nd->step_end;
+      orc_shard_complete(s, i, 1);
+      if (t < s->horizon && !s->status) s->status = orc_begin_step(nd, t);
+    }
+    fb_node_report r;
+    r.busy = nd->busy;
+    s->cmp[i] = nd->busy && nd->step_end == t_a;
+    if (s->cmp[i]) orc_shard_complete(s, i, 1);
+    r.emitted_at = -1;
+    r.pab_tokens = 0;
+    r.waiting = r.running = 0;
+    r.fresh = 0;
+    while (s->f_head[i] < s->f_tail[i] && s->fifo[i][s->f_head[i]].deliver_at <= t_a) {
+      const orc_delivery* d = &s->fifo[i][s->f_head[i]++];
+      r.emitted_at = d->emitted_at;
+      r.pab_tokens = d->pab;
+      r.waiting = (int32_t)d->waiting;
+      r.running = (int32_t)d->running;
+      r.fresh = 1;
+    }
+    local[i] = r;
+  }
+  return s->status;
+}
+
+int orc_cluster_shard_route_begin(orc_cluster_shard* s, int64_t e, const fb_node_report* all,
+                                  int32_t* stopped) {
+  if (e < 0 || e >= s->n_epochs || s->stopped || s->finished) return FB_ERR_USAGE;
+  const int64_t t_a = s->ep_t[e];
+  int any_busy = 0;
+  for (int i = 0; i < s->n_nodes; ++i) any_busy |= all[i].busy != 0;
+  if (t_a >= s->horizon && !any_busy) { /* cluster.cpp:191-192 */
+    s->stopped = 1;
+    *stopped = 1;
+    return FB_OK;
+  }
+  *stopped = 0;
+  for (int i = 0; i < s->n_nodes; ++i) { /* apply_report, cluster.cpp:60-73 */
+    orc_nview* v = &s->view[i];
+    if (!all[i].fresh || (v->has && all[i].emitted_at < v->t)) continue;
+    v->has = 1;
+    v->t = all[i].emitted_at;
+    v->pab = all[i].pab_tokens;
+    v->waiting = all[i].waiting;
+    v->running = all[i].running;
+    v->dec = 0;
+    v->inc = 0;
+  }
+  for (int64_t q = s->ep_lo[e]; q < s->ep_lo[e + 1]; ++q) {
+    const int target = orc_route(s->view, s->n_nodes, s->rows->prompt_len[q], &s->lb);
+    s->route[q] = target;
+    if (target >= s->node_lo && target < s->node_lo + s->n_local)
+      orc_enqueue(&s->nodes[target - s->node_lo], (int32_t)q, t_a);
+  }
+  s->n_routed = s->ep_lo[e + 1];
+  if (t_a < s->horizon)
+    for (int i = 0; i < s->n_local && !s->status; ++i)
+      if (!s->nodes[i].busy) s->status = orc_begin_step(&s->nodes[i], t_a);
+  s->e_done = e + 1;
+  return s->status;
+}
+
+int orc_cluster_shard_fetch(orc_cluster_shard* s, fb_instance_result* local_results,
+                            fb_record* records, int32_t* route_node, int64_t* n_routed,
+                            int32_t* incomplete) {
+  const int64_t nr = s->nr;
+  if (!s->finished) { /* run every local node to quiescence */
+    for (int i = 0; i < s->n_local && !s->status; ++i)
+      while (s->nodes[i].busy && !s->status) {
+        const int64_t t = s->nodes[i].step_end;
+        orc_shard_complete(s, i, 0);
+        if (t < s->horizon) s->status = orc_begin_step(&s->nodes[i], t);
+      }
+    s->finished = 1;
+  }
+  int live = s->n_routed < nr;
+  for (int i = 0; i < s->n_local; ++i) {
+    const orc_node* nd = &s->nodes[i];
+    live = live || nd->busy || nd->pend_head < nd->pend_tail || nd->n_waiting > 0 ||
+           nd->n_active > 0;
+  }
+  for (int i = 0; i < s->n_local; ++i) {
+    s->res[i].steps = s->nodes[i].step_counter;
+    s->res[i].incomplete = live;
+    s->res[i].status = s->status;
+    s->res[i].end_time_us = -1;
+    if (local_results) local_results[i] = s->res[i];
+  }
+  if (route_node)
+    for (int64_t q = 0; q < nr; ++q) route_node[q] = s->route[q];
+  if (n_routed) *n_routed = s->n_routed;
+  if (incomplete) *incomplete = live;
+  if (records) {
+    for (int64_t k = 0; k < nr; ++k) {
+      fb_record* o = &records[k];
+      const int node = s->route[k] - s->node_lo;
+      o->first_emit_us = -1;
+      o->max_tpot_ms = 0.0;
+      o->max_tpot_alt_ms = 0.0;
+      o->tokens_emitted = 0;
+      o->flags = 0;
+      if (s->route[k] < 0 || node < 0 || node >= s->n_local) continue;
+      const orc_node* nd = &s->nodes[node];
+      if (!(nd->flags[k] & FB_REC_ARRIVED)) continue;
+      o->first_emit_us = nd->first[k];
+      o->max_tpot_ms = nd->maxtp[k];
+      o->max_tpot_alt_ms = nd->maxtp_alt[k];
+      o->tokens_emitted = nd->nidx[k];
+      uint32_t f = nd->flags[k] & 0x7fffffffu;
+      if ((f & FB_REC_REJECTED) && nd->nidx[k] > 0) f &= ~(uint32_t)FB_REC_REJECTED;
+      o->flags = f;
+    }
+  }
+  return s->status;
+}
+
+void orc_cluster_shard_destroy(orc_cluster_shard* s) {
+  if (!s) return;
+  for (int i = 0; i < s->n_local; ++i) {
+    orc_node_free(&s->nodes[i]);
+    free(s->fifo[i]);
+  }
+  free(s->ep_t); free(s->ep_lo); free(s->inst); free(s->nodes); free(s->res); free(s->view);
+  free(s->fifo); free(s->f_head); free(s->f_tail); free(s->f_cap); free(s->cmp); free(s->route);
+  free(s);
+}

@@ -52,6 +52,23 @@ int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
                     const fb_lb_config* lb, int64_t horizon, fb_instance_result* node_results,
                     fb_record* records, int32_t* route_node, int32_t* incomplete_out);
 
+/* run_cluster's epoch decomposition for one rank of a node partition; the
+ * caller exchanges fb_node_reports between advance and route_begin. */
+typedef struct orc_cluster_shard orc_cluster_shard;
+int orc_cluster_partition(int32_t n_nodes, int32_t n_ranks, int32_t rank, int32_t* node_lo,
+                          int32_t* n_local);
+int orc_cluster_shard_create(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                             const fb_lb_config* lb, int64_t horizon, int32_t rank,
+                             int32_t n_ranks, orc_cluster_shard** out);
+int64_t orc_cluster_shard_epochs(const orc_cluster_shard* s);
+int orc_cluster_shard_advance(orc_cluster_shard* s, int64_t epoch, fb_node_report* local);
+int orc_cluster_shard_route_begin(orc_cluster_shard* s, int64_t epoch, const fb_node_report* all,
+                                  int32_t* stopped);
+int orc_cluster_shard_fetch(orc_cluster_shard* s, fb_instance_result* local_results,
+                            fb_record* records, int32_t* route_node, int64_t* n_routed,
+                            int32_t* incomplete);
+void orc_cluster_shard_destroy(orc_cluster_shard* s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,8 @@ FB_ERR_CONFIG = 3
 FB_ERR_PARSE = 4
 FB_ERR_CUDA = 5
 FB_ERR_CAPACITY = 6
+FB_ERR_TIMEOUT = 7
+FB_IPC_HANDLE_BYTES = 64
 
 POLICY_PREFILL_FIRST = 0
 POLICY_SARATHI = 1
@@ -220,6 +222,8 @@ def _np_dtype(struct):
     return np.dtype(np.ctypeslib.as_ctypes_type(np.dtype(struct)))
 
 
+NODE_REPORT_DTYPE = np.dtype([("emitted_at", "<i8"), ("pab_tokens", "<i8"), ("waiting", "<i4"),
+                              ("running", "<i4"), ("fresh", "<i4"), ("busy", "<i4")])  # fb_node_report
 RECORD_DTYPE = np.dtype(
     [("first_emit_us", "<i8"), ("max_tpot_ms", "<f8"), ("max_tpot_alt_ms", "<f8"),
      ("tokens_emitted", "<i4"), ("flags", "<u4")], align=True)

@@ -1,8 +1,13 @@
 """Cluster-level simulation (run_cluster, cluster.h:107-109) on the device.
 
-`LbConfig` mirrors cluster.h:36-47; `run_cluster` calls fb_run_cluster; `c5`
-builds BASELINE config 5 (64 nodes, pab_lb over fairbatch_pab nodes,
-SURVEY §8d).
+`LbConfig` mirrors cluster.h:36-47; `run_cluster` calls fb_run_cluster (one
+GPU); `run_cluster_dist` partitions the nodes over the ranks of a
+torch.distributed group (one GPU per rank) and runs the fb_cluster_shard_*
+protocol -- per dispatch epoch every node's report goes into every rank's
+exchange buffer over NVLink peer memory, then a replicated router routes the
+epoch's arrivals; `merge_shards` reassembles the single-GPU
+outputs.  `c5` builds BASELINE config 5 (64 nodes, pab_lb over fairbatch_pab
+nodes).
 """
 from __future__ import annotations
 
@@ -66,6 +71,148 @@ def run_cluster(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, device: int = 0
                                   int(horizon_us), _abi.vptr(res), _abi.vptr(rec),
                                   _abi.vptr(route), C.byref(inc), C.byref(ms)), "fb_run_cluster")
     return ClusterOutput(res[:n], rec[:len(rows)], route[:len(rows)], inc.value, ms.value)
+
+
+def partition(n_nodes: int, world: int, rank: int) -> tuple[int, int]:
+    """(node_lo, n_local) of `rank` -- fb_cluster_partition's contiguous ranges."""
+    if n_nodes < 1 or world < 1 or not 0 <= rank < world or world > n_nodes:
+        raise ValueError("bad cluster partition")
+    lo = n_nodes * rank // world
+    return lo, n_nodes * (rank + 1) // world - lo
+
+
+@dataclass
+class ShardOutput:
+    """One rank's share of a cluster run (fb_cluster_shard_fetch)."""
+
+    node_lo: int
+    node_results: np.ndarray  # RESULT_DTYPE of nodes [node_lo, node_lo + n_local)
+    records: np.ndarray       # per request; filled for requests routed to local nodes
+    route_node: np.ndarray    # identical on every rank
+    n_routed: int
+    incomplete: int
+    device_ms: float = 0.0
+
+
+def merge_shards(parts: list[ShardOutput], n_nodes: int) -> ClusterOutput:
+    """The single-GPU ClusterOutput from every rank's ShardOutput."""
+    parts = sorted(parts, key=lambda p: p.node_lo)
+    route = parts[0].route_node
+    for p in parts[1:]:
+        if not np.array_equal(p.route_node, route) or p.n_routed != parts[0].n_routed:
+            raise RuntimeError("ranks disagree on the routing decisions")
+    res = np.concatenate([p.node_results for p in parts])
+    if len(res) != n_nodes:
+        raise RuntimeError("shard outputs do not cover the cluster")
+    inc = int(any(p.incomplete for p in parts))
+    res["incomplete"] = inc
+    rec = parts[0].records.copy()
+    for p in parts[1:]:
+        own = (route >= p.node_lo) & (route < p.node_lo + len(p.node_results))
+        rec[own] = p.records[own]
+    return ClusterOutput(res, rec, route.copy(), inc, max(p.device_ms for p in parts))
+
+
+class ClusterShard:
+    """fb_cluster_shard_*: this rank's nodes of one cluster simulation."""
+
+    def __init__(self, rows: Rows, cfgs, lb: LbConfig, horizon_us: int, rank: int, world: int,
+                 device: int = 0):
+        L = fbgpu.lib()
+        self._L = L
+        self.n_nodes = len(cfgs)
+        self.n_rows = len(rows)
+        self.node_lo, self.n_local = partition(self.n_nodes, world, rank)
+        self._tr = rows.to_c()  # keep the host rows alive while the shard exists
+        nc = node_configs_c(cfgs)
+        lbc = lb.to_c()
+        h = C.c_void_p()
+        fbgpu._check(L.fb_cluster_shard_create(device, C.byref(self._tr), C.cast(nc, C.c_void_p),
+                                               self.n_nodes, C.byref(lbc), int(horizon_us),
+                                               rank, world, C.byref(h)),
+                     "fb_cluster_shard_create")
+        self._h = h
+
+    def exchange_handle(self) -> bytes:
+        buf = (C.c_ubyte * _abi.FB_IPC_HANDLE_BYTES)()
+        fbgpu._check(self._L.fb_cluster_shard_exchange_handle(self._h, buf),
+                     "fb_cluster_shard_exchange_handle")
+        return bytes(buf)
+
+    def exchange_ptr(self) -> int:
+        p = C.c_void_p()
+        fbgpu._check(self._L.fb_cluster_shard_exchange_ptr(self._h, C.byref(p)),
+                     "fb_cluster_shard_exchange_ptr")
+        return int(p.value)
+
+    def connect(self, handles: list[bytes]) -> None:
+        raw = b"".join(handles)
+        fbgpu._check(self._L.fb_cluster_shard_connect(self._h, raw), "fb_cluster_shard_connect")
+
+    def connect_ptrs(self, ptrs: list[int]) -> None:
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        fbgpu._check(self._L.fb_cluster_shard_connect_ptrs(self._h, arr),
+                     "fb_cluster_shard_connect_ptrs")
+
+    def reset(self) -> None:
+        fbgpu._check(self._L.fb_cluster_shard_reset(self._h), "fb_cluster_shard_reset")
+
+    def launch(self) -> None:
+        fbgpu._check(self._L.fb_cluster_shard_launch(self._h), "fb_cluster_shard_launch")
+
+    def wait(self) -> float:
+        ms = C.c_double(0)
+        fbgpu._check(self._L.fb_cluster_shard_wait(self._h, C.byref(ms)), "fb_cluster_shard_wait")
+        return ms.value
+
+    def fetch(self, device_ms: float = 0.0) -> ShardOutput:
+        res = np.zeros(max(1, self.n_local), _abi.RESULT_DTYPE)
+        rec = np.zeros(max(1, self.n_rows), _abi.RECORD_DTYPE)
+        route = np.zeros(max(1, self.n_rows), np.int32)
+        nrt = C.c_int64(0)
+        inc = C.c_int32(0)
+        fbgpu._check(self._L.fb_cluster_shard_fetch(self._h, _abi.vptr(res), _abi.vptr(rec),
+                                                    _abi.vptr(route), C.byref(nrt), C.byref(inc)),
+                     "fb_cluster_shard_fetch")
+        return ShardOutput(self.node_lo, res[:self.n_local], rec[:self.n_rows],
+                           route[:self.n_rows], nrt.value, inc.value, device_ms)
+
+    def close(self) -> None:
+        if self._h:
+            self._L.fb_cluster_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_cluster_dist(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, dist,
+                     device: int | None = None) -> ClusterOutput:
+    """run_cluster with the nodes partitioned over the ranks of `dist` (one
+    GPU per rank, NVLink peer memory between them); every rank returns the
+    merged single-GPU output."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    sh = ClusterShard(rows, cfgs, lb, horizon_us, rank, world, device)
+    try:
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, sh.exchange_handle())
+            sh.connect(handles)
+        sh.reset()
+        dist.barrier()  # every exchange counter is zero before any rank launches
+        sh.launch()
+        out = sh.fetch(sh.wait())
+    finally:
+        sh.close()
+    parts = [None] * world
+    dist.all_gather_object(parts, out)
+    return merge_shards(parts, len(cfgs))
 
 
 MODEL_7B = CostModel(5.0, 0.05, 0.0001)

@@ -495,28 +495,74 @@ int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
   return st;
 }
 
-// run_cluster (cluster.cpp:134-251): all nodes of one cluster in one CTA
-// (fb_cluster.cuh); routing decisions and node plans are exact.
-int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
-                   int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
-                   fb_instance_result* node_results, fb_record* records, int32_t* route_node,
-                   int32_t* incomplete_out, double* device_ms_out) {
+}  // extern "C"
+
+// ------------------------------------------------------------ cluster
+
+struct fb_cluster_shard {
+  fb_arena* a = nullptr;
+  int32_t n_nodes = 0, rank = 0, n_ranks = 1, node_lo = 0, n_local = 0;
+  int64_t nr = 0;
+  int blocks = 0;
+  bool connected = false, launched = false;
+  fbgpu::ClusterParamsHost cp{};
+  std::vector<void*> bufs;    // device allocations
+  std::vector<void*> opened;  // CUDA-IPC peer mappings
+  unsigned char* xbuf = nullptr;
+  int64_t* d_out = nullptr;
+  int32_t* d_route = nullptr;
+  ~fb_cluster_shard() {
+    if (a) cudaSetDevice(a->device);
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    for (void* p : bufs) cudaFree(p);
+    fb_arena_destroy(a);
+  }
+};
+
+extern "C" {
+
+int fb_cluster_partition(int32_t n_nodes, int32_t n_ranks, int32_t rank, int32_t* node_lo,
+                         int32_t* n_local) {
+  if (n_nodes < 1 || n_ranks < 1 || rank < 0 || rank >= n_ranks)
+    return set_error(FB_ERR_USAGE, "fb_cluster_partition: bad arguments");
+  if (n_ranks > n_nodes) return set_error(FB_ERR_USAGE, "more ranks than cluster nodes");
+  const int64_t lo = static_cast<int64_t>(n_nodes) * rank / n_ranks;
+  const int64_t hi = static_cast<int64_t>(n_nodes) * (rank + 1) / n_ranks;
+  if (node_lo) *node_lo = static_cast<int32_t>(lo);
+  if (n_local) *n_local = static_cast<int32_t>(hi - lo);
+  return FB_OK;
+}
+
+// run_cluster (cluster.cpp:134-251) for the nodes of one rank (fb_cluster.cuh).
+int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                            int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                            int32_t rank, int32_t n_ranks, fb_cluster_shard** out) {
+  if (!out) return set_error(FB_ERR_USAGE, "fb_cluster_shard_create: null output");
+  *out = nullptr;
   if (!rows || !node_cfgs || !lb) return set_error(FB_ERR_USAGE, "fb_run_cluster: null argument");
   if (n_nodes < 1) return set_error(FB_ERR_USAGE, "run_cluster requires at least one node");
   if (n_nodes > fbgpu::cluster_max_nodes())
-    return set_error(FB_ERR_USAGE, "fb_run_cluster: too many nodes for one CTA");
+    return set_error(FB_ERR_USAGE, "fb_run_cluster: more than 512 nodes");
+  if (n_ranks < 1 || n_ranks > fbgpu::cluster_max_ranks())
+    return set_error(FB_ERR_USAGE, "fb_cluster_shard_create: 1..8 ranks");
   if (lb->report_latency_us < 0) return set_error(FB_ERR_VALIDATION, "report_latency must be >= 0");
   if (lb->retry_reroute) return set_error(FB_ERR_USAGE, "retry_reroute is not supported");
   if (lb->policy != FB_LB_PAB && lb->policy != FB_LB_COUNT)
     return set_error(FB_ERR_USAGE, "unknown load-balancer policy");
+  int32_t lo = 0, nl = 0;
+  int st = fb_cluster_partition(n_nodes, n_ranks, rank, &lo, &nl);
+  if (st) return st;
   const int64_t nr = rows->n_rows;
-  std::vector<fb_instance> inst(static_cast<size_t>(n_nodes));
-  for (int i = 0; i < n_nodes; ++i) {
-    inst[i].cfg = node_cfgs[i];
+  std::vector<fb_instance> inst(static_cast<size_t>(nl));
+  for (int i = 0; i < nl; ++i) {
+    inst[i].cfg = node_cfgs[lo + i];
     inst[i].trace_off = 0;
     inst[i].n_req = nr;
     inst[i].horizon_us = horizon_us;
   }
+  // validate every node's config (all ranks reject the same clusters)
+  for (int i = 0; i < n_nodes; ++i)
+    if ((st = validate_engine(node_cfgs[i], i))) return st;
   // dispatch epochs: distinct arrival times and their request ranges
   std::vector<int64_t> ep_t, ep_lo;
   for (int64_t q = 0; q < nr; ++q) {
@@ -526,38 +572,51 @@ int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* nod
     }
   }
   ep_lo.push_back(nr);
-  fb_arena* a = nullptr;
-  int st = fb_arena_create(device, nullptr, &a);
-  if (st) return st;
-  struct Guard {
-    fb_arena* a;
-    std::vector<void*> bufs;
-    ~Guard() {
-      for (void* p : bufs) cudaFree(p);
-      fb_arena_destroy(a);
-    }
-  } guard{a, {}};
-  if ((st = fb_arena_load(a, rows, inst.data(), n_nodes, nullptr))) return st;
+  fb_cluster_shard* sh = new fb_cluster_shard();
+  struct Drop {
+    fb_cluster_shard*& p;
+    ~Drop() { delete p; }
+  } drop{sh};
+  sh->n_nodes = n_nodes;
+  sh->rank = rank;
+  sh->n_ranks = n_ranks;
+  sh->node_lo = lo;
+  sh->n_local = nl;
+  sh->nr = nr;
+  if ((st = fb_arena_create(device, nullptr, &sh->a))) return st;
+  if ((st = fb_arena_load(sh->a, rows, inst.data(), nl, nullptr))) return st;
   const int cap = lb->report_cap > 0 ? lb->report_cap : 4096;
   auto dalloc = [&](void** p, size_t bytes) -> cudaError_t {
     cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
-    if (e == cudaSuccess) guard.bufs.push_back(*p);
+    if (e == cudaSuccess) sh->bufs.push_back(*p);
     return e;
   };
-  int64_t *d_ept, *d_eplo, *d_rep, *d_out;
-  int32_t *d_routed, *d_route;
+  int64_t *d_ept, *d_eplo, *d_rep;
+  int32_t* d_routed;
   const int64_t ne = static_cast<int64_t>(ep_t.size());
   FB_CUDA(dalloc(reinterpret_cast<void**>(&d_ept), sizeof(int64_t) * (ne + 1)));
   FB_CUDA(dalloc(reinterpret_cast<void**>(&d_eplo), sizeof(int64_t) * (ne + 1)));
-  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_rep), sizeof(int64_t) * 4 * cap * n_nodes));
-  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_out), sizeof(int64_t) * 2));
-  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_routed), sizeof(int32_t) * n_nodes * (nr + 1)));
-  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_route), sizeof(int32_t) * (nr + 1)));
-  cudaStream_t s = a->stream;
-  if (ne > 0) FB_CUDA(cudaMemcpyAsync(d_ept, ep_t.data(), sizeof(int64_t) * ne, cudaMemcpyHostToDevice, s));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_rep), sizeof(int64_t) * 4 * cap * nl));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_out), sizeof(int64_t) * 4));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_routed), sizeof(int32_t) * nl * (nr + 1)));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_route), sizeof(int32_t) * (nr + 1)));
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->xbuf), fbgpu::cluster_xchg_bytes(n_nodes)));
+  cudaStream_t s = sh->a->stream;
+  if (ne > 0)
+    FB_CUDA(cudaMemcpyAsync(d_ept, ep_t.data(), sizeof(int64_t) * ne, cudaMemcpyHostToDevice, s));
   FB_CUDA(cudaMemcpyAsync(d_eplo, ep_lo.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice, s));
-  FB_CUDA(cudaMemsetAsync(d_route, 0xff, sizeof(int32_t) * (nr + 1), s));
-  fbgpu::ClusterParamsHost cp;
+  FB_CUDA(cudaMemsetAsync(sh->xbuf, 0, fbgpu::cluster_xchg_bytes(n_nodes), s));
+  FB_CUDA(cudaStreamSynchronize(s));
+  const int wpc = fbgpu::cluster_warps_per_cta(n_nodes, n_ranks);
+  int total = 0;
+  for (int r = 0; r < n_ranks; ++r) {
+    int32_t l2 = 0, n2 = 0;
+    fb_cluster_partition(n_nodes, n_ranks, r, &l2, &n2);
+    total += (n2 + wpc - 1) / wpc;
+  }
+  sh->blocks = (nl + wpc - 1) / wpc;
+  fbgpu::ClusterParamsHost& cp = sh->cp;
+  std::memset(&cp, 0, sizeof(cp));
   cp.n_nodes = n_nodes;
   cp.lb_policy = lb->policy;
   cp.interval = lb->report_interval_steps;
@@ -571,56 +630,171 @@ int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* nod
   cp.epoch_t = d_ept;
   cp.epoch_lo = d_eplo;
   cp.routed = d_routed;
-  cp.route_node = d_route;
+  cp.route_node = sh->d_route;
   cp.rep = d_rep;
-  cp.out = d_out;
+  cp.out = sh->d_out;
+  cp.node_lo = lo;
+  cp.n_local = nl;
+  cp.rank = rank;
+  cp.n_ranks = n_ranks;
+  cp.warps_per_cta = wpc;
+  cp.total_ctas = total;
+  cp.timeout_ns = int64_t(30) * 1000 * 1000 * 1000;
   if (fbgpu::cluster_param_bytes() != sizeof(cp))
     return set_error(FB_ERR_USAGE, "cluster parameter layout mismatch");
-  FB_CUDA(cudaEventRecord(a->ev0, s));
-  FB_CUDA(fbgpu::launch_cluster(a->params(0), &cp, s));
-  FB_CUDA(cudaEventRecord(a->ev1, s));
-  int64_t out[2] = {0, 0};
-  FB_CUDA(cudaMemcpyAsync(out, d_out, sizeof(out), cudaMemcpyDeviceToHost, s));
-  std::vector<int32_t> route(static_cast<size_t>(nr));
-  if (nr > 0) FB_CUDA(cudaMemcpyAsync(route.data(), d_route, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, s));
-  FB_CUDA(cudaStreamSynchronize(s));
+  if (n_ranks == 1) {
+    cp.xbuf[0] = sh->xbuf;
+    sh->connected = true;
+  }
+  *out = sh;
+  sh = nullptr;
+  return FB_OK;
+}
+
+int fb_cluster_shard_exchange_handle(fb_cluster_shard* s, void* handle_out) {
+  if (!s || !handle_out) return set_error(FB_ERR_USAGE, "fb_cluster_shard_exchange_handle: bad arguments");
+  static_assert(sizeof(cudaIpcMemHandle_t) == FB_IPC_HANDLE_BYTES, "IPC handle size");
+  FB_CUDA(cudaSetDevice(s->a->device));
+  cudaIpcMemHandle_t h;
+  FB_CUDA(cudaIpcGetMemHandle(&h, s->xbuf));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return FB_OK;
+}
+
+int fb_cluster_shard_exchange_ptr(fb_cluster_shard* s, void** dev_ptr_out) {
+  if (!s || !dev_ptr_out) return set_error(FB_ERR_USAGE, "fb_cluster_shard_exchange_ptr: bad arguments");
+  *dev_ptr_out = s->xbuf;
+  return FB_OK;
+}
+
+int fb_cluster_shard_connect(fb_cluster_shard* s, const void* handles) {
+  if (!s || !handles) return set_error(FB_ERR_USAGE, "fb_cluster_shard_connect: bad arguments");
+  if (s->launched) return set_error(FB_ERR_USAGE, "fb_cluster_shard_connect: shard is running");
+  FB_CUDA(cudaSetDevice(s->a->device));
+  for (void* p : s->opened) cudaIpcCloseMemHandle(p);
+  s->opened.clear();
+  for (int r = 0; r < s->n_ranks; ++r) {
+    if (r == s->rank) {
+      s->cp.xbuf[r] = s->xbuf;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const unsigned char*>(handles) + r * FB_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    FB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    s->opened.push_back(p);
+    s->cp.xbuf[r] = static_cast<unsigned char*>(p);
+  }
+  s->connected = true;
+  return FB_OK;
+}
+
+int fb_cluster_shard_connect_ptrs(fb_cluster_shard* s, void* const* dev_ptrs) {
+  if (!s || !dev_ptrs) return set_error(FB_ERR_USAGE, "fb_cluster_shard_connect_ptrs: bad arguments");
+  if (s->launched) return set_error(FB_ERR_USAGE, "fb_cluster_shard_connect_ptrs: shard is running");
+  for (int r = 0; r < s->n_ranks; ++r) {
+    if (!dev_ptrs[r]) return set_error(FB_ERR_USAGE, "fb_cluster_shard_connect_ptrs: null peer");
+    s->cp.xbuf[r] = static_cast<unsigned char*>(dev_ptrs[r]);
+  }
+  s->cp.xbuf[s->rank] = s->xbuf;
+  s->connected = true;
+  return FB_OK;
+}
+
+int fb_cluster_shard_reset(fb_cluster_shard* s) {
+  if (!s) return set_error(FB_ERR_USAGE, "fb_cluster_shard_reset: null shard");
+  if (s->launched) return set_error(FB_ERR_USAGE, "fb_cluster_shard_reset: shard is running");
+  FB_CUDA(cudaSetDevice(s->a->device));
+  int st = fb_arena_reset(s->a);
+  if (st) return st;
+  cudaStream_t q = s->a->stream;
+  FB_CUDA(cudaMemsetAsync(s->xbuf, 0, fbgpu::cluster_xchg_bytes(s->n_nodes), q));
+  FB_CUDA(cudaMemsetAsync(s->d_out, 0, sizeof(int64_t) * 4, q));
+  FB_CUDA(cudaMemsetAsync(s->d_route, 0xff, sizeof(int32_t) * (s->nr + 1), q));
+  FB_CUDA(cudaStreamSynchronize(q));
+  return FB_OK;
+}
+
+int fb_cluster_shard_launch(fb_cluster_shard* s) {
+  if (!s) return set_error(FB_ERR_USAGE, "fb_cluster_shard_launch: null shard");
+  if (!s->connected) return set_error(FB_ERR_USAGE, "fb_cluster_shard_launch: not connected");
+  if (s->launched) return set_error(FB_ERR_USAGE, "fb_cluster_shard_launch: already running");
+  FB_CUDA(cudaSetDevice(s->a->device));
+  cudaStream_t q = s->a->stream;
+  FB_CUDA(cudaEventRecord(s->a->ev0, q));
+  FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q));
+  FB_CUDA(cudaEventRecord(s->a->ev1, q));
+  s->launched = true;
+  return FB_OK;
+}
+
+int fb_cluster_shard_wait(fb_cluster_shard* s, double* device_ms_out) {
+  if (!s) return set_error(FB_ERR_USAGE, "fb_cluster_shard_wait: null shard");
+  if (!s->launched) return set_error(FB_ERR_USAGE, "fb_cluster_shard_wait: not launched");
+  FB_CUDA(cudaSetDevice(s->a->device));
+  s->launched = false;
+  FB_CUDA(cudaStreamSynchronize(s->a->stream));
   if (device_ms_out) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, a->ev0, a->ev1);
+    FB_CUDA(cudaEventElapsedTime(&ms, s->a->ev0, s->a->ev1));
     *device_ms_out = ms;
   }
+  int64_t out[4] = {0, 0, 0, 0};
+  FB_CUDA(cudaMemcpy(out, s->d_out, sizeof(out), cudaMemcpyDeviceToHost));
+  if (out[1] == FB_ERR_TIMEOUT)
+    return set_error(FB_ERR_TIMEOUT, "cluster: a peer rank never reached the epoch exchange");
   if (out[1] != FB_OK) return set_error(static_cast<int>(out[1]), "cluster: report FIFO overflow");
-  std::vector<fb_instance_result> res(static_cast<size_t>(n_nodes));
-  if ((st = fb_arena_fetch_results(a, res.data()))) return st;
+  return FB_OK;
+}
+
+int fb_cluster_shard_fetch(fb_cluster_shard* s, fb_instance_result* local_results,
+                           fb_record* records, int32_t* route_node, int64_t* n_routed,
+                           int32_t* incomplete) {
+  if (!s) return set_error(FB_ERR_USAGE, "fb_cluster_shard_fetch: null shard");
+  if (s->launched) return set_error(FB_ERR_USAGE, "fb_cluster_shard_fetch: call wait first");
+  FB_CUDA(cudaSetDevice(s->a->device));
+  fb_arena* a = s->a;
+  cudaStream_t q = a->stream;
+  const int64_t nr = s->nr;
+  int64_t out[4] = {0, 0, 0, 0};
+  FB_CUDA(cudaMemcpyAsync(out, s->d_out, sizeof(out), cudaMemcpyDeviceToHost, q));
+  std::vector<int32_t> route(static_cast<size_t>(nr));
+  if (nr > 0)
+    FB_CUDA(cudaMemcpyAsync(route.data(), s->d_route, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, q));
+  FB_CUDA(cudaStreamSynchronize(q));
+  std::vector<fb_instance_result> res(static_cast<size_t>(s->n_local));
+  int st = fb_arena_fetch_results(a, res.data());
+  if (st) return st;
   bool live = out[0] < nr;
   for (auto& r : res) live = live || r.incomplete;
   for (auto& r : res) {
     r.incomplete = live ? 1 : 0;
     r.end_time_us = -1;
   }
-  if (node_results) std::memcpy(node_results, res.data(), sizeof(fb_instance_result) * n_nodes);
+  if (local_results) std::memcpy(local_results, res.data(), sizeof(fb_instance_result) * s->n_local);
   if (route_node && nr > 0) std::memcpy(route_node, route.data(), sizeof(int32_t) * nr);
-  if (incomplete_out) *incomplete_out = live ? 1 : 0;
+  if (n_routed) *n_routed = out[0];
+  if (incomplete) *incomplete = live ? 1 : 0;
   if (records && nr > 0) {
     const int64_t n = a->n_rec;
     std::vector<int32_t> nidx(n);
     std::vector<uint32_t> flags(n);
     std::vector<int64_t> first(n);
     std::vector<double> mt(n), mta(n);
-    FB_CUDA(cudaMemcpyAsync(nidx.data(), a->nidx.p, n * 4, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(flags.data(), a->flags.p, n * 4, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(first.data(), a->first.p, n * 8, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(mt.data(), a->maxtp.p, n * 8, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(mta.data(), a->maxtp_alt.p, n * 8, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaStreamSynchronize(s));
-    for (int64_t q = 0; q < nr; ++q) {
-      fb_record& o = records[q];
-      const int node = route[q];
-      if (node < 0) {
+    FB_CUDA(cudaMemcpyAsync(nidx.data(), a->nidx.p, n * 4, cudaMemcpyDeviceToHost, q));
+    FB_CUDA(cudaMemcpyAsync(flags.data(), a->flags.p, n * 4, cudaMemcpyDeviceToHost, q));
+    FB_CUDA(cudaMemcpyAsync(first.data(), a->first.p, n * 8, cudaMemcpyDeviceToHost, q));
+    FB_CUDA(cudaMemcpyAsync(mt.data(), a->maxtp.p, n * 8, cudaMemcpyDeviceToHost, q));
+    FB_CUDA(cudaMemcpyAsync(mta.data(), a->maxtp_alt.p, n * 8, cudaMemcpyDeviceToHost, q));
+    FB_CUDA(cudaStreamSynchronize(q));
+    for (int64_t r = 0; r < nr; ++r) {
+      fb_record& o = records[r];
+      const int node = route[r] - s->node_lo;
+      if (route[r] < 0 || node < 0 || node >= s->n_local) {
         o = fb_record{-1, 0.0, 0.0, 0, 0u};
         continue;
       }
-      const int64_t k = static_cast<int64_t>(node) * nr + q;
+      const int64_t k = static_cast<int64_t>(node) * nr + r;
       uint32_t f = (flags[k] & ~fbgpu::kTpotViolated) | FB_REC_ARRIVED;
       if ((f & FB_REC_REJECTED) && nidx[k] > 0) f &= ~static_cast<uint32_t>(FB_REC_REJECTED);
       o.first_emit_us = first[k];
@@ -631,6 +805,23 @@ int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* nod
     }
   }
   return FB_OK;
+}
+
+void fb_cluster_shard_destroy(fb_cluster_shard* s) { delete s; }
+
+// run_cluster (cluster.cpp:134-251) on one GPU: a one-rank shard.
+int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                   int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                   fb_instance_result* node_results, fb_record* records, int32_t* route_node,
+                   int32_t* incomplete_out, double* device_ms_out) {
+  fb_cluster_shard* s = nullptr;
+  int st = fb_cluster_shard_create(device, rows, node_cfgs, n_nodes, lb, horizon_us, 0, 1, &s);
+  if (st) return st;
+  if (!(st = fb_cluster_shard_reset(s)) && !(st = fb_cluster_shard_launch(s)) &&
+      !(st = fb_cluster_shard_wait(s, device_ms_out)))
+    st = fb_cluster_shard_fetch(s, node_results, records, route_node, nullptr, incomplete_out);
+  fb_cluster_shard_destroy(s);
+  return st;
 }
 
 }  // extern "C"

@@ -1,24 +1,49 @@
-// fb_cluster.cuh -- run_cluster (cluster.cpp:134-251) in one persistent CTA.
+// fb_cluster.cuh -- run_cluster (cluster.cpp:134-251) on one or more GPUs.
 //
 // The global event loop is decomposed at dispatch epochs (the distinct
-// arrival times of the trace): between epochs the nodes are
-// independent run_node machines (their only coupling is the router), so per
-// epoch t_a
-//   A. every warp advances its nodes through all events before t_a (complete,
-//      report, begin) plus a completion at exactly t_a, then pops the node's
-//      newest report due by t_a (constant latency keeps delivery FIFO);
-//   B. warp 0 applies the fresh reports to the balancer's view (decrements
-//      reset, apply_report cluster.cpp:60-73) and routes the arrivals at t_a
-//      in trace order (route, cluster.cpp:75-112) with warp arg-max/arg-min;
-//   C. every idle node that received requests runs begin_step(t_a).
-// Nodes use the warp engine's memory path; the load estimate is K5 (pab over
-// the node's views, ordered fold).
+// arrival times of the trace).  Between epochs the nodes
+// are independent run_node machines; their only coupling is the router.  Per
+// epoch t_a:
+//   A. every node advances through its events before t_a (complete, report,
+//      begin) plus a completion at exactly t_a, and publishes a 32-byte
+//      NodeReport: its newest report delivered by t_a (constant latency keeps
+//      delivery FIFO) and whether it is busy when the clock reaches t_a;
+//   -- exchange barrier --
+//   B. the router applies the fresh reports of ALL nodes to the balancer's
+//      view (apply_report, cluster.cpp:60-73) and routes the arrivals at t_a
+//      in trace order (route, cluster.cpp:75-112);
+//   C. every idle node that received requests or completed at t_a runs
+//      begin_step(t_a).
+//
+// Layout: one persistent cooperative kernel per GPU, one warp per node (the
+// warp keeps its node's live requests in registers on the RR path across
+// epochs), W warps per CTA.  The router is replicated per CTA (warp 0, view in
+// shared memory) and deterministic, so phase B needs no second exchange.  The
+// NodeReports of epoch e go to slot e&1 of an exchange buffer that exists once
+// per rank; a warp stores its node's report into every rank's buffer (peer
+// memory over NVLink when ranks are GPUs of other processes, opened by CUDA
+// IPC) and each CTA then bumps every rank's arrival counter.  A CTA passes
+// epoch e when its own rank's counter reaches (e+1) * total CTAs.  Slot
+// parity is safe: a CTA can only write slot e&1 again (epoch e+2) after every
+// CTA of every rank arrived at barrier e+1, i.e. finished reading epoch e.
+// With one rank this is a single-GPU grid barrier on one buffer.
 #pragma once
 
 namespace fbgpu {
 
-constexpr int kClusterWarps = 32;
 constexpr int kClusterMaxNodes = 512;
+constexpr int kClusterMaxRanks = 8;
+constexpr int kClusterMaxWarps = 8;  // nodes (warps) per CTA
+constexpr int kXchgHeader = 256;     // [0] arrival counter (u64), padding
+
+// The per-epoch exchange record of one node (fb_node_report in fbgpu.h).
+struct NodeReport {
+  int64_t t;    // emitted_at of the newest report delivered by t_a, -1 none
+  int64_t pab;  // its prefill admission budget
+  int32_t waiting, running;
+  int32_t fresh;  // a report was delivered since the previous epoch
+  int32_t bz;     // node busy when the global clock reaches t_a
+};
 
 struct ClusterParams {
   int32_t n_nodes, lb_policy, interval, report_cap;
@@ -26,39 +51,102 @@ struct ClusterParams {
   double w_waiting, w_running;
   const int64_t* epoch_t;   // [n_epochs]
   const int64_t* epoch_lo;  // [n_epochs + 1] request ranges
-  int32_t* routed;          // [n_nodes * n_rows] rows in routing order per node
+  int32_t* routed;          // [n_local * n_rows] rows in routing order per local node
   int32_t* route_node;      // [n_rows]
-  int64_t* rep;             // [n_nodes * report_cap * 4] in-flight reports
-  int64_t* out;             // [0] requests routed, [1] status
+  int64_t* rep;             // [n_local * report_cap * 4] in-flight reports
+  int64_t* out;             // [0] requests routed, [1] status, [2] epochs run
+  int32_t node_lo, n_local;  // this rank: global nodes [node_lo, node_lo + n_local)
+  int32_t rank, n_ranks;
+  int32_t warps_per_cta, total_ctas;  // total_ctas: over all ranks
+  int64_t timeout_ns;                 // exchange wait limit
+  unsigned char* xbuf[kClusterMaxRanks];  // exchange buffer of every rank
 };
 
-struct ClusterSmem {
-  // balancer view (NodeView, cluster.h:55-69)
+// Router view (replicated per CTA) + the CTA's routing results.
+struct RouterSmem {
   int64_t v_t[kClusterMaxNodes], v_pab[kClusterMaxNodes], v_wait[kClusterMaxNodes];
   int64_t v_run[kClusterMaxNodes], v_dec[kClusterMaxNodes], v_inc[kClusterMaxNodes];
   int32_t v_has[kClusterMaxNodes];
-  // per-node bookkeeping mirrored from DevState
-  int64_t step_end[kClusterMaxNodes];
-  int64_t n_routed[kClusterMaxNodes];
-  int64_t rep_head[kClusterMaxNodes], rep_tail[kClusterMaxNodes];
-  int32_t busy[kClusterMaxNodes];
-  int32_t got[kClusterMaxNodes];  // routed something this epoch
-  // fresh report of this epoch
-  int64_t f_t[kClusterMaxNodes], f_pab[kClusterMaxNodes], f_wait[kClusterMaxNodes],
-      f_run[kClusterMaxNodes];
-  int32_t fresh[kClusterMaxNodes];
-  int32_t bz[kClusterMaxNodes];   // busy when the global clock reaches t_a
-  int32_t cmp[kClusterMaxNodes];  // completed exactly at t_a
-  int32_t status;
+  int64_t n_routed[kClusterMaxWarps];
+  int32_t got[kClusterMaxWarps];
+  int32_t abort;
+  int32_t pad;
 };
 
-__device__ __forceinline__ Inst cluster_node(const EngineParams& P, const ClusterParams& C,
-                                             int i, unsigned char* smem_warp) {
+__device__ __forceinline__ uint64_t* xchg_counter(unsigned char* x) {
+  return reinterpret_cast<uint64_t*>(x);
+}
+__device__ __forceinline__ NodeReport* xchg_reports(unsigned char* x, int n_nodes, int64_t e) {
+  return reinterpret_cast<NodeReport*>(x + kXchgHeader) + (e & 1) * n_nodes;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p, bool sys) {
+  uint64_t v;
+  if (sys) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  } else {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  }
+  return v;
+}
+
+__device__ __forceinline__ void red_release_add(uint64_t* p, bool sys) {
+  if (sys) {
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+  } else {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+  }
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Exchange barrier of epoch e (all CTAs of all ranks).  False on timeout.
+__device__ bool cluster_barrier(const ClusterParams& C, RouterSmem& rs, int64_t e) {
+  const bool sys = C.n_ranks > 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (sys) {
+      __threadfence_system();
+    } else {
+      __threadfence();
+    }
+    for (int p = 0; p < C.n_ranks; ++p) red_release_add(xchg_counter(C.xbuf[p]), sys);
+    const uint64_t target = static_cast<uint64_t>(e + 1) * static_cast<uint64_t>(C.total_ctas);
+    const uint64_t* ctr = xchg_counter(C.xbuf[C.rank]);
+    if (ld_acquire_u64(ctr, sys) < target) {
+      const uint64_t t0 = global_ns();
+      while (ld_acquire_u64(ctr, sys) < target) {
+        if (global_ns() - t0 > static_cast<uint64_t>(C.timeout_ns)) {
+          rs.abort = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return rs.abort == 0;
+}
+
+// One node, owned by one warp for the whole run.
+struct ClusterNode {
   Inst w;
-  w.id = i;
-  w.routed = C.routed + static_cast<int64_t>(i) * C.n_rows;
-  w.I = P.inst + i;
-  w.S = P.state[i];
+  TaskReg tk;
+  bool rr;
+  int64_t rep_head, rep_tail;
+};
+
+__device__ __forceinline__ void cluster_node_init(const EngineParams& P, const ClusterParams& C,
+                                                  int il, unsigned char* smem_warp,
+                                                  ClusterNode& nd) {
+  Inst& w = nd.w;
+  w.id = il;
+  w.routed = C.routed + static_cast<int64_t>(il) * C.n_rows;
+  w.I = P.inst + il;
+  w.S = P.state[il];
   w.toff = w.I->trace_off;
   w.roff = w.I->rec_off;
   w.nreq = w.I->n_req;
@@ -67,21 +155,33 @@ __device__ __forceinline__ Inst cluster_node(const EngineParams& P, const Cluste
   w.max_active = w.I->max_active;
   w.vl = P.vlist + w.roff;
   w.smem = smem_warp;
-  return w;
+  nd.tk = TaskReg{};
+  nd.rr = false;
+  nd.rep_head = nd.rep_tail = 0;
 }
 
 // Node::current_pab (engine.cpp:123-125): pab over the node's views at now.
-__device__ int64_t node_pab(const EngineParams& P, const Inst& w, int64_t now) {
+__device__ int64_t node_pab(const EngineParams& P, const ClusterNode& nd, int64_t now) {
+  const Inst& w = nd.w;
   const DevInst* I = w.I;
   const double Wm = us_to_ms(I->g_ttft), Tm = us_to_ms(I->g_tpot);
   const int64_t A = visible_count(w);
   const Scratch s = scratch_for(P, w, A);
   int64_t lmin = kInf, lpf = 0;
-  for (int64_t p = lane_id(); p < A; p += kWarp) {
-    const View v = load_view(P, w, p, now);
-    s.tcost[p] = pab_term(Wm, Tm, I->sb, I->sc, v.slack, v.ctx);
-    lmin = v.slack < lmin ? v.slack : lmin;
-    if (!v.decode) lpf += v.nw;
+  if (nd.rr) {  // lane p holds view p
+    if (lane_id() < A) {
+      const RView v = view_reg(nd.tk, now);
+      s.tcost[lane_id()] = pab_term(Wm, Tm, I->sb, I->sc, v.slack, v.ctx);
+      lmin = v.slack;
+      if (!v.decode) lpf = v.nw;
+    }
+  } else {
+    for (int64_t p = lane_id(); p < A; p += kWarp) {
+      const View v = load_view(P, w, p, now);
+      s.tcost[p] = pab_term(Wm, Tm, I->sb, I->sc, v.slack, v.ctx);
+      lmin = v.slack < lmin ? v.slack : lmin;
+      if (!v.decode) lpf += v.nw;
+    }
   }
   __syncwarp();
   const int64_t min_slack = warp_min_i64(lmin);
@@ -91,230 +191,285 @@ __device__ int64_t node_pab(const EngineParams& P, const Inst& w, int64_t now) {
 }
 
 // make_report (cluster.cpp:50-58) into the node's in-flight FIFO.
-__device__ void node_report(const EngineParams& P, const ClusterParams& C, ClusterSmem& cs,
-                            const Inst& w, int64_t now) {
-  const int i = static_cast<int>(w.id);
-  const int64_t pab = C.lb_policy == FB_LB_PAB ? node_pab(P, w, now) : 0;
-  if (lane_id() == 0) {
-    const int64_t tail = cs.rep_tail[i];
-    if (tail - cs.rep_head[i] >= C.report_cap) {
-      cs.status = FB_ERR_CAPACITY;
-    } else {
-      int64_t* r = C.rep + (static_cast<int64_t>(i) * C.report_cap + tail % C.report_cap) * 4;
+__device__ void node_report(const EngineParams& P, const ClusterParams& C, ClusterNode& nd,
+                            int64_t now, int32_t* status) {
+  const Inst& w = nd.w;
+  const int64_t pab = C.lb_policy == FB_LB_PAB ? node_pab(P, nd, now) : 0;
+  if (nd.rep_tail - nd.rep_head >= C.report_cap) {
+    *status = FB_ERR_CAPACITY;
+  } else {
+    if (lane_id() == 0) {
+      int64_t* r = C.rep + (w.id * C.report_cap + nd.rep_tail % C.report_cap) * 4;
       r[0] = now;
       r[1] = pab;
       r[2] = w.S.n_live - w.S.n_active;  // waiting_count (engine.h:133-135)
       r[3] = w.S.n_active;                // running_count
-      cs.rep_tail[i] = tail + 1;
     }
+    nd.rep_tail++;
   }
   __syncwarp();
 }
 
-// Runs node events before t_a (and the completion at t_a when `at_too`).
-__device__ void advance_node(const EngineParams& P, const ClusterParams& C, ClusterSmem& cs,
-                             Inst& w, int64_t t_a, bool at_too) {
-  while (w.S.busy && (w.S.step_end < t_a || (at_too && w.S.step_end == t_a))) {
-    const int64_t t = w.S.step_end;
-    w.S.t_last = t;
+// Node::complete_step on the current path (+ the step report).
+__device__ __forceinline__ void node_complete(const EngineParams& P, const ClusterParams& C,
+                                              ClusterNode& nd, bool report, int32_t* status) {
+  Inst& w = nd.w;
+  const int64_t t = w.S.step_end;
+  w.S.t_last = t;
+  if (nd.rr) {
+    complete_rr(P, w, nd.tk);
+  } else {
     complete_step(P, w);
-    if (C.interval > 0 && w.S.step_counter % static_cast<uint64_t>(C.interval) == 0)
-      node_report(P, C, cs, w, t);
-    if (t == t_a) break;  // begin at t_a waits for the routing
-    if (t < w.horizon) begin_step(P, w, t);
+  }
+  if (report && C.interval > 0 && w.S.step_counter % static_cast<uint64_t>(C.interval) == 0)
+    node_report(P, C, nd, t, status);
+}
+
+// Node::begin_step with the RR / memory path switch of run_instance.
+__device__ __forceinline__ void node_begin(const EngineParams& P, ClusterNode& nd, int64_t t) {
+  Inst& w = nd.w;
+  const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
+  if (nd.rr && upcoming > kWarp) {
+    rr_spill(P, w, nd.tk);
+    nd.rr = false;
+  } else if (!nd.rr && upcoming <= kWarp) {
+    rr_load(P, w, nd.tk);
+    nd.rr = true;
+    w.S.paths |= kPathRegister;
+  }
+  if (nd.rr) {
+    const Scratch s = carve_scratch(w.smem, kSmemSlots);
+    if (begin_rr(P, w, nd.tk, t, s) < 0) {  // keys outside the packed range
+      rr_spill(P, w, nd.tk);
+      nd.rr = false;
+      begin_step(P, w, t);
+      w.S.paths |= kPathMemory;
+    }
+  } else {
+    begin_step(P, w, t);
+    w.S.paths |= kPathMemory;
   }
 }
 
-__global__ void __launch_bounds__(kWarp * kClusterWarps, 1)
-cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ ClusterParams C) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ClusterSmem& cs = *reinterpret_cast<ClusterSmem*>(smem_raw);
-  unsigned char* scratch_base = smem_raw + ((sizeof(ClusterSmem) + 15) / 16) * 16;
-  const int warp = threadIdx.x / kWarp;
-  unsigned char* my = scratch_base + static_cast<size_t>(warp) * kSmemSlots * kScratchBytesPerSlot;
+// Phase A for one node: events before t_a, the completion at t_a, and the
+// NodeReport of epoch e stored into every rank's exchange buffer.
+__device__ void node_phase_a(const EngineParams& P, const ClusterParams& C, ClusterNode& nd,
+                             int64_t e, int64_t t_a, int32_t* cmp_out, int32_t* status) {
+  Inst& w = nd.w;
+  while (w.S.busy && w.S.step_end < t_a) {
+    const int64_t t = w.S.step_end;
+    node_complete(P, C, nd, true, status);
+    if (t < w.horizon) node_begin(P, nd, t);
+  }
+  const int32_t bz = w.S.busy != 0;  // busy when the global clock reaches t_a
+  const int32_t cmp = bz && w.S.step_end == t_a;
+  if (cmp) node_complete(P, C, nd, true, status);  // begin at t_a waits for the routing
+  *cmp_out = cmp;
+  NodeReport nr;
+  nr.t = -1;
+  nr.pab = 0;
+  nr.waiting = nr.running = 0;
+  nr.fresh = 0;
+  nr.bz = bz;
+  int64_t h = nd.rep_head;
+  while (h < nd.rep_tail) {  // newest report delivered by t_a
+    const int64_t* r = C.rep + (w.id * C.report_cap + h % C.report_cap) * 4;
+    if (r[0] + C.latency > t_a) break;
+    nr.t = r[0];
+    nr.pab = r[1];
+    nr.waiting = static_cast<int32_t>(r[2]);
+    nr.running = static_cast<int32_t>(r[3]);
+    nr.fresh = 1;
+    ++h;
+  }
+  nd.rep_head = h;
+  // lane p stores the 32-byte report into rank p's buffer
+  if (lane_id() < C.n_ranks) {
+    NodeReport* dst = xchg_reports(C.xbuf[lane_id()], C.n_nodes, e) + C.node_lo + w.id;
+    *dst = nr;
+    if (C.n_ranks > 1) __threadfence_system();
+  }
+  __syncwarp();
+}
+
+// Horizon rule (cluster.cpp:191-192): at t_a >= horizon the global loop only
+// runs while some node is busy.  Every CTA of every rank evaluates the same
+// reports, so all stop at the same epoch.
+__device__ __forceinline__ bool cluster_stopped(const ClusterParams& C, const NodeReport* all,
+                                                int64_t t_a) {
+  if (t_a < C.horizon) return false;
+  int mine = 0;
+  for (int i = threadIdx.x; i < C.n_nodes; i += blockDim.x) mine |= __ldcg(&all[i].bz);
+  return __syncthreads_or(mine) == 0;
+}
+
+// Phase B (warp 0 of each CTA): reports -> view, route the epoch's arrivals.
+__device__ void cluster_route(const EngineParams& P, const ClusterParams& C, RouterSmem& rs,
+                              const NodeReport* all, int64_t e, int node_base) {
   const int n = C.n_nodes;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    cs.v_has[i] = 0;
-    cs.v_t[i] = -1;
-    cs.v_pab[i] = cs.v_wait[i] = cs.v_run[i] = cs.v_dec[i] = cs.v_inc[i] = 0;
-    cs.busy[i] = 0;
-    cs.step_end[i] = 0;
-    cs.n_routed[i] = 0;
-    cs.rep_head[i] = cs.rep_tail[i] = 0;
-    cs.fresh[i] = 0;
-  }
-  if (threadIdx.x == 0) cs.status = FB_OK;
-  __syncthreads();
-  // initial reports at t = 0 (cluster.cpp:198)
-  for (int i = warp; i < n; i += kClusterWarps) {
-    const Inst w = cluster_node(P, C, i, my);
-    node_report(P, C, cs, w, 0);
-  }
-  __syncthreads();
-  int64_t e = 0;
-  for (; e < C.n_epochs; ++e) {
-    const int64_t t_a = C.epoch_t[e];
-    // A: advance, deliver
-    for (int i = warp; i < n; i += kClusterWarps) {
-      if (cs.busy[i] && cs.step_end[i] <= t_a) {
-        Inst w = cluster_node(P, C, i, my);
-        advance_node(P, C, cs, w, t_a, false);
-        const bool busy_at = w.S.busy != 0;  // busy when the clock reaches t_a
-        const bool ends_at = busy_at && w.S.step_end == t_a;
-        advance_node(P, C, cs, w, t_a, true);
-        if (lane_id() == 0) {
-          P.state[i] = w.S;
-          cs.busy[i] = w.S.busy;
-          cs.step_end[i] = w.S.step_end;
-          cs.bz[i] = busy_at;
-          cs.cmp[i] = ends_at;  // owes a begin_step(t_a) after the routing
-        }
-      } else if (lane_id() == 0) {
-        cs.bz[i] = cs.busy[i];
-        cs.cmp[i] = 0;
+  for (int i = lane_id(); i < n; i += kWarp) {
+    if (__ldcg(&all[i].fresh)) {
+      const int64_t t = __ldcg(&all[i].t);
+      if (!(rs.v_has[i] && t < rs.v_t[i])) {
+        rs.v_has[i] = 1;
+        rs.v_t[i] = t;
+        rs.v_pab[i] = __ldcg(&all[i].pab);
+        rs.v_wait[i] = __ldcg(&all[i].waiting);
+        rs.v_run[i] = __ldcg(&all[i].running);
+        rs.v_dec[i] = 0;
+        rs.v_inc[i] = 0;
       }
-      if (lane_id() == 0) {
-        int64_t h = cs.rep_head[i];
-        bool got = false;
-        while (h < cs.rep_tail[i]) {
-          const int64_t* r = C.rep + (static_cast<int64_t>(i) * C.report_cap + h % C.report_cap) * 4;
-          if (r[0] + C.latency > t_a) break;
-          cs.f_t[i] = r[0];
-          cs.f_pab[i] = r[1];
-          cs.f_wait[i] = r[2];
-          cs.f_run[i] = r[3];
-          got = true;
-          ++h;
-        }
-        cs.rep_head[i] = h;
-        cs.fresh[i] = got;
-        cs.got[i] = 0;
-      }
-      __syncwarp();
     }
-    __syncthreads();
-    // horizon: at t_a >= horizon the global loop only runs while a node is
-    // busy (cluster.cpp:191-192); nodes never begin at or after the horizon
-    bool any_busy = false;
-    for (int i = 0; i < n; ++i) any_busy |= cs.bz[i] != 0;
-    if (t_a >= C.horizon && !any_busy) break;
-    // B: reports -> view, route in trace order (warp 0)
-    if (warp == 0) {
+  }
+  __syncwarp();
+  for (int64_t q = C.epoch_lo[e]; q < C.epoch_lo[e + 1]; ++q) {
+    const int64_t prompt = P.prompt[q];
+    int chosen;
+    if (C.lb_policy == FB_LB_PAB) {
+      // best effective budget among nodes that fit the prompt, else overall;
+      // ties to the lowest node id
+      int64_t bf = INT64_MIN, ba = INT64_MIN;
+      int idf = INT32_MAX, ida = INT32_MAX;
       for (int i = lane_id(); i < n; i += kWarp) {
-        if (cs.fresh[i] && !(cs.v_has[i] && cs.f_t[i] < cs.v_t[i])) {
-          cs.v_has[i] = 1;
-          cs.v_t[i] = cs.f_t[i];
-          cs.v_pab[i] = cs.f_pab[i];
-          cs.v_wait[i] = cs.f_wait[i];
-          cs.v_run[i] = cs.f_run[i];
-          cs.v_dec[i] = 0;
-          cs.v_inc[i] = 0;
+        const int64_t eff = rs.v_pab[i] - rs.v_dec[i];
+        if (eff > ba) {
+          ba = eff;
+          ida = i;
+        }
+        if (eff >= prompt && eff > bf) {
+          bf = eff;
+          idf = i;
         }
       }
-      __syncwarp();
-      for (int64_t q = C.epoch_lo[e]; q < C.epoch_lo[e + 1]; ++q) {
-        const int64_t prompt = P.prompt[q];
-        int chosen;
-        if (C.lb_policy == FB_LB_PAB) {
-          // best effective budget among nodes that fit the prompt, else overall;
-          // ties to the lowest node id
-          int64_t bf = INT64_MIN, ba = INT64_MIN;
-          int idf = INT32_MAX, ida = INT32_MAX;
-          for (int i = lane_id(); i < n; i += kWarp) {
-            const int64_t eff = cs.v_pab[i] - cs.v_dec[i];
-            if (eff > ba) {
-              ba = eff;
-              ida = i;
-            }
-            if (eff >= prompt && eff > bf) {
-              bf = eff;
-              idf = i;
-            }
-          }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const int64_t b2 = __shfl_xor_sync(kFull, bf, o);
-            const int i2 = __shfl_xor_sync(kFull, idf, o);
-            if (b2 > bf || (b2 == bf && i2 < idf)) {
-              bf = b2;
-              idf = i2;
-            }
-            const int64_t a2 = __shfl_xor_sync(kFull, ba, o);
-            const int j2 = __shfl_xor_sync(kFull, ida, o);
-            if (a2 > ba || (a2 == ba && j2 < ida)) {
-              ba = a2;
-              ida = j2;
-            }
-          }
-          chosen = idf != INT32_MAX ? idf : ida;
-          if (lane_id() == 0) cs.v_dec[chosen] += prompt;
-        } else {
-          double best = 0.0;
-          int idb = INT32_MAX;
-          for (int i = lane_id(); i < n; i += kWarp) {
-            const double score =
-                dadd(dmul(C.w_waiting, static_cast<double>(cs.v_wait[i] + cs.v_inc[i])),
-                     dmul(C.w_running, static_cast<double>(cs.v_run[i])));
-            if (idb == INT32_MAX || score < best) {
-              best = score;
-              idb = i;
-            }
-          }
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t b2 = __shfl_xor_sync(kFull, bf, o);
+        const int i2 = __shfl_xor_sync(kFull, idf, o);
+        if (b2 > bf || (b2 == bf && i2 < idf)) {
+          bf = b2;
+          idf = i2;
+        }
+        const int64_t a2 = __shfl_xor_sync(kFull, ba, o);
+        const int j2 = __shfl_xor_sync(kFull, ida, o);
+        if (a2 > ba || (a2 == ba && j2 < ida)) {
+          ba = a2;
+          ida = j2;
+        }
+      }
+      chosen = idf != INT32_MAX ? idf : ida;
+      if (lane_id() == 0) rs.v_dec[chosen] += prompt;
+    } else {
+      double best = 0.0;
+      int idb = INT32_MAX;
+      for (int i = lane_id(); i < n; i += kWarp) {
+        const double score =
+            dadd(dmul(C.w_waiting, static_cast<double>(rs.v_wait[i] + rs.v_inc[i])),
+                 dmul(C.w_running, static_cast<double>(rs.v_run[i])));
+        if (idb == INT32_MAX || score < best) {
+          best = score;
+          idb = i;
+        }
+      }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double b2 = __shfl_xor_sync(kFull, best, o);
-            const int i2 = __shfl_xor_sync(kFull, idb, o);
-            if (i2 != INT32_MAX && (idb == INT32_MAX || b2 < best || (b2 == best && i2 < idb))) {
-              best = b2;
-              idb = i2;
-            }
-          }
-          chosen = idb;
-          if (lane_id() == 0) cs.v_inc[chosen] += 1;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double b2 = __shfl_xor_sync(kFull, best, o);
+        const int i2 = __shfl_xor_sync(kFull, idb, o);
+        if (i2 != INT32_MAX && (idb == INT32_MAX || b2 < best || (b2 == best && i2 < idb))) {
+          best = b2;
+          idb = i2;
         }
-        if (lane_id() == 0) {
-          const int64_t k = cs.n_routed[chosen];
-          C.routed[static_cast<int64_t>(chosen) * C.n_rows + k] = static_cast<int32_t>(q);
-          cs.n_routed[chosen] = k + 1;
-          cs.got[chosen] = 1;
-          C.route_node[q] = chosen;
-        }
-        __syncwarp();
       }
+      chosen = idb;
+      if (lane_id() == 0) rs.v_inc[chosen] += 1;
     }
-    __syncthreads();
-    // C: enqueue (visible at t_a) and begin_step(t_a) on idle nodes
-    for (int i = warp; i < n; i += kClusterWarps) {
-      if (cs.got[i] || cs.cmp[i]) {
-        Inst w = cluster_node(P, C, i, my);
-        w.S.arr = cs.n_routed[i];  // Node::enqueue
-        w.S.t_last = t_a;
-        if (!w.S.busy && t_a < w.horizon) begin_step(P, w, t_a);
-        if (lane_id() == 0) {
-          P.state[i] = w.S;
-          cs.busy[i] = w.S.busy;
-          cs.step_end[i] = w.S.step_end;
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-  }
-  // all arrivals routed (or the loop stopped): run every node to quiescence
-  for (int i = warp; i < n; i += kClusterWarps) {
-    Inst w = cluster_node(P, C, i, my);
-    advance_node(P, C, cs, w, kInf, false);
     if (lane_id() == 0) {
-      w.S.done = 1;
-      w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0) ? 1 : 0;
-      P.state[i] = w.S;
+      if (blockIdx.x == 0) C.route_node[q] = chosen;
+      const int k = chosen - node_base;  // Node::enqueue, on the owning CTA
+      if (k >= 0 && k < C.warps_per_cta && chosen - C.node_lo < C.n_local) {
+        const int64_t j = rs.n_routed[k];
+        C.routed[static_cast<int64_t>(chosen - C.node_lo) * C.n_rows + j] = static_cast<int32_t>(q);
+        rs.n_routed[k] = j + 1;
+        rs.got[k] = 1;
+      }
     }
     __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(kWarp * kClusterMaxWarps, 1)
+cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ ClusterParams C) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RouterSmem& rs = *reinterpret_cast<RouterSmem*>(smem_raw);
+  const int warp = threadIdx.x / kWarp;
+  unsigned char* my = smem_raw + ((sizeof(RouterSmem) + 15) / 16) * 16 +
+                      static_cast<size_t>(warp) * kSmemSlots * kScratchBytesPerSlot;
+  const int il = blockIdx.x * C.warps_per_cta + warp;  // local node of this warp
+  const bool owner = il < C.n_local;
+  const int node_base = C.node_lo + blockIdx.x * C.warps_per_cta;  // global id of warp 0's node
+  for (int i = threadIdx.x; i < C.n_nodes; i += blockDim.x) {
+    rs.v_has[i] = 0;
+    rs.v_t[i] = -1;
+    rs.v_pab[i] = rs.v_wait[i] = rs.v_run[i] = rs.v_dec[i] = rs.v_inc[i] = 0;
+  }
+  if (threadIdx.x < kClusterMaxWarps) {
+    rs.n_routed[threadIdx.x] = 0;
+    rs.got[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) rs.abort = 0;
+  int32_t status = FB_OK;
+  ClusterNode nd;
+  if (owner) {
+    cluster_node_init(P, C, il, my, nd);
+    node_report(P, C, nd, 0, &status);  // initial report (cluster.cpp:198)
+  }
   __syncthreads();
+  int64_t e = 0;
+  bool ok = true;
+  for (; e < C.n_epochs; ++e) {
+    const int64_t t_a = C.epoch_t[e];
+    int32_t cmp = 0;
+    if (owner) node_phase_a(P, C, nd, e, t_a, &cmp, &status);
+    if (!(ok = cluster_barrier(C, rs, e))) break;
+    const NodeReport* all = xchg_reports(C.xbuf[C.rank], C.n_nodes, e);
+    if (cluster_stopped(C, all, t_a)) break;
+    if (warp == 0) cluster_route(P, C, rs, all, e, node_base);
+    __syncthreads();
+    if (owner && (rs.got[warp] || cmp)) {  // Node::enqueue (visible at t_a), begin_step(t_a)
+      Inst& w = nd.w;
+      w.S.arr = rs.n_routed[warp];
+      w.S.t_last = t_a;
+      if (!w.S.busy && t_a < w.horizon) node_begin(P, nd, t_a);
+    }
+    __syncwarp();
+    if (owner && lane_id() == 0) rs.got[warp] = 0;
+  }
+  if (owner) {
+    Inst& w = nd.w;
+    if (ok) {  // all arrivals routed (or the loop stopped): run to quiescence
+      while (w.S.busy) {
+        const int64_t t = w.S.step_end;
+        node_complete(P, C, nd, false, &status);
+        if (t < w.horizon) node_begin(P, nd, t);
+      }
+    }
+    if (nd.rr) rr_spill(P, w, nd.tk);
+    if (lane_id() == 0) {
+      w.S.done = 1;
+      w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0) ? 1 : 0;
+      P.state[il] = w.S;
+      if (status != FB_OK)
+        atomicMax(reinterpret_cast<unsigned long long*>(C.out + 1),
+                  static_cast<unsigned long long>(status));
+    }
+  }
   if (threadIdx.x == 0) {
-    C.out[0] = e < C.n_epochs ? C.epoch_lo[e] : C.n_rows;
-    C.out[1] = cs.status;
+    if (!ok)
+      atomicMax(reinterpret_cast<unsigned long long*>(C.out + 1),
+                static_cast<unsigned long long>(FB_ERR_TIMEOUT));
+    if (blockIdx.x == 0) {
+      C.out[0] = e < C.n_epochs ? C.epoch_lo[e] : C.n_rows;
+      C.out[2] = e;
+    }
   }
 }
 

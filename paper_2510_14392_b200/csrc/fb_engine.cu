@@ -644,16 +644,41 @@ cudaError_t launch_reset(const EngineParams& p, int64_t n_rec, cudaStream_t st) 
 
 size_t cluster_param_bytes() { return sizeof(ClusterParams); }
 int cluster_max_nodes() { return kClusterMaxNodes; }
+int cluster_max_ranks() { return kClusterMaxRanks; }
+size_t cluster_xchg_bytes(int n_nodes) {
+  return kXchgHeader + 2 * sizeof(NodeReport) * static_cast<size_t>(n_nodes);
+}
 
-cudaError_t launch_cluster(const EngineParams& p, const void* cluster_params, cudaStream_t st) {
+int cluster_warps_per_cta(int n_nodes, int n_ranks) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms < 1) sms = 148;
+  const int max_local = (n_nodes + n_ranks - 1) / n_ranks;
+  int w = (max_local + sms - 1) / sms;  // spread nodes over the SMs
+  return w < 1 ? 1 : w;
+}
+
+size_t cluster_smem_bytes(int warps_per_cta) {
+  return ((sizeof(RouterSmem) + 15) / 16) * 16 +
+         static_cast<size_t>(warps_per_cta) * kSmemSlots * kScratchBytesPerSlot;
+}
+
+cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, int blocks,
+                           cudaStream_t st) {
+  static_assert(sizeof(ClusterParamsHost) == sizeof(ClusterParams), "cluster params layout");
   ClusterParams c;
-  std::memcpy(&c, cluster_params, sizeof(c));
-  const size_t smem = ((sizeof(ClusterSmem) + 15) / 16) * 16 +
-                      static_cast<size_t>(kClusterWarps) * kSmemSlots * kScratchBytesPerSlot;
-  cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem));
-  cluster_kernel<<<1, kWarp * kClusterWarps, smem, st>>>(p, c);
-  return cudaGetLastError();
+  std::memcpy(&c, &ch, sizeof(c));
+  if (c.warps_per_cta < 1 || c.warps_per_cta > kClusterMaxWarps) return cudaErrorInvalidValue;
+  const size_t smem = cluster_smem_bytes(c.warps_per_cta);
+  cudaError_t e = cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  EngineParams pp = p;
+  void* args[] = {&pp, &c};
+  // cooperative: every CTA must be co-resident for the epoch barrier
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cluster_kernel), dim3(blocks),
+                                     dim3(kWarp * c.warps_per_cta), args, smem, st);
 }
 
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaStream_t st) {

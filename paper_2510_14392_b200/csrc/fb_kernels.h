@@ -72,7 +72,8 @@ void unpack_state(const void* state, fb_instance_result* out);
 
 cudaError_t launch_reset(const EngineParams& p, int64_t n_rec_rows, cudaStream_t st);
 
-// Cluster (fb_cluster.cuh): ClusterParams is opaque to the host code here.
+// Cluster (fb_cluster.cuh): mirrors ClusterParams field for field.
+constexpr int kClusterHostMaxRanks = 8;
 struct ClusterParamsHost {
   int32_t n_nodes, lb_policy, interval, report_cap;
   int64_t latency, horizon, n_rows, n_epochs;
@@ -83,10 +84,21 @@ struct ClusterParamsHost {
   int32_t* route_node;
   int64_t* rep;
   int64_t* out;
+  int32_t node_lo, n_local;
+  int32_t rank, n_ranks;
+  int32_t warps_per_cta, total_ctas;
+  int64_t timeout_ns;
+  unsigned char* xbuf[kClusterHostMaxRanks];
 };
 size_t cluster_param_bytes();
 int cluster_max_nodes();
-cudaError_t launch_cluster(const EngineParams& p, const void* cluster_params, cudaStream_t st);
+int cluster_max_ranks();
+size_t cluster_xchg_bytes(int n_nodes);
+// Warps (nodes) per CTA, shared by all ranks, and this rank's CTA count.
+int cluster_warps_per_cta(int n_nodes, int n_ranks);
+size_t cluster_smem_bytes(int warps_per_cta);
+cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& c, int blocks,
+                           cudaStream_t st);
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g,
                           cudaStream_t st);
 

@@ -52,6 +52,10 @@ class CapacityError(FbError):
     pass
 
 
+class TimeoutError_(FbError):
+    """A peer rank never reached the cluster epoch exchange."""
+
+
 _ERRORS = {
     _abi.FB_ERR_VALIDATION: ValidationError,
     _abi.FB_ERR_USAGE: UsageError,
@@ -59,6 +63,7 @@ _ERRORS = {
     _abi.FB_ERR_PARSE: ParseError,
     _abi.FB_ERR_CUDA: CudaError,
     _abi.FB_ERR_CAPACITY: CapacityError,
+    _abi.FB_ERR_TIMEOUT: TimeoutError_,
 }
 
 _lib = None
@@ -103,6 +108,20 @@ def lib() -> C.CDLL:
         "fb_run_cluster": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,
                                      C.POINTER(_abi.LbConfig), i64, vp, vp, vp,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+        "fb_cluster_partition": (C.c_int, [i32, i32, i32, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32)]),
+        "fb_cluster_shard_create": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,
+                                              C.POINTER(_abi.LbConfig), i64, i32, i32,
+                                              C.POINTER(vp)]),
+        "fb_cluster_shard_exchange_handle": (C.c_int, [vp, vp]),
+        "fb_cluster_shard_exchange_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+        "fb_cluster_shard_connect": (C.c_int, [vp, vp]),
+        "fb_cluster_shard_connect_ptrs": (C.c_int, [vp, vp]),
+        "fb_cluster_shard_reset": (C.c_int, [vp]),
+        "fb_cluster_shard_launch": (C.c_int, [vp]),
+        "fb_cluster_shard_wait": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "fb_cluster_shard_fetch": (C.c_int, [vp, vp, vp, vp, pi64, C.POINTER(C.c_int32)]),
+        "fb_cluster_shard_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -155,6 +155,78 @@ class OracleLib(_CpuLib):
             raise RuntimeError(f"orc_run_cluster status {st}")
         return out
 
+    def run_cluster_dist(self, rows: Rows, cfgs, lb, horizon_us: int, dist):
+        """The multi-rank cluster protocol on the CPU: this rank's nodes through
+        orc_cluster_shard_*, the per-epoch fb_node_report allgather over
+        `dist` (gloo), and the product's merge_shards."""
+        import torch
+        from paper_2510_14392_b200.cluster import ShardOutput, merge_shards, node_configs_c
+        L = self.lib
+        vp = C.c_void_p
+        sig = {
+            "orc_cluster_shard_create": [C.POINTER(_abi.Trace), vp, C.c_int32,
+                                         C.POINTER(_abi.LbConfig), C.c_int64, C.c_int32,
+                                         C.c_int32, C.POINTER(vp)],
+            "orc_cluster_shard_epochs": [vp],
+            "orc_cluster_shard_advance": [vp, C.c_int64, vp],
+            "orc_cluster_shard_route_begin": [vp, C.c_int64, vp, C.POINTER(C.c_int32)],
+            "orc_cluster_shard_fetch": [vp, vp, vp, vp, C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int32)],
+            "orc_cluster_shard_destroy": [vp],
+            "orc_cluster_partition": [C.c_int32] * 3 + [C.POINTER(C.c_int32)] * 2,
+        }
+        for name, args in sig.items():
+            getattr(L, name).argtypes = args
+            getattr(L, name).restype = C.c_int
+        L.orc_cluster_shard_epochs.restype = C.c_int64
+        L.orc_cluster_shard_destroy.restype = None
+        rank, world = dist.get_rank(), dist.get_world_size()
+        n = len(cfgs)
+        lo, nl = C.c_int32(0), C.c_int32(0)
+        assert L.orc_cluster_partition(n, world, rank, C.byref(lo), C.byref(nl)) == 0
+        cap = max((n * (r + 1) // world) - (n * r // world) for r in range(world))
+        tr = rows.to_c()
+        nc = node_configs_c(cfgs)
+        lbc = lb.to_c()
+        h = vp()
+        st = L.orc_cluster_shard_create(C.byref(tr), C.cast(nc, vp), n, C.byref(lbc),
+                                        int(horizon_us), rank, world, C.byref(h))
+        if st:
+            raise RuntimeError(f"orc_cluster_shard_create status {st}")
+        try:
+            local = np.zeros(cap, _abi.NODE_REPORT_DTYPE)
+            stopped = C.c_int32(0)
+            for e in range(L.orc_cluster_shard_epochs(h)):
+                st = L.orc_cluster_shard_advance(h, e, _abi.vptr(local))
+                if st:
+                    raise RuntimeError(f"orc_cluster_shard_advance status {st}")
+                t = torch.from_numpy(local.view(np.int64).copy())
+                parts = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(parts, t)
+                all_rep = np.concatenate([
+                    p.numpy().view(_abi.NODE_REPORT_DTYPE)[:(n * (r + 1) // world) - (n * r // world)]
+                    for r, p in enumerate(parts)])
+                st = L.orc_cluster_shard_route_begin(h, e, _abi.vptr(all_rep), C.byref(stopped))
+                if st:
+                    raise RuntimeError(f"orc_cluster_shard_route_begin status {st}")
+                if stopped.value:
+                    break
+            res = np.zeros(max(1, nl.value), _abi.RESULT_DTYPE)
+            rec = np.zeros(max(1, len(rows)), _abi.RECORD_DTYPE)
+            route = np.zeros(max(1, len(rows)), np.int32)
+            nrt, inc = C.c_int64(0), C.c_int32(0)
+            st = L.orc_cluster_shard_fetch(h, _abi.vptr(res), _abi.vptr(rec), _abi.vptr(route),
+                                           C.byref(nrt), C.byref(inc))
+            if st:
+                raise RuntimeError(f"orc_cluster_shard_fetch status {st}")
+        finally:
+            L.orc_cluster_shard_destroy(h)
+        out = ShardOutput(lo.value, res[:nl.value], rec[:len(rows)], route[:len(rows)],
+                          nrt.value, inc.value)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, out)
+        return merge_shards(gathered, n)
+
     def run(self, batch: Batch, log: _abi.LogOpts | None = None, nthreads: int = 1) -> RunOutput:
         n = batch.n_instances
         rows = batch.rows

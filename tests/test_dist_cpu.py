@@ -79,3 +79,84 @@ def test_shard_batch_keeps_rows(oracle):
     a = oracle.run(sub).results
     b = oracle.run(batch).results[idx]
     assert a.tobytes() == b.tobytes()
+
+
+# ---------------------------------------------------------------- cluster (C5)
+
+def _cluster_worker(rank, world, port, q, names):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    import torch.distributed as dist
+    from backends import OracleLib
+    from catalog import cluster_cases
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = OracleLib()
+    for name, rows, cfgs, lb, hz in cluster_cases(orc.generate_bursty):
+        if name not in names or len(cfgs) < world:
+            continue
+        out = orc.run_cluster_dist(rows, cfgs, lb, hz, dist)
+        if rank == 0:
+            q.put((name, out.node_results.tobytes(), out.records.tobytes(),
+                   out.route_node.tobytes(), out.incomplete))
+    if rank == 0:
+        q.put(None)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_cluster_shards_equal_run_cluster(oracle, world):
+    """The multi-rank cluster protocol (node partition, per-epoch report
+    allgather, replicated router, merge_shards) reproduces run_cluster."""
+    from catalog import cluster_cases
+    names = ("pab0_8", "count0_8", "pab5000_8", "count37_3", "pab_hz10s_8", "pab20_2")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cluster_worker, args=(r, world, port, q, names))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {}
+    while True:
+        item = q.get(timeout=300)
+        if item is None:
+            break
+        got[item[0]] = item[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cases = {c[0]: c for c in cluster_cases(oracle.generate_bursty)}
+    checked = 0
+    for name in names:
+        _, rows, cfgs, lb, hz = cases[name]
+        if len(cfgs) < world:
+            continue
+        ref = oracle.run_cluster(rows, cfgs, lb, hz)
+        res, rec, route, inc = got[name]
+        assert res == ref.node_results.tobytes(), name
+        assert rec == ref.records.tobytes(), name
+        assert route == ref.route_node.tobytes(), name
+        assert inc == ref.incomplete, name
+        checked += 1
+    assert checked >= 5
+
+
+def test_cluster_partition_matches_abi():
+    import ctypes as C
+    from paper_2510_14392_b200 import fbgpu
+    from paper_2510_14392_b200.cluster import partition
+    L = fbgpu.lib()  # loads without a GPU; partition is host logic
+    for n in (1, 3, 8, 64, 511):
+        for w in range(1, min(n, 8) + 1):
+            seen = []
+            for r in range(w):
+                lo, nl = C.c_int32(), C.c_int32()
+                assert L.fb_cluster_partition(n, w, r, C.byref(lo), C.byref(nl)) == 0
+                assert (lo.value, nl.value) == partition(n, w, r)
+                seen.extend(range(lo.value, lo.value + nl.value))
+            assert seen == list(range(n))

@@ -294,3 +294,79 @@ def test_cluster_rejects_reroute(fb):
     cfgs = [engine_config("fairbatch", 2048, CostModel(5, 0.05, 1e-4), 500, 50)]
     with pytest.raises(fb.UsageError):
         run_cluster(rows, cfgs, LbConfig("pab_lb", 1, 0.0, retry_reroute=True), 10**9)
+
+
+@pytest.mark.parametrize("name,world", [("pab0_8", 2), ("count37_3", 3), ("pab5000_8", 4),
+                                        ("pab_hz10s_8", 2), ("c5_pab0_64", 8)])
+def test_cluster_shards_in_process_match_golden(golden, gpu_cluster_cases, name, world):
+    """The multi-rank protocol on one device: `world` shards (one persistent
+    kernel each, on its own stream, running concurrently) exchange their
+    node reports through each other's exchange buffers; the merged output
+    equals run_cluster's golden summary."""
+    from backends import cluster_summary
+    from paper_2510_14392_b200.cluster import ClusterShard, merge_shards
+    _, rows, cfgs, lb, hz = gpu_cluster_cases[name]
+    shards = [ClusterShard(rows, cfgs, lb, hz, r, world, 0) for r in range(world)]
+    try:
+        ptrs = [s.exchange_ptr() for s in shards]
+        for s in shards:
+            s.connect_ptrs(ptrs)
+        for s in shards:
+            s.reset()
+        for s in shards:
+            s.launch()
+        parts = [s.fetch(s.wait()) for s in shards]
+    finally:
+        for s in shards:
+            s.close()
+    out = merge_shards(parts, len(cfgs))
+    assert cluster_summary(out) == golden["clusters"][name]
+
+
+def _ipc_worker(rank, world, port, q, name):
+    import os
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    import torch.distributed as dist
+    from backends import cluster_summary
+    from catalog import cluster_cases
+    from paper_2510_14392_b200 import fbgpu
+    from paper_2510_14392_b200.cluster import run_cluster_dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    case = {c[0]: c for c in cluster_cases(fbgpu.generate_bursty)}[name]
+    _, rows, cfgs, lb, hz = case
+    rows = rows.truncated(120)  # processes time-slice one GPU: keep the epochs few
+    out = run_cluster_dist(rows, cfgs, lb, hz, dist, device=0)
+    if rank == 0:
+        q.put(cluster_summary(out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_cluster_two_processes_cuda_ipc(fb, oracle):
+    """run_cluster_dist across two processes: exchange buffers opened with
+    CUDA IPC (the multi-GPU path; here both processes share one device)."""
+    import socket
+    import torch.multiprocessing as mp
+    from backends import cluster_summary
+    from catalog import cluster_cases
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    name = "count37_3"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, name)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, rows, cfgs, lb, hz = {c[0]: c for c in cluster_cases(oracle.generate_bursty)}[name]
+    ref = oracle.run_cluster(rows.truncated(120), cfgs, lb, hz)
+    assert got == cluster_summary(ref)
