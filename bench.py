@@ -247,10 +247,13 @@ def run_ours(args) -> None:
     all_steps = float(n.item())
     value = all_steps / (max_ms / 1000.0)
 
-    # end to end through the C ABI with host buffers: H2D of the step's trace
-    # rows + instances, run, D2H of per-instance results and per-request records
+    # end to end through the C ABI with host buffers: the trace rows live in
+    # pinned host memory (fb_host_alloc) and every step uploads them plus the
+    # instance table (validated + packed on the host), runs, and downloads
+    # per-instance results and per-request records into a pinned buffer
+    batch.pin()
+    rec_out = fbgpu.pinned_empty(arena.record_rows(), _abi.RECORD_DTYPE)
     rows = batch.rows
-    inst = batch.instances_c()
     import ctypes as C
     h2d = rows.nbytes + C.sizeof(_abi.Instance) * batch.n_instances
     e2e_ms = []
@@ -261,7 +264,7 @@ def run_ours(args) -> None:
         arena.load(batch)
         arena.run()
         r2 = arena.results()
-        rec = arena.records()
+        rec = arena.records(out=rec_out)
         e2e_ms.append((time.perf_counter() - t0) * 1000.0)
     d2h = r2.nbytes + rec.nbytes
     assert r2.tobytes() == res.tobytes()

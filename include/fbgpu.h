@@ -323,9 +323,18 @@ int fb_arena_fetch_paths(fb_arena* arena, uint32_t* out);
 int fb_arena_fetch_log(fb_arena* arena, int64_t instance, fb_step_log* steps,
                        fb_plan_entry* entries, fb_reject_log* rejects);
 
+/* Page-locked host buffers.  Trace rows, instances and record outputs that
+ * live in memory from fb_host_alloc move by direct DMA; any other host
+ * pointer is staged through the arena's own pinned chunks.  Not a reference
+ * interface: the reference keeps everything in host memory. */
+int fb_host_alloc(size_t bytes, void** out);
+int fb_host_free(void* p);
+
 /* One-shot end-to-end run from host buffers: upload, run to quiescence,
  * download results and records (records may be NULL).  elapsed_ms_out (may be
- * NULL) receives the host wall time of the whole call. */
+ * NULL) receives the host wall time of the whole call.  Reuses one cached
+ * arena per device (serialised by a lock), so repeated calls pay no device
+ * allocation. */
 int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
                  int64_t n_instances, fb_instance_result* results,
                  fb_record* records, double* elapsed_ms_out);

@@ -178,6 +178,7 @@ class Batch:
         self._n_rows = 0
         self._inst: list[_abi.Instance] = []
         self._rows: Rows | None = None
+        self._inst_c = None  # cached ctypes instance table (rebuilt after changes)
         self.offered: list[float] = []
 
     def add_rows(self, rows: Rows) -> int:
@@ -190,6 +191,7 @@ class Batch:
     def add_instance(self, cfg: EngineConfig, trace_off: int, n_req: int, horizon_us: int,
                      offered_rps: float = 0.0) -> int:
         self._inst.append(_abi.Instance(cfg.to_c(), int(trace_off), int(n_req), int(horizon_us)))
+        self._inst_c = None
         self.offered.append(offered_rps)
         return len(self._inst) - 1
 
@@ -216,6 +218,7 @@ class Batch:
         for i, x in enumerate(other._inst):
             self._inst.append(_abi.Instance(x.cfg, off + x.trace_off, x.n_req, x.horizon_us))
             self.offered.append(other.offered[i])
+        self._inst_c = None
 
     @property
     def rows(self) -> Rows:
@@ -223,15 +226,28 @@ class Batch:
             self._rows = Rows.concat(self._parts)
         return self._rows
 
+    def pin(self) -> "Batch":
+        """Moves the trace rows into page-locked host memory (fb_host_alloc),
+        so uploads are direct DMA."""
+        from .fbgpu import pinned_copy
+        r = self.rows
+        self._rows = Rows(*(pinned_copy(getattr(r, k)) for k in
+                            ("arrival_us", "prompt_len", "output_len", "ttft_us", "tpot_us")))
+        self._parts = [self._rows]
+        return self
+
     @property
     def n_instances(self) -> int:
         return len(self._inst)
 
     def instances_c(self):
-        arr = (_abi.Instance * max(1, len(self._inst)))()
-        for i, x in enumerate(self._inst):
-            arr[i] = x
-        return arr
+        """The fb_instance table as one C array (built once per batch state)."""
+        if self._inst_c is None or len(self._inst_c) != max(1, len(self._inst)):
+            arr = (_abi.Instance * max(1, len(self._inst)))()
+            for i, x in enumerate(self._inst):
+                arr[i] = x
+            self._inst_c = arr
+        return self._inst_c
 
     def record_offsets(self) -> np.ndarray:
         off = np.zeros(len(self._inst) + 1, np.int64)

@@ -5,7 +5,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/fbgpu.h"
@@ -123,8 +125,86 @@ struct fb_arena {
   DevBuf<unsigned long long> work;
   DevBuf<int64_t> wide_list;
   DevBuf<int64_t> order;
+  DevBuf<fb_record> recbuf;  // device-packed records (AoS) for one D2H
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
+  // Pinned staging for copies from / to pageable host memory: two chunks,
+  // so the host memcpy of one overlaps the DMA of the other.
+  static constexpr size_t kStage = size_t(4) << 20;
+  unsigned char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+
+  cudaError_t ensure_stage() {
+    for (int b = 0; b < 2; ++b) {
+      if (stage[b]) continue;
+      cudaError_t e = cudaMallocHost(&stage[b], kStage);
+      if (e != cudaSuccess) return e;
+      e = cudaEventCreateWithFlags(&stage_ev[b], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  // Host -> device.  Pinned sources go by direct DMA (the caller keeps the
+  // buffer alive until the stream reaches the copy); pageable sources are
+  // staged, and the source may be reused on return.
+  cudaError_t h2d(void* dst, const void* src, size_t n) {
+    if (n == 0) return cudaSuccess;
+    if (is_pinned(src)) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, stream);
+    cudaError_t e = ensure_stage();
+    if (e != cudaSuccess) return e;
+    const unsigned char* s = static_cast<const unsigned char*>(src);
+    unsigned char* d = static_cast<unsigned char*>(dst);
+    for (size_t off = 0, c = 0; off < n; off += kStage, ++c) {
+      const int b = static_cast<int>(c & 1);
+      const size_t len = std::min(kStage, n - off);
+      if ((e = cudaEventSynchronize(stage_ev[b])) != cudaSuccess) return e;
+      std::memcpy(stage[b], s + off, len);
+      if ((e = cudaMemcpyAsync(d + off, stage[b], len, cudaMemcpyHostToDevice, stream)) !=
+          cudaSuccess)
+        return e;
+      if ((e = cudaEventRecord(stage_ev[b], stream)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  // Device -> host, complete on return.
+  cudaError_t d2h(void* dst, const void* src, size_t n) {
+    if (n == 0) return cudaStreamSynchronize(stream);
+    cudaError_t e;
+    if (is_pinned(dst)) {
+      if ((e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+        return e;
+      return cudaStreamSynchronize(stream);
+    }
+    if ((e = ensure_stage()) != cudaSuccess) return e;
+    const unsigned char* s = static_cast<const unsigned char*>(src);
+    unsigned char* d = static_cast<unsigned char*>(dst);
+    const size_t nch = (n + kStage - 1) / kStage;
+    auto issue = [&](size_t c) -> cudaError_t {
+      const int b = static_cast<int>(c & 1);
+      const size_t off = c * kStage, len = std::min(kStage, n - off);
+      cudaError_t e2 = cudaMemcpyAsync(stage[b], s + off, len, cudaMemcpyDeviceToHost, stream);
+      if (e2 != cudaSuccess) return e2;
+      return cudaEventRecord(stage_ev[b], stream);
+    };
+    for (size_t c = 0; c < nch && c < 2; ++c)
+      if ((e = issue(c)) != cudaSuccess) return e;
+    for (size_t c = 0; c < nch; ++c) {
+      const int b = static_cast<int>(c & 1);
+      const size_t off = c * kStage, len = std::min(kStage, n - off);
+      if ((e = cudaEventSynchronize(stage_ev[b])) != cudaSuccess) return e;
+      std::memcpy(d + off, stage[b], len);
+      if (c + 2 < nch && (e = issue(c + 2)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  static bool is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  }
 
   fbgpu::EngineParams params(int64_t max_events) const {
     fbgpu::EngineParams P;
@@ -168,6 +248,13 @@ struct fb_arena {
     work.release();
     wide_list.release();
     order.release();
+    recbuf.release();
+    for (int b = 0; b < 2; ++b) {
+      if (stage_ev[b]) cudaEventSynchronize(stage_ev[b]), cudaEventDestroy(stage_ev[b]);
+      if (stage[b]) cudaFreeHost(stage[b]);
+      stage[b] = nullptr;
+      stage_ev[b] = nullptr;
+    }
   }
 };
 
@@ -230,8 +317,17 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   if (!a || !rows || (n_instances > 0 && !instances) || n_instances < 0)
     return set_error(FB_ERR_USAGE, "fb_arena_load: bad arguments");
   FB_CUDA(cudaSetDevice(a->device));
-  // Validate everything before touching device state.
+  // Validate everything before touching device state.  Instances often share
+  // trace rows (A/B pairs, SLO grids): each distinct (rows, truth a) range is
+  // scanned once, validating and computing the per-range facts together.
   std::vector<int64_t> rec_off(static_cast<size_t>(n_instances) + 1, 0);
+  std::vector<int64_t> tpot_u(static_cast<size_t>(n_instances), -1);
+  std::vector<double> key(static_cast<size_t>(n_instances), 0.0);
+  struct RangeFacts {
+    int64_t tpot_u;
+    double key;
+  };
+  std::unordered_map<std::string, RangeFacts> memo;
   for (int64_t i = 0; i < n_instances; ++i) {
     const fb_instance& in = instances[i];
     if (in.trace_off < 0 || in.n_req < 0 || in.trace_off + in.n_req > rows->n_rows)
@@ -240,8 +336,30 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
       return set_error(FB_ERR_VALIDATION, "instance " + std::to_string(i) + ": too many requests");
     int st = validate_engine(in.cfg, i);
     if (st) return st;
-    st = validate_rows(*rows, in.trace_off, in.n_req, i);
-    if (st) return st;
+    const double a_us =
+        in.cfg.truth_model.a_ms * 1000.0 > 1.0 ? in.cfg.truth_model.a_ms * 1000.0 : 1.0;
+    std::string mk(3 * sizeof(int64_t), '\0');
+    std::memcpy(&mk[0], &in.trace_off, 8);
+    std::memcpy(&mk[8], &in.n_req, 8);
+    std::memcpy(&mk[16], &a_us, 8);
+    auto it = memo.find(mk);
+    if (it == memo.end()) {
+      st = validate_rows(*rows, in.trace_off, in.n_req, i);
+      if (st) return st;
+      RangeFacts f;
+      // a uniform tpot_slo makes init_time_budget's min over tasks a constant
+      f.tpot_u = in.n_req > 0 ? rows->tpot_us[in.trace_off] : -1;
+      // work-queue order key: predicted steps ~ max of arrival/a + output_len
+      f.key = 0.0;
+      for (int64_t r = in.trace_off; r < in.trace_off + in.n_req; ++r) {
+        if (rows->tpot_us[r] != f.tpot_u) f.tpot_u = -1;
+        const double v = static_cast<double>(rows->arrival_us[r]) / a_us + rows->output_len[r];
+        if (v > f.key) f.key = v;
+      }
+      it = memo.emplace(std::move(mk), f).first;
+    }
+    tpot_u[i] = it->second.tpot_u;
+    key[i] = it->second.key;
     rec_off[i + 1] = rec_off[i] + in.n_req;
   }
   fb_log_opts lo{};
@@ -278,57 +396,31 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   ENSURE(a->log_rejects, n_instances * static_cast<int64_t>(lo.reject_cap));
 #undef ENSURE
   std::vector<unsigned char> hinst(static_cast<size_t>(n_instances) * fbgpu::dev_inst_bytes());
-  for (int64_t i = 0; i < n_instances; ++i) {
-    // a uniform tpot_slo makes init_time_budget's min over tasks a constant
-    int64_t tpot_u = instances[i].n_req > 0 ? rows->tpot_us[instances[i].trace_off] : -1;
-    for (int64_t r = instances[i].trace_off; r < instances[i].trace_off + instances[i].n_req; ++r)
-      if (rows->tpot_us[r] != tpot_u) {
-        tpot_u = -1;
-        break;
-      }
+  for (int64_t i = 0; i < n_instances; ++i)
     fbgpu::pack_instance(instances[i], rec_off[i], i * lo.step_cap, i * lo.entry_cap,
-                         i * lo.reject_cap, tpot_u, hinst.data() + i * fbgpu::dev_inst_bytes());
-  }
+                         i * lo.reject_cap, tpot_u[i], hinst.data() + i * fbgpu::dev_inst_bytes());
   // Work-queue order: longest predicted run first, so the long-tailed
   // instances start in the first wave (scheduling only, no semantic effect).
-  // Predicted length in steps ~ max over requests of arrival/a + output_len.
   std::vector<int64_t> order(static_cast<size_t>(n_instances));
-  {
-    std::vector<double> key(static_cast<size_t>(n_instances), 0.0);
-    for (int64_t i = 0; i < n_instances; ++i) {
-      const fb_instance& in = instances[i];
-      const double a_us = in.cfg.truth_model.a_ms * 1000.0 > 1.0 ? in.cfg.truth_model.a_ms * 1000.0 : 1.0;
-      double k = 0.0;
-      for (int64_t r = in.trace_off; r < in.trace_off + in.n_req; ++r) {
-        const double v = static_cast<double>(rows->arrival_us[r]) / a_us + rows->output_len[r];
-        if (v > k) k = v;
-      }
-      key[i] = k;
-      order[i] = i;
-    }
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t x, int64_t y) { return key[x] > key[y]; });
-  }
+  for (int64_t i = 0; i < n_instances; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t x, int64_t y) { return key[x] > key[y]; });
   cudaStream_t s = a->stream;
-  if (n_instances > 0)
-    FB_CUDA(cudaMemcpyAsync(a->order.p, order.data(), sizeof(int64_t) * n_instances,
-                            cudaMemcpyHostToDevice, s));
-  if (n_rows > 0) {
-    FB_CUDA(cudaMemcpyAsync(a->arrival.p, rows->arrival_us, n_rows * 8, cudaMemcpyHostToDevice, s));
-    FB_CUDA(cudaMemcpyAsync(a->ttft.p, rows->ttft_us, n_rows * 8, cudaMemcpyHostToDevice, s));
-    FB_CUDA(cudaMemcpyAsync(a->tpot.p, rows->tpot_us, n_rows * 8, cudaMemcpyHostToDevice, s));
-    FB_CUDA(cudaMemcpyAsync(a->prompt.p, rows->prompt_len, n_rows * 4, cudaMemcpyHostToDevice, s));
-    FB_CUDA(cudaMemcpyAsync(a->output.p, rows->output_len, n_rows * 4, cudaMemcpyHostToDevice, s));
-  }
-  if (n_instances > 0)
-    FB_CUDA(cudaMemcpyAsync(a->inst.p, hinst.data(), hinst.size(), cudaMemcpyHostToDevice, s));
+  FB_CUDA(a->h2d(a->order.p, order.data(), sizeof(int64_t) * n_instances));
+  FB_CUDA(a->h2d(a->arrival.p, rows->arrival_us, n_rows * 8));
+  FB_CUDA(a->h2d(a->ttft.p, rows->ttft_us, n_rows * 8));
+  FB_CUDA(a->h2d(a->tpot.p, rows->tpot_us, n_rows * 8));
+  FB_CUDA(a->h2d(a->prompt.p, rows->prompt_len, n_rows * 4));
+  FB_CUDA(a->h2d(a->output.p, rows->output_len, n_rows * 4));
+  FB_CUDA(a->h2d(a->inst.p, hinst.data(), hinst.size()));
   a->n_rows = n_rows;
   a->n_inst = n_instances;
   a->n_rec = n_rec;
   a->log = lo;
   a->rec_off = std::move(rec_off);
   a->loaded = true;
-  // hinst must outlive the async copy
+  // order / hinst (staged, so already copied) and pinned caller rows must
+  // outlive the async copies
   FB_CUDA(cudaStreamSynchronize(s));
   return fb_arena_reset(a);
 }
@@ -389,37 +481,10 @@ int fb_arena_fetch_records(fb_arena* a, fb_record* out) {
   if (!a || !a->loaded || !out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_records");
   FB_CUDA(cudaSetDevice(a->device));
   const int64_t n = a->n_rec;
-  std::vector<int32_t> nidx(n);
-  std::vector<uint32_t> flags(n);
-  std::vector<int64_t> first(n);
-  std::vector<double> mt(n), mta(n);
-  std::vector<unsigned char> st(static_cast<size_t>(a->n_inst) * fbgpu::dev_state_bytes());
-  cudaStream_t s = a->stream;
-  if (n > 0) {
-    FB_CUDA(cudaMemcpyAsync(nidx.data(), a->nidx.p, n * 4, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(flags.data(), a->flags.p, n * 4, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(first.data(), a->first.p, n * 8, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(mt.data(), a->maxtp.p, n * 8, cudaMemcpyDeviceToHost, s));
-    FB_CUDA(cudaMemcpyAsync(mta.data(), a->maxtp_alt.p, n * 8, cudaMemcpyDeviceToHost, s));
-  }
-  if (!st.empty())
-    FB_CUDA(cudaMemcpyAsync(st.data(), a->state.p, st.size(), cudaMemcpyDeviceToHost, s));
-  FB_CUDA(cudaStreamSynchronize(s));
-  for (int64_t i = 0; i < a->n_inst; ++i) {
-    fb_instance_result r;
-    fbgpu::unpack_state(st.data() + i * fbgpu::dev_state_bytes(), &r);
-    const int64_t b = a->rec_off[i], e = a->rec_off[i + 1];
-    for (int64_t k = b; k < e; ++k) {
-      uint32_t f = flags[k] & ~fbgpu::kTpotViolated;
-      if (k - b < r.n_arrived) f |= FB_REC_ARRIVED;
-      if ((f & FB_REC_REJECTED) && nidx[k] > 0) f &= ~static_cast<uint32_t>(FB_REC_REJECTED);
-      out[k].first_emit_us = first[k];
-      out[k].max_tpot_ms = mt[k];
-      out[k].max_tpot_alt_ms = mta[k];
-      out[k].tokens_emitted = nidx[k];
-      out[k].flags = f;
-    }
-  }
+  cudaError_t e = a->recbuf.ensure(static_cast<size_t>(n));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc records");
+  FB_CUDA(fbgpu::launch_pack_records(a->params(0), a->recbuf.p, a->stream));
+  FB_CUDA(a->d2h(out, a->recbuf.p, sizeof(fb_record) * static_cast<size_t>(n)));
   return FB_OK;
 }
 
@@ -478,18 +543,40 @@ int fb_arena_fetch_log(fb_arena* a, int64_t i, fb_step_log* steps, fb_plan_entry
   return FB_OK;
 }
 
+int fb_host_alloc(size_t bytes, void** out) {
+  if (!out) return set_error(FB_ERR_USAGE, "fb_host_alloc: null output");
+  *out = nullptr;
+  FB_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+  return FB_OK;
+}
+
+int fb_host_free(void* p) {
+  if (p) FB_CUDA(cudaFreeHost(p));
+  return FB_OK;
+}
+
 int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
                  int64_t n_instances, fb_instance_result* results, fb_record* records,
                  double* elapsed_ms_out) {
   const auto t0 = std::chrono::steady_clock::now();
-  fb_arena* a = nullptr;
-  int st = fb_arena_create(device, nullptr, &a);
-  if (st) return st;
-  st = fb_arena_load(a, rows, instances, n_instances, nullptr);
+  // one cached arena per device: device buffers and pinned staging persist
+  static std::mutex mu;
+  static std::vector<fb_arena*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_error(FB_ERR_CUDA, "no CUDA device available (the product path has no CPU fallback)");
+  if (device < 0 || device >= ndev) return set_error(FB_ERR_USAGE, "device ordinal out of range");
+  if (cache.size() < static_cast<size_t>(ndev)) cache.resize(static_cast<size_t>(ndev), nullptr);
+  if (!cache[device]) {
+    int st = fb_arena_create(device, nullptr, &cache[device]);
+    if (st) return st;
+  }
+  fb_arena* a = cache[device];
+  int st = fb_arena_load(a, rows, instances, n_instances, nullptr);
   if (!st) st = fb_arena_run(a, 0, nullptr);
   if (!st && results) st = fb_arena_fetch_results(a, results);
   if (!st && records) st = fb_arena_fetch_records(a, records);
-  fb_arena_destroy(a);
   if (elapsed_ms_out)
     *elapsed_ms_out = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return st;

@@ -565,7 +565,52 @@ __global__ void reset_kernel(const __grid_constant__ EngineParams P, int64_t n_r
   }
 }
 
+// Per-request records in the ABI's AoS layout (fb_record), one warp per
+// instance, so a fetch is a single D2H.  Flag finishing as in
+// request_reports (metrics.cpp:60-116): ARRIVED for rows the event loop
+// enqueued, REJECTED only for requests that were never served.
+__global__ void pack_records_kernel(const __grid_constant__ EngineParams P, fb_record* out) {
+  const int64_t wpb = blockDim.x / kWarp;
+  for (int64_t i = blockIdx.x * wpb + threadIdx.x / kWarp; i < P.n_inst; i += gridDim.x * wpb) {
+    const int64_t b = P.inst[i].rec_off, n = P.inst[i].n_req;
+    const int64_t arrived = P.state[i].arr;
+    for (int64_t k = lane_id(); k < n; k += kWarp) {
+      const int64_t g = b + k;
+      const int32_t ni = P.nidx[g];
+      uint32_t f = P.flags[g] & ~kTpotViolated;
+      if (k < arrived) f |= FB_REC_ARRIVED;
+      if ((f & FB_REC_REJECTED) && ni > 0) f &= ~static_cast<uint32_t>(FB_REC_REJECTED);
+      fb_record r;
+      r.first_emit_us = P.first[g];
+      r.max_tpot_ms = P.maxtp[g];
+      r.max_tpot_alt_ms = P.maxtp_alt[g];
+      r.tokens_emitted = ni;
+      r.flags = f;
+      out[g] = r;
+    }
+  }
+}
+
 // ------------------------------------------------------------- host side
+
+#ifdef FB_WIDE_PROF
+extern "C" int fb_debug_wide_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_wide_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_wide_prof, z, sizeof(z));
+  }
+  return static_cast<int>(cudaDeviceSynchronize());
+}
+#endif
+
+cudaError_t launch_pack_records(const EngineParams& p, fb_record* out, cudaStream_t st) {
+  if (p.n_inst <= 0) return cudaSuccess;
+  int64_t blocks = (p.n_inst + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  pack_records_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(p, out);
+  return cudaGetLastError();
+}
 
 EngineGeometry engine_geometry(int device) {
   EngineGeometry g;

@@ -21,11 +21,34 @@
 
 namespace fbgpu {
 
+// Dev-only phase timers (tools/wide_prof.py builds a variant with
+// -DFB_WIDE_PROF): thread 0 accumulates clock64 deltas per phase.
+#ifdef FB_WIDE_PROF
+__device__ unsigned long long g_wide_prof[16];
+#define WPROF_START long long wp_t_ = clock64();
+#define WPROF(slot)                                                               \
+  if (threadIdx.x == 0) {                                                         \
+    const long long n_ = clock64();                                               \
+    atomicAdd(&g_wide_prof[slot], static_cast<unsigned long long>(n_ - wp_t_));   \
+    wp_t_ = n_;                                                                   \
+  }
+#define WPROF_COUNT(slot, v) \
+  if (threadIdx.x == 0) atomicAdd(&g_wide_prof[slot], static_cast<unsigned long long>(v));
+#else
+#define WPROF_START
+#define WPROF(slot)
+#define WPROF_COUNT(slot, v)
+#endif
+
 constexpr int kWideThreads = 512;
 constexpr int kWideWarps = kWideThreads / kWarp;
 constexpr int kWideWin = 2048;
 constexpr int kRadixBits = 11;
 constexpr int kRadixBins = 1 << kRadixBits;
+// Range-binned selection (wide_select_binned): 1024 linear bins per key group.
+constexpr int kGroupBins = 1024;
+constexpr int kSelBins = 4 * kGroupBins;
+constexpr int kRed = 8;  // values per warp in block_reduce
 
 struct WideSmem {
   uint64_t wkey[kWideWin];
@@ -35,8 +58,8 @@ struct WideSmem {
   int32_t wpos[kWideWin];
   uint32_t wnw[kWideWin];
   int32_t wtake[kWideWin];
-  uint32_t hist[kRadixBins];
-  int64_t red[kWideWarps * 4];
+  uint32_t hist[kSelBins];
+  int64_t red[kWideWarps * kRed];
   int64_t bcast[8];
   double dbcast[4];
   int32_t ibcast[8];
@@ -110,6 +133,30 @@ __device__ __forceinline__ uint64_t block_xor(uint64_t v, WideSmem& sm) {
   __syncthreads();
   return r;
 }
+// Block-wide minima of N int64 values at once (maxima: pass negations);
+// one pair of barriers for all of them.  Results in every thread.
+template <int N>
+__device__ __forceinline__ void block_min_n(int64_t (&v)[N], WideSmem& sm) {
+  static_assert(N <= kRed, "block_min_n");
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = warp_min(v[i]);
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) sm.red[wid() * kRed + i] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    int64_t x = kInf;
+    for (int q = 0; q < kWideWarps; ++q) {
+      const int64_t y = sm.red[q * kRed + i];
+      x = y < x ? y : x;
+    }
+    v[i] = x;
+  }
+  __syncthreads();
+}
+
 // Exclusive prefix count of `flag` over the block (thread order) plus the
 // block total.
 __device__ __forceinline__ int block_excl_count(bool flag, int& total, WideSmem& sm) {
@@ -161,6 +208,37 @@ __device__ __forceinline__ uint64_t wide_key(uint64_t klow, int policy, int64_t 
   const uint64_t seq = low & ((uint64_t(1) << 22) - 1);
   if (policy == FB_POLICY_SARATHI) return ((decode ? uint64_t(0) : uint64_t(1)) << 62) | seq;
   return seq;
+}
+
+// Ascending bitonic sort of sm.wkey / sm.wpos [0, K) (keys unique).
+__device__ __forceinline__ void wide_sort_window(int K, WideSmem& sm) {
+  int n2 = 1;
+  while (n2 < K) n2 <<= 1;
+  for (int i = K + threadIdx.x; i < n2; i += kWideThreads) {
+    sm.wkey[i] = ~uint64_t(0);
+    sm.wpos[i] = -1;
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {  // bitonic sort (keys unique)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += kWideThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = sm.wkey[i], b = sm.wkey[ixj];
+          const bool asc = (i & k) == 0;
+          if ((a > b) == asc) {
+            sm.wkey[i] = b;
+            sm.wkey[ixj] = a;
+            const int t = sm.wpos[i];
+            sm.wpos[i] = sm.wpos[ixj];
+            sm.wpos[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
 }
 
 // K2: the K = min(kWideWin, #{key > lo}) smallest keys above `lo` (all keys
@@ -242,33 +320,122 @@ __device__ int wide_select(const WideScratch& ws, int A, bool has_lo, uint64_t l
   }
   __syncthreads();
   const int K = sm.ibcast[4];
-  int n2 = 1;
-  while (n2 < K) n2 <<= 1;
-  for (int i = K + threadIdx.x; i < n2; i += kWideThreads) {
-    sm.wkey[i] = ~uint64_t(0);
-    sm.wpos[i] = -1;
+  wide_sort_window(K, sm);
+  return K;
+}
+
+// Linear key bins per group for the binned selection.  bin(key) is
+// nondecreasing in key, so the keys of bins [0, b] are exactly the smallest
+// keys.  Fair batching orders (urgent decode, prefill, relaxed decode) by
+// slack, sarathi (decode, prefill) by seq, prefill-first by seq.
+struct SelBins {
+  int64_t lo[3];
+  int32_t sh[3];
+};
+
+__device__ __forceinline__ int sel_bin(uint64_t klow, int policy, int64_t urgency,
+                                       const SelBins& b) {
+  const bool decode = (klow >> 63) != 0;
+  const uint64_t low = klow & ((uint64_t(1) << 62) - 1);
+  int g;
+  int64_t ord;
+  if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
+    ord = static_cast<int64_t>(low >> 22) - kPackSlack;
+    g = decode ? (ord < urgency ? 0 : 2) : 1;
+  } else {
+    ord = static_cast<int64_t>(low & ((uint64_t(1) << 22) - 1));
+    g = (policy == FB_POLICY_SARATHI && !decode) ? 1 : 0;
   }
+  int64_t d = (ord - b.lo[g]) >> b.sh[g];
+  d = d < 0 ? 0 : (d > kGroupBins - 1 ? kGroupBins - 1 : d);
+  return g * kGroupBins + static_cast<int>(d);
+}
+
+__device__ __forceinline__ void sel_range(SelBins& b, int g, int64_t lo, int64_t hi) {
+  b.lo[g] = lo;
+  int sh = 0;
+  if (hi > lo)
+    while (((hi - lo) >> sh) >= kGroupBins) ++sh;
+  b.sh[g] = sh;
+}
+
+// K2 (common case): the smallest keys above `lo` that fit one window, in two
+// streaming passes over the key stems -- a histogram over the group ranges,
+// then a gather of every key in the bins up to the last one whose inclusive
+// count still fits -- followed by the shared-memory bitonic sort.  Returns
+// the window size, or -1 when the first nonempty bin alone overflows the
+// window (the caller falls back to the exact radix select).
+__device__ int wide_select_binned(const WideScratch& ws, int A, bool has_lo, uint64_t lo,
+                                  int policy, int64_t urgency, const SelBins& sb,
+                                  WideSmem& sm) {
+  constexpr int U = 8;
+  for (int i = threadIdx.x; i < kSelBins; i += kWideThreads) sm.hist[i] = 0;
+  if (threadIdx.x == 0) sm.ibcast[4] = 0;
   __syncthreads();
-  for (int k = 2; k <= n2; k <<= 1) {  // bitonic sort (keys unique)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += kWideThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = sm.wkey[i], b = sm.wkey[ixj];
-          const bool asc = (i & k) == 0;
-          if ((a > b) == asc) {
-            sm.wkey[i] = b;
-            sm.wkey[ixj] = a;
-            const int t = sm.wpos[i];
-            sm.wpos[i] = sm.wpos[ixj];
-            sm.wpos[ixj] = t;
-          }
-        }
-      }
-      __syncthreads();
+  for (int b0 = 0; b0 < A; b0 += kWideThreads * U) {
+    uint64_t k[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int p = b0 + j * kWideThreads + threadIdx.x;
+      k[j] = p < A ? ws.klow[p] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int p = b0 + j * kWideThreads + threadIdx.x;
+      if (p < A && (!has_lo || wide_key(k[j], policy, urgency) > lo))
+        atomicAdd(&sm.hist[sel_bin(k[j], policy, urgency, sb)], 1u);
     }
   }
   __syncthreads();
+  constexpr int kPer = kSelBins / kWideThreads;
+  const int c0 = threadIdx.x * kPer;
+  int loc = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) loc += static_cast<int>(sm.hist[c0 + q]);
+  int tot;
+  const int before = block_excl_sum(loc, tot, sm);
+  if (tot <= kWideWin) {
+    if (threadIdx.x == 0) sm.ibcast[0] = kSelBins - 1;
+  } else if (before <= kWideWin && before + loc > kWideWin) {
+    int cum = before;
+    for (int q = 0; q < kPer; ++q) {
+      const int c = static_cast<int>(sm.hist[c0 + q]);
+      if (cum + c > kWideWin) {
+        sm.ibcast[0] = cum == 0 ? -1 : c0 + q - 1;  // last bin that still fits
+        break;
+      }
+      cum += c;
+    }
+  }
+  __syncthreads();
+  const int bmax = sm.ibcast[0];
+  if (bmax < 0) return -1;
+  for (int b0 = 0; b0 < A; b0 += kWideThreads * U) {
+    uint64_t k[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int p = b0 + j * kWideThreads + threadIdx.x;
+      k[j] = p < A ? ws.klow[p] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int p = b0 + j * kWideThreads + threadIdx.x;
+      const uint64_t key = wide_key(k[j], policy, urgency);
+      const bool sel = p < A && (!has_lo || key > lo) && sel_bin(k[j], policy, urgency, sb) <= bmax;
+      const unsigned m = __ballot_sync(kFull, sel);
+      int base = 0;
+      if (m && lane_id() == 0) base = atomicAdd(&sm.ibcast[4], __popc(m));
+      base = __shfl_sync(kFull, base, 0);
+      if (sel) {
+        const int slot = base + __popc(m & lanemask_lt());
+        sm.wkey[slot] = key;
+        sm.wpos[slot] = p;
+      }
+    }
+  }
+  __syncthreads();
+  const int K = sm.ibcast[4];
+  wide_sort_window(K, sm);
   return K;
 }
 
@@ -282,46 +449,202 @@ struct WideScan {
   bool done;
 };
 
-// Greedy pass over one sorted window (sched.cpp:129-232), thread 0.
-__device__ void wide_scan_window(WideScan& st, int K, int policy, const FormCfg& f, int n_dec,
-                                 double tc_min, double cc_min, const WideScratch& ws,
-                                 WideSmem& sm) {
+// Fair batching, the provably whole-admitted prefix of a sorted window,
+// found in parallel.  With tb0 the exact budget before the window and
+// S_k an upper bound (every partial rounded up) of the sum of the rounded
+// task costs tc_0..tc_k, the reference's running budget before task k is
+// t_k >= tb0 - S_{k-1} - k*u*tb0 (u = 2^-53, every intermediate in [0, tb0]),
+// so tb0 - S_k >= k*2^-52*tb0 (directed rounding) together with
+// N_k = sum of new tokens <= tok0 proves tc_k <= t_k and new_k <= tok_k:
+// task k is admitted whole, and the stop test is false before it (tc_k >=
+// tc_min).  Both conditions are monotone in k, so the proven tasks form a
+// prefix [0, m).  Thread 0 then folds the exact budget over the prefix in
+// the reference's order (one dependent subtraction per task) and the
+// serial scan resumes at m.  Returns m.
+__device__ int wide_admit_prefix(WideScan& st, int K, WideSmem& sm) {
+  if (threadIdx.x == 0) {
+    sm.dbcast[1] = st.tb;
+    sm.bcast[7] = st.done ? 0 : st.tok;
+  }
+  __syncthreads();
+  const double tb0 = sm.dbcast[1];
+  const int64_t tok0 = sm.bcast[7];
+  __syncthreads();
+  if (tok0 <= 0 || !(tb0 >= 0.0)) return 0;
+  constexpr int kPer = kWideWin / kWideThreads;
+  const int k0 = threadIdx.x * kPer;
+  double s_loc[kPer];
+  int64_t n_loc[kPer];
+  double s = 0.0;
+  int64_t n = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int k = k0 + q;
+    if (k < K) {
+      s = __dadd_ru(s, sm.wtc[k]);
+      n += static_cast<int64_t>(sm.wnw[k] & 0x7fffffffu);
+    }
+    s_loc[q] = s;
+    n_loc[q] = n;
+  }
+  // block exclusive scan of the thread totals (sums rounded up stay upper bounds)
+  double si = s;
+  int64_t ni = n;
+#pragma unroll
+  for (int o = 1; o < kWarp; o <<= 1) {
+    const double ys = __shfl_up_sync(kFull, si, o);
+    const int64_t yn = __shfl_up_sync(kFull, ni, o);
+    if (lane_id() >= o) {
+      si = __dadd_ru(ys, si);
+      ni += yn;
+    }
+  }
+  double* wsum = reinterpret_cast<double*>(sm.red);   // [kWideWarps]
+  int64_t* wtok = sm.red + kWideWarps;               // [kWideWarps]
+  if (lane_id() == kWarp - 1) {
+    wsum[wid()] = si;
+    wtok[wid()] = ni;
+  }
+  __syncthreads();
+  double ex_s = 0.0;
+  int64_t ex_n = 0;
+  for (int q = 0; q < wid(); ++q) {
+    ex_s = __dadd_ru(ex_s, wsum[q]);
+    ex_n += wtok[q];
+  }
+  {
+    const double ps = __shfl_up_sync(kFull, si, 1);
+    const int64_t pn = __shfl_up_sync(kFull, ni, 1);
+    if (lane_id() > 0) {
+      ex_s = __dadd_ru(ex_s, ps);
+      ex_n += pn;
+    }
+  }
+  __syncthreads();
+  int my_ok = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int k = k0 + q;
+    if (k < K) {
+      const double S = __dadd_ru(ex_s, s_loc[q]);
+      const int64_t N = ex_n + n_loc[q];
+      const double slack = __dsub_rd(tb0, S);
+      const double need = __dmul_ru(__dmul_ru(static_cast<double>(k), 0x1p-52), tb0);
+      if (N <= tok0 && slack >= need) my_ok++;
+    }
+  }
+  const int m = static_cast<int>(block_sum(my_ok, sm));
+  if (m == 0) return 0;
+  int64_t ctx_part = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int k = k0 + q;
+    if (k < m) {
+      sm.wtake[k] = static_cast<int32_t>(sm.wnw[k] & 0x7fffffffu);
+      ctx_part += sm.wcx[k];
+    }
+    if (k == m - 1) sm.bcast[6] = ex_n + n_loc[q];  // tokens of the prefix
+  }
+  const int64_t ctx_sum = block_sum(ctx_part, sm);  // (barriers publish bcast[6])
+  if (threadIdx.x == 0) {
+    const int64_t n_m = sm.bcast[6];
+    double tb = st.tb;
+    int k = 0;
+    for (; k + 4 <= m; k += 4) {
+      const double a0 = sm.wtc[k], a1 = sm.wtc[k + 1], a2 = sm.wtc[k + 2], a3 = sm.wtc[k + 3];
+      tb = dsub(dsub(dsub(dsub(tb, a0), a1), a2), a3);
+    }
+    for (; k < m; ++k) tb = dsub(tb, sm.wtc[k]);
+    st.tb = tb;
+    st.tok -= n_m;
+    st.E += m;
+    st.tn += n_m;
+    st.tctx += ctx_sum;
+    st.n_seen += m;
+  }
+  __syncthreads();
+  return m;
+}
+
+// Greedy pass over one sorted window (sched.cpp:129-232), thread 0.  The
+// scan state lives in registers for the loop.
+__device__ __forceinline__ void wide_scan_window(WideScan& st_io, int K, int policy,
+                                                 const FormCfg& f, int n_dec, double tc_min,
+                                                 double cc_min, WideSmem& sm, int k_start = 0) {
   if (threadIdx.x != 0) return;
+  WideScan st = st_io;
   const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+  if (fair) {
+    // consider (sched.cpp:129-166).  The stop test depends only on the
+    // budgets, which change only on an admission, so it is evaluated on entry
+    // and after each admission -- the same points at which the reference's
+    // per-task test could first fail.
+    double tb = st.tb;
+    int64_t tok = st.tok;
+    auto exhausted = [&]() -> bool {
+      if (tok <= 0 || tb < 0.0) return true;
+      if (tb < tc_min) {  // no task fits whole any more: stop if none can chunk
+        const double lim = ddiv(dsub(tb, cc_min), f.b);
+        const double dt = static_cast<double>(tok);
+        const double cpr = lim < dt ? lim : dt;
+        if (!(cc_min <= tb && floor(cpr) >= 1.0)) return true;
+      }
+      return false;
+    };
+    bool done = st.done || exhausted();
+    int k = k_start;
+    if (!done && k < K) {
+      double tc_n = sm.wtc[k], cc_n = sm.wcc[k];
+      uint32_t w_n = sm.wnw[k];
+      for (; k < K; ++k) {
+        const double tc = tc_n, cc = cc_n;
+        const int64_t nv = w_n & 0x7fffffffu;
+        if (k + 1 < K) {  // software prefetch of the next sorted task
+          tc_n = sm.wtc[k + 1];
+          cc_n = sm.wcc[k + 1];
+          w_n = sm.wnw[k + 1];
+        }
+        int64_t take = 0;
+        if (tc <= tb && nv <= tok) {
+          take = nv;
+          tb = dsub(tb, tc);
+          tok -= nv;
+        } else if (tok > 0 && cc <= tb) {
+          const double lim = ddiv(dsub(tb, cc), f.b);
+          const double dt = static_cast<double>(tok);
+          const double cp_real = lim < dt ? lim : dt;
+          const int64_t cp = static_cast<int64_t>(floor(cp_real));
+          if (cp >= 1) {
+            take = cp;
+            tb = dsub(tb, dadd(dmul(f.b, static_cast<double>(cp)), cc));
+            tok -= cp;
+          }
+        }
+        if (take > 0) {
+          sm.wtake[k] = static_cast<int32_t>(take);
+          st.E++;
+          st.tn += take;
+          st.tctx += sm.wcx[k];
+          if (exhausted()) {
+            ++k;
+            done = true;
+            break;
+          }
+        }
+      }
+    }
+    st.n_seen += k - k_start;
+    st.tb = tb;
+    st.tok = tok;
+    st.done = done;
+    st_io = st;
+    return;
+  }
   for (int k = 0; k < K && !st.done; ++k) {
     const uint32_t w = sm.wnw[k];
     const int64_t nv = w & 0x7fffffffu;
     int64_t take = 0;
-    if (fair) {
-      if (st.tok <= 0 || st.tb < 0.0) {
-        st.done = true;
-        break;
-      }
-      if (st.tb < tc_min) {  // no task fits whole any more: stop if none can chunk
-        const double lim = ddiv(dsub(st.tb, cc_min), f.b);
-        const double dt = static_cast<double>(st.tok);
-        const double cpr = lim < dt ? lim : dt;
-        if (!(cc_min <= st.tb && floor(cpr) >= 1.0)) {
-          st.done = true;
-          break;
-        }
-      }
-      const double tc = sm.wtc[k], cc = sm.wcc[k];
-      if (tc <= st.tb && nv <= st.tok) {
-        take = nv;
-        st.tb = dsub(st.tb, tc);
-        st.tok -= nv;
-      } else if (st.tok > 0 && cc <= st.tb) {
-        const double lim = ddiv(dsub(st.tb, cc), f.b);
-        const double dt = static_cast<double>(st.tok);
-        const double cp_real = lim < dt ? lim : dt;
-        const int64_t cp = static_cast<int64_t>(floor(cp_real));
-        if (cp >= 1) {
-          take = cp;
-          st.tb = dsub(st.tb, dadd(dmul(f.b, static_cast<double>(cp)), cc));
-          st.tok -= cp;
-        }
-      }
+    if (false) {
     } else if (policy == FB_POLICY_SARATHI) {
       if (st.n_seen < n_dec) {
         take = 1;
@@ -364,6 +687,7 @@ __device__ void wide_scan_window(WideScan& st, int K, int policy, const FormCfg&
       st.tctx += sm.wcx[k];
     }
   }
+  st_io = st;
 }
 
 // Node::complete_step (engine.cpp:204-254), block-wide.
@@ -512,7 +836,9 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   const DevInst* I = w.I;
   const WideScratch ws = wide_scratch(P, w);
   w.S.paths |= kPathWide;
+  WPROF_START
   if (w.S.pulled < w.S.arr) wide_pull(P, w, now, ws, sm);
+  WPROF(0)
   const int64_t A64 = visible_count(w);
   if (A64 == 0) return;
   const int A = static_cast<int>(A64);
@@ -520,31 +846,55 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
   const int64_t n_act = w.S.n_active;
 
-  // K1: one streaming pass over the views
-  int64_t l_tpot = kInf, l_dec = kInf, l_ctx = kInf, l_ndec = 0, l_bad = 0;
-  for (int64_t p = threadIdx.x; p < A; p += kWideThreads) {
-    const View v = load_view(P, w, p, now);
-    const bool fits = v.seq >= 0 && v.seq < kPackSeq &&
-                      (!fair || (v.slack >= -kPackSlack && v.slack < kPackSlack));
-    l_bad |= !fits;
-    const uint64_t sl = fair ? static_cast<uint64_t>(v.slack + kPackSlack) : 0;
-    ws.klow[p] = (v.decode ? (uint64_t(1) << 63) : 0) | (sl << 22) | static_cast<uint64_t>(v.seq);
-    ws.cx[p] = v.ctx;
-    ws.nwv[p] = static_cast<uint32_t>(v.nw);
-    ws.mark[p] = 0;
-    if (p < n_act) w.vl[p].y = 0;  // takes are rewritten for admitted tasks below
-    l_tpot = v.tpot < l_tpot ? v.tpot : l_tpot;
-    l_ctx = v.ctx < l_ctx ? v.ctx : l_ctx;
-    if (v.decode) {
-      l_ndec++;
-      l_dec = v.slack < l_dec ? v.slack : l_dec;
+  // K1: one streaming pass over the views, U views in flight per thread.
+  // Writes the key stem per view; everything else a selected task needs is
+  // re-read for the (few) selected tasks only.
+  constexpr int U = 4;
+  int64_t mn[7] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf};  // see below
+  int64_t l_cnt = 0;  // n_dec | bad << 40
+  for (int64_t b0 = 0; b0 < A; b0 += kWideThreads * U) {
+    View v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+      if (p < A) v[j] = load_view(P, w, p, now);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+      if (p >= A) continue;
+      const bool fits = v[j].seq >= 0 && v[j].seq < kPackSeq &&
+                        (!fair || (v[j].slack >= -kPackSlack && v[j].slack < kPackSlack));
+      if (!fits) l_cnt |= int64_t(1) << 40;
+      const uint64_t sl = fair ? static_cast<uint64_t>(v[j].slack + kPackSlack) : 0;
+      ws.klow[p] = (v[j].decode ? (uint64_t(1) << 63) : 0) | (sl << 22) |
+                   static_cast<uint64_t>(v[j].seq);
+      if (p < n_act) w.vl[p].y = 0;  // takes are rewritten for admitted tasks below
+      const int64_t ord = fair ? v[j].slack : v[j].seq;  // selection ordinal
+      mn[0] = v[j].tpot < mn[0] ? v[j].tpot : mn[0];
+      mn[2] = v[j].ctx < mn[2] ? v[j].ctx : mn[2];
+      if (v[j].decode) {
+        l_cnt++;
+        mn[1] = v[j].slack < mn[1] ? v[j].slack : mn[1];
+        mn[3] = ord < mn[3] ? ord : mn[3];
+        mn[4] = -ord < mn[4] ? -ord : mn[4];
+      } else {
+        mn[5] = ord < mn[5] ? ord : mn[5];
+        mn[6] = -ord < mn[6] ? -ord : mn[6];
+      }
     }
   }
-  const int64_t min_tpot = block_min(l_tpot, sm);
-  const int64_t min_dec = block_min(l_dec, sm);
-  const int64_t ctx_min = block_min(l_ctx, sm);
-  const int64_t n_dec = block_sum(l_ndec, sm);
-  if (block_sum(l_bad, sm) != 0) {  // keys outside the packed range: not supported here
+  // mins of: tpot, decode slack, ctx, decode ordinal, -decode ordinal,
+  // prefill ordinal, -prefill ordinal
+  block_min_n<7>(mn, sm);
+  const int64_t cnt = block_sum(l_cnt, sm);
+  const int64_t min_tpot = mn[0];
+  WPROF(1)
+  WPROF_COUNT(10, 1)
+  const int64_t min_dec = mn[1];
+  const int64_t ctx_min = mn[2];
+  const int64_t n_dec = cnt & ((int64_t(1) << 40) - 1);
+  if ((cnt >> 40) != 0) {  // keys outside the packed range: not supported here
     w.S.status = FB_ERR_VALIDATION;
     w.S.done = 1;
     return;
@@ -555,6 +905,23 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
     const int64_t init = n_dec == 0 ? min_tpot : (min_dec > min_tpot ? min_dec : min_tpot);
     urgency = init + min_tpot;
     init_ms = us_to_ms(init);
+  }
+  SelBins sb;
+  {
+    const int64_t dlo = mn[3], dhi = -mn[4], plo = mn[5], phi = -mn[6];
+    if (fair) {
+      sel_range(sb, 0, dlo, dhi < urgency - 1 ? dhi : urgency - 1);
+      sel_range(sb, 1, plo, phi);
+      sel_range(sb, 2, dlo > urgency ? dlo : urgency, dhi);
+    } else if (policy == FB_POLICY_SARATHI) {
+      sel_range(sb, 0, dlo, dhi);
+      sel_range(sb, 1, plo, phi);
+      sel_range(sb, 2, 0, 0);
+    } else {
+      sel_range(sb, 0, dlo < plo ? dlo : plo, dhi > phi ? dhi : phi);
+      sel_range(sb, 1, 0, 0);
+      sel_range(sb, 2, 0, 0);
+    }
   }
   const FormCfg f{policy, I->max_chunk, I->token_budget, I->sa, I->sb, I->sc};
   const double cc_min = dmul(f.c, static_cast<double>(ctx_min));
@@ -577,15 +944,20 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   uint64_t lo = 0;
   uint64_t esum = 0;
   int E_before = 0, Ew_before = 0;
+  int64_t l_pmax = -1;  // last view position of an admitted waiting task
   const bool log_on = P.log_on != 0;
   const int64_t entry_base = I->log_entry_off + w.S.log_entries;
   for (;;) {
-    const int K = wide_select(ws, A, has_lo, lo, policy, urgency, sm);
+    WPROF(1)
+    int K = wide_select_binned(ws, A, has_lo, lo, policy, urgency, sb, sm);
+    if (K < 0) K = wide_select(ws, A, has_lo, lo, policy, urgency, sm);
+    WPROF(2)
+    WPROF_COUNT(9, 1)
     if (K == 0) break;
     for (int k = threadIdx.x; k < K; k += kWideThreads) {
-      const int p = sm.wpos[k];
-      const uint32_t nwp = ws.nwv[p];
-      const int64_t cxp = ws.cx[p];
+      const View v = load_view(P, w, sm.wpos[k], now);
+      const uint32_t nwp = static_cast<uint32_t>(v.nw);
+      const int64_t cxp = v.ctx;
       const double cc = dmul(f.c, static_cast<double>(cxp));
       sm.wcc[k] = cc;
       sm.wcx[k] = cxp;
@@ -594,12 +966,16 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
       sm.wtake[k] = 0;
     }
     __syncthreads();
+    WPROF(3)
+    const int m0 = fair ? wide_admit_prefix(st, K, sm) : 0;
+    WPROF(11)
     if (threadIdx.x == 0) {
-      wide_scan_window(st, K, policy, f, static_cast<int>(n_dec), tc_min, cc_min, ws, sm);
+      wide_scan_window(st, K, policy, f, static_cast<int>(n_dec), tc_min, cc_min, sm, m0);
       sm.ibcast[7] = st.done ? 1 : 0;
     }
     __syncthreads();
     const bool done = sm.ibcast[7] != 0;
+    WPROF(4)
     // plan bookkeeping for this window, in admission order
     for (int k0 = 0; k0 < K; k0 += kWideThreads) {
       const int k = k0 + threadIdx.x;
@@ -625,12 +1001,14 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
         } else {
           ws.vtmp[Ew_before + widx] = make_int2(r, take);
           ws.mark[p] = 1;
+          l_pmax = p > l_pmax ? p : l_pmax;
         }
       }
       E_before += tot;
       Ew_before += totw;
     }
     __syncthreads();
+    WPROF(5)
     if (done || K < kWideWin) break;
     has_lo = true;
     lo = sm.wkey[K - 1];
@@ -651,16 +1029,24 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   // waiting -> active in plan order (engine.cpp:176-182): admitted waiting
   // are already in vtmp[0, n_w); the rest of the visible waiting follow in
   // their old order, then everything is copied back.
+  WPROF(5)
   const int n_w = Ew_before;
   if (n_w > 0) {
+    // Only [n_act, H) changes, H = one past the last admitted waiting task:
+    // [n_act, n_act + n_w) takes the admitted in plan order (already in
+    // vtmp), then the unadmitted of the range in their old order.  Marks are
+    // cleared on the way (they are all-zero between steps).
+    const int64_t nl_pmax = -block_min(-l_pmax, sm);
+    const int64_t H = nl_pmax + 1;
     int64_t run = 0;
-    for (int64_t b = n_act; b < A64; b += kWideThreads) {
+    for (int64_t b = n_act; b < H; b += kWideThreads) {
       const int64_t p = b + threadIdx.x;
       int2 v = make_int2(0, 0);
       bool un = false;
-      if (p < A64) {
+      if (p < H) {
         v = w.vl[p];
         un = ws.mark[p] == 0;
+        if (!un) ws.mark[p] = 0;
       }
       int tot;
       const int pos = block_excl_count(un, tot, sm);
@@ -668,10 +1054,10 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
       run += tot;
     }
     __syncthreads();
-    for (int64_t q = threadIdx.x; q < A64 - n_act; q += kWideThreads) w.vl[n_act + q] = ws.vtmp[q];
+    for (int64_t q = threadIdx.x; q < H - n_act; q += kWideThreads) w.vl[n_act + q] = ws.vtmp[q];
     __syncthreads();
   }
-
+  WPROF(6)
   // ground_truth_step_time_ms, costmodel.cpp:138-146
   double actual = predict_ms(I->ta, I->tb, I->tc, tn, tctx);
   const double amp = I->noise_amp;
@@ -710,6 +1096,7 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   w.S.busy = 1;
   w.S.step_end = now + dur;
   w.S.step_counter++;
+  WPROF(7)
   __syncthreads();
 }
 
@@ -718,6 +1105,10 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
 __device__ void wide_run(const EngineParams& P, Inst& w, WideSmem& sm) {
   const int64_t* arrival = P.arrival + w.toff;
   if (w.S.pending_begin) {
+    // escalation: the admitted-waiting marks start all-zero
+    const WideScratch ws = wide_scratch(P, w);
+    for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) ws.mark[q] = 0;
+    __syncthreads();
     w.S.pending_begin = 0;
     wide_begin(P, w, w.S.t_last, sm);
     if (w.S.done) return;
@@ -745,7 +1136,11 @@ __device__ void wide_run(const EngineParams& P, Inst& w, WideSmem& sm) {
       return;
     }
     w.S.t_last = t;
-    if (w.S.busy && t_step == t) wide_complete(P, w, sm);
+    if (w.S.busy && t_step == t) {
+      WPROF_START
+      wide_complete(P, w, sm);
+      WPROF(8)
+    }
     while (w.S.arr < w.nreq && arrival[w.S.arr] == t) w.S.arr++;
     if (!w.S.busy && t < w.horizon) {
       wide_begin(P, w, t, sm);

@@ -122,6 +122,8 @@ def lib() -> C.CDLL:
         "fb_cluster_shard_wait": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "fb_cluster_shard_fetch": (C.c_int, [vp, vp, vp, vp, pi64, C.POINTER(C.c_int32)]),
         "fb_cluster_shard_destroy": (None, [vp]),
+        "fb_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+        "fb_host_free": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -142,6 +144,42 @@ def device_count() -> int:
     n = C.c_int(0)
     _check(lib().fb_device_count(C.byref(n)), "fb_device_count")
     return n.value
+
+
+# ------------------------------------------------------------ pinned host memory
+
+class _Pinned:
+    """Owner of one fb_host_alloc block (freed when the last view dies)."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        _check(lib().fb_host_alloc(max(1, nbytes), C.byref(p)), "fb_host_alloc")
+        self.ptr = p.value
+        self.nbytes = nbytes
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            try:
+                lib().fb_host_free(C.c_void_p(self.ptr))
+            except Exception:
+                pass
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in page-locked host memory (direct DMA through the C ABI)."""
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+    owner = _Pinned(n * dtype.itemsize)
+    buf = (C.c_char * max(1, n * dtype.itemsize)).from_address(owner.ptr)
+    buf._fb_owner = owner  # keeps the block alive as long as any view
+    return np.frombuffer(buf, dtype=dtype, count=n).reshape(shape)
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    out = pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
 
 
 # ------------------------------------------------------------ trace generation
@@ -307,11 +345,18 @@ class Arena:
         _check(self._lib.fb_arena_fetch_results(self._h, _abi.vptr(out)), "fb_arena_fetch_results")
         return out[:self.n_instances]
 
-    def records(self) -> np.ndarray:
+    def records(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Per-request records; `out` (e.g. from pinned_empty) is filled in place."""
         n = self._lib.fb_arena_record_rows(self._h)
-        out = np.zeros(max(1, n), _abi.RECORD_DTYPE)
+        if out is None:
+            out = np.empty(max(1, n), _abi.RECORD_DTYPE)
+        elif out.dtype != _abi.RECORD_DTYPE or len(out) < n or not out.flags.c_contiguous:
+            raise ValueError("records out: need a contiguous RECORD_DTYPE array of n_rec rows")
         _check(self._lib.fb_arena_fetch_records(self._h, _abi.vptr(out)), "fb_arena_fetch_records")
         return out[:n]
+
+    def record_rows(self) -> int:
+        return int(self._lib.fb_arena_record_rows(self._h))
 
     def paths(self) -> np.ndarray:
         """Per instance FB_PATH_* bits: 1 register-resident, 2 warp memory, 4 CTA-wide."""

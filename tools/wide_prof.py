@@ -1,0 +1,33 @@
+"""Phase breakdown of the CTA-wide engine on C4 (dev tool).
+    tools/build_variant.sh wprof -DFB_WIDE_PROF
+    FBGPU_LIB=build/variants/wprof/libfbgpu.so python tools/wide_prof.py [n_inst]"""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_14392_b200 import fbgpu, workloads  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+batch = workloads.c4_batch(n_inst=n)
+a = fbgpu.Arena(0)
+a.load(batch)
+L = fbgpu.lib()
+buf = (C.c_ulonglong * 16)()
+a.run()
+a.synchronize()
+L.fb_debug_wide_prof(buf, 1)
+a.reset()
+a.run()
+a.synchronize()
+ms = a.last_run_ms()
+L.fb_debug_wide_prof(buf, 1)
+names = ["pull", "K1 views", "K2 select", "cost gather", "K3 scan", "bookkeeping", "moves",
+         "tail", "complete", "", "", "K3 prefix"]
+tot = sum(buf[i] for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 11))
+steps = buf[10]
+print(f"{n} instances, {ms:.3f} ms, {steps} wide steps, {buf[9]} windows")
+for i, nm in enumerate(names):
+    if not nm:
+        continue
+    print(f"  {nm:12s} {100 * buf[i] / max(tot, 1):5.1f}%  {buf[i] / max(steps, 1) / 1965:8.2f} us/step")
