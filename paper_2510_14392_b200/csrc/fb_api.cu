@@ -126,6 +126,13 @@ struct fb_arena {
   DevBuf<int64_t> wide_list;
   DevBuf<int64_t> order;
   DevBuf<fb_record> recbuf;  // device-packed records (AoS) for one D2H
+  // grid-wide wide engine
+  DevBuf<unsigned char> wg_slots;
+  DevBuf<int64_t> wg_partial;
+  DevBuf<uint32_t> wg_hist;
+  DevBuf<uint64_t> wg_ckey;
+  DevBuf<int32_t> wg_cpos;
+  DevBuf<unsigned long long> wg_bar;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
   // Pinned staging for copies from / to pageable host memory: two chunks,
@@ -237,6 +244,12 @@ struct fb_arena {
     P.wide_list = wide_list.p;
     P.order = order.p;
     P.max_events = max_events <= 0 ? INT64_MAX : max_events;
+    P.wg.slots = wg_slots.p;
+    P.wg.partial = wg_partial.p;
+    P.wg.hist = wg_hist.p;
+    P.wg.ckey = wg_ckey.p;
+    P.wg.cpos = wg_cpos.p;
+    P.wg.bar = wg_bar.p;
     return P;
   }
 
@@ -249,6 +262,8 @@ struct fb_arena {
     wide_list.release();
     order.release();
     recbuf.release();
+    wg_slots.release(); wg_partial.release(); wg_hist.release(); wg_ckey.release();
+    wg_cpos.release(); wg_bar.release();
     for (int b = 0; b < 2; ++b) {
       if (stage_ev[b]) cudaEventSynchronize(stage_ev[b]), cudaEventDestroy(stage_ev[b]);
       if (stage[b]) cudaFreeHost(stage[b]);
@@ -394,6 +409,15 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   ENSURE(a->log_steps, n_instances * static_cast<int64_t>(lo.step_cap));
   ENSURE(a->log_entries, n_instances * static_cast<int64_t>(lo.entry_cap));
   ENSURE(a->log_rejects, n_instances * static_cast<int64_t>(lo.reject_cap));
+  {
+    const fbgpu::WideGridSizes z = fbgpu::wide_grid_sizes(a->geo, n_rec);
+    ENSURE(a->wg_slots, z.slot_bytes);
+    ENSURE(a->wg_partial, z.partial_rows);
+    ENSURE(a->wg_hist, z.hist_words);
+    ENSURE(a->wg_ckey, z.cand_rows);
+    ENSURE(a->wg_cpos, z.cand_rows);
+    ENSURE(a->wg_bar, 4);  // barrier + three chunk counters
+  }
 #undef ENSURE
   std::vector<unsigned char> hinst(static_cast<size_t>(n_instances) * fbgpu::dev_inst_bytes());
   for (int64_t i = 0; i < n_instances; ++i)

@@ -602,6 +602,14 @@ extern "C" int fb_debug_wide_prof(unsigned long long* out, int reset) {
   }
   return static_cast<int>(cudaDeviceSynchronize());
 }
+extern "C" int fb_debug_cta_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_cta_prof, sizeof(unsigned long long) * 256 * 4);
+  if (reset) {
+    static unsigned long long z[256 * 4] = {};
+    cudaMemcpyToSymbol(g_cta_prof, z, sizeof(z));
+  }
+  return static_cast<int>(cudaDeviceSynchronize());
+}
 #endif
 
 cudaError_t launch_pack_records(const EngineParams& p, fb_record* out, cudaStream_t st) {
@@ -625,10 +633,25 @@ EngineGeometry engine_geometry(int device) {
   g.blocks = sms * per_sm;
   g.wide_threads = kWideThreads;
   g.wide_smem = sizeof(WideSmem);
-  g.wide_blocks = sms;
-  cudaFuncSetAttribute(wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(wide_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(g.wide_smem));
+  int wide_per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wide_per_sm, wide_grid_kernel, g.wide_threads,
+                                                g.wide_smem);
+  if (wide_per_sm < 1) wide_per_sm = 1;
+  g.wide_blocks = sms * wide_per_sm < kWgMaxSlots ? sms * wide_per_sm : kWgMaxSlots;
   return g;
+}
+
+WideGridSizes wide_grid_sizes(const EngineGeometry& g, int64_t n_rec) {
+  WideGridSizes z;
+  z.slot_bytes = sizeof(WideSlot) * static_cast<size_t>(g.wide_blocks);
+  // one partial row per (CTA, slot)
+  (void)n_rec;
+  z.partial_rows = static_cast<size_t>(g.wide_blocks) * g.wide_blocks * kK1Vals;
+  z.hist_words = static_cast<size_t>(g.wide_blocks) * kSelBins;
+  z.cand_rows = static_cast<size_t>(g.wide_blocks) * kWideWin;
+  return z;
 }
 
 void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
@@ -730,9 +753,14 @@ cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaSt
   cudaMemsetAsync(p.work, 0, 3 * sizeof(unsigned long long), st);
   engine_kernel<<<g.blocks, g.threads, g.smem, st>>>(p);
   // Escalated instances (more than kEscalateLive live requests) continue on
-  // the CTA-wide engine; with none escalated every CTA exits at once.
-  wide_kernel<<<g.wide_blocks, g.wide_threads, g.wide_smem, st>>>(p);
-  return cudaGetLastError();
+  // the grid-wide wide engine; with none escalated it exits after one barrier.
+  cudaMemsetAsync(p.wg.bar, 0, sizeof(unsigned long long), st);
+  EngineParams pp = p;
+  void* args[] = {&pp};
+  // cooperative: every CTA must be co-resident for the grid barriers
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(wide_grid_kernel),
+                                     dim3(g.wide_blocks), dim3(g.wide_threads), args,
+                                     g.wide_smem, st);
 }
 
 // ------------------------------------------------- pure scheduler kernels

@@ -12,6 +12,16 @@ namespace fbgpu {
 struct DevInst;
 struct DevState;
 
+// Buffers of the grid-wide wide engine (fb_wide.cuh), one slot per CTA.
+struct WideGridBufs {
+  void* slots;               // WideSlot[n_slots]
+  int64_t* partial;          // [max_chunks][8] K1 partial reductions
+  uint32_t* hist;            // [n_slots][kSelBins]
+  uint64_t* ckey;            // [n_slots][kWideWin] gathered window keys
+  int32_t* cpos;             // [n_slots][kWideWin] their view positions
+  unsigned long long* bar;   // grid barrier counter (zeroed per launch)
+};
+
 // Everything the engine kernel touches, as device pointers.
 struct EngineParams {
   const DevInst* inst;
@@ -45,6 +55,7 @@ struct EngineParams {
   int64_t* wide_list;
   const int64_t* order;  // work-queue order (longest predicted instance first); may be null
   int64_t max_events;  // per instance per launch
+  WideGridBufs wg;
 };
 
 // Per-launch geometry of the persistent engine kernel.
@@ -52,10 +63,15 @@ struct EngineGeometry {
   int blocks;
   int threads;
   size_t smem;
-  int wide_blocks;  // CTA-wide engine: one CTA per SM
+  int wide_blocks;  // grid-wide wide engine: one cooperative CTA (slot) per SM
   int wide_threads;
   size_t wide_smem;
 };
+// Sizes of the grid-wide wide engine's buffers for a given geometry.
+struct WideGridSizes {
+  size_t slot_bytes, partial_rows, hist_words, cand_rows;
+};
+WideGridSizes wide_grid_sizes(const EngineGeometry& g, int64_t n_rec);
 
 EngineGeometry engine_geometry(int device);
 size_t scratch_bytes_per_slot();

@@ -25,6 +25,7 @@ namespace fbgpu {
 // -DFB_WIDE_PROF): thread 0 accumulates clock64 deltas per phase.
 #ifdef FB_WIDE_PROF
 __device__ unsigned long long g_wide_prof[16];
+__device__ unsigned long long g_cta_prof[256][4];  // per CTA busy clocks: K1, hist, gather, owner
 #define WPROF_START long long wp_t_ = clock64();
 #define WPROF(slot)                                                               \
   if (threadIdx.x == 0) {                                                         \
@@ -145,15 +146,17 @@ __device__ __forceinline__ void block_min_n(int64_t (&v)[N], WideSmem& sm) {
     for (int i = 0; i < N; ++i) sm.red[wid() * kRed + i] = v[i];
   }
   __syncthreads();
+  if (wid() == 0) {  // lane q of warp 0 folds warp q's partials
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    int64_t x = kInf;
-    for (int q = 0; q < kWideWarps; ++q) {
-      const int64_t y = sm.red[q * kRed + i];
-      x = y < x ? y : x;
+    for (int i = 0; i < N; ++i) {
+      int64_t x = lane_id() < kWideWarps ? sm.red[lane_id() * kRed + i] : kInf;
+      x = warp_min(x);
+      if (lane_id() == 0) sm.red[kWideWarps * kRed - kRed + i] = x;  // last row: results
     }
-    v[i] = x;
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = sm.red[kWideWarps * kRed - kRed + i];
   __syncthreads();
 }
 
@@ -364,7 +367,8 @@ __device__ __forceinline__ void sel_range(SelBins& b, int g, int64_t lo, int64_t
 // then a gather of every key in the bins up to the last one whose inclusive
 // count still fits -- followed by the shared-memory bitonic sort.  Returns
 // the window size, or -1 when the first nonempty bin alone overflows the
-// window (the caller falls back to the exact radix select).
+// window (the caller falls back to the exact radix select).  sm.ibcast[1]
+// tells whether the window holds every remaining key.
 __device__ int wide_select_binned(const WideScratch& ws, int A, bool has_lo, uint64_t lo,
                                   int policy, int64_t urgency, const SelBins& sb,
                                   WideSmem& sm) {
@@ -394,6 +398,7 @@ __device__ int wide_select_binned(const WideScratch& ws, int A, bool has_lo, uin
   for (int q = 0; q < kPer; ++q) loc += static_cast<int>(sm.hist[c0 + q]);
   int tot;
   const int before = block_excl_sum(loc, tot, sm);
+  if (threadIdx.x == 0) sm.ibcast[1] = tot <= kWideWin ? 1 : 0;  // window takes all
   if (tot <= kWideWin) {
     if (threadIdx.x == 0) sm.ibcast[0] = kSelBins - 1;
   } else if (before <= kWideWin && before + loc > kWideWin) {
@@ -409,6 +414,7 @@ __device__ int wide_select_binned(const WideScratch& ws, int A, bool has_lo, uin
   }
   __syncthreads();
   const int bmax = sm.ibcast[0];
+  const int all = sm.ibcast[1];
   if (bmax < 0) return -1;
   for (int b0 = 0; b0 < A; b0 += kWideThreads * U) {
     uint64_t k[U];
@@ -436,6 +442,8 @@ __device__ int wide_select_binned(const WideScratch& ws, int A, bool has_lo, uin
   __syncthreads();
   const int K = sm.ibcast[4];
   wide_sort_window(K, sm);
+  if (threadIdx.x == 0) sm.ibcast[1] = all;
+  __syncthreads();
   return K;
 }
 
@@ -831,45 +839,72 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
   __syncthreads();
 }
 
-// Node::begin_step (engine.cpp:153-202), block-wide.
-__device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem& sm) {
-  const DevInst* I = w.I;
-  const WideScratch ws = wide_scratch(P, w);
-  w.S.paths |= kPathWide;
-  WPROF_START
-  if (w.S.pulled < w.S.arr) wide_pull(P, w, now, ws, sm);
-  WPROF(0)
-  const int64_t A64 = visible_count(w);
-  if (A64 == 0) return;
-  const int A = static_cast<int>(A64);
-  const int policy = w.policy;
-  const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
-  const int64_t n_act = w.S.n_active;
+// ------------------------------------------------ begin_step, in pieces
+//
+// Node::begin_step (engine.cpp:153-202) for an escalated node is split so
+// that its streaming stages (K1 views, K2 histogram + gather) can run on the
+// whole grid while the owner CTA runs the rest:
+//   wide_prepare   pull arrivals (PAB admission), visible count   [owner]
+//   wide_k1_views  K1 over a range of view positions               [any CTA]
+//   wide_step      init_time_budget / urgency / selection bins     [pure]
+//   wide_finish    K2 windows, K3 scan, plan, moves, truth time    [owner]
 
-  // K1: one streaming pass over the views, U views in flight per thread.
-  // Writes the key stem per view; everything else a selected task needs is
-  // re-read for the (few) selected tasks only.
+// K1 partial reductions over a view range: mins of tpot, decode slack, ctx,
+// decode ordinal, -decode ordinal, prefill ordinal, -prefill ordinal, and
+// n_dec | (bad << 40) in [7] (summed).
+constexpr int kK1Vals = 8;
+
+struct WideStep {
+  int64_t A, n_dec, min_tpot, min_dec, ctx_min, urgency;
+  double init_ms;
+  bool bad;
+  SelBins sb;
+};
+
+// Light view context for a K1 range (what load_view needs).
+__device__ __forceinline__ Inst wide_view_ctx(const EngineParams& P, int64_t inst) {
+  Inst w;
+  w.id = inst;
+  w.routed = nullptr;
+  w.I = P.inst + inst;
+  w.toff = w.I->trace_off;
+  w.roff = w.I->rec_off;
+  w.nreq = w.I->n_req;
+  w.horizon = w.I->horizon;
+  w.policy = w.I->policy;
+  w.max_active = w.I->max_active;
+  w.vl = P.vlist + w.roff;
+  w.smem = nullptr;
+  return w;
+}
+
+// K1 over view positions [p_lo, p_hi) by the calling CTA (U views in flight
+// per thread): writes each key stem and leaves the CTA-reduced partials in
+// every thread's r[].
+__device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst& w, int64_t p_lo,
+                                              int64_t p_hi, int64_t now, bool fair,
+                                              int64_t (&r)[kK1Vals], WideSmem& sm) {
+  const WideScratch ws = wide_scratch(P, w);
   constexpr int U = 4;
-  int64_t mn[7] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf};  // see below
-  int64_t l_cnt = 0;  // n_dec | bad << 40
-  for (int64_t b0 = 0; b0 < A; b0 += kWideThreads * U) {
+  int64_t mn[7] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf};
+  int64_t l_cnt = 0;
+  for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
     View v[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-      if (p < A) v[j] = load_view(P, w, p, now);
+      if (p < p_hi) v[j] = load_view(P, w, p, now);
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-      if (p >= A) continue;
+      if (p >= p_hi) continue;
       const bool fits = v[j].seq >= 0 && v[j].seq < kPackSeq &&
                         (!fair || (v[j].slack >= -kPackSlack && v[j].slack < kPackSlack));
       if (!fits) l_cnt |= int64_t(1) << 40;
       const uint64_t sl = fair ? static_cast<uint64_t>(v[j].slack + kPackSlack) : 0;
       ws.klow[p] = (v[j].decode ? (uint64_t(1) << 63) : 0) | (sl << 22) |
                    static_cast<uint64_t>(v[j].seq);
-      if (p < n_act) w.vl[p].y = 0;  // takes are rewritten for admitted tasks below
       const int64_t ord = fair ? v[j].slack : v[j].seq;  // selection ordinal
       mn[0] = v[j].tpot < mn[0] ? v[j].tpot : mn[0];
       mn[2] = v[j].ctx < mn[2] ? v[j].ctx : mn[2];
@@ -884,45 +919,92 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
       }
     }
   }
-  // mins of: tpot, decode slack, ctx, decode ordinal, -decode ordinal,
-  // prefill ordinal, -prefill ordinal
   block_min_n<7>(mn, sm);
   const int64_t cnt = block_sum(l_cnt, sm);
-  const int64_t min_tpot = mn[0];
-  WPROF(1)
+#pragma unroll
+  for (int q = 0; q < 7; ++q) r[q] = mn[q];
+  r[7] = cnt;
+}
+
+// Combines K1 partials (elementwise min of [0,7), sum of [7]).
+__device__ __forceinline__ void wide_k1_combine(int64_t (&acc)[kK1Vals], const int64_t* part) {
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const int64_t v = __ldcg(part + q);  // written by other CTAs: read from L2
+    acc[q] = v < acc[q] ? v : acc[q];
+  }
+  acc[7] += __ldcg(part + 7);
+}
+
+// init_time_budget (sched.cpp:90-106), urgency bound (sched.cpp:111-113) and
+// the selection bins from the reduced K1 values.
+__device__ __forceinline__ WideStep wide_step(const int64_t (&mn)[kK1Vals], int64_t A,
+                                              int policy) {
+  WideStep s;
+  const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+  s.A = A;
+  s.min_tpot = mn[0];
+  s.min_dec = mn[1];
+  s.ctx_min = mn[2];
+  s.n_dec = mn[7] & ((int64_t(1) << 40) - 1);
+  s.bad = (mn[7] >> 40) != 0;
+  s.init_ms = 0.0;
+  s.urgency = 0;
+  if (fair) {
+    const int64_t init =
+        s.n_dec == 0 ? s.min_tpot : (s.min_dec > s.min_tpot ? s.min_dec : s.min_tpot);
+    s.urgency = init + s.min_tpot;
+    s.init_ms = us_to_ms(init);
+  }
+  const int64_t dlo = mn[3], dhi = -mn[4], plo = mn[5], phi = -mn[6];
+  const int64_t urgency = s.urgency;
+  if (fair) {
+    sel_range(s.sb, 0, dlo, dhi < urgency - 1 ? dhi : urgency - 1);
+    sel_range(s.sb, 1, plo, phi);
+    sel_range(s.sb, 2, dlo > urgency ? dlo : urgency, dhi);
+  } else if (policy == FB_POLICY_SARATHI) {
+    sel_range(s.sb, 0, dlo, dhi);
+    sel_range(s.sb, 1, plo, phi);
+    sel_range(s.sb, 2, 0, 0);
+  } else {
+    sel_range(s.sb, 0, dlo < plo ? dlo : plo, dhi > phi ? dhi : phi);
+    sel_range(s.sb, 1, 0, 0);
+    sel_range(s.sb, 2, 0, 0);
+  }
+  return s;
+}
+
+// Pull (engine.cpp:127-151) and the visible count; 0 means no step.
+__device__ int64_t wide_prepare(const EngineParams& P, Inst& w, int64_t now, WideSmem& sm) {
+  w.S.paths |= kPathWide;
+  if (w.S.pulled < w.S.arr) wide_pull(P, w, now, wide_scratch(P, w), sm);
+  return visible_count(w);
+}
+
+// The rest of begin_step once K1 ran.  K0 >= 0: the first window (the K0
+// smallest keys; all of them when all0) is already sorted in sm.wkey /
+// sm.wpos; K0 < 0: select it here.
+__device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const WideStep& ss,
+                            int K0, bool all0, WideSmem& sm) {
+  const DevInst* I = w.I;
+  const WideScratch ws = wide_scratch(P, w);
+  WPROF_START
   WPROF_COUNT(10, 1)
-  const int64_t min_dec = mn[1];
-  const int64_t ctx_min = mn[2];
-  const int64_t n_dec = cnt & ((int64_t(1) << 40) - 1);
-  if ((cnt >> 40) != 0) {  // keys outside the packed range: not supported here
+  if (ss.bad) {  // keys outside the packed range: not supported here
     w.S.status = FB_ERR_VALIDATION;
     w.S.done = 1;
     return;
   }
-  double init_ms = 0.0;
-  int64_t urgency = 0;
-  if (fair) {
-    const int64_t init = n_dec == 0 ? min_tpot : (min_dec > min_tpot ? min_dec : min_tpot);
-    urgency = init + min_tpot;
-    init_ms = us_to_ms(init);
-  }
-  SelBins sb;
-  {
-    const int64_t dlo = mn[3], dhi = -mn[4], plo = mn[5], phi = -mn[6];
-    if (fair) {
-      sel_range(sb, 0, dlo, dhi < urgency - 1 ? dhi : urgency - 1);
-      sel_range(sb, 1, plo, phi);
-      sel_range(sb, 2, dlo > urgency ? dlo : urgency, dhi);
-    } else if (policy == FB_POLICY_SARATHI) {
-      sel_range(sb, 0, dlo, dhi);
-      sel_range(sb, 1, plo, phi);
-      sel_range(sb, 2, 0, 0);
-    } else {
-      sel_range(sb, 0, dlo < plo ? dlo : plo, dhi > phi ? dhi : phi);
-      sel_range(sb, 1, 0, 0);
-      sel_range(sb, 2, 0, 0);
-    }
-  }
+  const int64_t A64 = ss.A;
+  const int A = static_cast<int>(A64);
+  const int policy = w.policy;
+  const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+  const int64_t n_act = w.S.n_active;
+  const int64_t n_dec = ss.n_dec;
+  const int64_t ctx_min = ss.ctx_min;
+  const int64_t urgency = ss.urgency;
+  const double init_ms = ss.init_ms;
+  const SelBins& sb = ss.sb;
   const FormCfg f{policy, I->max_chunk, I->token_budget, I->sa, I->sb, I->sc};
   const double cc_min = dmul(f.c, static_cast<double>(ctx_min));
   const double tc_min = dadd(dmul(f.b, 1.0), cc_min);
@@ -949,8 +1031,18 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   const int64_t entry_base = I->log_entry_off + w.S.log_entries;
   for (;;) {
     WPROF(1)
-    int K = wide_select_binned(ws, A, has_lo, lo, policy, urgency, sb, sm);
-    if (K < 0) K = wide_select(ws, A, has_lo, lo, policy, urgency, sm);
+    int K = K0;
+    bool all = all0;
+    K0 = -1;
+    if (K < 0) {
+      K = wide_select_binned(ws, A, has_lo, lo, policy, urgency, sb, sm);
+      all = sm.ibcast[1] != 0;
+      __syncthreads();
+    }
+    if (K < 0) {
+      K = wide_select(ws, A, has_lo, lo, policy, urgency, sm);
+      all = K < kWideWin;
+    }
     WPROF(2)
     WPROF_COUNT(9, 1)
     if (K == 0) break;
@@ -1009,7 +1101,7 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
     }
     __syncthreads();
     WPROF(5)
-    if (done || K < kWideWin) break;
+    if (done || all) break;
     has_lo = true;
     lo = sm.wkey[K - 1];
     __syncthreads();
@@ -1100,20 +1192,139 @@ __device__ void wide_begin(const EngineParams& P, Inst& w, int64_t now, WideSmem
   __syncthreads();
 }
 
-// run_node's loop for an escalated instance; resumes a begin_step that the
-// warp engine deferred.
-__device__ void wide_run(const EngineParams& P, Inst& w, WideSmem& sm) {
-  const int64_t* arrival = P.arrival + w.toff;
-  if (w.S.pending_begin) {
-    // escalation: the admitted-waiting marks start all-zero
-    const WideScratch ws = wide_scratch(P, w);
-    for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) ws.mark[q] = 0;
-    __syncthreads();
-    w.S.pending_begin = 0;
-    wide_begin(P, w, w.S.t_last, sm);
-    if (w.S.done) return;
+// ------------------------------------------------ grid-wide wide engine
+//
+// Escalated nodes advance in lockstep iterations of one cooperative
+// persistent kernel (one CTA per SM).  CTA b owns slot b: it runs its node's
+// run_node event loop (engine.cpp:266-288) up to the next begin_step, then
+// every CTA of the grid streams the views of every beginning node:
+//
+//   owner  events, complete_step, arrivals, pull            | barrier
+//   grid   K1 views -> key stems + partial reductions       | barrier
+//   grid   K2a histogram of the key bins (bins from the      |
+//          combined K1 reductions: urgency, group ranges)    | barrier
+//   grid   K2b gather of the keys up to the window's last    |
+//          bin (from the node's histogram)                   | barrier
+//   owner  sort, K3 scan (proven prefix + serial tail), plan, moves, truth
+//
+// so the bandwidth-bound K1/K2 passes use all SMs whatever the number of
+// escalated nodes.  Each CTA takes an equal share of the iteration's views
+// (all beginning nodes' views end to end), so the passes are balanced; the
+// per-CTA partial reductions of a node are combined by whoever needs them.
+
+struct WideSlot {
+  int64_t inst;  // instance id, -1 = idle
+  int64_t A, n_act, now;
+  int32_t begin, policy;
+  int32_t ncand, pad;  // K2b: gathered window keys
+};
+
+// What a helper CTA needs of a slot, read from L2 (the slot is written by
+// another CTA).
+struct WgView {
+  int64_t inst, A, now;
+  int32_t policy;
+};
+__device__ __forceinline__ WgView wg_view(const WideSlot* s) {
+  const volatile WideSlot* v = s;
+  WgView o;
+  o.inst = v->inst;
+  o.A = v->A;
+  o.now = v->now;
+  o.policy = v->policy;
+  return o;
+}
+
+__device__ __forceinline__ void wg_barrier(unsigned long long* ctr, uint64_t gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(1ull) : "memory");
+    const uint64_t target = gen * static_cast<uint64_t>(gridDim.x);
+    uint64_t v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
   }
-  for (int64_t ev = 0; ev < P.max_events; ++ev) {
+  // the acquire load invalidates this SM's L1 (CCTL.IVALL), and the CTA
+  // barrier orders every thread's later loads after it
+  __syncthreads();
+}
+
+// Owner: stores the node's state and frees the slot.
+__device__ __forceinline__ void wg_release(const EngineParams& P, Inst& w, bool& have) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    P.state[w.id] = w.S;
+    if (!w.S.done) atomicAdd(&P.work[1], 1ull);
+  }
+  have = false;
+  __syncthreads();
+}
+
+// Owner: publishes a beginning node to the grid.
+__device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w, int64_t A,
+                                           int64_t now, WideSlot* my) {
+  uint32_t* hist = P.wg.hist + static_cast<size_t>(blockIdx.x) * kSelBins;
+  for (int q = threadIdx.x; q < kSelBins; q += kWideThreads) hist[q] = 0;
+  if (threadIdx.x == 0) {
+    my->inst = w.id;
+    my->A = A;
+    my->n_act = w.S.n_active;
+    my->now = now;
+    my->begin = 1;
+    my->policy = w.policy;
+    my->ncand = 0;
+  }
+}
+
+// Owner: runs the node's event loop until it must form a batch (returns
+// true, slot published) or the slot has no node left (returns false).
+__device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& ev,
+                           WideSlot* my, WideSmem& sm) {
+  for (;;) {
+    if (!have) {
+      if (threadIdx.x == 0) sm.bcast[0] = static_cast<int64_t>(atomicAdd(&P.work[2], 1ull));
+      __syncthreads();
+      const int64_t j = sm.bcast[0];
+      __syncthreads();
+      if (j >= static_cast<int64_t>(P.work[3])) {
+        if (threadIdx.x == 0) {
+          my->inst = -1;
+          my->begin = 0;
+        }
+        return false;
+      }
+      const int64_t i = P.wide_list[j];
+      w = wide_view_ctx(P, i);
+      w.S = P.state[i];
+      if (w.S.done) continue;
+      have = true;
+      ev = 0;
+      if (w.S.pending_begin) {
+        // escalation: admitted-waiting marks all-zero, in-flight takes cleared
+        // (the warp engine's memory path leaves consumed takes behind)
+        const WideScratch ws = wide_scratch(P, w);
+        for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) ws.mark[q] = 0;
+        for (int64_t q = threadIdx.x; q < w.S.n_active; q += kWideThreads) w.vl[q].y = 0;
+        __syncthreads();
+        w.S.pending_begin = 0;
+        const int64_t now = w.S.t_last;
+        const int64_t A = wide_prepare(P, w, now, sm);
+        if (A > 0) {
+          wg_publish(P, w, A, now, my);
+          return true;
+        }
+      }
+    }
+    if (ev >= P.max_events) {
+      wg_release(P, w, have);
+      continue;
+    }
+    ev++;
+    const int64_t* arrival = P.arrival + w.toff;
     if (w.S.busy) {
       // Arrivals strictly before the in-flight step's end only enqueue
       // (run_node's loop neither completes nor begins a step at those
@@ -1133,7 +1344,8 @@ __device__ void wide_run(const EngineParams& P, Inst& w, WideSmem& sm) {
       w.S.done = 1;
       w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0 ||
                         w.S.arr < w.nreq) ? 1 : 0;
-      return;
+      wg_release(P, w, have);
+      continue;
     }
     w.S.t_last = t;
     if (w.S.busy && t_step == t) {
@@ -1143,45 +1355,343 @@ __device__ void wide_run(const EngineParams& P, Inst& w, WideSmem& sm) {
     }
     while (w.S.arr < w.nreq && arrival[w.S.arr] == t) w.S.arr++;
     if (!w.S.busy && t < w.horizon) {
-      wide_begin(P, w, t, sm);
-      if (w.S.done) return;
+      const int64_t A = wide_prepare(P, w, t, sm);
+      if (A > 0) {
+        wg_publish(P, w, A, t, my);
+        return true;
+      }
     }
   }
 }
 
+// Block exclusive prefix sum of int64 values (thread order) plus the total.
+__device__ __forceinline__ int64_t block_excl_sum64(int64_t v, int64_t& total, WideSmem& sm) {
+  int64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < kWarp; o <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane_id() >= o) incl += y;
+  }
+  if (lane_id() == kWarp - 1) sm.red[wid()] = incl;
+  __syncthreads();
+  int64_t before = 0, tot = 0;
+  for (int q = 0; q < kWideWarps; ++q) {
+    const int64_t c = sm.red[q];
+    if (q < wid()) before += c;
+    tot += c;
+  }
+  __syncthreads();
+  total = tot;
+  return before + incl - v;
+}
+
+constexpr int kWgMaxSlots = 256;
+
+// Work split of one iteration: the views of all beginning slots, laid end to
+// end ([v0[t], v0[t+1]) for slot t), cut into gridDim.x equal ranges.
+struct WgSplit {
+  const int64_t* v0;  // smem, n_slots + 1 entries
+  int64_t V;
+  int G, n_slots;
+  __device__ __forceinline__ int64_t lo(int b) const { return (V * b) / G; }
+  // slot holding view x (v0[t] <= x < v0[t+1])
+  __device__ __forceinline__ int slot_of(int64_t x) const {
+    int a = 0, z = n_slots - 1;
+    while (a < z) {
+      const int mid = (a + z + 1) >> 1;
+      if (v0[mid] <= x) a = mid; else z = mid - 1;
+    }
+    return a;
+  }
+  // CTA whose range holds view x
+  __device__ __forceinline__ int cta_of(int64_t x) const {
+    int b = static_cast<int>((x * G) / V);
+    if (b >= G) b = G - 1;
+    while (b + 1 < G && lo(b + 1) <= x) ++b;
+    while (b > 0 && lo(b) > x) --b;
+    return b;
+  }
+};
+
+// Combined K1 reductions of slot t: the partials of every CTA whose range
+// meets the slot (read from L2).
+__device__ __forceinline__ void wg_combine(const EngineParams& P, const WgSplit& sp, int t,
+                                           int64_t (&acc)[kK1Vals]) {
+#pragma unroll
+  for (int k = 0; k < 7; ++k) acc[k] = kInf;
+  acc[7] = 0;
+  const int64_t a = sp.v0[t], z = sp.v0[t + 1];
+  if (z <= a) return;
+  const int b0 = sp.cta_of(a), b1 = sp.cta_of(z - 1);
+  for (int b = b0; b <= b1; ++b) {
+    const int64_t lo = sp.lo(b) > a ? sp.lo(b) : a;
+    const int64_t hi = sp.lo(b + 1) < z ? sp.lo(b + 1) : z;
+    if (hi <= lo) continue;
+    wide_k1_combine(acc, P.wg.partial + (static_cast<int64_t>(b) * sp.n_slots + t) * kK1Vals);
+  }
+}
+
+// The window of slot t from its global histogram: last bin whose inclusive
+// count fits (-1: the first nonempty bin overflows), and whether it holds
+// every key.  Results in every thread.
+__device__ __forceinline__ void wg_window(const EngineParams& P, int t, int& bmax, bool& all,
+                                          WideSmem& sm) {
+  const uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
+  constexpr int kPer = kSelBins / kWideThreads;
+  const int c0 = threadIdx.x * kPer;
+  uint32_t hv[kPer];
+  int loc = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    hv[k] = __ldcg(gh + c0 + k);
+    loc += static_cast<int>(hv[k]);
+  }
+  int tot;
+  const int before = block_excl_sum(loc, tot, sm);
+  if (tot <= kWideWin) {
+    if (threadIdx.x == 0) sm.ibcast[0] = kSelBins - 1;
+  } else if (before <= kWideWin && before + loc > kWideWin) {
+    int cum = before;
+    for (int k = 0; k < kPer; ++k) {
+      const int cnt = static_cast<int>(hv[k]);
+      if (cum + cnt > kWideWin) {
+        sm.ibcast[0] = cum == 0 ? -1 : c0 + k - 1;
+        break;
+      }
+      cum += cnt;
+    }
+  }
+  __syncthreads();
+  bmax = sm.ibcast[0];
+  all = tot <= kWideWin;
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kWideThreads, 1)
-wide_kernel(const __grid_constant__ EngineParams P) {
+wide_grid_kernel(const __grid_constant__ EngineParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WideSmem& sm = *reinterpret_cast<WideSmem*>(smem_raw);
-  __shared__ unsigned long long s_idx;
+  __shared__ int64_t s_v0[kWgMaxSlots + 1];
+  WideSlot* slots = reinterpret_cast<WideSlot*>(P.wg.slots);
+  WideSlot* my = slots + blockIdx.x;
+  const int n_slots = static_cast<int>(gridDim.x);
+  // The owner's node lives in shared memory between owner phases, so it
+  // holds no registers while the CTA streams other nodes' views.
+  __shared__ __align__(16) unsigned char s_wbuf[sizeof(Inst)];
+  Inst& s_w = *reinterpret_cast<Inst*>(s_wbuf);
+  __shared__ int s_have;
+  __shared__ int64_t s_ev;
+  if (threadIdx.x == 0) {
+    s_have = 0;
+    s_ev = 0;
+  }
+  __syncthreads();
+  uint64_t gen = 0;
+#ifdef FB_WIDE_PROF
+  long long gp_t = clock64();
+#define GPROF(slot)                                                                    \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                                           \
+    const long long n_ = clock64();                                                    \
+    atomicAdd(&g_wide_prof[slot], static_cast<unsigned long long>(n_ - gp_t));         \
+    gp_t = n_;                                                                         \
+  }
+#define CPROF_START long long cp_t_ = clock64();
+#define CPROF(k)                                                                       \
+  if (threadIdx.x == 0) g_cta_prof[blockIdx.x][k] += clock64() - cp_t_;
+#else
+#define GPROF(slot)
+#define CPROF_START
+#define CPROF(k)
+#endif
   for (;;) {
-    if (threadIdx.x == 0) s_idx = atomicAdd(&P.work[2], 1ull);
-    __syncthreads();
-    const unsigned long long j = s_idx;
-    __syncthreads();
-    if (j >= P.work[3]) break;
-    const int64_t i = P.wide_list[j];
-    Inst w;
-    w.id = i;
-    w.routed = nullptr;
-    w.I = P.inst + i;
-    w.S = P.state[i];
-    if (w.S.done) continue;
-    w.toff = w.I->trace_off;
-    w.roff = w.I->rec_off;
-    w.nreq = w.I->n_req;
-    w.horizon = w.I->horizon;
-    w.policy = w.I->policy;
-    w.max_active = w.I->max_active;
-    w.vl = P.vlist + w.roff;
-    w.smem = nullptr;
-    wide_run(P, w, sm);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      P.state[i] = w.S;
-      if (!w.S.done) atomicAdd(&P.work[1], 1ull);
+    // ---- owner: advance to the next begin_step
+    {
+      CPROF_START
+      Inst w = s_w;
+      bool have = s_have != 0;
+      int64_t ev = s_ev;
+      wg_advance(P, w, have, ev, my, sm);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_w = w;
+        s_have = have ? 1 : 0;
+        s_ev = ev;
+      }
+      CPROF(3)
     }
-    __syncthreads();
+    wg_barrier(P.wg.bar, ++gen);
+    GPROF(12)
+    // ---- work split (every CTA, from the published slots)
+    WgSplit sp;
+    {
+      int64_t a = 0;
+      if (threadIdx.x < n_slots) {
+        const volatile WideSlot* sl = slots + threadIdx.x;
+        if (sl->inst >= 0 && sl->begin) a = sl->A;
+      }
+      int64_t tot;
+      const int64_t before = block_excl_sum64(a, tot, sm);
+      if (threadIdx.x < n_slots) s_v0[threadIdx.x] = before;
+      if (threadIdx.x == 0) s_v0[n_slots] = tot;
+      __syncthreads();
+      sp.v0 = s_v0;
+      sp.V = tot;
+      sp.G = static_cast<int>(gridDim.x);
+      sp.n_slots = n_slots;
+    }
+    if (sp.V == 0) break;  // no node left anywhere
+    const int64_t my_lo = sp.lo(blockIdx.x), my_hi = sp.lo(blockIdx.x + 1);
+    const int t_first = my_hi > my_lo ? sp.slot_of(my_lo) : n_slots;
+    // ---- K1: views -> key stems + this CTA's partial reductions per slot
+    {
+      CPROF_START
+      for (int t = t_first; t < n_slots && s_v0[t] < my_hi; ++t) {
+        const int64_t a = s_v0[t] > my_lo ? s_v0[t] : my_lo;
+        const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
+        if (z <= a) continue;
+        const WgView sv = wg_view(slots + t);
+        const Inst wv = wide_view_ctx(P, sv.inst);
+        const bool fair = sv.policy == FB_POLICY_FAIRBATCH || sv.policy == FB_POLICY_FAIRBATCH_PAB;
+        int64_t r[kK1Vals];
+        wide_k1_views(P, wv, a - s_v0[t], z - s_v0[t], sv.now, fair, r, sm);
+        if (threadIdx.x == 0) {
+          int64_t* part =
+              P.wg.partial + (static_cast<int64_t>(blockIdx.x) * n_slots + t) * kK1Vals;
+#pragma unroll
+          for (int k = 0; k < kK1Vals; ++k) part[k] = r[k];
+        }
+      }
+      CPROF(0)
+    }
+    wg_barrier(P.wg.bar, ++gen);
+    GPROF(13)
+    // ---- K2a: histogram of the selection bins
+    {
+      CPROF_START
+      for (int t = t_first; t < n_slots && s_v0[t] < my_hi; ++t) {
+        const int64_t a = s_v0[t] > my_lo ? s_v0[t] : my_lo;
+        const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
+        if (z <= a) continue;
+        const WgView sv = wg_view(slots + t);
+        int64_t acc[kK1Vals];
+        wg_combine(P, sp, t, acc);
+        const WideStep ss = wide_step(acc, sv.A, sv.policy);
+        const Inst wv = wide_view_ctx(P, sv.inst);
+        const WideScratch ws = wide_scratch(P, wv);
+        const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
+        for (int k = threadIdx.x; k < kSelBins; k += kWideThreads) sm.hist[k] = 0;
+        __syncthreads();
+        constexpr int U = 8;
+        for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
+          uint64_t kl[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+            kl[j] = p < p_hi ? __ldcg(ws.klow + p) : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+            if (p < p_hi) atomicAdd(&sm.hist[sel_bin(kl[j], sv.policy, ss.urgency, ss.sb)], 1u);
+          }
+        }
+        __syncthreads();
+        uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
+        for (int k = threadIdx.x; k < kSelBins; k += kWideThreads) {
+          const uint32_t v = sm.hist[k];
+          if (v) atomicAdd(gh + k, v);
+        }
+        __syncthreads();
+      }
+      CPROF(1)
+    }
+    wg_barrier(P.wg.bar, ++gen);
+    GPROF(14)
+    // ---- K2b: gather the window's keys
+    {
+      CPROF_START
+      for (int t = t_first; t < n_slots && s_v0[t] < my_hi; ++t) {
+        const int64_t a = s_v0[t] > my_lo ? s_v0[t] : my_lo;
+        const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
+        if (z <= a) continue;
+        int bmax;
+        bool all;
+        wg_window(P, t, bmax, all, sm);
+        if (bmax < 0) continue;
+        const WgView sv = wg_view(slots + t);
+        int64_t acc[kK1Vals];
+        wg_combine(P, sp, t, acc);
+        const WideStep ss = wide_step(acc, sv.A, sv.policy);
+        const Inst wv = wide_view_ctx(P, sv.inst);
+        const WideScratch ws = wide_scratch(P, wv);
+        const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
+        uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
+        int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
+        int32_t* ncand = &slots[t].ncand;
+        constexpr int U = 8;
+        for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
+          uint64_t kl[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+            kl[j] = p < p_hi ? __ldcg(ws.klow + p) : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+            const bool sel = p < p_hi && sel_bin(kl[j], sv.policy, ss.urgency, ss.sb) <= bmax;
+            const unsigned m = __ballot_sync(kFull, sel);
+            int base = 0;
+            if (m && lane_id() == 0) base = atomicAdd(ncand, __popc(m));
+            base = __shfl_sync(kFull, base, 0);
+            if (sel) {
+              const int slot = base + __popc(m & lanemask_lt());
+              ck[slot] = wide_key(kl[j], sv.policy, ss.urgency);
+              cp[slot] = static_cast<int32_t>(p);
+            }
+          }
+        }
+      }
+      CPROF(2)
+    }
+    wg_barrier(P.wg.bar, ++gen);
+    GPROF(15)
+    // ---- owner: the rest of begin_step
+    if (s_have) {
+      Inst w = s_w;
+      bool have = true;
+      const int t = static_cast<int>(blockIdx.x);
+      const volatile WideSlot* vs = my;
+      int64_t acc[kK1Vals];
+      wg_combine(P, sp, t, acc);
+      const WideStep ss = wide_step(acc, vs->A, w.policy);
+      int bmax;
+      bool all0;
+      wg_window(P, t, bmax, all0, sm);
+      int K0 = -1;
+      if (bmax >= 0) {
+        K0 = vs->ncand;
+        const uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
+        const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
+        for (int k = threadIdx.x; k < K0; k += kWideThreads) {
+          sm.wkey[k] = __ldcg(ck + k);
+          sm.wpos[k] = __ldcg(cp + k);
+        }
+        __syncthreads();
+        wide_sort_window(K0, sm);
+      } else {
+        all0 = false;
+      }
+      wide_finish(P, w, vs->now, ss, K0, all0, sm);
+      __syncthreads();
+      if (w.S.done) wg_release(P, w, have);
+      if (threadIdx.x == 0) {
+        s_w = w;
+        s_have = have ? 1 : 0;
+      }
+      __syncthreads();
+    }
+    GPROF(9)
   }
 }
 
