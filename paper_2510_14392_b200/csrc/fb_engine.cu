@@ -595,9 +595,9 @@ __global__ void pack_records_kernel(const __grid_constant__ EngineParams P, fb_r
 
 #ifdef FB_WIDE_PROF
 extern "C" int fb_debug_wide_prof(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_wide_prof, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_wide_prof, sizeof(unsigned long long) * 24);
   if (reset) {
-    unsigned long long z[16] = {};
+    unsigned long long z[24] = {};
     cudaMemcpyToSymbol(g_wide_prof, z, sizeof(z));
   }
   return static_cast<int>(cudaDeviceSynchronize());

@@ -24,7 +24,7 @@ namespace fbgpu {
 // Dev-only phase timers (tools/wide_prof.py builds a variant with
 // -DFB_WIDE_PROF): thread 0 accumulates clock64 deltas per phase.
 #ifdef FB_WIDE_PROF
-__device__ unsigned long long g_wide_prof[16];
+__device__ unsigned long long g_wide_prof[24];
 __device__ unsigned long long g_cta_prof[256][4];  // per CTA busy clocks: K1, hist, gather, owner
 #define WPROF_START long long wp_t_ = clock64();
 #define WPROF(slot)                                                               \
@@ -69,7 +69,7 @@ struct WideSmem {
 // Per-instance global scratch (72 bytes per request slot, see Scratch).
 struct WideScratch {
   uint64_t* klow;  // [p] decode<<63 | (slack+2^39)<<22 | seq   (stem of the key)
-  int64_t* cx;     // [p] context
+  int64_t* dl0;    // [r] arrival + ttft_slo of request r (filled at escalation)
   int2* vtmp;      // reorder buffer / PAB terms
   uint32_t* nwv;   // [p] new tokens | decode bit
   int32_t* mark;   // [p] admitted-waiting flag
@@ -80,7 +80,7 @@ __device__ __forceinline__ WideScratch wide_scratch(const EngineParams& P, const
   unsigned char* base = P.gscratch + w.roff * kScratchBytesPerSlot;
   const size_t n = static_cast<size_t>(w.nreq);
   s.klow = reinterpret_cast<uint64_t*>(base);
-  s.cx = reinterpret_cast<int64_t*>(base + 8 * n);
+  s.dl0 = reinterpret_cast<int64_t*>(base + 8 * n);
   s.vtmp = reinterpret_cast<int2*>(base + 16 * n);
   s.nwv = reinterpret_cast<uint32_t*>(base + 24 * n);
   s.mark = reinterpret_cast<int32_t*>(base + 28 * n);
@@ -213,32 +213,88 @@ __device__ __forceinline__ uint64_t wide_key(uint64_t klow, int policy, int64_t 
   return seq;
 }
 
-// Ascending bitonic sort of sm.wkey / sm.wpos [0, K) (keys unique).
-__device__ __forceinline__ void wide_sort_window(int K, WideSmem& sm) {
-  int n2 = 1;
-  while (n2 < K) n2 <<= 1;
-  for (int i = K + threadIdx.x; i < n2; i += kWideThreads) {
-    sm.wkey[i] = ~uint64_t(0);
-    sm.wpos[i] = -1;
+// Ascending bitonic sort of sm.wkey / sm.wpos [0, K) (keys unique).  Each
+// thread holds kPerT consecutive elements in registers: strides below kPerT
+// are in-thread compare-exchanges, strides up to one warp's span are
+// shuffles, and only the longer strides go through shared memory (2
+// barriers each) -- 10 of the 66 stages for a full window.
+constexpr int kPerT = kWideWin / kWideThreads;  // 4
+__device__ __forceinline__ void bitonic_cx(uint64_t& a, int32_t& pa, uint64_t b, int32_t pb,
+                                           bool take_min) {
+  const bool sw = take_min ? (b < a) : (b > a);
+  if (sw) {
+    a = b;
+    pa = pb;
+  }
+}
+__device__ void wide_sort_window(int K, WideSmem& sm) {
+  uint64_t k[kPerT];
+  int32_t v[kPerT];
+  const int e0 = threadIdx.x * kPerT;
+#pragma unroll
+  for (int q = 0; q < kPerT; ++q) {
+    const int e = e0 + q;
+    k[q] = e < K ? sm.wkey[e] : ~uint64_t(0);
+    v[q] = e < K ? sm.wpos[e] : -1;
   }
   __syncthreads();
-  for (int k = 2; k <= n2; k <<= 1) {  // bitonic sort (keys unique)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += kWideThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = sm.wkey[i], b = sm.wkey[ixj];
-          const bool asc = (i & k) == 0;
+  constexpr int kWarpSpan = kWarp * kPerT;  // 128 elements per warp
+  for (int kk = 2; kk <= kWideWin; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= kWarpSpan) {
+#pragma unroll
+        for (int q = 0; q < kPerT; ++q) {
+          sm.wkey[e0 + q] = k[q];
+          sm.wpos[e0 + q] = v[q];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kPerT; ++q) {
+          const int e = e0 + q;
+          const bool asc = (e & kk) == 0, lower = (e & j) == 0;
+          bitonic_cx(k[q], v[q], sm.wkey[e ^ j], sm.wpos[e ^ j], lower == asc);
+        }
+        __syncthreads();
+      } else if (j >= kPerT) {
+        const int lm = j / kPerT;  // lane distance
+#pragma unroll
+        for (int q = 0; q < kPerT; ++q) {
+          const int e = e0 + q;
+          const uint64_t b = __shfl_xor_sync(kFull, k[q], lm);
+          const int32_t pb = __shfl_xor_sync(kFull, v[q], lm);
+          const bool asc = (e & kk) == 0, lower = (e & j) == 0;
+          bitonic_cx(k[q], v[q], b, pb, lower == asc);
+        }
+      } else {
+        // in-thread strides (j = 2, 1), register indices fixed at compile time
+        static_assert(kPerT == 4, "in-thread stages assume 4 elements per thread");
+        auto cx = [&](uint64_t& a, int32_t& pa, uint64_t& b, int32_t& pb, int e) {
+          const bool asc = (e & kk) == 0;
           if ((a > b) == asc) {
-            sm.wkey[i] = b;
-            sm.wkey[ixj] = a;
-            const int t = sm.wpos[i];
-            sm.wpos[i] = sm.wpos[ixj];
-            sm.wpos[ixj] = t;
+            const uint64_t tk = a;
+            a = b;
+            b = tk;
+            const int32_t tv = pa;
+            pa = pb;
+            pb = tv;
           }
+        };
+        if (j == 2) {
+          cx(k[0], v[0], k[2], v[2], e0);
+          cx(k[1], v[1], k[3], v[3], e0 + 1);
+        } else {
+          cx(k[0], v[0], k[1], v[1], e0);
+          cx(k[2], v[2], k[3], v[3], e0 + 2);
         }
       }
-      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kPerT; ++q) {
+    const int e = e0 + q;
+    if (e < K) {
+      sm.wkey[e] = k[q];
+      sm.wpos[e] = v[q];
     }
   }
   __syncthreads();
@@ -330,10 +386,13 @@ __device__ int wide_select(const WideScratch& ws, int A, bool has_lo, uint64_t l
 // Linear key bins per group for the binned selection.  bin(key) is
 // nondecreasing in key, so the keys of bins [0, b] are exactly the smallest
 // keys.  Fair batching orders (urgent decode, prefill, relaxed decode) by
-// slack, sarathi (decode, prefill) by seq, prefill-first by seq.
+// (slack, seq) -- the ordinal is the stem's low 62 bits, so equal slacks
+// (a prefill batch's decodes share first-token times) still spread over
+// bins by seq; sarathi (decode, prefill) and prefill-first order by seq.
 struct SelBins {
   int64_t lo[3];
   int32_t sh[3];
+  int64_t urg;  // fair batching: urgency bound as an ordinal
 };
 
 __device__ __forceinline__ int sel_bin(uint64_t klow, int policy, int64_t urgency,
@@ -343,8 +402,8 @@ __device__ __forceinline__ int sel_bin(uint64_t klow, int policy, int64_t urgenc
   int g;
   int64_t ord;
   if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
-    ord = static_cast<int64_t>(low >> 22) - kPackSlack;
-    g = decode ? (ord < urgency ? 0 : 2) : 1;
+    ord = static_cast<int64_t>(low);
+    g = decode ? (ord < b.urg ? 0 : 2) : 1;
   } else {
     ord = static_cast<int64_t>(low & ((uint64_t(1) << 22) - 1));
     g = (policy == FB_POLICY_SARATHI && !decode) ? 1 : 0;
@@ -354,12 +413,20 @@ __device__ __forceinline__ int sel_bin(uint64_t klow, int policy, int64_t urgenc
   return g * kGroupBins + static_cast<int>(d);
 }
 
-__device__ __forceinline__ void sel_range(SelBins& b, int g, int64_t lo, int64_t hi) {
+// Bins of group g over ordinals [lo, hi] holding about `count` keys.  The
+// bin width is chosen so that, at uniform density, one window (kWideWin
+// keys) spans about half the group's bins; ordinals past the last bin are
+// clamped into it (any nondecreasing binning is exact -- the width only sets
+// how full a window gets).
+__device__ __forceinline__ void sel_range(SelBins& b, int g, int64_t lo, int64_t hi,
+                                          int64_t count) {
   b.lo[g] = lo;
-  int sh = 0;
-  if (hi > lo)
-    while (((hi - lo) >> sh) >= kGroupBins) ++sh;
-  b.sh[g] = sh;
+  int64_t span = hi > lo ? hi - lo : 0;
+  if (count > 2 * kWideWin) span = span / (count / (2 * kWideWin));
+  // smallest sh with (span >> sh) < kGroupBins
+  const int bits = span > 0 ? 64 - __clzll(static_cast<unsigned long long>(span)) : 0;
+  b.sh[g] = bits > 10 ? bits - 10 : 0;
+  static_assert(kGroupBins == 1024, "sel_range: 10-bit bin index");
 }
 
 // K2 (common case): the smallest keys above `lo` that fit one window, in two
@@ -849,9 +916,10 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
 //   wide_step      init_time_budget / urgency / selection bins     [pure]
 //   wide_finish    K2 windows, K3 scan, plan, moves, truth time    [owner]
 
-// K1 partial reductions over a view range: mins of tpot, decode slack, ctx,
-// decode ordinal, -decode ordinal, prefill ordinal, -prefill ordinal, and
-// n_dec | (bad << 40) in [7] (summed).
+// K1 partial reductions over a view range: mins of tpot, ctx, decode
+// ordinal, -decode ordinal, prefill ordinal, -prefill ordinal (ordinal =
+// (slack + 2^39) << 22 | seq for fair batching, seq otherwise), [6] unused,
+// and n_dec | (keys outside the packed range << 40) in [7] (summed).
 constexpr int kK1Vals = 8;
 
 struct WideStep {
@@ -878,51 +946,75 @@ __device__ __forceinline__ Inst wide_view_ctx(const EngineParams& P, int64_t ins
   return w;
 }
 
-// K1 over view positions [p_lo, p_hi) by the calling CTA (U views in flight
-// per thread): writes each key stem and leaves the CTA-reduced partials in
-// every thread's r[].
+// K1 over view positions [p_lo, p_hi) by the calling CTA, U views in flight
+// per thread (build_task_views, engine.cpp:51-81; slack, slo.h:45-61).
+// Per view it reads the row index, then prompt, prefilled, next index, seq,
+// the TTFT deadline (precomputed per request) and the first-token time --
+// all independent -- plus tpot unless the node's tpot_slo is uniform.  For a
+// prefill view next_idx == 0 and first == -1, so one expression gives both
+// phases' slack.  Writes the key stem; the reductions stay in every thread's
+// r[].
 __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst& w, int64_t p_lo,
                                               int64_t p_hi, int64_t now, bool fair,
                                               int64_t (&r)[kK1Vals], WideSmem& sm) {
   const WideScratch ws = wide_scratch(P, w);
+  const int64_t tpu = w.I->tpot_uniform;
   constexpr int U = 4;
-  int64_t mn[7] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf};
+  int64_t mn[6] = {kInf, kInf, kInf, kInf, kInf, kInf};
   int64_t l_cnt = 0;
   for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
-    View v[U];
+    int32_t rr[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-      if (p < p_hi) v[j] = load_view(P, w, p, now);
+      rr[j] = p < p_hi ? w.vl[p].x : -1;
+    }
+    int32_t prompt[U], pf[U], ni[U], seq[U];
+    int64_t dl0[U], first[U], tpot[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (rr[j] < 0) continue;
+      const int64_t g = w.roff + rr[j];
+      const int64_t row = w.toff + rr[j];
+      prompt[j] = P.prompt[row];
+      pf[j] = P.prefilled[g];
+      ni[j] = P.nidx[g];
+      seq[j] = P.seq[g];
+      dl0[j] = ws.dl0[rr[j]];
+      first[j] = P.first[g];
+      tpot[j] = tpu >= 0 ? tpu : P.tpot[row];
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
+      if (rr[j] < 0) continue;
       const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-      if (p >= p_hi) continue;
-      const bool fits = v[j].seq >= 0 && v[j].seq < kPackSeq &&
-                        (!fair || (v[j].slack >= -kPackSlack && v[j].slack < kPackSlack));
-      if (!fits) l_cnt |= int64_t(1) << 40;
-      const uint64_t sl = fair ? static_cast<uint64_t>(v[j].slack + kPackSlack) : 0;
-      ws.klow[p] = (v[j].decode ? (uint64_t(1) << 63) : 0) | (sl << 22) |
-                   static_cast<uint64_t>(v[j].seq);
-      const int64_t ord = fair ? v[j].slack : v[j].seq;  // selection ordinal
-      mn[0] = v[j].tpot < mn[0] ? v[j].tpot : mn[0];
-      mn[2] = v[j].ctx < mn[2] ? v[j].ctx : mn[2];
-      if (v[j].decode) {
+      const bool decode = pf[j] >= prompt[j];
+      const int64_t anchor = (first[j] >= 0 && first[j] < dl0[j]) ? first[j] : dl0[j];
+      const int64_t slack = anchor + tpot[j] * static_cast<int64_t>(ni[j]) - now;
+      const int64_t ctx = decode ? static_cast<int64_t>(prompt[j]) + ni[j] : pf[j];
+      if (static_cast<uint32_t>(seq[j]) >= static_cast<uint32_t>(kPackSeq)) l_cnt |= int64_t(1) << 40;
+      const uint64_t sl = fair ? static_cast<uint64_t>(slack + kPackSlack) : 0;
+      ws.klow[p] = (decode ? (uint64_t(1) << 63) : 0) | (sl << 22) | static_cast<uint64_t>(seq[j]);
+      if (fair && (slack < -kPackSlack || slack >= kPackSlack)) l_cnt |= int64_t(1) << 40;
+      const int64_t ord = fair ? static_cast<int64_t>((sl << 22) | static_cast<uint64_t>(seq[j]))
+                               : seq[j];  // selection ordinal
+      mn[0] = tpot[j] < mn[0] ? tpot[j] : mn[0];
+      mn[1] = ctx < mn[1] ? ctx : mn[1];
+      if (decode) {
         l_cnt++;
-        mn[1] = v[j].slack < mn[1] ? v[j].slack : mn[1];
-        mn[3] = ord < mn[3] ? ord : mn[3];
-        mn[4] = -ord < mn[4] ? -ord : mn[4];
+        mn[2] = ord < mn[2] ? ord : mn[2];
+        mn[3] = -ord < mn[3] ? -ord : mn[3];
       } else {
-        mn[5] = ord < mn[5] ? ord : mn[5];
-        mn[6] = -ord < mn[6] ? -ord : mn[6];
+        mn[4] = ord < mn[4] ? ord : mn[4];
+        mn[5] = -ord < mn[5] ? -ord : mn[5];
       }
     }
   }
-  block_min_n<7>(mn, sm);
+  block_min_n<6>(mn, sm);
   const int64_t cnt = block_sum(l_cnt, sm);
 #pragma unroll
-  for (int q = 0; q < 7; ++q) r[q] = mn[q];
+  for (int q = 0; q < 6; ++q) r[q] = mn[q];
+  r[6] = kInf;
   r[7] = cnt;
 }
 
@@ -942,11 +1034,14 @@ __device__ __forceinline__ WideStep wide_step(const int64_t (&mn)[kK1Vals], int6
                                               int policy) {
   WideStep s;
   const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+  const int64_t dlo = mn[2], dhi = -mn[3], plo = mn[4], phi = -mn[5];
   s.A = A;
   s.min_tpot = mn[0];
-  s.min_dec = mn[1];
-  s.ctx_min = mn[2];
+  s.ctx_min = mn[1];
   s.n_dec = mn[7] & ((int64_t(1) << 40) - 1);
+  // fair batching: the decode ordinal's high part is the slack
+  s.min_dec = s.n_dec > 0 ? (dlo >> 22) - kPackSlack : kInf;
+  // packed keys need seq < 2^22 and (fair) slack in [-2^39, 2^39)
   s.bad = (mn[7] >> 40) != 0;
   s.init_ms = 0.0;
   s.urgency = 0;
@@ -956,20 +1051,26 @@ __device__ __forceinline__ WideStep wide_step(const int64_t (&mn)[kK1Vals], int6
     s.urgency = init + s.min_tpot;
     s.init_ms = us_to_ms(init);
   }
-  const int64_t dlo = mn[3], dhi = -mn[4], plo = mn[5], phi = -mn[6];
-  const int64_t urgency = s.urgency;
+  const int64_t n_pf = A - s.n_dec;
+  s.sb.urg = 0;
   if (fair) {
-    sel_range(s.sb, 0, dlo, dhi < urgency - 1 ? dhi : urgency - 1);
-    sel_range(s.sb, 1, plo, phi);
-    sel_range(s.sb, 2, dlo > urgency ? dlo : urgency, dhi);
+    // decodes with slack < urgency <=> ordinal < (urgency + 2^39) << 22
+    const int64_t u = s.urgency < -kPackSlack ? -kPackSlack
+                                              : (s.urgency > kPackSlack ? kPackSlack : s.urgency);
+    const int64_t urg = (u + kPackSlack) << 22;
+    s.sb.urg = urg;
+    // UD and ND share the decode count (the urgency split is not counted)
+    sel_range(s.sb, 0, dlo, dhi < urg - 1 ? dhi : urg - 1, s.n_dec);
+    sel_range(s.sb, 1, plo, phi, n_pf);
+    sel_range(s.sb, 2, dlo > urg ? dlo : urg, dhi, s.n_dec);
   } else if (policy == FB_POLICY_SARATHI) {
-    sel_range(s.sb, 0, dlo, dhi);
-    sel_range(s.sb, 1, plo, phi);
-    sel_range(s.sb, 2, 0, 0);
+    sel_range(s.sb, 0, dlo, dhi, s.n_dec);
+    sel_range(s.sb, 1, plo, phi, n_pf);
+    sel_range(s.sb, 2, 0, 0, 0);
   } else {
-    sel_range(s.sb, 0, dlo < plo ? dlo : plo, dhi > phi ? dhi : phi);
-    sel_range(s.sb, 1, 0, 0);
-    sel_range(s.sb, 2, 0, 0);
+    sel_range(s.sb, 0, dlo < plo ? dlo : plo, dhi > phi ? dhi : phi, A);
+    sel_range(s.sb, 1, 0, 0, 0);
+    sel_range(s.sb, 2, 0, 0, 0);
   }
   return s;
 }
@@ -1307,7 +1408,10 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
         // escalation: admitted-waiting marks all-zero, in-flight takes cleared
         // (the warp engine's memory path leaves consumed takes behind)
         const WideScratch ws = wide_scratch(P, w);
-        for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) ws.mark[q] = 0;
+        for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) {
+          ws.mark[q] = 0;
+          ws.dl0[q] = P.arrival[w.toff + q] + P.ttft[w.toff + q];  // slo.h:45-61 anchor
+        }
         for (int64_t q = threadIdx.x; q < w.S.n_active; q += kWideThreads) w.vl[q].y = 0;
         __syncthreads();
         w.S.pending_begin = 0;
@@ -1390,10 +1494,11 @@ constexpr int kWgMaxSlots = 256;
 // Work split of one iteration: the views of all beginning slots, laid end to
 // end ([v0[t], v0[t+1]) for slot t), cut into gridDim.x equal ranges.
 struct WgSplit {
-  const int64_t* v0;  // smem, n_slots + 1 entries
+  const int64_t* v0;   // smem, n_slots + 1 entries
+  const int64_t* clo;  // smem, G + 1 entries: first view of CTA b
   int64_t V;
   int G, n_slots;
-  __device__ __forceinline__ int64_t lo(int b) const { return (V * b) / G; }
+  __device__ __forceinline__ int64_t lo(int b) const { return clo[b]; }
   // slot holding view x (v0[t] <= x < v0[t+1])
   __device__ __forceinline__ int slot_of(int64_t x) const {
     int a = 0, z = n_slots - 1;
@@ -1467,11 +1572,92 @@ __device__ __forceinline__ void wg_window(const EngineParams& P, int t, int& bma
   __syncthreads();
 }
 
+// Owner: the window's K gathered key stems of slot t, sorted into sm.wkey /
+// sm.wpos.  The stems arrive in arbitrary order; their bins (nondecreasing
+// in key) give a counting sort with the node's histogram as bin offsets, and
+// each key's place inside its bin is its rank among the bin's keys (keys are
+// unique), counted by the key's thread.  A bin of more than kBinSortMax keys
+// (heavy slack ties) falls back to the bitonic sort.
+constexpr int kBinSortMax = 64;
+__device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int policy,
+                            const WideStep& ss, WideSmem& sm) {
+  const uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
+  uint32_t* start = sm.hist;                                // [bin] first slot
+  uint32_t* cur = reinterpret_cast<uint32_t*>(sm.wcc);      // [bin] fill cursor
+  uint64_t* tkey = reinterpret_cast<uint64_t*>(sm.wtc);     // bin-ordered keys
+  int32_t* tpos = sm.wtake;                                 // their positions
+  constexpr int kPer = kSelBins / kWideThreads;
+  const int c0 = threadIdx.x * kPer;
+  uint32_t hv[kPer];
+  int loc = 0, mx = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    hv[k] = c0 + k <= bmax ? __ldcg(gh + c0 + k) : 0u;
+    loc += static_cast<int>(hv[k]);
+    mx = static_cast<int>(hv[k]) > mx ? static_cast<int>(hv[k]) : mx;
+  }
+  int tot;
+  int run = block_excl_sum(loc, tot, sm);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    start[c0 + k] = static_cast<uint32_t>(run);
+    cur[c0 + k] = static_cast<uint32_t>(run);
+    run += static_cast<int>(hv[k]);
+  }
+  const int64_t bigbin = -block_min(-static_cast<int64_t>(mx), sm);
+  WPROF_COUNT(16, bigbin > kBinSortMax ? 1 : 0)
+  WPROF_COUNT(17, bigbin)
+  WPROF_COUNT(18, K)
+  WPROF_COUNT(19, bmax)
+  const uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
+  const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
+  if (bigbin > kBinSortMax) {
+    for (int k = threadIdx.x; k < K; k += kWideThreads) {
+      sm.wkey[k] = wide_key(__ldcg(ck + k), policy, ss.urgency);
+      sm.wpos[k] = __ldcg(cp + k);
+    }
+    __syncthreads();
+    wide_sort_window(K, sm);
+    return;
+  }
+  int kb[kWideWin / kWideThreads];  // this thread's keys' bins
+#pragma unroll
+  for (int q = 0; q < kWideWin / kWideThreads; ++q) {
+    const int k = threadIdx.x + q * kWideThreads;
+    kb[q] = -1;
+    if (k < K) {
+      const uint64_t kl = __ldcg(ck + k);
+      const int b = sel_bin(kl, policy, ss.urgency, ss.sb);
+      const uint32_t dst = atomicAdd(&cur[b], 1u);
+      tkey[dst] = wide_key(kl, policy, ss.urgency);
+      tpos[dst] = __ldcg(cp + k);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += kWideThreads) {
+    const uint64_t x = tkey[k];
+    // bin of slot k: the last bin whose start is <= k (binary search)
+    int lo = 0, hi = bmax;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (static_cast<int>(start[mid]) <= k) lo = mid; else hi = mid - 1;
+    }
+    const int b0 = static_cast<int>(start[lo]), b1 = static_cast<int>(cur[lo]);
+    int rank = 0;
+    for (int q = b0; q < b1; ++q) rank += tkey[q] < x;
+    sm.wkey[b0 + rank] = x;
+    sm.wpos[b0 + rank] = tpos[k];
+  }
+  (void)kb;
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kWideThreads, 1)
 wide_grid_kernel(const __grid_constant__ EngineParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WideSmem& sm = *reinterpret_cast<WideSmem*>(smem_raw);
   __shared__ int64_t s_v0[kWgMaxSlots + 1];
+  __shared__ int64_t s_clo[kWgMaxSlots + 1];
   WideSlot* slots = reinterpret_cast<WideSlot*>(P.wg.slots);
   WideSlot* my = slots + blockIdx.x;
   const int n_slots = static_cast<int>(gridDim.x);
@@ -1533,8 +1719,11 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       const int64_t before = block_excl_sum64(a, tot, sm);
       if (threadIdx.x < n_slots) s_v0[threadIdx.x] = before;
       if (threadIdx.x == 0) s_v0[n_slots] = tot;
+      for (int b = threadIdx.x; b <= static_cast<int>(gridDim.x); b += kWideThreads)
+        s_clo[b] = (tot * b) / static_cast<int64_t>(gridDim.x);
       __syncthreads();
       sp.v0 = s_v0;
+      sp.clo = s_clo;
       sp.V = tot;
       sp.G = static_cast<int>(gridDim.x);
       sp.n_slots = n_slots;
@@ -1646,7 +1835,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
             base = __shfl_sync(kFull, base, 0);
             if (sel) {
               const int slot = base + __popc(m & lanemask_lt());
-              ck[slot] = wide_key(kl[j], sv.policy, ss.urgency);
+              ck[slot] = kl[j];  // key stem; the owner derives bin and key
               cp[slot] = static_cast<int32_t>(p);
             }
           }
@@ -1658,6 +1847,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     GPROF(15)
     // ---- owner: the rest of begin_step
     if (s_have) {
+      WPROF_START
       Inst w = s_w;
       bool have = true;
       const int t = static_cast<int>(blockIdx.x);
@@ -1671,14 +1861,9 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       int K0 = -1;
       if (bmax >= 0) {
         K0 = vs->ncand;
-        const uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
-        const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
-        for (int k = threadIdx.x; k < K0; k += kWideThreads) {
-          sm.wkey[k] = __ldcg(ck + k);
-          sm.wpos[k] = __ldcg(cp + k);
-        }
-        __syncthreads();
-        wide_sort_window(K0, sm);
+        WPROF(0)
+        wg_bin_sort(P, t, K0, bmax, w.policy, ss, sm);
+        WPROF(1)
       } else {
         all0 = false;
       }

@@ -13,7 +13,7 @@ batch = workloads.c4_batch(n_inst=n)
 a = fbgpu.Arena(0)
 a.load(batch)
 L = fbgpu.lib()
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 24)()
 a.run()
 a.synchronize()
 L.fb_debug_wide_prof(buf, 1)
@@ -24,11 +24,13 @@ a.run()
 a.synchronize()
 ms = a.last_run_ms()
 L.fb_debug_wide_prof(buf, 1)
-names = ["", "", "K2 select (later windows)", "cost gather", "K3 scan", "bookkeeping", "moves",
+names = ["owner combine+window+cands", "owner sort", "K2 select (later windows)", "cost gather", "K3 scan", "bookkeeping", "moves",
          "tail", "complete", "", "", "K3 prefix"]
-tot = sum(buf[i] for i in (2, 3, 4, 5, 6, 7, 8, 11))
+tot = sum(buf[i] for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 11))
 steps = buf[10]
 print(f"{n} instances, {ms:.3f} ms, {steps} wide steps")
+print(f"  bin sort: {buf[16]} bitonic fallbacks, mean max-bin {buf[17] / max(steps, 1):.1f}, "
+      f"mean window {buf[18] / max(steps, 1):.0f} keys, mean last bin {buf[19] / max(steps, 1):.0f}")
 gnames = {12: "advance+barrier", 13: "grid K1+barrier", 14: "grid hist+barrier",
           15: "grid gather+barrier", 9: "owner finish (CTA 0)"}
 gt = sum(buf[i] for i in gnames)
