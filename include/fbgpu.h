@@ -309,6 +309,9 @@ int fb_arena_synchronize(fb_arena* arena);
 
 /* Device time of the last fb_arena_run (CUDA events on the arena stream). */
 int fb_arena_last_run_ms(fb_arena* arena, float* ms_out);
+/* The same run split into the warp engine and the grid-wide wide engine
+ * (nodes with more than 512 live requests). */
+int fb_arena_last_run_split_ms(fb_arena* arena, float* warp_ms, float* wide_ms);
 
 int fb_arena_fetch_results(fb_arena* arena, fb_instance_result* out);
 /* Records for instance rows: out has sum over instances of n_req rows, in

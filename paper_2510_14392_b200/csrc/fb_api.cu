@@ -133,7 +133,7 @@ struct fb_arena {
   DevBuf<uint64_t> wg_ckey;
   DevBuf<int32_t> wg_cpos;
   DevBuf<unsigned long long> wg_bar;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evm = nullptr;  // evm: warp -> wide engine
   bool timed = false;
   // Pinned staging for copies from / to pageable host memory: two chunks,
   // so the host memcpy of one overlaps the DMA of the other.
@@ -305,6 +305,7 @@ int fb_arena_create(int device, void* stream, fb_arena** out) {
   }
   cudaEventCreate(&a->ev0);
   cudaEventCreate(&a->ev1);
+  cudaEventCreate(&a->evm);
   a->geo = fbgpu::engine_geometry(device);
   cudaError_t e = a->work.ensure(4);
   if (e != cudaSuccess) {
@@ -322,6 +323,7 @@ int fb_arena_destroy(fb_arena* a) {
   a->release();
   if (a->ev0) cudaEventDestroy(a->ev0);
   if (a->ev1) cudaEventDestroy(a->ev1);
+  if (a->evm) cudaEventDestroy(a->evm);
   if (a->own_stream) cudaStreamDestroy(a->stream);
   delete a;
   return FB_OK;
@@ -461,7 +463,8 @@ int fb_arena_run(fb_arena* a, int64_t max_events, int64_t* n_active_out) {
   FB_CUDA(cudaSetDevice(a->device));
   const fbgpu::EngineParams P = a->params(max_events);
   FB_CUDA(cudaEventRecord(a->ev0, a->stream));
-  if (a->n_inst > 0) FB_CUDA(fbgpu::launch_engine(P, a->geo, a->stream));
+  if (a->n_inst > 0) FB_CUDA(fbgpu::launch_engine(P, a->geo, a->stream, a->evm));
+  if (a->n_inst == 0) FB_CUDA(cudaEventRecord(a->evm, a->stream));
   FB_CUDA(cudaEventRecord(a->ev1, a->stream));
   a->timed = true;
   if (n_active_out) {
@@ -470,6 +473,14 @@ int fb_arena_run(fb_arena* a, int64_t max_events, int64_t* n_active_out) {
     FB_CUDA(cudaStreamSynchronize(a->stream));
     *n_active_out = a->n_inst > 0 ? static_cast<int64_t>(h[1]) : 0;
   }
+  return FB_OK;
+}
+
+int fb_arena_last_run_split_ms(fb_arena* a, float* warp_ms, float* wide_ms) {
+  if (!a || !warp_ms || !wide_ms || !a->timed) return set_error(FB_ERR_USAGE, "no timed run");
+  FB_CUDA(cudaEventSynchronize(a->ev1));
+  FB_CUDA(cudaEventElapsedTime(warp_ms, a->ev0, a->evm));
+  FB_CUDA(cudaEventElapsedTime(wide_ms, a->evm, a->ev1));
   return FB_OK;
 }
 

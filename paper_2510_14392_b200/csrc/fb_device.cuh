@@ -47,12 +47,16 @@ __device__ __forceinline__ double predict_ms(double a, double b, double c,
 // d*(1+2^-51) <= 1000*j*m (evaluated with upward / downward rounding) proves
 // x_j <= m and the std::max leaves m unchanged.  Otherwise x_j is computed
 // exactly in the reference's operation order.  d >= 0, 1 <= j < 2^31.
+// The divisions, out of line (rarely reached: keeps the hot loops compact).
+static __device__ __noinline__ double max_ratio_div(double m, int64_t d, int32_t j) {
+  const double x = ddiv(us_to_ms(d), static_cast<double>(j));
+  return m < x ? x : m;
+}
 __device__ __forceinline__ void max_ratio(double& m, int64_t d, int32_t j) {
   const double lhs = __dmul_ru(static_cast<double>(d), 1.0 + 0x1p-51);
   const double rhs = __dmul_rd(__dmul_rd(1000.0, static_cast<double>(j)), m);
   if (lhs <= rhs) return;
-  const double x = ddiv(us_to_ms(d), static_cast<double>(j));
-  if (m < x) m = x;
+  m = max_ratio_div(m, d, j);
 }
 
 // -------------------------------------------------------------- rng.h
@@ -71,6 +75,13 @@ __device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t stream) 
 __device__ __forceinline__ double keyed_uniform(uint64_t seed, uint64_t ord) {
   uint64_t s = derive_seed(seed, ord);  // rng.h:91-94
   return dmul(static_cast<double>(splitmix64(s) >> 11), 0x1.0p-53);
+}
+// ground_truth_step_time_ms's noise factor (costmodel.cpp:138-146):
+// actual * (1 + amp * (2u - 1)), out of line (noise is off in most runs).
+static __device__ __noinline__ double apply_noise(double actual, double amp, uint64_t seed,
+                                           uint64_t ord) {
+  const double u = dsub(dmul(2.0, keyed_uniform(seed, ord)), 1.0);
+  return dmul(actual, dadd(1.0, dmul(amp, u)));
 }
 
 // ------------------------------------------------------------- warp utils

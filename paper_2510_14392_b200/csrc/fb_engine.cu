@@ -332,8 +332,7 @@ __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t 
   double actual = predict_ms(I->ta, I->tb, I->tc, o.total_new, o.total_ctx);
   const double amp = I->noise_amp;
   if (amp != 0.0) {
-    const double u = dsub(dmul(2.0, keyed_uniform(I->noise_seed, w.S.step_counter)), 1.0);
-    actual = dmul(actual, dadd(1.0, dmul(amp, u)));
+    actual = apply_noise(actual, amp, I->noise_seed, w.S.step_counter);
   }
   int64_t dur = ms_to_us(actual);
   if (dur < 1) dur = 1;  // engine.cpp:196-198
@@ -749,9 +748,11 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, i
                                      dim3(kWarp * c.warps_per_cta), args, smem, st);
 }
 
-cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaStream_t st) {
+cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaStream_t st,
+                          cudaEvent_t between) {
   cudaMemsetAsync(p.work, 0, 3 * sizeof(unsigned long long), st);
   engine_kernel<<<g.blocks, g.threads, g.smem, st>>>(p);
+  if (between) cudaEventRecord(between, st);
   // Escalated instances (more than kEscalateLive live requests) continue on
   // the grid-wide wide engine; with none escalated it exits after one barrier.
   cudaMemsetAsync(p.wg.bar, 0, sizeof(unsigned long long), st);

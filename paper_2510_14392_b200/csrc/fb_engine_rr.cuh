@@ -393,8 +393,7 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   double actual = predict_ms(I->ta, I->tb, I->tc, tn, tctx);
   const double amp = I->noise_amp;
   if (amp != 0.0) {
-    const double u = dsub(dmul(2.0, keyed_uniform(I->noise_seed, w.S.step_counter)), 1.0);
-    actual = dmul(actual, dadd(1.0, dmul(amp, u)));
+    actual = apply_noise(actual, amp, I->noise_seed, w.S.step_counter);
   }
   int64_t dur = ms_to_us(actual);
   if (dur < 1) dur = 1;

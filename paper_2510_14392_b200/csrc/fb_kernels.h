@@ -117,8 +117,10 @@ int cluster_warps_per_cta(int n_nodes, int n_ranks);
 size_t cluster_smem_bytes(int warps_per_cta);
 cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& c, int blocks,
                            cudaStream_t st);
+// Warp engine, then the grid-wide wide engine; `between` (may be null) is
+// recorded between the two launches.
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g,
-                          cudaStream_t st);
+                          cudaStream_t st, cudaEvent_t between = nullptr);
 
 // Pure scheduler surface.  `scratch` must hold total_tasks slots.
 cudaError_t launch_form_batch(const fb_task_view* tasks, const int64_t* set_off,

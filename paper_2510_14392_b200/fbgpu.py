@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         "fb_arena_run": (C.c_int, [vp, i64, pi64]),
         "fb_arena_synchronize": (C.c_int, [vp]),
         "fb_arena_last_run_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
+        "fb_arena_last_run_split_ms": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "fb_arena_fetch_results": (C.c_int, [vp, vp]),
         "fb_arena_fetch_records": (C.c_int, [vp, vp]),
         "fb_arena_record_rows": (i64, [vp]),
@@ -339,6 +340,13 @@ class Arena:
         ms = C.c_float(0)
         _check(self._lib.fb_arena_last_run_ms(self._h, C.byref(ms)), "fb_arena_last_run_ms")
         return ms.value
+
+    def last_run_split_ms(self) -> tuple[float, float]:
+        """(warp engine ms, grid-wide wide engine ms) of the last run."""
+        a, b = C.c_float(0), C.c_float(0)
+        _check(self._lib.fb_arena_last_run_split_ms(self._h, C.byref(a), C.byref(b)),
+               "fb_arena_last_run_split_ms")
+        return a.value, b.value
 
     def results(self) -> np.ndarray:
         out = np.zeros(max(1, self.n_instances), _abi.RESULT_DTYPE)
