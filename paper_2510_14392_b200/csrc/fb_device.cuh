@@ -230,7 +230,11 @@ struct Scratch {
   double* tcost;    // [k] b*new + c*ctx (or PAB term [p])
   double* ccost;    // [k] c*ctx
 };
-constexpr int kScratchBytesPerSlot = 8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8 + 8;
+// 64 bytes carved per slot (Scratch) + 16 so that every instance's region
+// (rec_off * kScratchBytesPerSlot) is 16-byte aligned and holds the wide
+// engine's 52 bytes per slot plus its 16-byte view records.
+constexpr int kScratchBytesPerSlot = 80;
+static_assert(kScratchBytesPerSlot >= 8 + 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8 + 8, "Scratch slot");
 
 __device__ __forceinline__ Scratch carve_scratch(unsigned char* base, int cap) {
   Scratch s;

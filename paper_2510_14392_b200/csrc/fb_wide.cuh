@@ -67,23 +67,33 @@ struct WideSmem {
 };
 
 // Per-instance global scratch (72 bytes per request slot, see Scratch).
+// Per-request view record of an escalated node (request index r): the
+// K1-relevant progress, mirrored from the SoA arena at escalation and kept
+// in step by pull / complete, so K1 reads one 32-byte record per view (two
+// 16-byte loads) instead of seven gathers.
+struct __align__(16) WRec {
+  int64_t dl0;    // arrival + ttft_slo (slo.h:45-61 anchor)
+  int64_t first;  // time of token 0, -1 none
+  int32_t prompt, prefilled, nidx, seq;
+};
+
+// Per-instance global scratch (kScratchBytesPerSlot per request slot).
 struct WideScratch {
+  WRec* rec;       // [r] view records
   uint64_t* klow;  // [p] decode<<63 | (slack+2^39)<<22 | seq   (stem of the key)
-  int64_t* dl0;    // [r] arrival + ttft_slo of request r (filled at escalation)
   int2* vtmp;      // reorder buffer / PAB terms
-  uint32_t* nwv;   // [p] new tokens | decode bit
   int32_t* mark;   // [p] admitted-waiting flag
 };
 
 __device__ __forceinline__ WideScratch wide_scratch(const EngineParams& P, const Inst& w) {
+  static_assert(kScratchBytesPerSlot % 16 == 0 && kScratchBytesPerSlot >= 52, "wide scratch");
   WideScratch s;
   unsigned char* base = P.gscratch + w.roff * kScratchBytesPerSlot;
   const size_t n = static_cast<size_t>(w.nreq);
-  s.klow = reinterpret_cast<uint64_t*>(base);
-  s.dl0 = reinterpret_cast<int64_t*>(base + 8 * n);
-  s.vtmp = reinterpret_cast<int2*>(base + 16 * n);
-  s.nwv = reinterpret_cast<uint32_t*>(base + 24 * n);
-  s.mark = reinterpret_cast<int32_t*>(base + 28 * n);
+  s.rec = reinterpret_cast<WRec*>(base);
+  s.klow = reinterpret_cast<uint64_t*>(base + 32 * n);
+  s.vtmp = reinterpret_cast<int2*>(base + 40 * n);
+  s.mark = reinterpret_cast<int32_t*>(base + 48 * n);
   return s;
 }
 
@@ -213,12 +223,14 @@ __device__ __forceinline__ uint64_t wide_key(uint64_t klow, int policy, int64_t 
   return seq;
 }
 
-// Ascending bitonic sort of sm.wkey / sm.wpos [0, K) (keys unique).  Each
-// thread holds kPerT consecutive elements in registers: strides below kPerT
-// are in-thread compare-exchanges, strides up to one warp's span are
-// shuffles, and only the longer strides go through shared memory (2
-// barriers each) -- 10 of the 66 stages for a full window.
+// Ascending sort of sm.wkey / sm.wpos [0, K) (keys unique; K <= kWideWin).
+// Each warp sorts a run of 128 elements in registers (4 consecutive per lane:
+// bitonic network, in-thread strides 1-2, shuffle strides 4-64, no barrier),
+// then four merge-path rounds double the runs (128 -> 2048): every thread
+// finds where its 4 outputs start by a binary search on the two input runs
+// (co-rank) and merges them sequentially.  Padding keys (~0) sort last.
 constexpr int kPerT = kWideWin / kWideThreads;  // 4
+constexpr int kRun = kWarp * kPerT;             // 128
 __device__ __forceinline__ void bitonic_cx(uint64_t& a, int32_t& pa, uint64_t b, int32_t pb,
                                            bool take_min) {
   const bool sw = take_min ? (b < a) : (b > a);
@@ -228,46 +240,31 @@ __device__ __forceinline__ void bitonic_cx(uint64_t& a, int32_t& pa, uint64_t b,
   }
 }
 __device__ void wide_sort_window(int K, WideSmem& sm) {
+  static_assert(kPerT == 4 && kWideWin == kRun * kWideWarps, "sort layout");
   uint64_t k[kPerT];
   int32_t v[kPerT];
-  const int e0 = threadIdx.x * kPerT;
+  const int e0 = threadIdx.x * kPerT;  // global element index of k[0]
+  const int l0 = lane_id() * kPerT;    // index inside the warp's run
 #pragma unroll
   for (int q = 0; q < kPerT; ++q) {
     const int e = e0 + q;
     k[q] = e < K ? sm.wkey[e] : ~uint64_t(0);
     v[q] = e < K ? sm.wpos[e] : -1;
   }
-  __syncthreads();
-  constexpr int kWarpSpan = kWarp * kPerT;  // 128 elements per warp
-  for (int kk = 2; kk <= kWideWin; kk <<= 1) {
+  // 1. warp runs of 128, ascending
+  for (int kk = 2; kk <= kRun; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= kWarpSpan) {
+      if (j >= kPerT) {
+        const int lm = j / kPerT;
 #pragma unroll
         for (int q = 0; q < kPerT; ++q) {
-          sm.wkey[e0 + q] = k[q];
-          sm.wpos[e0 + q] = v[q];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kPerT; ++q) {
-          const int e = e0 + q;
-          const bool asc = (e & kk) == 0, lower = (e & j) == 0;
-          bitonic_cx(k[q], v[q], sm.wkey[e ^ j], sm.wpos[e ^ j], lower == asc);
-        }
-        __syncthreads();
-      } else if (j >= kPerT) {
-        const int lm = j / kPerT;  // lane distance
-#pragma unroll
-        for (int q = 0; q < kPerT; ++q) {
-          const int e = e0 + q;
+          const int e = l0 + q;
           const uint64_t b = __shfl_xor_sync(kFull, k[q], lm);
           const int32_t pb = __shfl_xor_sync(kFull, v[q], lm);
           const bool asc = (e & kk) == 0, lower = (e & j) == 0;
           bitonic_cx(k[q], v[q], b, pb, lower == asc);
         }
       } else {
-        // in-thread strides (j = 2, 1), register indices fixed at compile time
-        static_assert(kPerT == 4, "in-thread stages assume 4 elements per thread");
         auto cx = [&](uint64_t& a, int32_t& pa, uint64_t& b, int32_t& pb, int e) {
           const bool asc = (e & kk) == 0;
           if ((a > b) == asc) {
@@ -280,24 +277,66 @@ __device__ void wide_sort_window(int K, WideSmem& sm) {
           }
         };
         if (j == 2) {
-          cx(k[0], v[0], k[2], v[2], e0);
-          cx(k[1], v[1], k[3], v[3], e0 + 1);
+          cx(k[0], v[0], k[2], v[2], l0);
+          cx(k[1], v[1], k[3], v[3], l0 + 1);
         } else {
-          cx(k[0], v[0], k[1], v[1], e0);
-          cx(k[2], v[2], k[3], v[3], e0 + 2);
+          cx(k[0], v[0], k[1], v[1], l0);
+          cx(k[2], v[2], k[3], v[3], l0 + 2);
         }
       }
     }
   }
+  uint64_t* src = sm.wkey;
+  int32_t* spos = sm.wpos;
+  uint64_t* dst = reinterpret_cast<uint64_t*>(sm.wtc);
+  int32_t* dpos = sm.wtake;
 #pragma unroll
   for (int q = 0; q < kPerT; ++q) {
-    const int e = e0 + q;
-    if (e < K) {
-      sm.wkey[e] = k[q];
-      sm.wpos[e] = v[q];
-    }
+    src[e0 + q] = k[q];
+    spos[e0 + q] = v[q];
   }
   __syncthreads();
+  // 2. merge-path rounds
+  for (int L = kRun; L < kWideWin; L <<= 1) {
+    const int g0 = (e0 / (2 * L)) * (2 * L);  // this pair of runs
+    const int i = e0 - g0;                    // first output inside the pair
+    const uint64_t* A = src + g0;
+    const uint64_t* B = A + L;
+    // co-rank: a + b = i with A[a-1] < B[b] and B[b-1] < A[a]
+    int lo = i > L ? i - L : 0, hi = i < L ? i : L;
+    while (lo < hi) {
+      const int a = (lo + hi) >> 1;
+      if (A[a] < B[i - a - 1]) lo = a + 1; else hi = a;
+    }
+    int a = lo, b = i - lo;
+#pragma unroll
+    for (int q = 0; q < kPerT; ++q) {
+      const bool takeA = b >= L || (a < L && A[a] < B[b]);
+      if (takeA) {
+        dst[e0 + q] = A[a];
+        dpos[e0 + q] = spos[g0 + a];
+        ++a;
+      } else {
+        dst[e0 + q] = B[b];
+        dpos[e0 + q] = spos[g0 + L + b];
+        ++b;
+      }
+    }
+    __syncthreads();
+    uint64_t* t = src;
+    src = dst;
+    dst = t;
+    int32_t* tp = spos;
+    spos = dpos;
+    dpos = tp;
+  }
+  if (src != sm.wkey) {
+    for (int e = threadIdx.x; e < K; e += kWideThreads) {
+      sm.wkey[e] = src[e];
+      sm.wpos[e] = spos[e];
+    }
+    __syncthreads();
+  }
 }
 
 // K2: the K = min(kWideWin, #{key > lo}) smallest keys above `lo` (all keys
@@ -408,7 +447,10 @@ __device__ __forceinline__ int sel_bin(uint64_t klow, int policy, int64_t urgenc
     ord = static_cast<int64_t>(low & ((uint64_t(1) << 22) - 1));
     g = (policy == FB_POLICY_SARATHI && !decode) ? 1 : 0;
   }
-  int64_t d = (ord - b.lo[g]) >> b.sh[g];
+  // select, not index: a dynamic index would put the bins in local memory
+  const int64_t lo = g == 0 ? b.lo[0] : (g == 1 ? b.lo[1] : b.lo[2]);
+  const int sh = g == 0 ? b.sh[0] : (g == 1 ? b.sh[1] : b.sh[2]);
+  int64_t d = (ord - lo) >> sh;
   d = d < 0 ? 0 : (d > kGroupBins - 1 ? kGroupBins - 1 : d);
   return g * kGroupBins + static_cast<int>(d);
 }
@@ -768,6 +810,7 @@ __device__ __forceinline__ void wide_scan_window(WideScan& st_io, int K, int pol
 // Node::complete_step (engine.cpp:204-254), block-wide.
 __device__ void wide_complete(const EngineParams& P, Inst& w, WideSmem& sm) {
   const int64_t t = w.S.step_end;
+  const WideScratch ws = wide_scratch(P, w);
   int any = 0;
   for (int64_t p = threadIdx.x; p < w.S.n_active; p += kWideThreads) {
     const int2 v = w.vl[p];
@@ -784,6 +827,10 @@ __device__ void wide_complete(const EngineParams& P, Inst& w, WideSmem& sm) {
       }
       bool fin = false;
       if (emit) fin = emit_token(P, g, row, t);
+      WRec& rec = ws.rec[v.x];  // keep the view record in step
+      rec.prefilled = pf;
+      rec.nidx = P.nidx[g];
+      rec.first = P.first[g];
       w.vl[p] = make_int2(fin ? -1 : v.x, 0);
       any |= fin;
     }
@@ -820,6 +867,7 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
     for (int64_t j = threadIdx.x; j < k; j += kWideThreads) {
       const int64_t r = arrival_row(w, w.S.pulled + j);
       P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter + j);
+      ws.rec[r].seq = static_cast<int32_t>(w.S.seq_counter + j);
       w.vl[w.S.n_live + j] = make_int2(static_cast<int>(r), 0);
     }
     __syncthreads();
@@ -859,6 +907,7 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
           vis = (w.S.n_live - w.S.n_active) < slots;
         }
         P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter);
+        ws.rec[r].seq = static_cast<int32_t>(w.S.seq_counter);
         w.vl[w.S.n_live] = make_int2(static_cast<int>(r), 0);
         w.S.seq_counter++;
         w.S.n_live++;
@@ -948,9 +997,9 @@ __device__ __forceinline__ Inst wide_view_ctx(const EngineParams& P, int64_t ins
 
 // K1 over view positions [p_lo, p_hi) by the calling CTA, U views in flight
 // per thread (build_task_views, engine.cpp:51-81; slack, slo.h:45-61).
-// Per view it reads the row index, then prompt, prefilled, next index, seq,
-// the TTFT deadline (precomputed per request) and the first-token time --
-// all independent -- plus tpot unless the node's tpot_slo is uniform.  For a
+// Per view it reads the row index, then the request's 32-byte view record
+// (TTFT deadline, first-token time, prompt, prefilled, next index, seq), plus
+// tpot unless the node's tpot_slo is uniform.  For a
 // prefill view next_idx == 0 and first == -1, so one expression gives both
 // phases' slack.  Writes the key stem; the reductions stay in every thread's
 // r[].
@@ -974,15 +1023,15 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (rr[j] < 0) continue;
-      const int64_t g = w.roff + rr[j];
-      const int64_t row = w.toff + rr[j];
-      prompt[j] = P.prompt[row];
-      pf[j] = P.prefilled[g];
-      ni[j] = P.nidx[g];
-      seq[j] = P.seq[g];
-      dl0[j] = ws.dl0[rr[j]];
-      first[j] = P.first[g];
-      tpot[j] = tpu >= 0 ? tpu : P.tpot[row];
+      const int4* rp = reinterpret_cast<const int4*>(ws.rec + rr[j]);
+      const int4 a = rp[0], b = rp[1];
+      dl0[j] = (static_cast<int64_t>(static_cast<uint32_t>(a.y)) << 32) | static_cast<uint32_t>(a.x);
+      first[j] = (static_cast<int64_t>(static_cast<uint32_t>(a.w)) << 32) | static_cast<uint32_t>(a.z);
+      prompt[j] = b.x;
+      pf[j] = b.y;
+      ni[j] = b.z;
+      seq[j] = b.w;
+      tpot[j] = tpu >= 0 ? tpu : P.tpot[w.toff + rr[j]];
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -1409,7 +1458,15 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
         const WideScratch ws = wide_scratch(P, w);
         for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) {
           ws.mark[q] = 0;
-          ws.dl0[q] = P.arrival[w.toff + q] + P.ttft[w.toff + q];  // slo.h:45-61 anchor
+          const int64_t g = w.roff + q, row = w.toff + q;
+          WRec r;
+          r.dl0 = P.arrival[row] + P.ttft[row];  // slo.h:45-61 anchor
+          r.first = P.first[g];
+          r.prompt = P.prompt[row];
+          r.prefilled = P.prefilled[g];
+          r.nidx = P.nidx[g];
+          r.seq = P.seq[g];
+          ws.rec[q] = r;
         }
         for (int64_t q = threadIdx.x; q < w.S.n_active; q += kWideThreads) w.vl[q].y = 0;
         __syncthreads();
@@ -1538,8 +1595,8 @@ __device__ __forceinline__ void wg_combine(const EngineParams& P, const WgSplit&
 // The window of slot t from its global histogram: last bin whose inclusive
 // count fits (-1: the first nonempty bin overflows), and whether it holds
 // every key.  Results in every thread.
-__device__ __forceinline__ void wg_window(const EngineParams& P, int t, int& bmax, bool& all,
-                                          WideSmem& sm) {
+__device__ __forceinline__ void wg_window(const EngineParams& P, int t, int64_t A, int& bmax,
+                                          bool& all, WideSmem& sm) {
   const uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
   constexpr int kPer = kSelBins / kWideThreads;
   const int c0 = threadIdx.x * kPer;
@@ -1567,7 +1624,7 @@ __device__ __forceinline__ void wg_window(const EngineParams& P, int t, int& bma
   }
   __syncthreads();
   bmax = sm.ibcast[0];
-  all = tot <= kWideWin;
+  all = A <= kWideWin;  // first window of the step: every key is above nothing
   __syncthreads();
 }
 
@@ -1619,11 +1676,9 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
     wide_sort_window(K, sm);
     return;
   }
-  int kb[kWideWin / kWideThreads];  // this thread's keys' bins
 #pragma unroll
   for (int q = 0; q < kWideWin / kWideThreads; ++q) {
     const int k = threadIdx.x + q * kWideThreads;
-    kb[q] = -1;
     if (k < K) {
       const uint64_t kl = __ldcg(ck + k);
       const int b = sel_bin(kl, policy, ss.urgency, ss.sb);
@@ -1647,7 +1702,6 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
     sm.wkey[b0 + rank] = x;
     sm.wpos[b0 + rank] = tpos[k];
   }
-  (void)kb;
   __syncthreads();
 }
 
@@ -1784,10 +1838,34 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
           }
         }
         __syncthreads();
+        // Flush only up to this segment's own crossing bin (the first whose
+        // cumulative count exceeds a window): the node's global crossing bin
+        // can only come earlier (counts only add), so every bin up to it is
+        // complete in the global histogram.
         uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
-        for (int k = threadIdx.x; k < kSelBins; k += kWideThreads) {
-          const uint32_t v = sm.hist[k];
-          if (v) atomicAdd(gh + k, v);
+        constexpr int kPer = kSelBins / kWideThreads;
+        const int c0 = threadIdx.x * kPer;
+        int loc = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) loc += static_cast<int>(sm.hist[c0 + k]);
+        int tot;
+        const int before = block_excl_sum(loc, tot, sm);
+        int64_t cross = kSelBins;
+        if (before <= kWideWin && before + loc > kWideWin) {
+          int cum = before;
+          for (int k = 0; k < kPer; ++k) {
+            cum += static_cast<int>(sm.hist[c0 + k]);
+            if (cum > kWideWin) {
+              cross = c0 + k;
+              break;
+            }
+          }
+        }
+        cross = block_min(cross, sm);
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+          const uint32_t v = sm.hist[c0 + k];
+          if (v && c0 + k <= cross) atomicAdd(gh + c0 + k, v);
         }
         __syncthreads();
       }
@@ -1802,11 +1880,11 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const int64_t a = s_v0[t] > my_lo ? s_v0[t] : my_lo;
         const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
         if (z <= a) continue;
+        const WgView sv = wg_view(slots + t);
         int bmax;
         bool all;
-        wg_window(P, t, bmax, all, sm);
+        wg_window(P, t, sv.A, bmax, all, sm);
         if (bmax < 0) continue;
-        const WgView sv = wg_view(slots + t);
         int64_t acc[kK1Vals];
         wg_combine(P, sp, t, acc);
         const WideStep ss = wide_step(acc, sv.A, sv.policy);
@@ -1856,7 +1934,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       const WideStep ss = wide_step(acc, vs->A, w.policy);
       int bmax;
       bool all0;
-      wg_window(P, t, bmax, all0, sm);
+      wg_window(P, t, vs->A, bmax, all0, sm);
       int K0 = -1;
       if (bmax >= 0) {
         K0 = vs->ncand;
