@@ -516,11 +516,20 @@ engine_kernel(const __grid_constant__ EngineParams P) {
   const int warp = threadIdx.x / kWarp;
   unsigned char* my = smem + static_cast<size_t>(warp) * kSmemSlots * kScratchBytesPerSlot;
   for (;;) {
-    unsigned long long i = 0;
-    if (lane_id() == 0) i = atomicAdd(&P.work[0], 1ull);
+    unsigned long long i = static_cast<unsigned long long>(P.n_inst);
+    if (lane_id() == 0) {
+      for (int q = 0; q < kQueues; ++q) {
+        const int64_t len = P.qoff[q + 1] - P.qoff[q];
+        if (static_cast<int64_t>(*(volatile unsigned long long*)&P.work[4 + q]) >= len) continue;
+        const unsigned long long k = atomicAdd(&P.work[4 + q], 1ull);
+        if (static_cast<int64_t>(k) < len) {
+          i = static_cast<unsigned long long>(P.order[P.qoff[q] + static_cast<int64_t>(k)]);
+          break;
+        }
+      }
+    }
     i = __shfl_sync(kFull, i, 0);
     if (i >= static_cast<unsigned long long>(P.n_inst)) break;
-    if (P.order) i = static_cast<unsigned long long>(P.order[i]);
     Inst w;
     w.id = static_cast<int64_t>(i);
     w.routed = nullptr;
@@ -625,6 +634,7 @@ EngineGeometry engine_geometry(int device) {
   g.smem = static_cast<size_t>(kWarpsPerBlock) * kSmemSlots * kScratchBytesPerSlot;
   int sms = 148, per_sm = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  g.sms = sms;
   cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(g.smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, g.threads, g.smem);
@@ -751,6 +761,8 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, i
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaStream_t st,
                           cudaEvent_t between) {
   cudaMemsetAsync(p.work, 0, 3 * sizeof(unsigned long long), st);
+  cudaMemsetAsync(p.work + 4, 0, kQueues * sizeof(unsigned long long), st);
+  static_assert(4 + kQueues <= 16, "work counters");
   engine_kernel<<<g.blocks, g.threads, g.smem, st>>>(p);
   if (between) cudaEventRecord(between, st);
   // Escalated instances (more than kEscalateLive live requests) continue on
