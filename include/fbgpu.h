@@ -326,6 +326,23 @@ int fb_arena_fetch_paths(fb_arena* arena, uint32_t* out);
 int fb_arena_fetch_log(fb_arena* arena, int64_t instance, fb_step_log* steps,
                        fb_plan_entry* entries, fb_reject_log* rejects);
 
+/* Per-instance ScenarioReport aggregates computed on the device
+ * (scenario_report, metrics.cpp:171-205; nearest-rank percentiles,
+ * metrics.cpp:118-135) over the requests that arrived.  offered_rps,
+ * slo_violation_rate = 1 - good/total and effective_rps = offered * good/total
+ * are host arithmetic on these counts. */
+typedef struct fb_percentiles {
+  double p50, p95, p99;
+  int64_t count;
+} fb_percentiles;
+typedef struct fb_summary {
+  int64_t total_requests, rejected, finished, good;
+  int64_t ttft_violations;  /* no first token or emits[0] > ttft (acceptance.cpp:105) */
+  int64_t envelope_misses;  /* some token j>=1 past its envelope (acceptance.cpp:106-111) */
+  fb_percentiles ttft_ms, max_tpot_ms, max_tpot_alt_ms;
+} fb_summary;
+int fb_arena_fetch_summaries(fb_arena* arena, fb_summary* out);
+
 /* Page-locked host buffers.  Trace rows, instances and record outputs that
  * live in memory from fb_host_alloc move by direct DMA; any other host
  * pointer is staged through the arena's own pinned chunks.  Not a reference

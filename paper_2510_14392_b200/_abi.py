@@ -249,7 +249,26 @@ BATCHPLAN_DTYPE = np.dtype(
     [("predicted_ms", "<f8"), ("time_budget_used_ms", "<f8"), ("token_budget_used", "<i8"),
      ("init_time_budget_ms", "<f8"), ("entry_off", "<i8"), ("n_entries", "<i8")], align=True)
 
-for _st, _dt in ((Record, RECORD_DTYPE), (InstanceResult, RESULT_DTYPE), (StepLog, STEPLOG_DTYPE),
+class Percentiles(C.Structure):
+    _fields_ = [("p50", C.c_double), ("p95", C.c_double), ("p99", C.c_double),
+                ("count", C.c_int64)]
+
+
+class Summary(C.Structure):
+    """fb_summary: per-instance ScenarioReport aggregates (metrics.cpp:171-205)."""
+    _fields_ = [("total_requests", C.c_int64), ("rejected", C.c_int64), ("finished", C.c_int64),
+                ("good", C.c_int64), ("ttft_violations", C.c_int64),
+                ("envelope_misses", C.c_int64), ("ttft_ms", Percentiles),
+                ("max_tpot_ms", Percentiles), ("max_tpot_alt_ms", Percentiles)]
+
+
+_PCT = [("p50", "<f8"), ("p95", "<f8"), ("p99", "<f8"), ("count", "<i8")]
+SUMMARY_DTYPE = np.dtype(
+    [("total_requests", "<i8"), ("rejected", "<i8"), ("finished", "<i8"), ("good", "<i8"),
+     ("ttft_violations", "<i8"), ("envelope_misses", "<i8"), ("ttft_ms", _PCT),
+     ("max_tpot_ms", _PCT), ("max_tpot_alt_ms", _PCT)], align=True)
+
+for _st, _dt in ((Summary, SUMMARY_DTYPE), (Record, RECORD_DTYPE), (InstanceResult, RESULT_DTYPE), (StepLog, STEPLOG_DTYPE),
                  (PlanEntry, ENTRY_DTYPE), (RejectLog, REJECT_DTYPE), (LogCounts, LOGCOUNT_DTYPE),
                  (TaskView, TASKVIEW_DTYPE), (PlanEntryId, PLANENTRYID_DTYPE),
                  (BatchPlan, BATCHPLAN_DTYPE)):

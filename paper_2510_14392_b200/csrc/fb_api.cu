@@ -127,6 +127,8 @@ struct fb_arena {
   DevBuf<int64_t> order;
   DevBuf<int64_t> qinfo;  // [kQueues + 1] queue offsets
   DevBuf<fb_record> recbuf;  // device-packed records (AoS) for one D2H
+  DevBuf<fb_summary> sumbuf;  // per-instance aggregates
+  DevBuf<uint64_t> sumvals;   // their value series (one u64 per request row)
   // grid-wide wide engine
   DevBuf<unsigned char> wg_slots;
   DevBuf<int64_t> wg_partial;
@@ -265,6 +267,8 @@ struct fb_arena {
     order.release();
     qinfo.release();
     recbuf.release();
+    sumbuf.release();
+    sumvals.release();
     wg_slots.release(); wg_partial.release(); wg_hist.release(); wg_ckey.release();
     wg_cpos.release(); wg_bar.release();
     for (int b = 0; b < 2; ++b) {
@@ -544,6 +548,17 @@ int fb_arena_fetch_records(fb_arena* a, fb_record* out) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc records");
   FB_CUDA(fbgpu::launch_pack_records(a->params(0), a->recbuf.p, a->stream));
   FB_CUDA(a->d2h(out, a->recbuf.p, sizeof(fb_record) * static_cast<size_t>(n)));
+  return FB_OK;
+}
+
+int fb_arena_fetch_summaries(fb_arena* a, fb_summary* out) {
+  if (!a || !a->loaded || !out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_summaries");
+  FB_CUDA(cudaSetDevice(a->device));
+  cudaError_t e = a->sumbuf.ensure(static_cast<size_t>(a->n_inst));
+  if (e == cudaSuccess) e = a->sumvals.ensure(static_cast<size_t>(a->n_rec));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc summaries");
+  FB_CUDA(fbgpu::launch_summaries(a->params(0), a->sumbuf.p, a->sumvals.p, a->stream));
+  FB_CUDA(a->d2h(out, a->sumbuf.p, sizeof(fb_summary) * static_cast<size_t>(a->n_inst)));
   return FB_OK;
 }
 

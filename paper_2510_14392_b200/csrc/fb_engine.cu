@@ -427,6 +427,7 @@ __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t 
 #include "fb_engine_rr.cuh"
 #include "fb_wide.cuh"
 #include "fb_cluster.cuh"
+#include "fb_summary.cuh"
 
 namespace fbgpu {
 
@@ -619,6 +620,14 @@ extern "C" int fb_debug_cta_prof(unsigned long long* out, int reset) {
   return static_cast<int>(cudaDeviceSynchronize());
 }
 #endif
+
+cudaError_t launch_summaries(const EngineParams& p, fb_summary* out, uint64_t* vals,
+                             cudaStream_t st) {
+  if (p.n_inst <= 0) return cudaSuccess;
+  int64_t blocks = p.n_inst < 148 * 8 ? p.n_inst : 148 * 8;
+  summarize_kernel<<<static_cast<int>(blocks), kSumThreads, 0, st>>>(p, out, vals);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pack_records(const EngineParams& p, fb_record* out, cudaStream_t st) {
   if (p.n_inst <= 0) return cudaSuccess;

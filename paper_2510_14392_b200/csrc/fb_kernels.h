@@ -99,6 +99,10 @@ void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
 void unpack_state(const void* state, fb_instance_result* out);
 
 cudaError_t launch_reset(const EngineParams& p, int64_t n_rec_rows, cudaStream_t st);
+// Per-instance ScenarioReport aggregates (fb_summary.cuh); vals holds one
+// u64 per request row (value series of large instances).
+cudaError_t launch_summaries(const EngineParams& p, fb_summary* out, uint64_t* vals,
+                             cudaStream_t st);
 // Records in fb_record layout, indexed by rec_off + row.
 cudaError_t launch_pack_records(const EngineParams& p, fb_record* out, cudaStream_t st);
 

@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
         "fb_arena_last_run_split_ms": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "fb_arena_fetch_results": (C.c_int, [vp, vp]),
         "fb_arena_fetch_records": (C.c_int, [vp, vp]),
+        "fb_arena_fetch_summaries": (C.c_int, [vp, vp]),
         "fb_arena_record_rows": (i64, [vp]),
         "fb_arena_fetch_log_counts": (C.c_int, [vp, vp]),
         "fb_arena_fetch_log": (C.c_int, [vp, i64, vp, vp, vp]),
@@ -362,6 +363,14 @@ class Arena:
             raise ValueError("records out: need a contiguous RECORD_DTYPE array of n_rec rows")
         _check(self._lib.fb_arena_fetch_records(self._h, _abi.vptr(out)), "fb_arena_fetch_records")
         return out[:n]
+
+    def summaries(self) -> np.ndarray:
+        """Per-instance ScenarioReport aggregates computed on the device
+        (SUMMARY_DTYPE rows; see reports.summary_report)."""
+        out = np.zeros(max(1, self.n_instances), _abi.SUMMARY_DTYPE)
+        _check(self._lib.fb_arena_fetch_summaries(self._h, _abi.vptr(out)),
+               "fb_arena_fetch_summaries")
+        return out[:self.n_instances]
 
     def record_rows(self) -> int:
         return int(self._lib.fb_arena_record_rows(self._h))

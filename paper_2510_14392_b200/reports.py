@@ -96,3 +96,28 @@ def goodput(records: np.ndarray, offered: float) -> float:
     arrived = (records["flags"] & _abi.REC_ARRIVED) != 0
     n = max(1, int(arrived.sum()))
     return offered * float(good_mask(records[arrived]).sum()) / n
+
+
+def summary_report(row, offered: float, name: str = "", alt_tpot: bool = False) -> ScenarioReport:
+    """ScenarioReport from one device summary row (fb_arena_fetch_summaries):
+    the counts and percentiles come from the device, the rates are the
+    host arithmetic of scenario_report (metrics.cpp:190-196)."""
+    rep = ScenarioReport(name=name, offered_rps=offered)
+    rep.total_requests = int(row["total_requests"])
+    rep.rejected = int(row["rejected"])
+    rep.finished = int(row["finished"])
+    rep.good = int(row["good"])
+    frac = 0.0 if rep.total_requests == 0 else rep.good / rep.total_requests
+    rep.slo_violation_rate = 1.0 - frac
+    rep.effective_rps = offered * frac
+
+    def pct(r):
+        return PercentileRow(float(r["p50"]), float(r["p95"]), float(r["p99"]), int(r["count"]))
+
+    rep.ttft = pct(row["ttft_ms"])
+    rep.max_tpot = pct(row["max_tpot_ms"])
+    if alt_tpot:
+        rep.max_tpot_alt = pct(row["max_tpot_alt_ms"])
+    rep.ttft_violations = int(row["ttft_violations"])
+    rep.envelope_misses = int(row["envelope_misses"])
+    return rep

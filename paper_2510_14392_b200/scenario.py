@@ -289,11 +289,9 @@ def _run_points(points, device=0):
     a = fbgpu.Arena(device)
     a.load(b)
     a.run()
-    rec = a.records()
+    summ = a.summaries()  # aggregated on the device: no per-request records shipped
     a.close()
-    ro = b.record_offsets()
-    return [reports.scenario_report(rec[ro[i]:ro[i + 1]], offs[i].arrival_us,
-                                    offs[i].offered_rps()) for i in range(b.n_instances)]
+    return [reports.summary_report(summ[i], offs[i].offered_rps()) for i in range(b.n_instances)]
 
 
 def sweep_scenario(sc: Scenario, scales, policies, device: int = 0) -> list[SweepRow]:

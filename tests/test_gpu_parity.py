@@ -370,3 +370,31 @@ def test_cluster_two_processes_cuda_ipc(fb, oracle):
     _, rows, cfgs, lb, hz = {c[0]: c for c in cluster_cases(oracle.generate_bursty)}[name]
     ref = oracle.run_cluster(rows.truncated(120), cfgs, lb, hz)
     assert got == cluster_summary(ref)
+
+
+# ------------------------------------------------------- device aggregates
+
+
+@pytest.mark.parametrize("name", sorted(SCENARIOS))
+def test_device_summaries_match_host_reports(fb, gpu, name):
+    """fb_arena_fetch_summaries (on-device scenario_report, metrics.cpp:171-205)
+    equals the host aggregation of the byte-identical records, field for
+    field: counts, and nearest-rank p50/p95/p99 as exact doubles (the wide
+    scenario has > 2048 values per series: the radix-select path)."""
+    from paper_2510_14392_b200 import reports
+    batch = SCENARIOS[name](gpu.generate_bursty)
+    a = fb.Arena(0)
+    a.load(batch)
+    a.run()
+    summ = a.summaries()
+    rec = a.records()
+    a.close()
+    off = batch.record_offsets()
+    rows = batch.rows
+    for i in range(batch.n_instances):
+        x = batch.instance(i)
+        r = rec[off[i]:off[i + 1]]
+        arr = rows.arrival_us[x.trace_off:x.trace_off + x.n_req]
+        host = reports.scenario_report(r, arr, 1.0, alt_tpot=True)
+        dev = reports.summary_report(summ[i], 1.0, alt_tpot=True)
+        assert dev == host, (name, i)
