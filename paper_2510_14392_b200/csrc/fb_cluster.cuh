@@ -119,8 +119,9 @@ __device__ bool cluster_barrier(const ClusterParams& C, RouterSmem& rs, int64_t 
     const uint64_t* ctr = xchg_counter(C.xbuf[C.rank]);
     if (ld_acquire_u64(ctr, sys) < target) {
       const uint64_t t0 = global_ns();
-      while (ld_acquire_u64(ctr, sys) < target) {
-        if (global_ns() - t0 > static_cast<uint64_t>(C.timeout_ns)) {
+      for (uint32_t spin = 1; ld_acquire_u64(ctr, sys) < target; ++spin) {
+        // the timer read is costly: check the timeout every 64 polls
+        if ((spin & 63) == 0 && global_ns() - t0 > static_cast<uint64_t>(C.timeout_ns)) {
           rs.abort = 1;
           break;
         }

@@ -13,6 +13,7 @@
 // estimation (pull_pab / pab kernel).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "fb_kernels.h"
@@ -741,7 +742,13 @@ int cluster_warps_per_cta(int n_nodes, int n_ranks) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms < 1) sms = 148;
   const int max_local = (n_nodes + n_ranks - 1) / n_ranks;
-  int w = (max_local + sms - 1) / sms;  // spread nodes over the SMs
+  // Full CTAs of kClusterMaxWarps nodes: the per-epoch exchange barrier
+  // then has few participants (C5, 64 nodes: 8 CTAs 208 ms vs 64 CTAs of
+  // one node 227 ms); more nodes than SMs x 8 still spread over every SM.
+  int w = (max_local + sms - 1) / sms;
+  if (w < kClusterMaxWarps) w = max_local < kClusterMaxWarps ? max_local : kClusterMaxWarps;
+  if (w > kClusterMaxWarps) w = kClusterMaxWarps;
+  (void)sms;
   return w < 1 ? 1 : w;
 }
 
