@@ -170,7 +170,7 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
     arena.load(batch)
     arena.run()
     arena.synchronize()
-    tot, wide = [], []
+    tot, wide, phases = [], [], []
     for _ in range(reps):
         arena.reset()
         arena.run()
@@ -178,8 +178,18 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
         w, g = arena.last_run_split_ms()
         tot.append(w + g)
         wide.append(g)
+        phases.append(arena.wide_phases()[0])
     r = arena.results()
     arena.close()
+    ph = {k: statistics.median(p[k] for p in phases) for k in phases[0]}
+    # the slack/selection kernels proper: K1 views (envelope slack, key
+    # stems) + K2 histogram + K2 gather, each phase timed on the device up to
+    # and including its closing grid barrier; algorithmic bytes 32 per
+    # visible task
+    sel_ms = ph["k1_views"] + ph["k2_hist"] + ph["k2_gather"]
+    sel_bytes = 32 * int(r["sum_visible"].sum())
+    sel_ach = sel_bytes / (sel_ms / 1000.0) / 1e9
+    k1_ach = sel_bytes / (ph["k1_views"] / 1000.0) / 1e9
     steps = int(r["steps"].sum())
     alg = int(32 * r["sum_visible"].sum() + 64 * r["sum_entries"].sum()
               + 64 * r["n_arrived"].sum())
@@ -192,7 +202,13 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": None,
                          "kernel": "engine_kernel+wide_grid_kernel (whole pass)",
-                         "alg_bytes_per_launch": alg, "peak_source": peak_kind}}
+                         "alg_bytes_per_launch": alg, "peak_source": peak_kind},
+            "phases_ms": ph,
+            "roofline_slack_selection": {
+                "bound": "hbm", "achieved": sel_ach, "peak": peak, "unit": "GB/s",
+                "frac": sel_ach / peak, "phases": "K1 views + K2a histogram + K2b gather",
+                "alg_bytes": sel_bytes, "ms": sel_ms,
+                "k1_views_achieved": k1_ach, "k1_views_frac": k1_ach / peak}}
 
 
 def run_reference(args) -> None:

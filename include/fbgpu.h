@@ -312,6 +312,11 @@ int fb_arena_last_run_ms(fb_arena* arena, float* ms_out);
 /* The same run split into the warp engine and the grid-wide wide engine
  * (nodes with more than 512 live requests). */
 int fb_arena_last_run_split_ms(fb_arena* arena, float* warp_ms, float* wide_ms);
+/* Phase clock of the last run's grid-wide wide engine (wall time seen by
+ * CTA 0, each phase including its closing grid barrier): ms_out[5] =
+ * {owner advance, K1 views, K2a histogram, K2b gather, owner finish};
+ * *iterations (may be NULL) = lockstep iterations. */
+int fb_arena_wide_phases(fb_arena* arena, double* ms_out, int64_t* iterations);
 
 int fb_arena_fetch_results(fb_arena* arena, fb_instance_result* out);
 /* Records for instance rows: out has sum over instances of n_req rows, in

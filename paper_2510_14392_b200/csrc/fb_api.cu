@@ -430,7 +430,7 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
     ENSURE(a->wg_hist, z.hist_words);
     ENSURE(a->wg_ckey, z.cand_rows);
     ENSURE(a->wg_cpos, z.cand_rows);
-    ENSURE(a->wg_bar, 4);  // barrier + three chunk counters
+    ENSURE(a->wg_bar, 16);  // barrier counter + phase clock
   }
 #undef ENSURE
   std::vector<unsigned char> hinst(static_cast<size_t>(n_instances) * fbgpu::dev_inst_bytes());
@@ -509,6 +509,17 @@ int fb_arena_last_run_split_ms(fb_arena* a, float* warp_ms, float* wide_ms) {
   FB_CUDA(cudaEventSynchronize(a->ev1));
   FB_CUDA(cudaEventElapsedTime(warp_ms, a->ev0, a->evm));
   FB_CUDA(cudaEventElapsedTime(wide_ms, a->evm, a->ev1));
+  return FB_OK;
+}
+
+int fb_arena_wide_phases(fb_arena* a, double* ms_out, int64_t* iterations) {
+  if (!a || !a->loaded || !ms_out) return set_error(FB_ERR_USAGE, "fb_arena_wide_phases");
+  FB_CUDA(cudaSetDevice(a->device));
+  unsigned long long h[16] = {};
+  FB_CUDA(cudaMemcpyAsync(h, a->wg_bar.p, sizeof(h), cudaMemcpyDeviceToHost, a->stream));
+  FB_CUDA(cudaStreamSynchronize(a->stream));
+  for (int k = 0; k < 5; ++k) ms_out[k] = static_cast<double>(h[8 + k]) * 1e-6;
+  if (iterations) *iterations = static_cast<int64_t>(h[13]);
   return FB_OK;
 }
 

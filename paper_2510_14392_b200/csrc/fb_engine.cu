@@ -783,7 +783,7 @@ cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g, cudaSt
   if (between) cudaEventRecord(between, st);
   // Escalated instances (more than kEscalateLive live requests) continue on
   // the grid-wide wide engine; with none escalated it exits after one barrier.
-  cudaMemsetAsync(p.wg.bar, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(p.wg.bar, 0, 16 * sizeof(unsigned long long), st);  // barrier + phase clock
   EngineParams pp = p;
   void* args[] = {&pp};
   // cooperative: every CTA must be co-resident for the grid barriers

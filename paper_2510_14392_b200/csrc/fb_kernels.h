@@ -19,7 +19,8 @@ struct WideGridBufs {
   uint32_t* hist;            // [n_slots][kSelBins]
   uint64_t* ckey;            // [n_slots][kWideWin] gathered window keys
   int32_t* cpos;             // [n_slots][kWideWin] their view positions
-  unsigned long long* bar;   // grid barrier counter (zeroed per launch)
+  unsigned long long* bar;   // [0] grid barrier counter, [8..12] phase ns, [13] iterations
+                             // (zeroed per launch)
 };
 
 // Everything the engine kernel touches, as device pointers.

@@ -1726,6 +1726,19 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
   }
   __syncthreads();
   uint64_t gen = 0;
+  // Always-on phase clock (CTA 0, %globaltimer ns) -> wg.bar[8 + phase],
+  // wg.bar[13] = iterations; read by fb_arena_wide_phases.
+  uint64_t ph_t = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ph_t));
+  auto phase = [&](int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      uint64_t n;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n));
+      P.wg.bar[8 + k] += n - ph_t;
+      ph_t = n;
+    }
+  };
 #ifdef FB_WIDE_PROF
   long long gp_t = clock64();
 #define GPROF(slot)                                                                    \
@@ -1760,6 +1773,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     }
     wg_barrier(P.wg.bar, ++gen);
     GPROF(12)
+    phase(0);
     // ---- work split (every CTA, from the published slots)
     WgSplit sp;
     {
@@ -1807,6 +1821,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     }
     wg_barrier(P.wg.bar, ++gen);
     GPROF(13)
+    phase(1);
     // ---- K2a: histogram of the selection bins
     {
       CPROF_START
@@ -1873,6 +1888,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     }
     wg_barrier(P.wg.bar, ++gen);
     GPROF(14)
+    phase(2);
     // ---- K2b: gather the window's keys
     {
       CPROF_START
@@ -1922,6 +1938,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     }
     wg_barrier(P.wg.bar, ++gen);
     GPROF(15)
+    phase(3);
     // ---- owner: the rest of begin_step
     if (s_have) {
       WPROF_START
@@ -1954,6 +1971,8 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       __syncthreads();
     }
     GPROF(9)
+    phase(4);
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.wg.bar[13]++;
   }
 }
 

@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "fb_arena_synchronize": (C.c_int, [vp]),
         "fb_arena_last_run_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
         "fb_arena_last_run_split_ms": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+        "fb_arena_wide_phases": (C.c_int, [vp, C.POINTER(C.c_double), pi64]),
         "fb_arena_fetch_results": (C.c_int, [vp, vp]),
         "fb_arena_fetch_records": (C.c_int, [vp, vp]),
         "fb_arena_fetch_summaries": (C.c_int, [vp, vp]),
@@ -348,6 +349,14 @@ class Arena:
         _check(self._lib.fb_arena_last_run_split_ms(self._h, C.byref(a), C.byref(b)),
                "fb_arena_last_run_split_ms")
         return a.value, b.value
+
+    def wide_phases(self) -> tuple[dict, int]:
+        """Phase clock of the last run's grid-wide wide engine: ({phase: ms}, iterations)."""
+        ms = (C.c_double * 5)()
+        it = C.c_int64(0)
+        _check(self._lib.fb_arena_wide_phases(self._h, ms, C.byref(it)), "fb_arena_wide_phases")
+        names = ("owner_advance", "k1_views", "k2_hist", "k2_gather", "owner_finish_cta0")
+        return dict(zip(names, list(ms))), it.value
 
     def results(self) -> np.ndarray:
         out = np.zeros(max(1, self.n_instances), _abi.RESULT_DTYPE)
