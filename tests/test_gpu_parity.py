@@ -398,3 +398,84 @@ def test_device_summaries_match_host_reports(fb, gpu, name):
         host = reports.scenario_report(r, arr, 1.0, alt_tpot=True)
         dev = reports.summary_report(summ[i], 1.0, alt_tpot=True)
         assert dev == host, (name, i)
+
+
+# ------------------------------------------------------- edge cases / API paths
+
+
+def test_stepwise_wide_engine_matches_one_shot(gpu):
+    """Event-budgeted driving of escalated (> 512 live) nodes: the grid-wide
+    engine releases a node mid-run and picks it up in the next launch, with
+    its view records, marks and takes persisting across launches."""
+    batch = SCENARIOS["wide"](gpu.generate_bursty)
+    one = gpu.run(batch)
+    for budget in (13, 64):
+        inc = gpu.run(batch, max_events=budget)
+        assert summarize(one.results, one.records) == summarize(inc.results, inc.records), budget
+
+
+def test_summaries_mid_run_do_not_perturb(fb, gpu):
+    """fb_arena_fetch_summaries between event-budgeted runs (its scratch is
+    separate from the engines' persistent state)."""
+    batch = SCENARIOS["wide"](gpu.generate_bursty)
+    ref = gpu.run(batch)
+    a = fb.Arena(0)
+    a.load(batch)
+    while a.run(29, sync=True) > 0:
+        a.summaries()
+    assert a.results().tobytes() == ref.results.tobytes()
+    assert a.records().tobytes() == ref.records.tobytes()
+    a.close()
+
+
+def test_empty_and_degenerate_batches(fb, oracle):
+    """No instances; instances with zero requests next to normal and wide ones;
+    a horizon of zero (no step may begin)."""
+    from paper_2510_14392_b200.batch import CostModel, Rows, engine_config
+    a = fb.Arena(0)
+    a.load(Batch())
+    a.run()
+    assert len(a.results()) == 0 and len(a.records()) == 0 and len(a.summaries()) == 0
+    cfg = engine_config("fairbatch", 2048, CostModel(5, 0.05, 1e-4), 500, 50)
+    b = Batch()
+    b.add(Rows.empty(), cfg, 10**9)
+    b.extend(SCENARIOS["c2_subset"](fb.generate_bursty).subset([0, 1]))
+    b.add(Rows([0, 10], [64, 64], [4, 4], [500_000] * 2, [50_000] * 2), cfg, 0)
+    b.add(Rows.empty(), cfg, 0)
+    a.load(b)
+    a.run()
+    got_r, got_c = a.results(), a.records()
+    want = oracle.run(b)
+    assert got_r.tobytes() == want.results.tobytes()
+    assert got_c.tobytes() == want.records.tobytes()
+    s = a.summaries()
+    assert s[0]["total_requests"] == 0 and s[0]["ttft_ms"]["count"] == 0
+    a.close()
+
+
+def test_pinned_buffers_match_pageable(fb):
+    """Uploads from fb_host_alloc memory and records into a pinned buffer
+    (direct DMA) equal the staged pageable path byte for byte."""
+    batch = workloads.c2_batch(n_seeds=32)
+    a = fb.Arena(0)
+    a.load(batch)
+    a.run()
+    r1, c1 = a.results().copy(), a.records().copy()
+    batch.pin()
+    out = fb.pinned_empty(a.record_rows(), _abi.RECORD_DTYPE)
+    a.load(batch)
+    a.run()
+    assert a.results().tobytes() == r1.tobytes()
+    assert a.records(out=out).tobytes() == c1.tobytes()
+    a.close()
+
+
+def test_run_batch_cached_arena_resizes(fb, gpu):
+    """fb_run_batch reuses one arena per device: a large batch, then a small
+    one, then the large one again, each equal to a fresh arena's run."""
+    big = SCENARIOS["c2_subset"](gpu.generate_bursty)
+    small = big.subset([3])
+    for b in (big, small, big):
+        res, rec, _ = fb.run_batch(b)
+        out = gpu.run(b)
+        assert res.tobytes() == out.results.tobytes() and rec.tobytes() == out.records.tobytes()
