@@ -21,7 +21,10 @@
 
 namespace fbgpu {
 
-constexpr int kWarpsPerBlock = 8;
+#ifndef FB_WARPS_PER_BLOCK
+#define FB_WARPS_PER_BLOCK 8
+#endif
+constexpr int kWarpsPerBlock = FB_WARPS_PER_BLOCK;
 constexpr int kSmemSlots = 64;  // visible tasks held in shared-memory scratch
 #ifndef FB_ENGINE_BLOCKS_PER_SM
 #define FB_ENGINE_BLOCKS_PER_SM 2
