@@ -1,0 +1,248 @@
+// fb_cluster.cu -- run_cluster on the device (fb_cluster.cuh) and the pure
+// scheduler surface (form_batch / init_time_budget / pab over task sets);
+// one full warp per node / task set (kTile = 32).
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#define FB_TILE 32
+#include "fb_engine_dev.cuh"
+#include "fb_cluster.cuh"
+
+namespace fbgpu {
+
+size_t cluster_param_bytes() { return sizeof(ClusterParams); }
+int cluster_max_nodes() { return kClusterMaxNodes; }
+int cluster_max_ranks() { return kClusterMaxRanks; }
+size_t cluster_xchg_bytes(int n_nodes) {
+  return kXchgHeader + 2 * sizeof(NodeReport) * static_cast<size_t>(n_nodes);
+}
+
+int cluster_warps_per_cta(int n_nodes, int n_ranks) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms < 1) sms = 148;
+  const int max_local = (n_nodes + n_ranks - 1) / n_ranks;
+  // Full CTAs of kClusterMaxWarps nodes: the per-epoch exchange barrier
+  // then has few participants (C5, 64 nodes: 8 CTAs 208 ms vs 64 CTAs of
+  // one node 227 ms); more nodes than SMs x 8 still spread over every SM.
+  int w = (max_local + sms - 1) / sms;
+  if (w < kClusterMaxWarps) w = max_local < kClusterMaxWarps ? max_local : kClusterMaxWarps;
+  if (w > kClusterMaxWarps) w = kClusterMaxWarps;
+  (void)sms;
+  return w < 1 ? 1 : w;
+}
+
+size_t cluster_smem_bytes(int warps_per_cta) {
+  return ((sizeof(RouterSmem) + 15) / 16) * 16 +
+         static_cast<size_t>(warps_per_cta) * kSmemSlots * kScratchBytesPerSlot;
+}
+
+cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, int blocks,
+                           cudaStream_t st) {
+  static_assert(sizeof(ClusterParamsHost) == sizeof(ClusterParams), "cluster params layout");
+  ClusterParams c;
+  std::memcpy(&c, &ch, sizeof(c));
+  if (c.warps_per_cta < 1 || c.warps_per_cta > kClusterMaxWarps) return cudaErrorInvalidValue;
+  const size_t smem = cluster_smem_bytes(c.warps_per_cta);
+  cudaError_t e = cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  EngineParams pp = p;
+  void* args[] = {&pp, &c};
+  // cooperative: every CTA must be co-resident for the epoch barrier
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cluster_kernel), dim3(blocks),
+                                     dim3(kWarp * c.warps_per_cta), args, smem, st);
+}
+
+// ------------------------------------------------- pure scheduler kernels
+
+__device__ __forceinline__ Scratch set_scratch(unsigned char* smem_warp, unsigned char* g,
+                                               int64_t off, int64_t n) {
+  if (n <= kSmemSlots) return carve_scratch(smem_warp, kSmemSlots);
+  return carve_scratch(g + off * kScratchBytesPerSlot, static_cast<int>(n));
+}
+
+// form_batch (sched.cpp:234-246) per task set, one warp per set.
+__global__ void __launch_bounds__(kWarp * kWarpsPerBlock)
+form_batch_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restrict__ set_off,
+                  const fb_scheduler_config* __restrict__ cfgs, int64_t n_sets,
+                  fb_plan_entry_id* __restrict__ entries, fb_batch_plan* __restrict__ plans,
+                  unsigned char* gscratch, int* status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x / kWarp;
+  unsigned char* my = smem + static_cast<size_t>(warp) * kSmemSlots * kScratchBytesPerSlot;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
+  for (int64_t set = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; set < n_sets;
+       set += nwarps) {
+    const int64_t off = set_off[set];
+    const int64_t n = set_off[set + 1] - off;
+    const fb_scheduler_config cfg = cfgs[set];
+    const bool fair = cfg.policy == FB_POLICY_FAIRBATCH || cfg.policy == FB_POLICY_FAIRBATCH_PAB;
+    if (n == 0) {
+      if (lane_id() == 0) {
+        if (fair) atomicExch(status, FB_ERR_USAGE);  // init_time_budget on empty
+        fb_batch_plan pl = {};
+        pl.entry_off = off;
+        plans[set] = pl;
+      }
+      continue;
+    }
+    const Scratch s = set_scratch(my, gscratch, off, n);
+    ViewAcc acc;
+    for (int64_t p = lane_id(); p < n; p += kWarp) {
+      const fb_task_view t = tasks[off + p];
+      const bool decode = t.phase == FB_PHASE_DECODE;
+      s.slack[p] = t.slack_us;
+      s.seq[p] = t.arrival_seq;
+      s.ctx[p] = t.context;
+      s.nw[p] = t.new_tokens | (decode ? static_cast<int32_t>(kDecodeBit) : 0);
+      s.req[p] = static_cast<int32_t>(p);
+      acc.add(decode, t.slack_us, t.tpot_us);
+    }
+    __syncwarp();
+    acc.reduce();
+    FormCfg f;
+    f.policy = cfg.policy;
+    f.max_chunk = cfg.max_chunk;
+    f.token_budget = cfg.token_budget;
+    f.a = cfg.model.a_ms;
+    f.b = cfg.model.b_ms;
+    f.c = cfg.model.c_ms;
+    const int Ai = static_cast<int>(n);
+    const FormOut o = form_batch_warp(s, Ai, acc, f, /*seq_unique=*/false);
+    int run = 0;
+    for (int k0 = 0; k0 < Ai; k0 += kWarp) {
+      const int k = k0 + lane_id();
+      int tk = 0, p = 0;
+      if (k < Ai) {
+        p = s.order[k];
+        tk = s.take[k];
+      }
+      const unsigned m = __ballot_sync(kFull, tk > 0);
+      if (tk > 0) {
+        fb_plan_entry_id e;
+        e.request_id = tasks[off + p].request_id;
+        e.new_tokens = tk;
+        e.reserved = 0;
+        entries[off + run + __popc(m & lanemask_lt())] = e;
+      }
+      run += __popc(m);
+    }
+    if (lane_id() == 0) {
+      fb_batch_plan pl;
+      const bool empty = o.n_entries == 0;
+      pl.predicted_ms = o.predicted_ms;
+      pl.time_budget_used_ms = empty ? 0.0 : o.predicted_ms;
+      pl.token_budget_used = empty ? 0 : o.total_new;
+      pl.init_time_budget_ms = o.init_ms;
+      pl.entry_off = off;
+      pl.n_entries = o.n_entries;
+      plans[set] = pl;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void init_time_budget_kernel(const fb_task_view* __restrict__ tasks,
+                                        const int64_t* __restrict__ set_off, int64_t n_sets,
+                                        int64_t* out, int* status) {
+  const int warp = threadIdx.x / kWarp;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x / kWarp);
+  for (int64_t set = static_cast<int64_t>(blockIdx.x) * (blockDim.x / kWarp) + warp;
+       set < n_sets; set += nwarps) {
+    const int64_t off = set_off[set];
+    const int64_t n = set_off[set + 1] - off;
+    ViewAcc acc;
+    for (int64_t p = lane_id(); p < n; p += kWarp) {
+      const fb_task_view t = tasks[off + p];
+      acc.add(t.phase == FB_PHASE_DECODE, t.slack_us, t.tpot_us);
+    }
+    acc.reduce();
+    if (lane_id() == 0) {
+      if (n == 0) {
+        atomicExch(status, FB_ERR_USAGE);
+        out[set] = 0;
+      } else {
+        out[set] = acc.n_dec == 0 ? acc.min_tpot
+                                  : (acc.min_dec > acc.min_tpot ? acc.min_dec : acc.min_tpot);
+      }
+    }
+  }
+}
+
+// K5 standalone: pab (sched.cpp:248-278) per task set.
+__global__ void __launch_bounds__(kWarp * kWarpsPerBlock)
+pab_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restrict__ set_off,
+           const fb_cost_model* __restrict__ models, const int64_t* __restrict__ ttft,
+           const int64_t* __restrict__ tpot, int64_t n_sets, int64_t* out,
+           unsigned char* gscratch) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x / kWarp;
+  unsigned char* my = smem + static_cast<size_t>(warp) * kSmemSlots * kScratchBytesPerSlot;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarpsPerBlock;
+  for (int64_t set = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp; set < n_sets;
+       set += nwarps) {
+    const int64_t off = set_off[set];
+    const int64_t n = set_off[set + 1] - off;
+    const fb_cost_model m = models[set];
+    const double Wm = us_to_ms(ttft[set]), Tm = us_to_ms(tpot[set]);
+    const Scratch s = set_scratch(my, gscratch, off, n);
+    int64_t lmin = kInf, lpf = 0;
+    for (int64_t p = lane_id(); p < n; p += kWarp) {
+      const fb_task_view t = tasks[off + p];
+      s.tcost[p] = pab_term(Wm, Tm, m.b_ms, m.c_ms, t.slack_us, t.context);
+      lmin = t.slack_us < lmin ? t.slack_us : lmin;
+      if (t.phase == FB_PHASE_PREFILL) lpf += t.new_tokens;
+    }
+    __syncwarp();
+    const int64_t min_slack = warp_min(lmin);
+    const int64_t pf = warp_sum(lpf);
+    const double r_tasks = ordered_fold(s.tcost, static_cast<int>(n));
+    if (lane_id() == 0)
+      out[set] = pab_close(Wm, Tm, m.a_ms, m.b_ms, m.c_ms, n > 0, min_slack, r_tasks, pf);
+    __syncwarp();
+  }
+}
+
+static int set_blocks(int64_t n_sets) {
+  int64_t b = (n_sets + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (b < 1) b = 1;
+  if (b > 148 * 8) b = 148 * 8;
+  return static_cast<int>(b);
+}
+
+cudaError_t launch_form_batch(const fb_task_view* tasks, const int64_t* set_off,
+                              const fb_scheduler_config* cfgs, int64_t n_sets,
+                              fb_plan_entry_id* entries, fb_batch_plan* plans,
+                              unsigned char* scratch, int* status, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * kSmemSlots * kScratchBytesPerSlot;
+  cudaFuncSetAttribute(form_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  form_batch_kernel<<<set_blocks(n_sets), kWarp * kWarpsPerBlock, smem, st>>>(
+      tasks, set_off, cfgs, n_sets, entries, plans, scratch, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_time_budget(const fb_task_view* tasks, const int64_t* set_off,
+                                    int64_t n_sets, int64_t* out, int* status,
+                                    cudaStream_t st) {
+  init_time_budget_kernel<<<set_blocks(n_sets), kWarp * kWarpsPerBlock, 0, st>>>(
+      tasks, set_off, n_sets, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pab(const fb_task_view* tasks, const int64_t* set_off,
+                       const fb_cost_model* models, const int64_t* ttft, const int64_t* tpot,
+                       int64_t n_sets, int64_t* out, unsigned char* scratch, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * kSmemSlots * kScratchBytesPerSlot;
+  cudaFuncSetAttribute(pab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  pab_kernel<<<set_blocks(n_sets), kWarp * kWarpsPerBlock, smem, st>>>(
+      tasks, set_off, models, ttft, tpot, n_sets, out, scratch);
+  return cudaGetLastError();
+}
+
+}  // namespace fbgpu

@@ -145,6 +145,104 @@ __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t v) {
   return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
+// ------------------------------------------------------------- tile utils
+//
+// The warp engine simulates one node per *tile* of kTile lanes: a half-warp
+// in the engine kernel (two nodes advance per warp instruction when their
+// control flow agrees), a full warp in the cluster and pure-scheduler
+// kernels.  Every lane-collective on the per-node paths goes through these:
+// masks name only the tile, so the two tiles of a warp stay correct whether
+// they run converged or diverged.  Ballots / match results and lane indices
+// are tile-relative.
+#ifndef FB_TILE
+#define FB_TILE 32
+#endif
+constexpr int kTile = FB_TILE;
+static_assert(kTile == 16 || kTile == 32, "tile of 16 or 32 lanes");
+
+__device__ __forceinline__ int tile_lane() { return threadIdx.x & (kTile - 1); }
+__device__ __forceinline__ int tile_base() { return (threadIdx.x & (kWarp - 1)) & ~(kTile - 1); }
+__device__ __forceinline__ unsigned tile_mask() {
+  return kTile == kWarp ? kFull : (((1u << kTile) - 1u) << tile_base());
+}
+__device__ __forceinline__ void tile_sync() { __syncwarp(tile_mask()); }
+__device__ __forceinline__ unsigned tile_ballot(bool p) {
+  if (kTile == kWarp) return __ballot_sync(kFull, p);
+  return __ballot_sync(tile_mask(), p) >> tile_base();
+}
+__device__ __forceinline__ bool tile_all(bool p) { return __all_sync(tile_mask(), p); }
+__device__ __forceinline__ bool tile_any(bool p) { return __any_sync(tile_mask(), p); }
+__device__ __forceinline__ unsigned tile_match_any(unsigned v) {
+  if (kTile == kWarp) return __match_any_sync(kFull, v);
+  return __match_any_sync(tile_mask(), v) >> tile_base();
+}
+__device__ __forceinline__ unsigned tile_lanemask_lt() { return (1u << tile_lane()) - 1u; }
+template <typename T>
+__device__ __forceinline__ T tile_shfl(T v, int src) {
+  return __shfl_sync(tile_mask(), v, src, kTile);
+}
+template <typename T>
+__device__ __forceinline__ T tile_shfl_xor(T v, int o) {
+  return __shfl_xor_sync(tile_mask(), v, o, kTile);
+}
+template <typename T>
+__device__ __forceinline__ T tile_shfl_up(T v, int o) {
+  return __shfl_up_sync(tile_mask(), v, o, kTile);
+}
+template <typename T>
+__device__ __forceinline__ T tile_min(T v) {
+#pragma unroll
+  for (int o = kTile / 2; o > 0; o >>= 1) {
+    T w = tile_shfl_xor(v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T tile_max(T v) {
+#pragma unroll
+  for (int o = kTile / 2; o > 0; o >>= 1) {
+    T w = tile_shfl_xor(v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T tile_sum(T v) {  // integers only (exact)
+#pragma unroll
+  for (int o = kTile / 2; o > 0; o >>= 1) v += tile_shfl_xor(v, o);
+  return v;
+}
+__device__ __forceinline__ int64_t tile_min_i64(int64_t v) {
+  const bool none = v == kInf;
+  const bool fits = none || (v >= INT32_MIN && v < INT32_MAX);
+  if (tile_all(fits)) {
+    const int m = __reduce_min_sync(tile_mask(), none ? INT32_MAX : static_cast<int>(v));
+    return m == INT32_MAX ? kInf : static_cast<int64_t>(m);
+  }
+  return tile_min(v);
+}
+__device__ __forceinline__ int64_t tile_sum_small(int64_t v) {
+  const uint32_t lo = static_cast<uint32_t>(v) & 0xffffffu;
+  const uint32_t hi = static_cast<uint32_t>(static_cast<uint64_t>(v) >> 24);
+  return (static_cast<int64_t>(__reduce_add_sync(tile_mask(), hi)) << 24) +
+         static_cast<int64_t>(__reduce_add_sync(tile_mask(), lo));
+}
+__device__ __forceinline__ uint32_t tile_add_u32(uint32_t v) {
+  return __reduce_add_sync(tile_mask(), v);
+}
+__device__ __forceinline__ int tile_min_i32(int v) { return __reduce_min_sync(tile_mask(), v); }
+__device__ __forceinline__ double tile_sum_ru(double v) {
+#pragma unroll
+  for (int o = kTile / 2; o > 0; o >>= 1) v = __dadd_ru(v, tile_shfl_xor(v, o));
+  return v;
+}
+__device__ __forceinline__ uint64_t tile_xor_u64(uint64_t v) {
+  const uint32_t lo = __reduce_xor_sync(tile_mask(), static_cast<uint32_t>(v));
+  const uint32_t hi = __reduce_xor_sync(tile_mask(), static_cast<uint32_t>(v >> 32));
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
 // ---------------------------------------------------------- device layouts
 
 // Immutable per-instance parameters (from fb_instance).

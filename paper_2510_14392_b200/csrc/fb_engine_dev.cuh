@@ -1,0 +1,537 @@
+// fb_engine_dev.cuh -- the warp engine's device code: one tile (kTile lanes;
+// a half-warp in the engine kernel, a full warp in the cluster and
+// pure-scheduler kernels) simulates one Node instance (engine.h:111-176):
+// task views, the memory-path begin/complete step, the register-resident
+// path (fb_engine_rr.cuh) and run_node's event loop.  Included by
+// fb_engine.cu (kTile = 16) and fb_cluster.cu (kTile = 32).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "fb_kernels.h"
+#include "fb_sched.cuh"
+
+namespace fbgpu {
+
+#ifndef FB_WARPS_PER_BLOCK
+#define FB_WARPS_PER_BLOCK 8
+#endif
+constexpr int kWarpsPerBlock = FB_WARPS_PER_BLOCK;
+constexpr int kSmemSlots = 64;  // visible tasks held in shared-memory scratch
+#ifndef FB_ENGINE_BLOCKS_PER_SM
+#define FB_ENGINE_BLOCKS_PER_SM 2
+#endif
+constexpr int kEngineBlocksPerSm = FB_ENGINE_BLOCKS_PER_SM;  // register cap for occupancy
+constexpr int64_t kEscalateLive = 512;  // live requests beyond which a node goes CTA-wide
+
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-uniform view of one instance while a warp owns it.
+struct Inst {
+  int64_t id;
+  const int32_t* routed;  // cluster node: pending slot -> trace row (else identity)
+  const DevInst* I;
+  DevState S;
+  int64_t toff, roff, nreq, horizon;
+  int32_t policy, max_active;
+  int2* vl;
+  unsigned char* smem;  // this warp's shared scratch
+};
+
+// Trace row of the q-th request that reached this node (run_node: the trace
+// itself; cluster nodes: the router's append order).
+__device__ __forceinline__ int64_t arrival_row(const Inst& w, int64_t q) {
+  return w.routed ? static_cast<int64_t>(w.routed[q]) : q;
+}
+
+__device__ __forceinline__ int64_t visible_count(const Inst& w) {
+  int64_t nw = w.S.n_live - w.S.n_active;
+  if (w.max_active > 0) {
+    int64_t slots = static_cast<int64_t>(w.max_active) - w.S.n_active;
+    if (slots < 0) slots = 0;
+    if (nw > slots) nw = slots;
+  }
+  return w.S.n_active + nw;
+}
+
+__device__ __forceinline__ Scratch scratch_for(const EngineParams& P, const Inst& w,
+                                               int64_t A) {
+  if (A <= kSmemSlots) return carve_scratch(w.smem, kSmemSlots);
+  return carve_scratch(P.gscratch + w.roff * kScratchBytesPerSlot, static_cast<int>(w.nreq));
+}
+
+// K1: one task view (build_task_views, engine.cpp:51-81; slack, slo.h:45-61).
+struct View {
+  int32_t r;
+  int32_t nw;  // new tokens | kDecodeBit
+  int64_t slack, ctx, tpot, seq;
+  bool decode;
+};
+
+__device__ __forceinline__ View load_view(const EngineParams& P, const Inst& w,
+                                          int64_t p, int64_t now) {
+  View v;
+  v.r = w.vl[p].x;
+  const int64_t g = w.roff + v.r;
+  const int64_t row = w.toff + v.r;
+  const int32_t prompt = P.prompt[row];
+  const int32_t pf = P.prefilled[g];
+  const int32_t ni = P.nidx[g];
+  v.tpot = P.tpot[row];
+  const int64_t ttft_deadline = P.arrival[row] + P.ttft[row];
+  v.seq = P.seq[g];
+  if (pf < prompt) {
+    v.decode = false;
+    v.nw = prompt - pf;
+    v.ctx = pf;
+    v.slack = ttft_deadline + v.tpot * static_cast<int64_t>(ni) - now;
+  } else {
+    v.decode = true;
+    v.nw = 1 | static_cast<int32_t>(kDecodeBit);
+    v.ctx = static_cast<int64_t>(prompt) + ni;
+    int64_t anchor = ttft_deadline;
+    const int64_t f = P.first[g];
+    if (f >= 0 && f < anchor) anchor = f;  // min(arrival+ttft, first emit)
+    v.slack = anchor + v.tpot * static_cast<int64_t>(ni) - now;
+  }
+  return v;
+}
+
+// Token emission (engine.cpp:211-232) + online RequestReport bookkeeping
+// (metrics.cpp:42-60, 196-214).  Returns true when the request finished.
+__device__ __forceinline__ bool emit_token(const EngineParams& P, int64_t g, int64_t row,
+                                           int64_t t) {
+  const int32_t idx = P.nidx[g];
+  const int64_t arr = P.arrival[row];
+  const int64_t ttft = P.ttft[row];
+  const int64_t tpot = P.tpot[row];
+  uint32_t fl = P.flags[g];
+  if (idx == 0) {
+    P.first[g] = t;
+    if (t - arr <= ttft) fl |= FB_REC_MET_TTFT;
+  } else {
+    const int64_t d = t - P.first[g];
+    if (d > tpot * static_cast<int64_t>(idx)) fl |= kTpotViolated;
+    double m = P.maxtp[g];
+    max_ratio(m, d, idx);  // std::max(best, x)
+    P.maxtp[g] = m;
+    if (idx >= 2) {
+      double ma = P.maxtp_alt[g];
+      max_ratio(ma, d, idx - 1);
+      P.maxtp_alt[g] = ma;
+    }
+    if (t - arr > ttft + tpot * static_cast<int64_t>(idx)) fl |= FB_REC_ENV_MISS;
+  }
+  const int32_t ni = idx + 1;
+  P.nidx[g] = ni;
+  const bool fin = ni >= P.output[row];
+  if (fin) {
+    fl |= FB_REC_FINISHED;
+    if (!(fl & kTpotViolated)) fl |= FB_REC_MET_TPOT;
+  }
+  P.flags[g] = fl;
+  return fin;
+}
+
+// Order-preserving removal of finished entries (row < 0) from vlist[0, n_live)
+// (active_.erase, engine.cpp:228-229), clearing the in-flight takes.
+__device__ __forceinline__ void compact_vlist(Inst& w) {
+  const int64_t n = w.S.n_live;
+  int64_t out = 0;
+  int64_t removed_active = 0;
+  for (int64_t b = 0; b < n; b += kTile) {
+    const int64_t p = b + tile_lane();
+    int2 v = make_int2(-1, 0);
+    if (p < n) v = w.vl[p];
+    const bool keep = p < n && v.x >= 0;
+    const unsigned m = tile_ballot(keep);
+    const unsigned rm = tile_ballot(p < n && !keep && p < w.S.n_active);
+    tile_sync();
+    if (keep) w.vl[out + __popc(m & tile_lanemask_lt())] = make_int2(v.x, 0);
+    out += __popc(m);
+    removed_active += __popc(rm);
+    tile_sync();
+  }
+  w.S.n_live = out;
+  w.S.n_active -= removed_active;
+}
+
+// Node::complete_step, engine.cpp:204-254.  In-flight plan entries are the
+// active tasks with a nonzero take (plan order only affects the event log).
+static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w) {
+  const int64_t t = w.S.step_end;
+  bool any_fin = false;
+  for (int64_t b = 0; b < w.S.n_active; b += kTile) {
+    const int64_t p = b + tile_lane();
+    bool fin = false;
+    if (p < w.S.n_active) {
+      const int2 v = w.vl[p];
+      if (v.y > 0) {
+        const int64_t g = w.roff + v.x;
+        const int64_t row = w.toff + v.x;
+        const int32_t prompt = P.prompt[row];
+        int32_t pf = P.prefilled[g];
+        bool emit = true;
+        if (pf < prompt) {
+          pf += v.y;
+          P.prefilled[g] = pf;
+          emit = pf >= prompt;  // the completing chunk yields token 0
+        }
+        if (emit) fin = emit_token(P, g, row, t);
+        if (fin) w.vl[p].x = -1;
+      }
+    }
+    any_fin |= tile_any(fin);
+  }
+  tile_sync();
+  if (any_fin) compact_vlist(w);
+  w.S.busy = 0;
+}
+
+// Node::pull_arrivals without admission control (engine.cpp:127-151).
+__device__ __forceinline__ void pull_plain(const EngineParams& P, Inst& w) {
+  const int64_t k = w.S.arr - w.S.pulled;
+  for (int64_t j = tile_lane(); j < k; j += kTile) {
+    const int64_t r = arrival_row(w, w.S.pulled + j);
+    P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter + j);
+    w.vl[w.S.n_live + j] = make_int2(static_cast<int>(r), 0);
+  }
+  tile_sync();
+  w.S.seq_counter += k;
+  w.S.n_live += k;
+  w.S.pulled = w.S.arr;
+}
+
+// K5: Node::pull_arrivals with PAB admission (engine.cpp:127-151, pab
+// sched.cpp:248-278).  The view fold is computed once in view order; every
+// admitted, visible arrival then appends exactly one term, which is the same
+// left-to-right fold the reference recomputes per arrival.
+static __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
+  const DevInst* I = w.I;
+  const double Wm = us_to_ms(I->g_ttft), Tm = us_to_ms(I->g_tpot);
+  const double a = I->sa, b = I->sb, c = I->sc;
+  int64_t A = visible_count(w);
+  const Scratch s = scratch_for(P, w, A);
+  int64_t lmin = kInf, lpf = 0;
+  for (int64_t p = tile_lane(); p < A; p += kTile) {
+    const View v = load_view(P, w, p, now);
+    s.tcost[p] = pab_term(Wm, Tm, b, c, v.slack, v.ctx);
+    lmin = v.slack < lmin ? v.slack : lmin;
+    if (!v.decode) lpf += v.nw;
+  }
+  tile_sync();
+  int64_t min_slack = tile_min_i64(lmin);
+  int64_t pf_tok = tile_sum_small(lpf);
+  double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
+  for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
+    const int64_t r = arrival_row(w, q);
+    const int64_t row = w.toff + r;
+    const int64_t prompt = P.prompt[row];
+    const int64_t budget = pab_close(Wm, Tm, a, b, c, A > 0, min_slack, r_tasks, pf_tok);
+    if (prompt <= budget) {  // admit, sched.h:113-115
+      bool vis = true;
+      if (w.max_active > 0) {
+        int64_t slots = static_cast<int64_t>(w.max_active) - w.S.n_active;
+        if (slots < 0) slots = 0;
+        vis = (w.S.n_live - w.S.n_active) < slots;
+      }
+      if (tile_lane() == 0) {
+        P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter);
+        w.vl[w.S.n_live] = make_int2(static_cast<int>(r), 0);
+      }
+      w.S.seq_counter++;
+      w.S.n_live++;
+      if (vis) {
+        const int64_t slack = P.arrival[row] + P.ttft[row] - now;  // fresh prefill
+        r_tasks = dadd(r_tasks, pab_term(Wm, Tm, b, c, slack, 0));
+        min_slack = slack < min_slack ? slack : min_slack;
+        pf_tok += prompt;
+        A++;
+      }
+    } else {
+      if (tile_lane() == 0) {
+        P.flags[w.roff + r] |= FB_REC_REJECTED;
+        if (P.log_on) {
+          if (w.S.log_rejects < P.log_reject_cap) {
+            fb_reject_log& rl = P.log_rejects[I->log_reject_off + w.S.log_rejects];
+            rl.t_us = now;
+            rl.pab_tokens = budget;
+            rl.req = static_cast<int32_t>(r);
+            rl.reserved = 0;
+          }
+        }
+      }
+      if (P.log_on) {
+        if (w.S.log_rejects < P.log_reject_cap) {
+          w.S.log_rejects++;
+        } else {
+          w.S.log_trunc = 1;
+        }
+      }
+      w.S.digest = fb_digest_reject(w.S.digest, now, static_cast<uint32_t>(r), budget);
+      w.S.n_rejected++;
+    }
+  }
+  tile_sync();
+  w.S.pulled = w.S.arr;
+}
+
+// Node::begin_step, engine.cpp:153-202.  Returns false when there is nothing
+// to schedule (no step launched, no step ordinal consumed).
+static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
+  const DevInst* I = w.I;
+  if (w.S.pulled < w.S.arr) {
+    if (w.policy == FB_POLICY_FAIRBATCH_PAB) {
+      pull_pab(P, w, now);
+    } else {
+      pull_plain(P, w);
+    }
+  }
+  const int64_t A = visible_count(w);
+  if (A == 0) return false;
+  const Scratch s = scratch_for(P, w, A);
+
+  // K1: views, envelope slack and the init_time_budget reductions.
+  ViewAcc acc;
+  for (int64_t p = tile_lane(); p < A; p += kTile) {
+    const View v = load_view(P, w, p, now);
+    s.slack[p] = v.slack;
+    s.seq[p] = v.seq;
+    s.ctx[p] = v.ctx;
+    s.nw[p] = v.nw;
+    s.req[p] = v.r;
+    acc.add(v.decode, v.slack, v.tpot);
+  }
+  tile_sync();
+  acc.reduce();
+
+  // K2 + K3
+  FormCfg f;
+  f.policy = w.policy;
+  f.max_chunk = I->max_chunk;
+  f.token_budget = I->token_budget;
+  f.a = I->sa;
+  f.b = I->sb;
+  f.c = I->sc;
+  const int Ai = static_cast<int>(A);
+  const FormOut o = form_batch_warp(s, Ai, acc, f, /*seq_unique=*/true);
+
+  // ground_truth_step_time_ms, costmodel.cpp:138-146
+  double actual = predict_ms(I->ta, I->tb, I->tc, o.total_new, o.total_ctx);
+  const double amp = I->noise_amp;
+  if (amp != 0.0) {
+    actual = apply_noise(actual, amp, I->noise_seed, w.S.step_counter);
+  }
+  int64_t dur = ms_to_us(actual);
+  if (dur < 1) dur = 1;  // engine.cpp:196-198
+
+  // Bookkeeping over the plan in admission order: digest, log, and the
+  // waiting -> active move (engine.cpp:176-182) as new vlist positions.
+  const int64_t n_act = w.S.n_active;
+  const bool log_ok = P.log_on && w.S.log_steps < P.log_step_cap &&
+                      w.S.log_entries + o.n_entries <= P.log_entry_cap;
+  const int64_t entry_base = I->log_entry_off + w.S.log_entries;
+  int run_all = 0, run_w = 0;
+  uint64_t esum = 0;
+  for (int k0 = 0; k0 < Ai; k0 += kTile) {
+    const int k = k0 + tile_lane();
+    int tk = 0, p = 0;
+    if (k < Ai) {
+      p = s.order[k];
+      tk = s.take[k];
+    }
+    const bool adm = tk > 0;
+    const unsigned m = tile_ballot(adm);
+    const bool wadm = adm && p >= n_act;
+    const unsigned mw = tile_ballot(wadm);
+    if (adm) {
+      const int idx = run_all + __popc(m & tile_lanemask_lt());
+      const int r = s.req[p];
+      esum ^= fb_digest_entry(static_cast<uint32_t>(idx), static_cast<uint32_t>(r),
+                              static_cast<uint32_t>(tk));
+      if (log_ok) P.log_entries[entry_base + idx] = fb_plan_entry{r, tk};
+    }
+    if (k < Ai) {
+      const int64_t np = p < n_act ? p : (wadm ? n_act + run_w + __popc(mw & tile_lanemask_lt()) : -1);
+      s.slack[p] = (np << 32) | static_cast<uint32_t>(tk);
+    }
+    run_all += __popc(m);
+    run_w += __popc(mw);
+  }
+  tile_sync();
+  esum = tile_xor_u64(esum);
+  // unadmitted visible waiting keep their relative order after the movers
+  int run_u = 0;
+  const int64_t base_u = n_act + run_w;
+  for (int64_t p0 = n_act; p0 < A; p0 += kTile) {
+    const int64_t p = p0 + tile_lane();
+    bool un = false;
+    if (p < A) un = (s.slack[p] >> 32) < 0;
+    const unsigned mu = tile_ballot(un);
+    if (un) s.slack[p] = (static_cast<int64_t>(base_u + run_u + __popc(mu & tile_lanemask_lt())) << 32);
+    run_u += __popc(mu);
+  }
+  tile_sync();
+  for (int64_t p = tile_lane(); p < A; p += kTile) {
+    const int64_t pk = s.slack[p];
+    w.vl[pk >> 32] = make_int2(s.req[p], static_cast<int32_t>(pk & 0xffffffff));
+  }
+  tile_sync();
+
+  if (P.log_on) {
+    if (log_ok) {
+      if (tile_lane() == 0) {
+        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
+        sl.t_us = now;
+        sl.duration_us = dur;
+        sl.predicted_ms = o.predicted_ms;
+        sl.actual_ms = actual;
+        sl.total_new = o.total_new;
+        sl.total_ctx = o.total_ctx;
+        sl.init_budget_ms = o.init_ms;
+        sl.entry_off = w.S.log_entries;
+        sl.n_entries = o.n_entries;
+      }
+      w.S.log_steps++;
+      w.S.log_entries += o.n_entries;
+    } else {
+      w.S.log_trunc = 1;
+    }
+  }
+  w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(o.n_entries), esum,
+                              o.predicted_ms, actual);
+  w.S.sum_visible += A;
+  w.S.sum_entries += o.n_entries;
+  w.S.sum_new += o.total_new;
+  w.S.n_active = n_act + run_w;
+  w.S.busy = 1;
+  w.S.step_end = now + dur;
+  w.S.step_counter++;
+  return true;
+}
+
+}  // namespace fbgpu
+
+#include "fb_engine_rr.cuh"
+
+namespace fbgpu {
+
+// run_node's event loop (engine.cpp:266-288) for up to max_events times t.
+// Steps run on the register-resident path while at most 32 requests are live
+// and on the memory path otherwise; the switch happens at step boundaries.
+// Per-instance loop state of run_node's event loop.
+struct RunCtx {
+  TaskReg tk;
+  bool rr;           // live requests held in registers (fb_engine_rr.cuh)
+  int64_t next_arr;  // arrival time of the next trace row
+  int64_t ev;        // events processed in this launch
+};
+
+__device__ __forceinline__ void run_begin(const EngineParams& P, const Inst& w, RunCtx& c) {
+  c.tk = TaskReg{};
+  c.rr = false;
+  c.next_arr = w.S.arr < w.nreq ? P.arrival[w.toff + w.S.arr] : kInf;
+  c.ev = 0;
+}
+
+// One iteration of run_node's event loop (engine.cpp:266-288).  Returns true
+// when the node stops for this launch: quiescent (done), handed to the wide
+// engine, or out of its event budget -- its registers are spilled then.
+// Steps run on the register-resident path while at most kTile requests are
+// live and on the memory path otherwise; the switch happens at step
+// boundaries.
+__device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx& c,
+                                          const Scratch& s) {
+  const int64_t* arrival = P.arrival + w.toff;
+  if (c.ev >= P.max_events) {
+    if (c.rr) rr_spill(P, w, c.tk);
+    return true;
+  }
+  c.ev++;
+  if (w.S.busy && c.next_arr < w.S.step_end) {
+    // Arrivals strictly before the in-flight step's end only enqueue
+    // (run_node's loop neither completes nor begins a step at those times):
+    // consume them a tile at a time.
+    for (;;) {
+      const int64_t q = w.S.arr + tile_lane();
+      const bool early = q < w.nreq && arrival[q] < w.S.step_end;
+      const int n = __popc(tile_ballot(early));
+      w.S.arr += n;
+      if (n < kTile) break;
+    }
+    c.next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
+  }
+  const int64_t t_step = w.S.busy ? w.S.step_end : kInf;
+  const int64_t t = t_step < c.next_arr ? t_step : c.next_arr;
+  if (t == kInf || (!w.S.busy && t >= w.horizon)) {
+    if (c.rr) rr_spill(P, w, c.tk);
+    w.S.done = 1;
+    w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0 ||
+                      w.S.arr < w.nreq) ? 1 : 0;
+    return true;
+  }
+  w.S.t_last = t;
+  if (w.S.busy && t_step == t) {
+    if (c.rr) {
+      complete_rr(P, w, c.tk);
+    } else {
+      complete_step(P, w);
+    }
+  }
+  while (c.next_arr == t) {  // Node::enqueue (visible at its arrival time)
+    w.S.arr++;
+    c.next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
+  }
+  if (!w.S.busy && t < w.horizon) {
+    const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
+    if (upcoming > kEscalateLive) {  // hand over to the wide engine
+      if (c.rr) rr_spill(P, w, c.tk);
+      w.S.pending_begin = 1;
+      w.S.escalated = 1;
+      if (tile_lane() == 0) {
+        const unsigned long long slot = atomicAdd(&P.work[3], 1ull);
+        P.wide_list[slot] = w.id;
+      }
+      return true;
+    }
+    if (c.rr && upcoming > kTile) {
+      rr_spill(P, w, c.tk);
+      c.rr = false;
+    } else if (!c.rr && upcoming <= kTile) {
+      rr_load(P, w, c.tk);
+      c.rr = true;
+      w.S.paths |= kPathRegister;
+    }
+    if (c.rr) {
+      if (begin_rr(P, w, c.tk, t, s) < 0) {  // keys outside the packed range
+        rr_spill(P, w, c.tk);
+        c.rr = false;
+        begin_step(P, w, t);
+        w.S.paths |= kPathMemory;
+      }
+    } else {
+      begin_step(P, w, t);
+      w.S.paths |= kPathMemory;
+    }
+  }
+  return false;
+}
+
+// run_node's event loop for up to max_events events (one node per tile).
+static __device__ void run_instance(const EngineParams& P, Inst& w) {
+  RunCtx c;
+  run_begin(P, w, c);
+  const Scratch s = carve_scratch(w.smem, kSmemSlots);
+  while (!run_event(P, w, c, s)) {
+  }
+}
+
+}  // namespace fbgpu

@@ -25,19 +25,19 @@ struct TaskReg {
 };
 
 __device__ __forceinline__ void permute_task(TaskReg& t, int src) {
-  t.r = __shfl_sync(kFull, t.r, src);
-  t.seq = __shfl_sync(kFull, t.seq, src);
-  t.prompt = __shfl_sync(kFull, t.prompt, src);
-  t.output = __shfl_sync(kFull, t.output, src);
-  t.prefilled = __shfl_sync(kFull, t.prefilled, src);
-  t.nidx = __shfl_sync(kFull, t.nidx, src);
-  t.take = __shfl_sync(kFull, t.take, src);
-  t.flags = __shfl_sync(kFull, t.flags, src);
-  t.dl0 = __shfl_sync(kFull, t.dl0, src);
-  t.tpot = __shfl_sync(kFull, t.tpot, src);
-  t.first = __shfl_sync(kFull, t.first, src);
-  t.maxtp = __shfl_sync(kFull, t.maxtp, src);
-  t.maxtp_alt = __shfl_sync(kFull, t.maxtp_alt, src);
+  t.r = tile_shfl(t.r, src);
+  t.seq = tile_shfl(t.seq, src);
+  t.prompt = tile_shfl(t.prompt, src);
+  t.output = tile_shfl(t.output, src);
+  t.prefilled = tile_shfl(t.prefilled, src);
+  t.nidx = tile_shfl(t.nidx, src);
+  t.take = tile_shfl(t.take, src);
+  t.flags = tile_shfl(t.flags, src);
+  t.dl0 = tile_shfl(t.dl0, src);
+  t.tpot = tile_shfl(t.tpot, src);
+  t.first = tile_shfl(t.first, src);
+  t.maxtp = tile_shfl(t.maxtp, src);
+  t.maxtp_alt = tile_shfl(t.maxtp_alt, src);
 }
 
 // A request entering the node (Node::pull_arrivals, engine.cpp:146-149).
@@ -94,17 +94,17 @@ __device__ __forceinline__ void load_task(const EngineParams& P, const Inst& w, 
 
 // Memory path -> registers (at a step boundary).
 __device__ __forceinline__ void rr_load(const EngineParams& P, const Inst& w, TaskReg& t) {
-  if (lane_id() < w.S.n_live) load_task(P, w, lane_id(), t);
+  if (tile_lane() < w.S.n_live) load_task(P, w, tile_lane(), t);
 }
 
 // Registers -> memory path / end of launch.
 __device__ __forceinline__ void rr_spill(const EngineParams& P, const Inst& w,
                                          const TaskReg& t) {
-  if (lane_id() < w.S.n_live) {
+  if (tile_lane() < w.S.n_live) {
     flush_task(P, w, t);
-    w.vl[lane_id()] = make_int2(t.r, t.take);
+    w.vl[tile_lane()] = make_int2(t.r, t.take);
   }
-  __syncwarp();
+  tile_sync();
 }
 
 // Token emission on registers (engine.cpp:211-232, metrics.cpp:42-60,196-214).
@@ -132,7 +132,7 @@ __device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
 // Node::complete_step (engine.cpp:204-254) on registers.
 __device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, TaskReg& t) {
   const int64_t now = w.S.step_end;
-  const int lane = lane_id();
+  const int lane = tile_lane();
   const bool live = lane < w.S.n_live;
   bool fin = false;
   if (live && t.take > 0) {
@@ -145,9 +145,9 @@ __device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, Task
     if (fin) flush_task(P, w, t);
   }
   t.take = 0;
-  const unsigned finm = __ballot_sync(kFull, fin);
+  const unsigned finm = tile_ballot(fin);
   if (finm) {  // order-preserving removal from active_ (engine.cpp:228-229)
-    const unsigned keep = __ballot_sync(kFull, live && !fin);
+    const unsigned keep = tile_ballot(live && !fin);
     const int nk = __popc(keep);
     const int src = lane < nk ? static_cast<int>(__fns(keep, 0, lane + 1)) : lane;
     permute_task(t, src);
@@ -185,7 +185,7 @@ __device__ __forceinline__ RView view_reg(const TaskReg& t, int64_t now) {
 // guarantees n_live + pending <= 32.
 __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg& t,
                                         int64_t now, const Scratch& s) {
-  const int lane = lane_id();
+  const int lane = tile_lane();
   if (w.policy != FB_POLICY_FAIRBATCH_PAB) {
     const int64_t k = w.S.arr - w.S.pulled;
     const int j = lane - static_cast<int>(w.S.n_live);
@@ -207,9 +207,9 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
     lmin = v.slack;
     if (!v.decode) lpf = v.nw;
   }
-  __syncwarp();
-  int64_t min_slack = warp_min_i64(lmin);
-  int64_t pf_tok = warp_sum_small(lpf);
+  tile_sync();
+  int64_t min_slack = tile_min_i64(lmin);
+  int64_t pf_tok = tile_sum_small(lpf);
   double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
   for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
     const int64_t r = arrival_row(w, q);
@@ -255,7 +255,7 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
       w.S.n_rejected++;
     }
   }
-  __syncwarp();
+  tile_sync();
   w.S.pulled = w.S.arr;
 }
 
@@ -266,7 +266,7 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
 __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg& t,
                                         int64_t now, const Scratch& s) {
   const DevInst* I = w.I;
-  const int lane = lane_id();
+  const int lane = tile_lane();
   if (w.S.pulled < w.S.arr) pull_rr(P, w, t, now, s);
   const int A = static_cast<int>(visible_count(w));
   if (A == 0) return 0;
@@ -277,9 +277,9 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   // K1: views + init_time_budget reductions (sched.cpp:90-106)
   const RView v = view_reg(t, now);
   const int64_t tpot_u = I->tpot_uniform;
-  const int64_t min_tpot = tpot_u >= 0 ? tpot_u : warp_min_i64(vis ? t.tpot : kInf);
-  const int64_t min_dec = warp_min_i64(vis && v.decode ? v.slack : kInf);
-  const int n_dec = __popc(__ballot_sync(kFull, vis && v.decode));
+  const int64_t min_tpot = tpot_u >= 0 ? tpot_u : tile_min_i64(vis ? t.tpot : kInf);
+  const int64_t min_dec = tile_min_i64(vis && v.decode ? v.slack : kInf);
+  const int n_dec = __popc(tile_ballot(vis && v.decode));
   double init_ms = 0.0;
   int64_t urgency = 0;
   if (fair) {
@@ -291,7 +291,7 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   // K2: packed key (group, slack, seq) and rank by counting
   const bool fits = !vis || (t.seq >= 0 && t.seq < kPackSeq &&
                              (!fair || (v.slack >= -kPackSlack && v.slack < kPackSlack)));
-  if (!__all_sync(kFull, fits)) return -1;
+  if (!tile_all(fits)) return -1;
   // Ranks are counted on 32-bit keys whenever that is exact: sarathi /
   // prefill-first keys (group, seq) fit in 32 bits; fair-batching keys use
   // their high half when it is distinct across the visible tasks (the order of
@@ -304,8 +304,8 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
     key = (g << 62) | (static_cast<uint64_t>(v.slack + kPackSlack) << 22) |
           static_cast<uint64_t>(t.seq);
     k32 = vis ? static_cast<uint32_t>(key >> 32) : 0xffffffffu;  // visible hi <= 0xbfffffff
-    const unsigned same = __match_any_sync(kFull, k32);
-    use32 = __all_sync(kFull, !vis || same == (1u << lane));
+    const unsigned same = tile_match_any(k32);
+    use32 = tile_all(!vis || same == (1u << lane));
   } else {
     const uint32_t g = policy == FB_POLICY_SARATHI ? (v.decode ? 0u : 1u) : 0u;
     key = (static_cast<uint64_t>(g) << 62) | static_cast<uint64_t>(t.seq);
@@ -316,14 +316,14 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   int rank = 0;
   if (use32) {
 #pragma unroll 8
-    for (int q = 0; q < A; ++q) rank += __shfl_sync(kFull, k32, q) < k32;
+    for (int q = 0; q < A; ++q) rank += tile_shfl(k32, q) < k32;
   } else {
 #pragma unroll 8
-    for (int q = 0; q < A; ++q) rank += __shfl_sync(kFull, key, q) < key;
+    for (int q = 0; q < A; ++q) rank += tile_shfl(key, q) < key;
   }
   if (!vis) rank = lane;
   s.order[rank] = lane;
-  __syncwarp();
+  tile_sync();
   const int pk = s.order[lane];  // view position at sorted rank `lane` (k < A)
 
   // K3: sorted costs (sched.cpp:142-144) -> shared scratch -> greedy scan
@@ -331,11 +331,11 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   const double cc = dmul(f.c, static_cast<double>(v.ctx));
   const double tc = dadd(dmul(f.b, static_cast<double>(v.nw)), cc);
   const uint32_t nwp = static_cast<uint32_t>(v.nw) | (v.decode ? kDecodeBit : 0u);
-  const double tc_s = __shfl_sync(kFull, tc, pk);
-  const double cc_s = __shfl_sync(kFull, cc, pk);
-  const uint32_t nw_s = __shfl_sync(kFull, nwp, pk);
-  const int64_t ctx_s = __shfl_sync(kFull, v.ctx, pk);
-  const int32_t r_s = __shfl_sync(kFull, t.r, pk);
+  const double tc_s = tile_shfl(tc, pk);
+  const double cc_s = tile_shfl(cc, pk);
+  const uint32_t nw_s = tile_shfl(nwp, pk);
+  const int64_t ctx_s = tile_shfl(v.ctx, pk);
+  const int32_t r_s = tile_shfl(t.r, pk);
   // Fair batching, everything fits: the greedy pass admits every task whole
   // iff each prefix fits.  Exact sufficient test without the serial pass:
   // with tb0 = init - a, S = sum of the (already rounded) task costs and
@@ -346,8 +346,8 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   bool all_fit = false;
   if (fair) {
     const double tb0 = dsub(init_ms, f.a);
-    const double s_up = warp_sum_ru(vis ? tc : 0.0);
-    const int64_t n_new = warp_sum_small(vis ? static_cast<int64_t>(v.nw) : 0);
+    const double s_up = tile_sum_ru(vis ? tc : 0.0);
+    const int64_t n_new = tile_sum_small(vis ? static_cast<int64_t>(v.nw) : 0);
     all_fit = tb0 >= 0.0 && n_new <= f.token_budget &&
               __dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0);
   }
@@ -361,7 +361,7 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
       s.khi[lane] = nw_s;
       s.take[lane] = 0;
     }
-    __syncwarp();
+    tile_sync();
     if (fair) {
       scan_fairbatch(s, A, init_ms, f);
     } else if (policy == FB_POLICY_SARATHI) {
@@ -373,17 +373,17 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   }
 
   // finalize_plan (sched.cpp:37-48) + digest + log, in admission order
-  const unsigned madm = __ballot_sync(kFull, take_s > 0);
+  const unsigned madm = tile_ballot(take_s > 0);
   const int E = __popc(madm);
-  const int64_t tn = warp_sum_small(take_s);
-  const int64_t tctx = warp_sum_small(take_s > 0 ? ctx_s : 0);
+  const int64_t tn = tile_sum_small(take_s);
+  const int64_t tctx = tile_sum_small(take_s > 0 ? ctx_s : 0);
   const double predicted = E == 0 ? 0.0 : predict_ms(f.a, f.b, f.c, tn, tctx);
-  const int idx = __popc(madm & lanemask_lt());
+  const int idx = __popc(madm & tile_lanemask_lt());
   const uint64_t eh = take_s > 0 ? fb_digest_entry(static_cast<uint32_t>(idx),
                                                    static_cast<uint32_t>(r_s),
                                                    static_cast<uint32_t>(take_s))
                                  : 0;
-  const uint64_t esum = warp_xor_u64(eh);
+  const uint64_t esum = tile_xor_u64(eh);
   const bool log_ok = P.log_on && w.S.log_steps < P.log_step_cap &&
                       w.S.log_entries + E <= P.log_entry_cap;
   if (log_ok && take_s > 0)
@@ -401,21 +401,21 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   // takes back to view positions; waiting -> active in plan order
   // (engine.cpp:176-182) as a shuffle permutation
   const int n_act = static_cast<int>(w.S.n_active);
-  const int32_t take_v = __shfl_sync(kFull, take_s, vis ? rank : lane);
+  const int32_t take_v = tile_shfl(take_s, vis ? rank : lane);
   t.take = vis ? take_v : 0;
-  const unsigned mw = __ballot_sync(kFull, take_s > 0 && pk >= n_act);
+  const unsigned mw = tile_ballot(take_s > 0 && pk >= n_act);
   const int n_w = __popc(mw);
   if (n_w > 0) {
-    const int widx = __popc(mw & lanemask_lt());
-    const int widx_v = __shfl_sync(kFull, widx, vis ? rank : lane);
+    const int widx = __popc(mw & tile_lanemask_lt());
+    const int widx_v = tile_shfl(widx, vis ? rank : lane);
     const bool un = vis && lane >= n_act && t.take == 0;
-    const unsigned mu = __ballot_sync(kFull, un);
+    const unsigned mu = tile_ballot(un);
     int dest = lane;
     if (vis && lane >= n_act)
-      dest = t.take > 0 ? n_act + widx_v : n_act + n_w + __popc(mu & lanemask_lt());
-    __syncwarp();
+      dest = t.take > 0 ? n_act + widx_v : n_act + n_w + __popc(mu & tile_lanemask_lt());
+    tile_sync();
     s.order[dest] = lane;
-    __syncwarp();
+    tile_sync();
     const int src = s.order[lane];
     permute_task(t, src);
   }

@@ -42,9 +42,9 @@ struct ViewAcc {
     }
   }
   __device__ __forceinline__ void reduce() {
-    min_tpot = warp_min_i64(min_tpot);
-    min_dec = warp_min_i64(min_dec);
-    n_dec = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(n_dec)));
+    min_tpot = tile_min_i64(min_tpot);
+    min_dec = tile_min_i64(min_dec);
+    n_dec = static_cast<int32_t>(__reduce_add_sync(tile_mask(), static_cast<uint32_t>(n_dec)));
   }
 };
 
@@ -65,7 +65,7 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
   const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
   bool ok = seq_unique;
   if (ok) {
-    for (int p = lane_id(); p < A; p += kWarp) {
+    for (int p = tile_lane(); p < A; p += kTile) {
       const int64_t sq = s.seq[p];
       bool f = sq >= 0 && sq < kPackSeq;
       if (fair) {
@@ -75,8 +75,8 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
       ok = ok && f;
     }
   }
-  const bool packed = __all_sync(kFull, ok);
-  for (int p = lane_id(); p < A; p += kWarp) {
+  const bool packed = tile_all(ok);
+  for (int p = tile_lane(); p < A; p += kTile) {
     const bool decode = (static_cast<uint32_t>(s.nw[p]) & kDecodeBit) != 0;
     uint64_t g, sl = 0;
     if (fair) {
@@ -92,7 +92,7 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
     }
     s.khi[p] = (g << 62) | sl;
   }
-  __syncwarp();
+  tile_sync();
   return packed;
 }
 
@@ -102,19 +102,19 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
 // position so the result is always a permutation.
 __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed) {
   if (packed) {
-    for (int p0 = 0; p0 < A; p0 += kWarp) {
-      const int p = p0 + lane_id();
+    for (int p0 = 0; p0 < A; p0 += kTile) {
+      const int p = p0 + tile_lane();
       const uint64_t kh = p < A ? s.khi[p] : 0;
       int rank = 0;
 #pragma unroll 4
       for (int q = 0; q < A; ++q) rank += s.khi[q] < kh;
       if (p < A) s.order[rank] = p;
     }
-    __syncwarp();
+    tile_sync();
     return;
   }
-  for (int p0 = 0; p0 < A; p0 += kWarp) {
-    const int p = p0 + lane_id();
+  for (int p0 = 0; p0 < A; p0 += kTile) {
+    const int p = p0 + tile_lane();
     uint64_t kh = 0;
     int64_t ks = 0;
     if (p < A) {
@@ -129,7 +129,7 @@ __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed)
     }
     if (p < A) s.order[rank] = p;
   }
-  __syncwarp();
+  tile_sync();
 }
 
 // K3a: per sorted position, the state-independent costs (sched.cpp:142-144)
@@ -137,7 +137,7 @@ __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed)
 __device__ __forceinline__ void gather_sorted(const Scratch& s, int A, double b,
                                               double c) {
   // khi / seq are free after rank_order (which ends in __syncwarp).
-  for (int k = lane_id(); k < A; k += kWarp) {
+  for (int k = tile_lane(); k < A; k += kTile) {
     {
       const int p = s.order[k];
       const int32_t nwv = s.nw[p];
@@ -151,7 +151,7 @@ __device__ __forceinline__ void gather_sorted(const Scratch& s, int A, double b,
       s.take[k] = 0;
     }
   }
-  __syncwarp();
+  tile_sync();
 }
 
 // K3b: the greedy `consider` pass of form_batch_fairbatching
@@ -161,7 +161,7 @@ __device__ __forceinline__ void gather_sorted(const Scratch& s, int A, double b,
 // b > 0 and c*ctx >= 0).
 __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
                                                double init_ms, const FormCfg& f) {
-  if (lane_id() == 0) {
+  if (tile_lane() == 0) {
     double tb = dsub(init_ms, f.a);
     int64_t tok = f.token_budget;
     for (int k = 0; k < A; ++k) {
@@ -186,14 +186,14 @@ __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
       }
     }
   }
-  __syncwarp();
+  tile_sync();
 }
 
 // K3b': form_batch_sarathi (sched.cpp:172-206); sorted decodes first.
 __device__ __forceinline__ void scan_sarathi(const Scratch& s, int A, int n_dec,
                                              const FormCfg& f) {
-  for (int k = lane_id(); k < n_dec; k += kWarp) s.take[k] = 1;
-  if (lane_id() == 0) {
+  for (int k = tile_lane(); k < n_dec; k += kTile) s.take[k] = 1;
+  if (tile_lane() == 0) {
     int64_t remaining = f.token_budget - n_dec;
     if (remaining < 0) remaining = 0;
     for (int k = n_dec; k < A; ++k) {
@@ -207,13 +207,13 @@ __device__ __forceinline__ void scan_sarathi(const Scratch& s, int A, int n_dec,
       remaining -= chunk;
     }
   }
-  __syncwarp();
+  tile_sync();
 }
 
 // K3b'': form_batch_prefill_first (sched.cpp:208-232); fifo order.
 __device__ __forceinline__ void scan_prefill_first(const Scratch& s, int A,
                                                    const FormCfg& f) {
-  if (lane_id() == 0) {
+  if (tile_lane() == 0) {
     int64_t budget = f.token_budget;
     for (int k = 0; k < A; ++k) {
       if (budget <= 0) break;
@@ -232,7 +232,7 @@ __device__ __forceinline__ void scan_prefill_first(const Scratch& s, int A,
       budget -= take;
     }
   }
-  __syncwarp();
+  tile_sync();
 }
 
 // Whole K2+K3 pipeline after K1 filled s.{slack,seq,ctx,nw} for [0, A) and
@@ -265,7 +265,7 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
   // finalize_plan, sched.cpp:37-48 (integer sums: any order is exact)
   int32_t e = 0;
   int64_t tn = 0, tc = 0;
-  for (int k = lane_id(); k < A; k += kWarp) {
+  for (int k = tile_lane(); k < A; k += kTile) {
     const int32_t tk = s.take[k];
     if (tk > 0) {
       e++;
@@ -273,9 +273,9 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
       tc += s.seq[k];
     }
   }
-  out.n_entries = static_cast<int32_t>(__reduce_add_sync(kFull, static_cast<uint32_t>(e)));
-  out.total_new = warp_sum_small(tn);
-  out.total_ctx = warp_sum_small(tc);
+  out.n_entries = static_cast<int32_t>(__reduce_add_sync(tile_mask(), static_cast<uint32_t>(e)));
+  out.total_new = tile_sum_small(tn);
+  out.total_ctx = tile_sum_small(tc);
   out.predicted_ms = out.n_entries == 0 ? 0.0 : predict_ms(f.a, f.b, f.c, out.total_new, out.total_ctx);
   return out;
 }
@@ -311,10 +311,10 @@ __device__ __forceinline__ int64_t pab_close(double W, double T, double a, doubl
 // order-dependent sum, SURVEY §7 hard part 3).  Result is warp-uniform.
 __device__ __forceinline__ double ordered_fold(const double* v, int A) {
   double r = 0.0;
-  if (lane_id() == 0) {
+  if (tile_lane() == 0) {
     for (int p = 0; p < A; ++p) r = dadd(r, v[p]);
   }
-  return __shfl_sync(kFull, r, 0);
+  return tile_shfl(r, 0);
 }
 
 }  // namespace fbgpu
