@@ -35,10 +35,12 @@ FB_HD uint64_t fb_mix64(uint64_t z) {
 
 FB_HD uint64_t fb_rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
 
-/* Hash of the k-th plan entry (k = admission position). */
+/* Hash of the k-th plan entry (k = admission position): a multiply on the
+ * (position, request) word -- a bijection -- plus the tokens, one xorshift. */
 FB_HD uint64_t fb_digest_entry(uint32_t k, uint32_t req, uint32_t new_tokens) {
-  return fb_mix64((((uint64_t)k << 32) | (uint64_t)req) ^
-                  ((uint64_t)new_tokens * 0x9e3779b97f4a7c15ULL));
+  uint64_t z = (((uint64_t)k << 32) | (uint64_t)req) * 0x9e3779b97f4a7c15ULL;
+  z ^= (uint64_t)new_tokens * 0xc2b2ae3d27d4eb4fULL;
+  return z ^ (z >> 29);
 }
 
 FB_HD uint64_t fb_digest_bits(double x) {
@@ -51,14 +53,16 @@ FB_HD uint64_t fb_digest_bits(double x) {
   return u;
 }
 
-/* entry_sum = XOR over k of fb_digest_entry(k, req_k, new_k). */
+/* entry_sum = XOR over k of fb_digest_entry(k, req_k, new_k).  One chained
+ * mix per step over the step's fields (time, entry sum, entry count,
+ * predicted and ground-truth step-time bit patterns). */
 FB_HD uint64_t fb_digest_step(uint64_t h, int64_t t_us, uint32_t n_entries,
                               uint64_t entry_sum, double predicted_ms,
                               double actual_ms) {
-  h = fb_mix64(h ^ (uint64_t)t_us);
-  h = fb_mix64(h ^ entry_sum ^ fb_rotl64((uint64_t)n_entries | 0x5354455000000000ULL, 19));
-  h = fb_mix64(h ^ fb_digest_bits(predicted_ms) ^ fb_rotl64(fb_digest_bits(actual_ms), 29));
-  return h;
+  uint64_t x = (uint64_t)t_us * 0x9e3779b97f4a7c15ULL;
+  x ^= entry_sum ^ fb_rotl64((uint64_t)n_entries | 0x5354455000000000ULL, 19);
+  x ^= fb_rotl64(fb_digest_bits(predicted_ms), 7) ^ fb_rotl64(fb_digest_bits(actual_ms), 37);
+  return fb_mix64(h ^ x);
 }
 
 FB_HD uint64_t fb_digest_reject(uint64_t h, int64_t t_us, uint32_t req,
