@@ -1632,9 +1632,10 @@ __device__ __forceinline__ void wg_window(const EngineParams& P, int t, int64_t 
 // sm.wpos.  The stems arrive in arbitrary order; their bins (nondecreasing
 // in key) give a counting sort with the node's histogram as bin offsets, and
 // each key's place inside its bin is its rank among the bin's keys (keys are
-// unique), counted by the key's thread.  A bin of more than kBinSortMax keys
-// (heavy slack ties) falls back to the bitonic sort.
-constexpr int kBinSortMax = 64;
+// unique), counted by the key's thread: sum over bins of count^2 compares.
+// When that exceeds kBinRankWork (heavy slack ties crowding a few bins) the
+// merge sort is cheaper.
+constexpr int64_t kBinRankWork = int64_t(1) << 20;
 __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int policy,
                             const WideStep& ss, WideSmem& sm) {
   const uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
@@ -1645,12 +1646,13 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
   constexpr int kPer = kSelBins / kWideThreads;
   const int c0 = threadIdx.x * kPer;
   uint32_t hv[kPer];
-  int loc = 0, mx = 0;
+  int loc = 0;
+  int64_t sq = 0;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     hv[k] = c0 + k <= bmax ? __ldcg(gh + c0 + k) : 0u;
     loc += static_cast<int>(hv[k]);
-    mx = static_cast<int>(hv[k]) > mx ? static_cast<int>(hv[k]) : mx;
+    sq += static_cast<int64_t>(hv[k]) * hv[k];
   }
   int tot;
   int run = block_excl_sum(loc, tot, sm);
@@ -1660,14 +1662,14 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
     cur[c0 + k] = static_cast<uint32_t>(run);
     run += static_cast<int>(hv[k]);
   }
-  const int64_t bigbin = -block_min(-static_cast<int64_t>(mx), sm);
-  WPROF_COUNT(16, bigbin > kBinSortMax ? 1 : 0)
-  WPROF_COUNT(17, bigbin)
+  const int64_t rank_work = block_sum(sq, sm);
+  WPROF_COUNT(16, rank_work > kBinRankWork ? 1 : 0)
+  WPROF_COUNT(17, rank_work)
   WPROF_COUNT(18, K)
   WPROF_COUNT(19, bmax)
   const uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
   const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
-  if (bigbin > kBinSortMax) {
+  if (rank_work > kBinRankWork) {
     for (int k = threadIdx.x; k < K; k += kWideThreads) {
       sm.wkey[k] = wide_key(__ldcg(ck + k), policy, ss.urgency);
       sm.wpos[k] = __ldcg(cp + k);
