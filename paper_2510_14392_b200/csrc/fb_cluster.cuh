@@ -37,7 +37,7 @@ constexpr int kClusterMaxWarps = 8;  // nodes (warps) per CTA
 constexpr int kXchgHeader = 256;     // [0] arrival counter (u64), padding
 
 // The per-epoch exchange record of one node (fb_node_report in fbgpu.h).
-struct NodeReport {
+struct __align__(16) NodeReport {
   int64_t t;    // emitted_at of the newest report delivered by t_a, -1 none
   int64_t pab;  // its prefill admission budget
   int32_t waiting, running;
@@ -109,11 +109,10 @@ __device__ bool cluster_barrier(const ClusterParams& C, RouterSmem& rs, int64_t 
   const bool sys = C.n_ranks > 1;
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (sys) {
-      __threadfence_system();
-    } else {
-      __threadfence();
-    }
+    // red.release orders this CTA's earlier stores (observed by this thread
+    // through the CTA barrier) before the arrival; peer-memory stores of a
+    // multi-rank run also get a system-scope fence
+    if (sys) __threadfence_system();
     for (int p = 0; p < C.n_ranks; ++p) red_release_add(xchg_counter(C.xbuf[p]), sys);
     const uint64_t target = static_cast<uint64_t>(e + 1) * static_cast<uint64_t>(C.total_ctas);
     const uint64_t* ctr = xchg_counter(C.xbuf[C.rank]);
@@ -309,14 +308,17 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
                               const NodeReport* all, int64_t e, int node_base) {
   const int n = C.n_nodes;
   for (int i = lane_id(); i < n; i += kWarp) {
-    if (__ldcg(&all[i].fresh)) {
-      const int64_t t = __ldcg(&all[i].t);
+    // the whole 32-byte report in two 16-byte loads (one round trip)
+    const int4* rp = reinterpret_cast<const int4*>(all + i);
+    const int4 a = __ldcg(rp), b = __ldcg(rp + 1);
+    if (b.z) {  // fresh
+      const int64_t t = (static_cast<int64_t>(a.y) << 32) | static_cast<uint32_t>(a.x);
       if (!(rs.v_has[i] && t < rs.v_t[i])) {
         rs.v_has[i] = 1;
         rs.v_t[i] = t;
-        rs.v_pab[i] = __ldcg(&all[i].pab);
-        rs.v_wait[i] = __ldcg(&all[i].waiting);
-        rs.v_run[i] = __ldcg(&all[i].running);
+        rs.v_pab[i] = (static_cast<int64_t>(a.w) << 32) | static_cast<uint32_t>(a.z);
+        rs.v_wait[i] = b.x;
+        rs.v_run[i] = b.y;
         rs.v_dec[i] = 0;
         rs.v_inc[i] = 0;
       }
