@@ -348,6 +348,15 @@ typedef struct fb_summary {
 } fb_summary;
 int fb_arena_fetch_summaries(fb_arena* arena, fb_summary* out);
 
+/* Envelope-lead series (envelope_lead_series, metrics.cpp:137-169) per
+ * instance.  fb_arena_set_lead enables the run-time accounting for the next
+ * load/reset (bucket_us > 0; at most cap series points per instance; 0
+ * disables).  fb_arena_fetch_lead fills out[instance * cap + k] = lead tokens
+ * at t = k * bucket_us and n_out[instance] = points (-1 when cap was too
+ * small).  Single nodes only (not cluster shards). */
+int fb_arena_set_lead(fb_arena* arena, int64_t bucket_us, int32_t cap);
+int fb_arena_fetch_lead(fb_arena* arena, int64_t* out, int32_t* n_out);
+
 /* Page-locked host buffers.  Trace rows, instances and record outputs that
  * live in memory from fb_host_alloc move by direct DMA; any other host
  * pointer is staged through the arena's own pinned chunks.  Not a reference

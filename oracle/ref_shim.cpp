@@ -453,6 +453,24 @@ int ref_event_log(const fb_trace* rows, const fb_instance* inst, const char* tmp
   }
 }
 
+// The reference's envelope-lead series (metrics.cpp:137-169) of one
+// instance: run_node, request_reports, envelope_lead_series(bucket).
+int ref_lead_series(const fb_trace* rows, const fb_instance* inst, int64_t bucket_us,
+                    int64_t* lead_out, int64_t cap, int64_t* n_out) {
+  try {
+    const Trace tr = instance_trace(rows, *inst);
+    const EventLog log = run_node(tr, to_engine(inst->cfg), inst->horizon_us);
+    const std::vector<EventLog> logs{log};
+    const auto series = envelope_lead_series(request_reports(logs), bucket_us);
+    *n_out = static_cast<int64_t>(series.size());
+    if (*n_out > cap) return fail(FB_ERR_CAPACITY, "buffer too small");
+    for (size_t k = 0; k < series.size(); ++k) lead_out[k] = series[k].lead_tokens;
+    return FB_OK;
+  } catch (const std::exception& e) {
+    return map_exception(e);
+  }
+}
+
 int ref_generate_bursty(const fb_burst_profile* p, int64_t horizon_us, int64_t cap,
                         int64_t* arrival_us, int32_t* prompt_len,
                         int32_t* output_len, int64_t* ttft_us, int64_t* tpot_us,

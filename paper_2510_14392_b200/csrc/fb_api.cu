@@ -128,6 +128,13 @@ struct fb_arena {
   DevBuf<int64_t> qinfo;  // [kQueues + 1] queue offsets
   DevBuf<fb_record> recbuf;  // device-packed records (AoS) for one D2H
   DevBuf<fb_summary> sumbuf;  // per-instance aggregates
+  // envelope-lead series (fb_arena_set_lead)
+  int64_t lead_bucket = 0;
+  int32_t lead_cap = 0;
+  DevBuf<unsigned long long> lead_hist;
+  DevBuf<long long> lead_tmax;
+  DevBuf<int32_t> lead_flags, lead_n;
+  DevBuf<int64_t> lead_out, lastem;
   DevBuf<uint64_t> sumvals;   // their value series (one u64 per request row)
   // grid-wide wide engine
   DevBuf<unsigned char> wg_slots;
@@ -248,6 +255,12 @@ struct fb_arena {
     P.order = order.p;
     P.qoff = qinfo.p;
     P.max_events = max_events <= 0 ? INT64_MAX : max_events;
+    P.lead_bucket = lead_bucket;
+    P.lead_cap = lead_cap;
+    P.lead_hist = lead_hist.p;
+    P.lead_tmax = lead_tmax.p;
+    P.lead_flags = lead_flags.p;
+    P.lastem = lastem.p;
     P.wg.slots = wg_slots.p;
     P.wg.partial = wg_partial.p;
     P.wg.hist = wg_hist.p;
@@ -268,6 +281,8 @@ struct fb_arena {
     qinfo.release();
     recbuf.release();
     sumbuf.release();
+    lead_hist.release(); lead_tmax.release(); lead_flags.release(); lead_n.release();
+    lead_out.release(); lastem.release();
     sumvals.release();
     wg_slots.release(); wg_partial.release(); wg_hist.release(); wg_ckey.release();
     wg_cpos.release(); wg_bar.release();
@@ -423,6 +438,12 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   ENSURE(a->log_steps, n_instances * static_cast<int64_t>(lo.step_cap));
   ENSURE(a->log_entries, n_instances * static_cast<int64_t>(lo.entry_cap));
   ENSURE(a->log_rejects, n_instances * static_cast<int64_t>(lo.reject_cap));
+  ENSURE(a->lastem, n_rec);
+  if (a->lead_bucket > 0) {
+    ENSURE(a->lead_hist, n_instances * 2 * static_cast<int64_t>(a->lead_cap));
+    ENSURE(a->lead_tmax, n_instances);
+    ENSURE(a->lead_flags, n_instances);
+  }
   {
     const fbgpu::WideGridSizes z = fbgpu::wide_grid_sizes(a->geo, n_rec);
     ENSURE(a->wg_slots, z.slot_bytes);
@@ -482,6 +503,12 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
 int fb_arena_reset(fb_arena* a) {
   if (!a || !a->loaded) return set_error(FB_ERR_USAGE, "fb_arena_reset: arena not loaded");
   FB_CUDA(cudaSetDevice(a->device));
+  if (a->lead_bucket > 0 && a->n_inst > 0) {
+    FB_CUDA(cudaMemsetAsync(a->lead_hist.p, 0,
+                            sizeof(unsigned long long) * a->n_inst * 2 * a->lead_cap, a->stream));
+    FB_CUDA(cudaMemsetAsync(a->lead_tmax.p, 0xff, sizeof(long long) * a->n_inst, a->stream));
+    FB_CUDA(cudaMemsetAsync(a->lead_flags.p, 0, sizeof(int32_t) * a->n_inst, a->stream));
+  }
   FB_CUDA(fbgpu::launch_reset(a->params(0), a->n_rec, a->stream));
   return FB_OK;
 }
@@ -570,6 +597,35 @@ int fb_arena_fetch_summaries(fb_arena* a, fb_summary* out) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc summaries");
   FB_CUDA(fbgpu::launch_summaries(a->params(0), a->sumbuf.p, a->sumvals.p, a->stream));
   FB_CUDA(a->d2h(out, a->sumbuf.p, sizeof(fb_summary) * static_cast<size_t>(a->n_inst)));
+  return FB_OK;
+}
+
+int fb_arena_set_lead(fb_arena* a, int64_t bucket_us, int32_t cap) {
+  if (!a) return set_error(FB_ERR_USAGE, "fb_arena_set_lead: null arena");
+  if (bucket_us < 0 || (bucket_us > 0 && cap < 1))
+    return set_error(FB_ERR_VALIDATION, "lead series bucket must be > 0 (0 disables), cap >= 1");
+  a->lead_bucket = bucket_us;
+  a->lead_cap = bucket_us > 0 ? cap : 0;
+  if (a->loaded && bucket_us > 0) {
+    cudaError_t e = a->lead_hist.ensure(static_cast<size_t>(a->n_inst) * 2 * cap);
+    if (e == cudaSuccess) e = a->lead_tmax.ensure(static_cast<size_t>(a->n_inst));
+    if (e == cudaSuccess) e = a->lead_flags.ensure(static_cast<size_t>(a->n_inst));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc lead");
+  }
+  return FB_OK;
+}
+
+int fb_arena_fetch_lead(fb_arena* a, int64_t* out, int32_t* n_out) {
+  if (!a || !a->loaded || !out || !n_out) return set_error(FB_ERR_USAGE, "fb_arena_fetch_lead");
+  if (a->lead_bucket <= 0) return set_error(FB_ERR_USAGE, "lead series not enabled (fb_arena_set_lead)");
+  FB_CUDA(cudaSetDevice(a->device));
+  const size_t cells = static_cast<size_t>(a->n_inst) * a->lead_cap;
+  cudaError_t e = a->lead_out.ensure(cells);
+  if (e == cudaSuccess) e = a->lead_n.ensure(static_cast<size_t>(a->n_inst));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc lead out");
+  FB_CUDA(fbgpu::launch_lead(a->params(0), a->lead_out.p, a->lead_n.p, a->stream));
+  FB_CUDA(a->d2h(n_out, a->lead_n.p, sizeof(int32_t) * static_cast<size_t>(a->n_inst)));
+  FB_CUDA(a->d2h(out, a->lead_out.p, sizeof(int64_t) * cells));
   return FB_OK;
 }
 

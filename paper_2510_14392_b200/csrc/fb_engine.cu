@@ -84,6 +84,7 @@ __global__ void reset_kernel(const __grid_constant__ EngineParams P, int64_t n_r
     P.first[i] = -1;
     P.maxtp[i] = 0.0;
     P.maxtp_alt[i] = 0.0;
+    P.lastem[i] = -1;
   }
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < P.n_inst;
        i += stride) {
@@ -145,6 +146,13 @@ cudaError_t launch_summaries(const EngineParams& p, fb_summary* out, uint64_t* v
   if (p.n_inst <= 0) return cudaSuccess;
   int64_t blocks = p.n_inst < 148 * 8 ? p.n_inst : 148 * 8;
   summarize_kernel<<<static_cast<int>(blocks), kSumThreads, 0, st>>>(p, out, vals);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lead(const EngineParams& p, int64_t* out, int32_t* n_out, cudaStream_t st) {
+  if (p.n_inst <= 0 || p.lead_bucket <= 0) return cudaSuccess;
+  int64_t blocks = p.n_inst < 148 * 8 ? p.n_inst : 148 * 8;
+  lead_kernel<<<static_cast<int>(blocks), kSumThreads, 0, st>>>(p, out, n_out);
   return cudaGetLastError();
 }
 

@@ -141,6 +141,32 @@ __device__ __forceinline__ bool emit_token(const EngineParams& P, int64_t g, int
   return fin;
 }
 
+// Envelope-lead bookkeeping (envelope_lead_series, metrics.cpp:137-169),
+// called by one lane per step that emitted: n_emit tokens at `now`, of which
+// finishing requests' output lengths sum to fin_tokens.
+__device__ __forceinline__ void lead_account(const EngineParams& P, int64_t inst, int64_t now,
+                                             uint32_t n_emit, int64_t fin_tokens) {
+  const int64_t k = (now + P.lead_bucket - 1) / P.lead_bucket;  // first grid point >= now
+  if (k >= P.lead_cap) {
+    atomicOr(&P.lead_flags[inst], 1);
+    return;
+  }
+  unsigned long long* row = P.lead_hist + inst * 2 * static_cast<int64_t>(P.lead_cap);
+  if (n_emit) atomicAdd(&row[k], static_cast<unsigned long long>(n_emit));
+  if (fin_tokens) atomicAdd(&row[P.lead_cap + k], static_cast<unsigned long long>(fin_tokens));
+  atomicMax(&P.lead_tmax[inst], static_cast<long long>(now));
+}
+
+// The tile's emissions of one step into the lead accounting (out of line:
+// off the hot loop when the series is disabled).
+static __device__ __noinline__ void lead_step(const EngineParams& P, const Inst& w, int64_t now,
+                                              bool emit, bool fin, int32_t r, int32_t output) {
+  if (fin) P.lastem[w.roff + r] = now;
+  const uint32_t ne = __popc(tile_ballot(emit));
+  const int64_t nf = tile_sum_small(fin ? output : 0);
+  if (tile_lane() == 0 && ne) lead_account(P, w.id, now, ne, nf);
+}
+
 // Order-preserving removal of finished entries (row < 0) from vlist[0, n_live)
 // (active_.erase, engine.cpp:228-229), clearing the in-flight takes.
 __device__ __forceinline__ void compact_vlist(Inst& w) {
@@ -169,6 +195,8 @@ __device__ __forceinline__ void compact_vlist(Inst& w) {
 static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w) {
   const int64_t t = w.S.step_end;
   bool any_fin = false;
+  uint32_t lemit = 0;
+  int64_t lfin = 0;
   for (int64_t b = 0; b < w.S.n_active; b += kTile) {
     const int64_t p = b + tile_lane();
     bool fin = false;
@@ -187,9 +215,19 @@ static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w
         }
         if (emit) fin = emit_token(P, g, row, t);
         if (fin) w.vl[p].x = -1;
+        if (P.lead_bucket > 0) {
+          if (fin) P.lastem[g] = t;
+          lemit += emit;
+          lfin += fin ? P.output[row] : 0;
+        }
       }
     }
     any_fin |= tile_any(fin);
+  }
+  if (P.lead_bucket > 0) {
+    const uint32_t ne = tile_add_u32(lemit);
+    const int64_t nf = tile_sum_small(lfin);
+    if (tile_lane() == 0 && (ne || nf)) lead_account(P, w.id, t, ne, nf);
   }
   tile_sync();
   if (any_fin) compact_vlist(w);

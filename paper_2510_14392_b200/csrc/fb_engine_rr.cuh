@@ -134,9 +134,9 @@ __device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, Task
   const int64_t now = w.S.step_end;
   const int lane = tile_lane();
   const bool live = lane < w.S.n_live;
-  bool fin = false;
+  bool fin = false, emit = false;
   if (live && t.take > 0) {
-    bool emit = true;
+    emit = true;
     if (t.prefilled < t.prompt) {
       t.prefilled += t.take;
       emit = t.prefilled >= t.prompt;  // the completing chunk yields token 0
@@ -145,6 +145,7 @@ __device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, Task
     if (fin) flush_task(P, w, t);
   }
   t.take = 0;
+  if (P.lead_bucket > 0) lead_step(P, w, now, emit, fin, t.r, t.output);
   const unsigned finm = tile_ballot(fin);
   if (finm) {  // order-preserving removal from active_ (engine.cpp:228-229)
     const unsigned keep = tile_ballot(live && !fin);

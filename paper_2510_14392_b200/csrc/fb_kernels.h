@@ -64,6 +64,15 @@ struct EngineParams {
   // order[qoff[q] .. qoff[q+1]) is queue q; work[4 + q] its next index.
   const int64_t* order;
   const int64_t* qoff;  // [kQueues + 1]
+  // envelope-lead accounting (lead_bucket > 0): per instance, emitted tokens
+  // [0, cap) and finished requests' output tokens [cap, 2 cap) per bucket
+  // index ceil(t / bucket); latest emission; overflow flag
+  int64_t lead_bucket;
+  int32_t lead_cap, pad_lead;
+  unsigned long long* lead_hist;  // [n_inst][2 cap]
+  long long* lead_tmax;           // [n_inst]
+  int32_t* lead_flags;            // [n_inst]
+  int64_t* lastem;                // [rec_off + row] last token of a finished request (lead on)
   int64_t max_events;  // per instance per launch
   WideGridBufs wg;
 };
@@ -104,6 +113,9 @@ cudaError_t launch_reset(const EngineParams& p, int64_t n_rec_rows, cudaStream_t
 // u64 per request row (value series of large instances).
 cudaError_t launch_summaries(const EngineParams& p, fb_summary* out, uint64_t* vals,
                              cudaStream_t st);
+// Envelope-lead series per instance (fb_summary.cuh) into out[inst][cap];
+// n_out[inst] = points, or -1 when the bucket capacity overflowed.
+cudaError_t launch_lead(const EngineParams& p, int64_t* out, int32_t* n_out, cudaStream_t st);
 // Records in fb_record layout, indexed by rec_off + row.
 cudaError_t launch_pack_records(const EngineParams& p, fb_record* out, cudaStream_t st);
 

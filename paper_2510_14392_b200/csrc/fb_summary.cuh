@@ -199,4 +199,63 @@ summarize_kernel(const __grid_constant__ EngineParams P, fb_summary* out, uint64
   }
 }
 
+// Envelope-lead series (envelope_lead_series, metrics.cpp:137-169) of every
+// instance at t_k = k * bucket, k = 0 .. floor(t_max / bucket):
+//   lead(t) = sum over requests in decode at t of (emitted by t - required by t)
+//           = C(t) - F(t) - R(t)
+// with C the emissions at or before t (run-time histogram), F the output
+// lengths of requests whose last token came at or before t (run-time
+// histogram), R the envelope's required tokens of the requests in decode at
+// t (first token <= t < last token of a finished request), accumulated here.
+__global__ void __launch_bounds__(kSumThreads)
+lead_kernel(const __grid_constant__ EngineParams P, int64_t* out, int32_t* n_out) {
+  const int64_t B = P.lead_bucket, cap = P.lead_cap;
+  for (int64_t i = blockIdx.x; i < P.n_inst; i += gridDim.x) {
+    const long long tmax = P.lead_tmax[i];
+    const int64_t K = tmax >= 0 ? tmax / B + 1 : 1;
+    int64_t* R = out + i * cap;
+    if (K > cap || P.lead_flags[i]) {
+      if (threadIdx.x == 0) n_out[i] = -1;
+      continue;
+    }
+    for (int64_t k = threadIdx.x; k < K; k += kSumThreads) R[k] = 0;
+    __syncthreads();
+    const DevInst* I = P.inst + i;
+    const int64_t b = I->rec_off, toff = I->trace_off, n = P.state[i].arr;
+    for (int64_t r = threadIdx.x; r < n; r += kSumThreads) {
+      const int64_t first = P.first[b + r];
+      if (first < 0) continue;
+      const int64_t row = toff + r;
+      const int64_t k0 = (first + B - 1) / B;
+      int64_t k1 = K;
+      if (P.flags[b + r] & FB_REC_FINISHED) {
+        const int64_t kl = (P.lastem[b + r] + B - 1) / B;  // in decode while t < last
+        k1 = kl < K ? kl : K;
+      }
+      const int64_t ddl = P.arrival[row] + P.ttft[row];
+      const int64_t tpot = P.tpot[row];
+      const int64_t outl = P.output[row];
+      for (int64_t k = k0; k < k1; ++k) {
+        const int64_t t = k * B;
+        if (t < ddl) continue;
+        int64_t req = (t - ddl) / tpot + 1;
+        if (req > outl) req = outl;
+        atomicAdd(reinterpret_cast<unsigned long long*>(R + k), static_cast<unsigned long long>(req));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long* h = P.lead_hist + i * 2 * cap;
+      int64_t c = 0, f = 0;
+      for (int64_t k = 0; k < K; ++k) {
+        c += static_cast<int64_t>(h[k]);
+        f += static_cast<int64_t>(h[cap + k]);
+        R[k] = c - f - R[k];
+      }
+      n_out[i] = static_cast<int32_t>(K);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace fbgpu

@@ -812,6 +812,7 @@ __device__ void wide_complete(const EngineParams& P, Inst& w, WideSmem& sm) {
   const int64_t t = w.S.step_end;
   const WideScratch ws = wide_scratch(P, w);
   int any = 0;
+  int64_t lemit = 0, lfin = 0;
   for (int64_t p = threadIdx.x; p < w.S.n_active; p += kWideThreads) {
     const int2 v = w.vl[p];
     if (v.y > 0) {
@@ -827,6 +828,11 @@ __device__ void wide_complete(const EngineParams& P, Inst& w, WideSmem& sm) {
       }
       bool fin = false;
       if (emit) fin = emit_token(P, g, row, t);
+      if (P.lead_bucket > 0) {
+        if (fin) P.lastem[g] = t;
+        lemit += emit;
+        lfin += fin ? P.output[row] : 0;
+      }
       WRec& rec = ws.rec[v.x];  // keep the view record in step
       rec.prefilled = pf;
       rec.nidx = P.nidx[g];
@@ -834,6 +840,11 @@ __device__ void wide_complete(const EngineParams& P, Inst& w, WideSmem& sm) {
       w.vl[p] = make_int2(fin ? -1 : v.x, 0);
       any |= fin;
     }
+  }
+  if (P.lead_bucket > 0) {
+    const int64_t ne = block_sum(lemit, sm);
+    const int64_t nf = block_sum(lfin, sm);
+    if (threadIdx.x == 0 && ne) lead_account(P, w.id, t, static_cast<uint32_t>(ne), nf);
   }
   if (__syncthreads_or(any)) {  // order-preserving removal (engine.cpp:228-229)
     const int64_t n = w.S.n_live;

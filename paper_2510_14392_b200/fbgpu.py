@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
         "fb_arena_fetch_results": (C.c_int, [vp, vp]),
         "fb_arena_fetch_records": (C.c_int, [vp, vp]),
         "fb_arena_fetch_summaries": (C.c_int, [vp, vp]),
+        "fb_arena_set_lead": (C.c_int, [vp, i64, i32]),
+        "fb_arena_fetch_lead": (C.c_int, [vp, vp, vp]),
         "fb_arena_record_rows": (i64, [vp]),
         "fb_arena_fetch_log_counts": (C.c_int, [vp, vp]),
         "fb_arena_fetch_log": (C.c_int, [vp, i64, vp, vp, vp]),
@@ -380,6 +382,21 @@ class Arena:
         _check(self._lib.fb_arena_fetch_summaries(self._h, _abi.vptr(out)),
                "fb_arena_fetch_summaries")
         return out[:self.n_instances]
+
+    def set_lead(self, bucket_us: int, cap: int) -> None:
+        """Enable envelope-lead accounting (applies from the next load/reset)."""
+        _check(self._lib.fb_arena_set_lead(self._h, int(bucket_us), int(cap)), "fb_arena_set_lead")
+        self._lead_cap = int(cap)
+
+    def lead(self) -> list:
+        """envelope_lead_series per instance (lead tokens at t = k * bucket);
+        None where the point capacity was too small."""
+        cap = self._lead_cap
+        out = np.zeros((max(1, self.n_instances), cap), np.int64)
+        n = np.zeros(max(1, self.n_instances), np.int32)
+        _check(self._lib.fb_arena_fetch_lead(self._h, _abi.vptr(out), _abi.vptr(n)),
+               "fb_arena_fetch_lead")
+        return [None if n[i] < 0 else out[i, :n[i]].copy() for i in range(self.n_instances)]
 
     def record_rows(self) -> int:
         return int(self._lib.fb_arena_record_rows(self._h))

@@ -348,6 +348,25 @@ class RefLib(_CpuLib):
                 raise RuntimeError(f"ref_event_log status {st}")
             return buf.raw[: n.value].decode()
 
+    def lead_series(self, batch: Batch, i: int, bucket_us: int) -> np.ndarray:
+        """The reference's envelope_lead_series (metrics.cpp:137-169) of instance i."""
+        fn = self.lib.ref_lead_series
+        fn.restype = C.c_int
+        tr = batch.rows.to_c()
+        inst = batch.instance(i)
+        n = C.c_int64(0)
+        cap = 4096
+        while True:
+            out = np.zeros(cap, np.int64)
+            st = fn(C.byref(tr), C.byref(inst), C.c_int64(bucket_us), _abi.vptr(out),
+                    C.c_int64(cap), C.byref(n))
+            if st == _abi.FB_ERR_CAPACITY:
+                cap = n.value
+                continue
+            if st:
+                raise RuntimeError(f"ref_lead_series status {st}")
+            return out[: n.value]
+
     def run_node_batch(self, batch: Batch, nthreads: int = 1, records: bool = True) -> RunOutput:
         n = batch.n_instances
         tr = batch.rows.to_c()

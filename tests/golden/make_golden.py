@@ -27,6 +27,7 @@ from backends import RefLib, cluster_summary  # noqa: E402
 from catalog import (SCENARIOS, TRACE_PROFILES, cluster_cases, rows_digest,  # noqa: E402
                      summarize)
 from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views  # noqa: E402
+from tests_golden_cases import LEAD_CASES  # noqa: E402
 from paper_2510_14392_b200.batch import ms_to_us  # noqa: E402
 
 
@@ -70,6 +71,12 @@ def main() -> None:
         batch = SCENARIOS[name](ref.generate_bursty)
         gold["event_logs"][name] = [
             hashlib.sha256(ref.event_log(batch, i, "/tmp/_golden_ev.jsonl").encode()).hexdigest()
+            for i in range(batch.n_instances)]
+    gold["lead"] = {}
+    for name, bucket_ms in LEAD_CASES.items():
+        batch = SCENARIOS[name](ref.generate_bursty)
+        gold["lead"][name] = [
+            hashlib.sha256(ref.lead_series(batch, i, ms_to_us(bucket_ms)).tobytes()).hexdigest()
             for i in range(batch.n_instances)]
     import acceptance_cases as ac
 

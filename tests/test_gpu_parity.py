@@ -479,3 +479,34 @@ def test_run_batch_cached_arena_resizes(fb, gpu):
         res, rec, _ = fb.run_batch(b)
         out = gpu.run(b)
         assert res.tobytes() == out.results.tobytes() and rec.tobytes() == out.records.tobytes()
+
+
+@pytest.mark.parametrize("name", ["c1", "pab_overload", "wide", "c2_subset"])
+def test_lead_series_matches_reference(fb, gpu, golden, name):
+    """Envelope-lead series on the device (run-time emission histograms +
+    post-run envelope sums) equals the reference's envelope_lead_series
+    (metrics.cpp:137-169) point for point, for every instance; the engine's
+    decisions are unaffected by the accounting."""
+    import hashlib
+    from tests_golden_cases import LEAD_CASES
+    batch = SCENARIOS[name](gpu.generate_bursty)
+    a = fb.Arena(0)
+    a.set_lead(ms_to_us(LEAD_CASES[name]), 1 << 14)
+    a.load(batch)
+    a.run()
+    series = a.lead()
+    res = a.results()
+    a.close()
+    assert [hashlib.sha256(s.tobytes()).hexdigest() for s in series] == golden["lead"][name]
+    plain = gpu.run(batch)
+    assert res.tobytes() == plain.results.tobytes()
+
+
+def test_lead_capacity_overflow_reported(fb, gpu):
+    batch = SCENARIOS["c1"](gpu.generate_bursty)
+    a = fb.Arena(0)
+    a.set_lead(ms_to_us(500.0), 8)  # far too few points for a 250 s run
+    a.load(batch)
+    a.run()
+    assert all(s is None for s in a.lead())
+    a.close()
