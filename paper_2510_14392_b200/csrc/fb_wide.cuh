@@ -1377,13 +1377,21 @@ struct WideSlot {
   int64_t A, n_act, now;
   int32_t begin, policy;
   int32_t ncand, pad;  // K2b: gathered window keys
+  // per-iteration results, written once by the CTA that completes a phase's
+  // last view range of the node (views counted in k1_done / hist_done)
+  unsigned long long k1_done, hist_done;
+  int64_t red[kK1Vals];  // combined K1 reductions
+  int64_t urgency;
+  SelBins sb;
+  int32_t bmax, all;     // window: last bin, holds every key
 };
 
 // What a helper CTA needs of a slot, read from L2 (the slot is written by
 // another CTA).
 struct WgView {
-  int64_t inst, A, now;
-  int32_t policy;
+  int64_t inst, A, now, urgency;
+  int32_t policy, bmax;
+  SelBins sb;
 };
 __device__ __forceinline__ WgView wg_view(const WideSlot* s) {
   const volatile WideSlot* v = s;
@@ -1392,6 +1400,14 @@ __device__ __forceinline__ WgView wg_view(const WideSlot* s) {
   o.A = v->A;
   o.now = v->now;
   o.policy = v->policy;
+  o.urgency = v->urgency;
+  o.bmax = v->bmax;
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    o.sb.lo[g] = v->sb.lo[g];
+    o.sb.sh[g] = v->sb.sh[g];
+  }
+  o.sb.urg = v->sb.urg;
   return o;
 }
 
@@ -1437,6 +1453,9 @@ __device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w,
     my->begin = 1;
     my->policy = w.policy;
     my->ncand = 0;
+    my->k1_done = 0;
+    my->hist_done = 0;
+    my->bmax = -2;
   }
 }
 
@@ -1828,6 +1847,26 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
               P.wg.partial + (static_cast<int64_t>(blockIdx.x) * n_slots + t) * kK1Vals;
 #pragma unroll
           for (int k = 0; k < kK1Vals; ++k) part[k] = r[k];
+          // the CTA that completes the node's views combines everyone's
+          // partials once (init budget, urgency, selection bins)
+          __threadfence();
+          const unsigned long long seg = static_cast<unsigned long long>(z - a);
+          if (atomicAdd(&slots[t].k1_done, seg) + seg == static_cast<unsigned long long>(sv.A)) {
+            __threadfence();
+            int64_t acc[kK1Vals];
+            wg_combine(P, sp, t, acc);
+            const WideStep ss = wide_step(acc, sv.A, sv.policy);
+            volatile WideSlot* vs = slots + t;
+#pragma unroll
+            for (int k = 0; k < kK1Vals; ++k) vs->red[k] = acc[k];
+            vs->urgency = ss.urgency;
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+              vs->sb.lo[g] = ss.sb.lo[g];
+              vs->sb.sh[g] = ss.sb.sh[g];
+            }
+            vs->sb.urg = ss.sb.urg;
+          }
         }
       }
       CPROF(0)
@@ -1843,9 +1882,6 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
         if (z <= a) continue;
         const WgView sv = wg_view(slots + t);
-        int64_t acc[kK1Vals];
-        wg_combine(P, sp, t, acc);
-        const WideStep ss = wide_step(acc, sv.A, sv.policy);
         const Inst wv = wide_view_ctx(P, sv.inst);
         const WideScratch ws = wide_scratch(P, wv);
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
@@ -1862,7 +1898,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
 #pragma unroll
           for (int j = 0; j < U; ++j) {
             const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-            if (p < p_hi) atomicAdd(&sm.hist[sel_bin(kl[j], sv.policy, ss.urgency, ss.sb)], 1u);
+            if (p < p_hi) atomicAdd(&sm.hist[sel_bin(kl[j], sv.policy, sv.urgency, sv.sb)], 1u);
           }
         }
         __syncthreads();
@@ -1896,6 +1932,26 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
           if (v && c0 + k <= cross) atomicAdd(gh + c0 + k, v);
         }
         __syncthreads();
+        // the CTA that completes the node's histogram picks its window once
+        if (threadIdx.x == 0) {
+          __threadfence();
+          const unsigned long long seg = static_cast<unsigned long long>(z - a);
+          sm.ibcast[6] =
+              atomicAdd(&slots[t].hist_done, seg) + seg == static_cast<unsigned long long>(sv.A);
+        }
+        __syncthreads();
+        if (sm.ibcast[6]) {
+          __threadfence();
+          int bmax;
+          bool all;
+          wg_window(P, t, sv.A, bmax, all, sm);
+          if (threadIdx.x == 0) {
+            volatile WideSlot* vs = slots + t;
+            vs->bmax = bmax;
+            vs->all = all ? 1 : 0;
+          }
+        }
+        __syncthreads();
       }
       CPROF(1)
     }
@@ -1910,13 +1966,8 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
         if (z <= a) continue;
         const WgView sv = wg_view(slots + t);
-        int bmax;
-        bool all;
-        wg_window(P, t, sv.A, bmax, all, sm);
+        const int bmax = sv.bmax;
         if (bmax < 0) continue;
-        int64_t acc[kK1Vals];
-        wg_combine(P, sp, t, acc);
-        const WideStep ss = wide_step(acc, sv.A, sv.policy);
         const Inst wv = wide_view_ctx(P, sv.inst);
         const WideScratch ws = wide_scratch(P, wv);
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
@@ -1934,7 +1985,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
 #pragma unroll
           for (int j = 0; j < U; ++j) {
             const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-            const bool sel = p < p_hi && sel_bin(kl[j], sv.policy, ss.urgency, ss.sb) <= bmax;
+            const bool sel = p < p_hi && sel_bin(kl[j], sv.policy, sv.urgency, sv.sb) <= bmax;
             const unsigned m = __ballot_sync(kFull, sel);
             int base = 0;
             if (m && lane_id() == 0) base = atomicAdd(ncand, __popc(m));
@@ -1960,11 +2011,11 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       const int t = static_cast<int>(blockIdx.x);
       const volatile WideSlot* vs = my;
       int64_t acc[kK1Vals];
-      wg_combine(P, sp, t, acc);
+#pragma unroll
+      for (int k = 0; k < kK1Vals; ++k) acc[k] = vs->red[k];
       const WideStep ss = wide_step(acc, vs->A, w.policy);
-      int bmax;
-      bool all0;
-      wg_window(P, t, vs->A, bmax, all0, sm);
+      const int bmax = vs->bmax;
+      bool all0 = vs->all != 0;
       int K0 = -1;
       if (bmax >= 0) {
         K0 = vs->ncand;
