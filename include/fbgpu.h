@@ -384,7 +384,7 @@ typedef struct fb_lb_config {
   int64_t report_latency_us;     /* delivery delay of a report */
   double w_waiting;              /* count_lb weights */
   double w_running;
-  int32_t retry_reroute; /* must be 0 (rerouting is not supported) */
+  int32_t retry_reroute; /* route a PAB-rejected request once more (one rank only) */
   int32_t report_cap;    /* per-node in-flight report capacity (0 = default 4096) */
 } fb_lb_config;
 

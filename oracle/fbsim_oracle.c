@@ -844,8 +844,9 @@ static void orc_node_alloc(orc_node* nd, const fb_instance* inst, const fb_trace
   nd->flags = (uint32_t*)calloc(nn, sizeof(uint32_t));
   nd->active = (int32_t*)malloc(nn * sizeof(int32_t));
   nd->waiting = (int32_t*)malloc(nn * sizeof(int32_t));
-  nd->pend_row = (int32_t*)malloc(nn * sizeof(int32_t));
-  nd->pend_vis = (int64_t*)malloc(nn * sizeof(int64_t));
+  /* a rerouted request can reach the same node twice (retry_reroute) */
+  nd->pend_row = (int32_t*)malloc(2 * nn * sizeof(int32_t));
+  nd->pend_vis = (int64_t*)malloc(2 * nn * sizeof(int64_t));
   nd->views = (fb_task_view*)malloc(nn * sizeof(fb_task_view));
   nd->plan_e = (fb_plan_entry_id*)malloc(nn * sizeof(fb_plan_entry_id));
   for (int64_t i = 0; i < n; ++i) nd->first[i] = -1;
@@ -902,13 +903,12 @@ static int orc_route(orc_nview* v, int n, int64_t prompt, const fb_lb_config* lb
   return chosen;
 }
 
-/* run_cluster, cluster.cpp:134-251 (retry_reroute unsupported). */
+/* run_cluster, cluster.cpp:134-251. */
 int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
                     const fb_lb_config* lb, int64_t horizon, fb_instance_result* node_results,
                     fb_record* records, int32_t* route_node, int32_t* incomplete_out) {
   if (n_nodes < 1) return FB_ERR_USAGE;
   if (lb->report_latency_us < 0) return FB_ERR_VALIDATION;
-  if (lb->retry_reroute) return FB_ERR_USAGE;
   const int n = n_nodes;
   const int64_t nr = rows->n_rows;
   fb_instance* inst = (fb_instance*)calloc((size_t)n, sizeof(fb_instance));
@@ -925,8 +925,8 @@ int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
     inst[i].horizon_us = horizon;
     orc_node_alloc(&nodes[i], &inst[i], rows, &res[i]);
   }
-  if (route_node)
-    for (int64_t k = 0; k < nr; ++k) route_node[k] = -1;
+  int32_t* rt = (int32_t*)malloc(((size_t)nr + 1) * sizeof(int32_t)); /* last target */
+  for (int64_t k = 0; k < nr; ++k) rt[k] = -1;
 #define ORC_PUSH(d)                                                        \
   do {                                                                     \
     if (dtail == dcap) {                                                   \
@@ -940,6 +940,8 @@ int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
     }                                                                      \
     dq[dtail++] = (d);                                                     \
   } while (0)
+  /* retry_reroute bookkeeping per request: bit 0 retried, bit 1 ever rejected */
+  uint8_t* rstate = (uint8_t*)calloc((size_t)nr + 1, 1);
   for (int i = 0; i < n; ++i) ORC_PUSH(orc_make_report(&nodes[i], i, 0, pab_lb, lb->report_latency_us));
   int64_t arr = 0;
   int status = FB_OK;
@@ -974,13 +976,36 @@ int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
     }
     while (arr < nr && rows->arrival_us[arr] == t) { /* route on arrival */
       const int target = orc_route(view, n, rows->prompt_len[arr], lb);
-      if (route_node) route_node[arr] = target;
+      rt[arr] = target;
       orc_enqueue(&nodes[target], (int32_t)arr, t);
       ++arr;
     }
-    if (t < horizon) {
-      for (int i = 0; i < n && !status; ++i)
-        if (!nodes[i].busy) status = orc_begin_step(&nodes[i], t);
+    if (t < horizon) { /* begin_step, rejected requests rerouted once (cluster.cpp:222-237) */
+      int progress = 1;
+      while (progress && !status) {
+        progress = 0;
+        for (int i = 0; i < n && !status; ++i) {
+          if (nodes[i].busy) continue;
+          const int64_t h0 = nodes[i].pend_head, rej0 = nodes[i].res->n_rejected;
+          status = orc_begin_step(&nodes[i], t);
+          if (nodes[i].res->n_rejected == rej0) continue;
+          /* drain_rejects: this pull's rejected rows in pull order; a stale flag
+             can only sit on a row that was already retried */
+          for (int64_t q = h0; q < nodes[i].pend_head; ++q) {
+            const int32_t r = nodes[i].pend_row[q];
+            if (!(nodes[i].flags[r] & FB_REC_REJECTED)) continue;
+            const uint8_t was = rstate[r];
+            rstate[r] |= 2;
+            if (lb->retry_reroute && !(was & 1)) {
+              rstate[r] |= 1;
+              const int target = orc_route(view, n, rows->prompt_len[r], lb);
+              rt[r] = target;
+              orc_enqueue(&nodes[target], r, t);
+              progress = 1;
+            }
+          }
+        }
+      }
     }
     if (status) break;
   }
@@ -1008,19 +1033,25 @@ int orc_run_cluster(const fb_trace* rows, const fb_engine_config* cfgs, int32_t 
       const orc_node* nd = &nodes[i];
       for (int64_t k = 0; k < nr; ++k) {
         if (!(nd->flags[k] & FB_REC_ARRIVED)) continue;
+        /* a rerouted request: the record of the node it was routed to last */
+        if (rt[k] != i) continue;
         records[k].first_emit_us = nd->first[k];
         records[k].max_tpot_ms = nd->maxtp[k];
         records[k].max_tpot_alt_ms = nd->maxtp_alt[k];
         records[k].tokens_emitted = nd->nidx[k];
         uint32_t f = nd->flags[k] & 0x7fffffffu;
+        /* rejected only if never served anywhere (metrics.cpp:96-98) */
+        if (rstate[k] & 2) f |= FB_REC_REJECTED;
         if ((f & FB_REC_REJECTED) && nd->nidx[k] > 0) f &= ~(uint32_t)FB_REC_REJECTED;
         records[k].flags = f;
       }
     }
   }
+  if (route_node)
+    for (int64_t k = 0; k < nr; ++k) route_node[k] = rt[k];
   if (incomplete_out) *incomplete_out = live;
   for (int i = 0; i < n; ++i) orc_node_free(&nodes[i]);
-  free(nodes); free(inst); free(res); free(view); free(dq);
+  free(nodes); free(inst); free(res); free(view); free(dq); free(rstate); free(rt);
   return status;
 }
 

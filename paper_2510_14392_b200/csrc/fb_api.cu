@@ -739,6 +739,7 @@ struct fb_cluster_shard {
   unsigned char* xbuf = nullptr;
   int64_t* d_out = nullptr;
   int32_t* d_route = nullptr;
+  uint8_t* d_row_state = nullptr;  // retry_reroute: bit 0 retried, bit 1 ever rejected
   ~fb_cluster_shard() {
     if (a) cudaSetDevice(a->device);
     for (void* p : opened) cudaIpcCloseMemHandle(p);
@@ -774,7 +775,8 @@ int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_co
   if (n_ranks < 1 || n_ranks > fbgpu::cluster_max_ranks())
     return set_error(FB_ERR_USAGE, "fb_cluster_shard_create: 1..8 ranks");
   if (lb->report_latency_us < 0) return set_error(FB_ERR_VALIDATION, "report_latency must be >= 0");
-  if (lb->retry_reroute) return set_error(FB_ERR_USAGE, "retry_reroute is not supported");
+  if (lb->retry_reroute && n_ranks != 1)
+    return set_error(FB_ERR_USAGE, "retry_reroute runs on one rank");
   if (lb->policy != FB_LB_PAB && lb->policy != FB_LB_COUNT)
     return set_error(FB_ERR_USAGE, "unknown load-balancer policy");
   int32_t lo = 0, nl = 0;
@@ -826,7 +828,17 @@ int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_co
   FB_CUDA(dalloc(reinterpret_cast<void**>(&d_eplo), sizeof(int64_t) * (ne + 1)));
   FB_CUDA(dalloc(reinterpret_cast<void**>(&d_rep), sizeof(int64_t) * 4 * cap * nl));
   FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_out), sizeof(int64_t) * 4));
-  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_routed), sizeof(int32_t) * nl * (nr + 1)));
+  // a rerouted request reaches a second node (possibly the same one): the
+  // routed lists then hold up to 2 * nr entries
+  const int64_t stride = lb->retry_reroute ? 2 * nr + 1 : nr;
+  FB_CUDA(dalloc(reinterpret_cast<void**>(&d_routed), sizeof(int32_t) * nl * (stride + 1)));
+  int64_t* d_fifo = nullptr;
+  int64_t fifo_cap = 0;
+  if (lb->retry_reroute) {
+    fifo_cap = static_cast<int64_t>(cap) * n_nodes;
+    FB_CUDA(dalloc(reinterpret_cast<void**>(&d_fifo), sizeof(int64_t) * 6 * fifo_cap));
+    FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_row_state), nr + 1));
+  }
   FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_route), sizeof(int32_t) * (nr + 1)));
   FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->xbuf), fbgpu::cluster_xchg_bytes(n_nodes)));
   cudaStream_t s = sh->a->stream;
@@ -868,6 +880,11 @@ int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_co
   cp.warps_per_cta = wpc;
   cp.total_ctas = total;
   cp.timeout_ns = int64_t(30) * 1000 * 1000 * 1000;
+  cp.route_stride = stride;
+  cp.retry_reroute = lb->retry_reroute ? 1 : 0;
+  cp.fifo_cap = static_cast<int32_t>(fifo_cap);
+  cp.fifo = d_fifo;
+  cp.row_state = sh->d_row_state;
   if (fbgpu::cluster_param_bytes() != sizeof(cp))
     return set_error(FB_ERR_USAGE, "cluster parameter layout mismatch");
   if (n_ranks == 1) {
@@ -939,6 +956,7 @@ int fb_cluster_shard_reset(fb_cluster_shard* s) {
   FB_CUDA(cudaMemsetAsync(s->xbuf, 0, fbgpu::cluster_xchg_bytes(s->n_nodes), q));
   FB_CUDA(cudaMemsetAsync(s->d_out, 0, sizeof(int64_t) * 4, q));
   FB_CUDA(cudaMemsetAsync(s->d_route, 0xff, sizeof(int32_t) * (s->nr + 1), q));
+  if (s->d_row_state) FB_CUDA(cudaMemsetAsync(s->d_row_state, 0, s->nr + 1, q));
   FB_CUDA(cudaStreamSynchronize(q));
   return FB_OK;
 }
@@ -950,7 +968,11 @@ int fb_cluster_shard_launch(fb_cluster_shard* s) {
   FB_CUDA(cudaSetDevice(s->a->device));
   cudaStream_t q = s->a->stream;
   FB_CUDA(cudaEventRecord(s->a->ev0, q));
-  FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q));
+  if (s->cp.retry_reroute) {
+    FB_CUDA(fbgpu::launch_cluster_serial(s->a->params(0), s->cp, q));
+  } else {
+    FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q));
+  }
   FB_CUDA(cudaEventRecord(s->a->ev1, q));
   s->launched = true;
   return FB_OK;
@@ -1009,6 +1031,9 @@ int fb_cluster_shard_fetch(fb_cluster_shard* s, fb_instance_result* local_result
     std::vector<uint32_t> flags(n);
     std::vector<int64_t> first(n);
     std::vector<double> mt(n), mta(n);
+    std::vector<uint8_t> rst(s->d_row_state ? nr : 0);
+    if (s->d_row_state)
+      FB_CUDA(cudaMemcpyAsync(rst.data(), s->d_row_state, nr, cudaMemcpyDeviceToHost, q));
     FB_CUDA(cudaMemcpyAsync(nidx.data(), a->nidx.p, n * 4, cudaMemcpyDeviceToHost, q));
     FB_CUDA(cudaMemcpyAsync(flags.data(), a->flags.p, n * 4, cudaMemcpyDeviceToHost, q));
     FB_CUDA(cudaMemcpyAsync(first.data(), a->first.p, n * 8, cudaMemcpyDeviceToHost, q));
@@ -1024,6 +1049,9 @@ int fb_cluster_shard_fetch(fb_cluster_shard* s, fb_instance_result* local_result
       }
       const int64_t k = static_cast<int64_t>(node) * nr + r;
       uint32_t f = (flags[k] & ~fbgpu::kTpotViolated) | FB_REC_ARRIVED;
+      // rejected only if never served anywhere (metrics.cpp:96-98): a rerouted
+      // request may be rejected at one node and served at the next
+      if (!rst.empty() && (rst[r] & 2)) f |= FB_REC_REJECTED;
       if ((f & FB_REC_REJECTED) && nidx[k] > 0) f &= ~static_cast<uint32_t>(FB_REC_REJECTED);
       o.first_emit_us = first[k];
       o.max_tpot_ms = mt[k];

@@ -57,6 +57,25 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, i
                                      dim3(kWarp * c.warps_per_cta), args, smem, st);
 }
 
+size_t cluster_serial_smem_bytes() {
+  return ((sizeof(SerialSmem) + 15) / 16) * 16 + static_cast<size_t>(kSmemSlots) * kScratchBytesPerSlot;
+}
+
+// retry_reroute: the literal global loop on one warp (fb_cluster.cuh).
+cudaError_t launch_cluster_serial(const EngineParams& p, const ClusterParamsHost& ch,
+                                  cudaStream_t st) {
+  ClusterParams c;
+  std::memcpy(&c, &ch, sizeof(c));
+  if (c.n_ranks != 1 || c.fifo_cap < 1 || !c.fifo || !c.row_state) return cudaErrorInvalidValue;
+  const size_t smem = cluster_serial_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(cluster_serial_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cluster_serial_kernel<<<1, kWarp, smem, st>>>(p, c);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------- pure scheduler kernels
 
 __device__ __forceinline__ Scratch set_scratch(unsigned char* smem_warp, unsigned char* g,

@@ -60,6 +60,10 @@ struct ClusterParams {
   int32_t warps_per_cta, total_ctas;  // total_ctas: over all ranks
   int64_t timeout_ns;                 // exchange wait limit
   unsigned char* xbuf[kClusterMaxRanks];  // exchange buffer of every rank
+  int64_t route_stride;               // routed-list capacity per local node
+  int32_t retry_reroute, fifo_cap;    // serial engine (retry_reroute)
+  int64_t* fifo;                      // [fifo_cap * 6] in-flight reports
+  uint8_t* row_state;                 // [n_rows] bit 0 retried, bit 1 ever rejected
 };
 
 // Router view (replicated per CTA) + the CTA's routing results.
@@ -144,7 +148,7 @@ __device__ __forceinline__ void cluster_node_init(const EngineParams& P, const C
                                                   ClusterNode& nd) {
   Inst& w = nd.w;
   w.id = il;
-  w.routed = C.routed + static_cast<int64_t>(il) * C.n_rows;
+  w.routed = C.routed + static_cast<int64_t>(il) * C.route_stride;
   w.I = P.inst + il;
   w.S = P.state[il];
   w.toff = w.I->trace_off;
@@ -303,6 +307,75 @@ __device__ __forceinline__ bool cluster_stopped(const ClusterParams& C, const No
   return __syncthreads_or(mine) == 0;
 }
 
+// route (cluster.cpp:75-112) of one request by warp 0 over the replicated
+// view: pab_lb picks the largest effective budget among nodes that fit the
+// prompt (else overall), count_lb the smallest weighted count; ties to the
+// lowest node id.  Updates the view's local decrements.  Returns the node.
+__device__ __forceinline__ int cluster_pick(const ClusterParams& C, RouterSmem& rs,
+                                            int64_t prompt) {
+  const int n = C.n_nodes;
+  int chosen;
+  if (C.lb_policy == FB_LB_PAB) {
+    // best effective budget among nodes that fit the prompt, else overall;
+    // ties to the lowest node id
+    int64_t bf = INT64_MIN, ba = INT64_MIN;
+    int idf = INT32_MAX, ida = INT32_MAX;
+    for (int i = lane_id(); i < n; i += kWarp) {
+      const int64_t eff = rs.v_pab[i] - rs.v_dec[i];
+      if (eff > ba) {
+        ba = eff;
+        ida = i;
+      }
+      if (eff >= prompt && eff > bf) {
+        bf = eff;
+        idf = i;
+      }
+    }
+  #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t b2 = __shfl_xor_sync(kFull, bf, o);
+      const int i2 = __shfl_xor_sync(kFull, idf, o);
+      if (b2 > bf || (b2 == bf && i2 < idf)) {
+        bf = b2;
+        idf = i2;
+      }
+      const int64_t a2 = __shfl_xor_sync(kFull, ba, o);
+      const int j2 = __shfl_xor_sync(kFull, ida, o);
+      if (a2 > ba || (a2 == ba && j2 < ida)) {
+        ba = a2;
+        ida = j2;
+      }
+    }
+    chosen = idf != INT32_MAX ? idf : ida;
+    if (lane_id() == 0) rs.v_dec[chosen] += prompt;
+  } else {
+    double best = 0.0;
+    int idb = INT32_MAX;
+    for (int i = lane_id(); i < n; i += kWarp) {
+      const double score =
+          dadd(dmul(C.w_waiting, static_cast<double>(rs.v_wait[i] + rs.v_inc[i])),
+               dmul(C.w_running, static_cast<double>(rs.v_run[i])));
+      if (idb == INT32_MAX || score < best) {
+        best = score;
+        idb = i;
+      }
+    }
+  #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double b2 = __shfl_xor_sync(kFull, best, o);
+      const int i2 = __shfl_xor_sync(kFull, idb, o);
+      if (i2 != INT32_MAX && (idb == INT32_MAX || b2 < best || (b2 == best && i2 < idb))) {
+        best = b2;
+        idb = i2;
+      }
+    }
+    chosen = idb;
+    if (lane_id() == 0) rs.v_inc[chosen] += 1;
+  }
+  __syncwarp();
+  return chosen;
+}
+
 // Phase B (warp 0 of each CTA): reports -> view, route the epoch's arrivals.
 __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, RouterSmem& rs,
                               const NodeReport* all, int64_t e, int node_base) {
@@ -326,71 +399,14 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
   }
   __syncwarp();
   for (int64_t q = C.epoch_lo[e]; q < C.epoch_lo[e + 1]; ++q) {
-    const int64_t prompt = P.prompt[q];
-    int chosen;
-    if (C.lb_policy == FB_LB_PAB) {
-      // best effective budget among nodes that fit the prompt, else overall;
-      // ties to the lowest node id
-      int64_t bf = INT64_MIN, ba = INT64_MIN;
-      int idf = INT32_MAX, ida = INT32_MAX;
-      for (int i = lane_id(); i < n; i += kWarp) {
-        const int64_t eff = rs.v_pab[i] - rs.v_dec[i];
-        if (eff > ba) {
-          ba = eff;
-          ida = i;
-        }
-        if (eff >= prompt && eff > bf) {
-          bf = eff;
-          idf = i;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const int64_t b2 = __shfl_xor_sync(kFull, bf, o);
-        const int i2 = __shfl_xor_sync(kFull, idf, o);
-        if (b2 > bf || (b2 == bf && i2 < idf)) {
-          bf = b2;
-          idf = i2;
-        }
-        const int64_t a2 = __shfl_xor_sync(kFull, ba, o);
-        const int j2 = __shfl_xor_sync(kFull, ida, o);
-        if (a2 > ba || (a2 == ba && j2 < ida)) {
-          ba = a2;
-          ida = j2;
-        }
-      }
-      chosen = idf != INT32_MAX ? idf : ida;
-      if (lane_id() == 0) rs.v_dec[chosen] += prompt;
-    } else {
-      double best = 0.0;
-      int idb = INT32_MAX;
-      for (int i = lane_id(); i < n; i += kWarp) {
-        const double score =
-            dadd(dmul(C.w_waiting, static_cast<double>(rs.v_wait[i] + rs.v_inc[i])),
-                 dmul(C.w_running, static_cast<double>(rs.v_run[i])));
-        if (idb == INT32_MAX || score < best) {
-          best = score;
-          idb = i;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double b2 = __shfl_xor_sync(kFull, best, o);
-        const int i2 = __shfl_xor_sync(kFull, idb, o);
-        if (i2 != INT32_MAX && (idb == INT32_MAX || b2 < best || (b2 == best && i2 < idb))) {
-          best = b2;
-          idb = i2;
-        }
-      }
-      chosen = idb;
-      if (lane_id() == 0) rs.v_inc[chosen] += 1;
-    }
+    const int chosen = cluster_pick(C, rs, P.prompt[q]);
     if (lane_id() == 0) {
       if (blockIdx.x == 0) C.route_node[q] = chosen;
       const int k = chosen - node_base;  // Node::enqueue, on the owning CTA
       if (k >= 0 && k < C.warps_per_cta && chosen - C.node_lo < C.n_local) {
         const int64_t j = rs.n_routed[k];
-        C.routed[static_cast<int64_t>(chosen - C.node_lo) * C.n_rows + j] = static_cast<int32_t>(q);
+        C.routed[static_cast<int64_t>(chosen - C.node_lo) * C.route_stride + j] =
+            static_cast<int32_t>(q);
         rs.n_routed[k] = j + 1;
         rs.got[k] = 1;
       }
@@ -473,6 +489,188 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
       C.out[0] = e < C.n_epochs ? C.epoch_lo[e] : C.n_rows;
       C.out[2] = e;
     }
+  }
+}
+
+// ---------------------------------------------------------- retry_reroute
+//
+// run_cluster with lb.retry_reroute (cluster.cpp:222-237): a request that PAB
+// admission rejects is routed once more, at once, and may wake a node that
+// was already passed at the same instant -- a dependency inside one event
+// time that the epoch decomposition above cannot express.  This engine
+// replays the reference's global loop literally: one warp walks every node in
+// index order at each event time t (the minimum over busy step ends, the next
+// arrival and the head of the report FIFO), with the nodes' state in global
+// memory between visits and the memory path for every step.  One rank only.
+
+struct SerialSmem {
+  RouterSmem rs;
+  int64_t n_routed[kClusterMaxNodes];  // routed-list length per node
+};
+
+// The node's warp-uniform state, loaded from P.state (the memory path keeps
+// everything else in global memory).
+__device__ __forceinline__ void serial_load(const EngineParams& P, const ClusterParams& C,
+                                            int i, unsigned char* scratch, ClusterNode& nd) {
+  cluster_node_init(P, C, i, scratch, nd);
+}
+
+__device__ __forceinline__ void serial_store(const EngineParams& P, const ClusterNode& nd) {
+  if (lane_id() == 0) P.state[nd.w.id] = nd.w.S;
+  __syncwarp();
+}
+
+// make_report (cluster.cpp:50-58) into the global FIFO: [deliver_at,
+// emitted_at, pab, waiting, running, node].
+__device__ void serial_report(const EngineParams& P, const ClusterParams& C, ClusterNode& nd,
+                              int64_t now, int64_t head, int64_t& tail, int32_t* status) {
+  const Inst& w = nd.w;
+  const int64_t pab = C.lb_policy == FB_LB_PAB ? node_pab(P, nd, now) : 0;
+  if (tail - head >= C.fifo_cap) {
+    *status = FB_ERR_CAPACITY;
+  } else {
+    if (lane_id() == 0) {
+      int64_t* r = C.fifo + (tail % C.fifo_cap) * 6;
+      r[0] = now + C.latency;
+      r[1] = now;
+      r[2] = pab;
+      r[3] = w.S.n_live - w.S.n_active;
+      r[4] = w.S.n_active;
+      r[5] = w.id;
+    }
+    ++tail;
+  }
+  __syncwarp();
+}
+
+// route_request (cluster.cpp:171-175): pick, log the target, Node::enqueue.
+__device__ __forceinline__ void serial_route(const EngineParams& P, const ClusterParams& C,
+                                             SerialSmem& ss, int64_t row) {
+  const int chosen = cluster_pick(C, ss.rs, P.prompt[row]);
+  if (lane_id() == 0) {
+    C.route_node[row] = chosen;
+    const int64_t j = ss.n_routed[chosen];
+    C.routed[static_cast<int64_t>(chosen) * C.route_stride + j] = static_cast<int32_t>(row);
+    ss.n_routed[chosen] = j + 1;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWarp, 1)
+cluster_serial_kernel(const __grid_constant__ EngineParams P,
+                      const __grid_constant__ ClusterParams C) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SerialSmem& ss = *reinterpret_cast<SerialSmem*>(smem_raw);
+  RouterSmem& rs = ss.rs;
+  unsigned char* scratch = smem_raw + ((sizeof(SerialSmem) + 15) / 16) * 16;
+  const int n = C.n_nodes;
+  for (int i = lane_id(); i < n; i += kWarp) {
+    rs.v_has[i] = 0;
+    rs.v_t[i] = -1;
+    rs.v_pab[i] = rs.v_wait[i] = rs.v_run[i] = rs.v_dec[i] = rs.v_inc[i] = 0;
+    ss.n_routed[i] = 0;
+  }
+  __syncwarp();
+  int32_t status = FB_OK;
+  int64_t head = 0, tail = 0;
+  ClusterNode nd;
+  for (int i = 0; i < n; ++i) {  // initial reports (cluster.cpp:178)
+    serial_load(P, C, i, scratch, nd);
+    serial_report(P, C, nd, 0, head, tail, &status);
+  }
+  int64_t arr = 0, iters = 0;
+  for (;; ++iters) {
+    int64_t lt = kInf;
+    for (int i = lane_id(); i < n; i += kWarp) {
+      const DevState& st = P.state[i];
+      if (st.busy && st.step_end < lt) lt = st.step_end;
+    }
+    int64_t t = warp_min_i64(lt);
+    const bool any_busy = t != kInf;
+    if (arr < C.n_rows && P.arrival[arr] < t) t = P.arrival[arr];
+    if (head < tail && C.fifo[(head % C.fifo_cap) * 6] < t) t = C.fifo[(head % C.fifo_cap) * 6];
+    if (t == kInf || (!any_busy && t >= C.horizon)) break;
+    // 1) step completions in node order, then the boundary report
+    for (int i = 0; i < n; ++i) {
+      const DevState& st = P.state[i];
+      if (!(st.busy && st.step_end == t)) continue;
+      serial_load(P, C, i, scratch, nd);
+      nd.w.S.t_last = t;
+      complete_step(P, nd.w);
+      if (C.interval > 0 && nd.w.S.step_counter % static_cast<uint64_t>(C.interval) == 0)
+        serial_report(P, C, nd, t, head, tail, &status);
+      serial_store(P, nd);
+    }
+    // 2) report deliveries due by t (apply_report, cluster.cpp:60-73)
+    while (head < tail && C.fifo[(head % C.fifo_cap) * 6] <= t) {
+      const int64_t* r = C.fifo + (head % C.fifo_cap) * 6;
+      const int i = static_cast<int>(r[5]);
+      if (lane_id() == 0 && !(rs.v_has[i] && r[1] < rs.v_t[i])) {
+        rs.v_has[i] = 1;
+        rs.v_t[i] = r[1];
+        rs.v_pab[i] = r[2];
+        rs.v_wait[i] = r[3];
+        rs.v_run[i] = r[4];
+        rs.v_dec[i] = 0;
+        rs.v_inc[i] = 0;
+      }
+      __syncwarp();
+      ++head;
+    }
+    // 3) arrivals at exactly t, in trace order
+    for (; arr < C.n_rows && P.arrival[arr] == t; ++arr) serial_route(P, C, ss, arr);
+    // 4) begin_step on idle nodes; a first rejection is routed again at once
+    if (t < C.horizon) {
+      bool progress = true;
+      while (progress) {
+        progress = false;
+        for (int i = 0; i < n; ++i) {
+          if (P.state[i].busy) continue;
+          serial_load(P, C, i, scratch, nd);
+          Inst& w = nd.w;
+          w.S.arr = ss.n_routed[i];
+          const int64_t p0 = w.S.pulled, rej0 = w.S.n_rejected;
+          if (w.S.pulled < w.S.arr || w.S.n_live > 0) {
+            w.S.t_last = t;
+            begin_step(P, w, t);
+            w.S.paths |= kPathMemory;
+          }
+          const int64_t p1 = w.S.pulled;
+          const bool rejected = w.S.n_rejected != rej0;
+          serial_store(P, nd);
+          if (!rejected) continue;
+          // drain_rejects: the pulled rows flagged rejected, in pull order (a
+          // stale flag can only sit on a row already retried, so it is inert)
+          for (int64_t q = p0; q < p1; ++q) {
+            const int64_t row = w.routed[q];
+            if (!(P.flags[w.roff + row] & FB_REC_REJECTED)) continue;
+            const uint8_t rsv = C.row_state[row];
+            if (lane_id() == 0) C.row_state[row] = rsv | 3;
+            __syncwarp();
+            if (!(rsv & 1) && C.retry_reroute) {
+              serial_route(P, C, ss, row);
+              progress = true;
+            }
+          }
+        }
+      }
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    serial_load(P, C, i, scratch, nd);
+    Inst& w = nd.w;
+    w.S.arr = ss.n_routed[i];
+    if (lane_id() == 0) {
+      w.S.done = 1;
+      w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0) ? 1 : 0;
+      P.state[i] = w.S;
+    }
+    __syncwarp();
+  }
+  if (lane_id() == 0) {
+    C.out[0] = arr;
+    C.out[1] = status;
+    C.out[2] = iters;
   }
 }
 

@@ -136,6 +136,10 @@ struct ClusterParamsHost {
   int32_t warps_per_cta, total_ctas;
   int64_t timeout_ns;
   unsigned char* xbuf[kClusterHostMaxRanks];
+  int64_t route_stride;
+  int32_t retry_reroute, fifo_cap;
+  int64_t* fifo;
+  uint8_t* row_state;
 };
 size_t cluster_param_bytes();
 int cluster_max_nodes();
@@ -144,6 +148,8 @@ size_t cluster_xchg_bytes(int n_nodes);
 // Warps (nodes) per CTA, shared by all ranks, and this rank's CTA count.
 int cluster_warps_per_cta(int n_nodes, int n_ranks);
 size_t cluster_smem_bytes(int warps_per_cta);
+cudaError_t launch_cluster_serial(const EngineParams& p, const ClusterParamsHost& c,
+                                  cudaStream_t st);
 cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& c, int blocks,
                            cudaStream_t st);
 // Warp engine, then the grid-wide wide engine; `between` (may be null) is

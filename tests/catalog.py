@@ -177,6 +177,32 @@ def cluster_cases(gen):
     return out
 
 
+def reroute_cluster_cases(gen):
+    """run_cluster with retry_reroute (cluster.cpp:222-237): the
+    test_cluster.cpp:225-250 trace (a giant prompt saturates one node), and
+    overloaded PAB clusters whose admission rejects (then reroutes) requests."""
+    from paper_2510_14392_b200.batch import Rows
+    from paper_2510_14392_b200.cluster import LbConfig
+    t_model = CostModel(5.0, 0.01, 0.0001)
+    out = []
+    rows = Rows([0, 1000, 2000], [45_000, 45_000, 9000], [300, 300, 20],
+                [500_000] * 3, [50_000] * 3)
+    cfg = engine_config("fairbatch_pab", 8192, t_model, 500, 50)
+    out.append(("rr_giant_2", rows, [cfg, cfg], LbConfig("pab_lb", 1, 0.0, retry_reroute=True),
+                ms_to_us(3_600_000.0)))
+    prof = profile(4.0, 40.0, 800, 1600, 2000, 6000, 120, 260, 11)
+    rows_o = gen(prof, ms_to_us(20_000.0))
+    for name, nn, lat, pol in (("rr_pab0_4", 4, 0.0, "pab_lb"), ("rr_pab30_3", 3, 30.0, "pab_lb"),
+                               ("rr_count0_4", 4, 0.0, "count_lb")):
+        cfgs = [engine_config("fairbatch_pab", 2048, MODEL, 500, 50) for _ in range(nn)]
+        out.append((name, rows_o, cfgs, LbConfig(pol, 1, lat, retry_reroute=True),
+                    ms_to_us(3.6e6)))
+    # the same overload without rerouting (rejected requests stay rejected)
+    cfgs = [engine_config("fairbatch_pab", 2048, MODEL, 500, 50) for _ in range(4)]
+    out.append(("rr_off_pab0_4", rows_o, cfgs, LbConfig("pab_lb", 1, 0.0), ms_to_us(3.6e6)))
+    return out
+
+
 def summarize(results: np.ndarray, records: np.ndarray) -> dict:
     """Compact, exact summary of a run for fixtures."""
     keys = ("steps", "plan_digest", "end_time_us", "n_arrived", "n_rejected", "sum_entries",

@@ -24,8 +24,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import numpy as np  # noqa: E402
 
 from backends import RefLib, cluster_summary  # noqa: E402
-from catalog import (SCENARIOS, TRACE_PROFILES, cluster_cases, rows_digest,  # noqa: E402
-                     summarize)
+from catalog import (SCENARIOS, TRACE_PROFILES, cluster_cases, reroute_cluster_cases,  # noqa: E402
+                     rows_digest, summarize)
 from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views  # noqa: E402
 from tests_golden_cases import LEAD_CASES  # noqa: E402
 from paper_2510_14392_b200.batch import ms_to_us  # noqa: E402
@@ -91,7 +91,8 @@ def main() -> None:
                           lambda r, c, lb, h: ref.run_cluster(r, c, lb, h).records),
     }
     gold["clusters"] = {}
-    for name, rows, cfgs, lb, hz in cluster_cases(ref.generate_bursty):
+    for name, rows, cfgs, lb, hz in (cluster_cases(ref.generate_bursty) +
+                                     reroute_cluster_cases(ref.generate_bursty)):
         gold["clusters"][name] = cluster_summary(ref.run_cluster(rows, cfgs, lb, hz, check=True))
     corpus = acceptance_corpus(10_000)
     gold["fuzz"] = {}

@@ -287,13 +287,33 @@ def test_cluster_matches_golden(golden, gpu_cluster_cases, name):
     assert cluster_summary(out) == golden["clusters"][name]
 
 
-def test_cluster_rejects_reroute(fb):
-    from paper_2510_14392_b200.cluster import LbConfig, run_cluster
+@pytest.fixture(scope="module")
+def gpu_reroute_cases(fb):
+    from catalog import reroute_cluster_cases
+    return {c[0]: c for c in reroute_cluster_cases(fb.generate_bursty)}
+
+
+@pytest.mark.parametrize("name", ["rr_giant_2", "rr_pab0_4", "rr_pab30_3", "rr_count0_4",
+                                  "rr_off_pab0_4"])
+def test_cluster_reroute_matches_golden(golden, gpu_reroute_cases, name):
+    """retry_reroute (cluster.cpp:222-237) on the serial cluster engine:
+    digests, routing (last target) and merged records equal the reference's."""
+    from backends import cluster_summary
+    from paper_2510_14392_b200.cluster import run_cluster
+    _, rows, cfgs, lb, hz = gpu_reroute_cases[name]
+    out = run_cluster(rows, cfgs, lb, hz)
+    assert cluster_summary(out) == golden["clusters"][name]
+
+
+def test_cluster_reroute_is_single_rank(fb):
+    """The reroute engine replays the global loop on one GPU: a multi-rank
+    shard with retry_reroute is a usage error, not a silent divergence."""
+    from paper_2510_14392_b200.cluster import ClusterShard, LbConfig
     from paper_2510_14392_b200.batch import CostModel, Rows, engine_config
-    rows = Rows([0], [10], [5], [500_000], [50_000])
-    cfgs = [engine_config("fairbatch", 2048, CostModel(5, 0.05, 1e-4), 500, 50)]
+    rows = Rows([0, 0], [10, 10], [5, 5], [500_000] * 2, [50_000] * 2)
+    cfgs = [engine_config("fairbatch_pab", 2048, CostModel(5, 0.05, 1e-4), 500, 50)] * 2
     with pytest.raises(fb.UsageError):
-        run_cluster(rows, cfgs, LbConfig("pab_lb", 1, 0.0, retry_reroute=True), 10**9)
+        ClusterShard(rows, cfgs, LbConfig("pab_lb", 1, 0.0, retry_reroute=True), 10**9, 0, 2)
 
 
 @pytest.mark.parametrize("name,world", [("pab0_8", 2), ("count37_3", 3), ("pab5000_8", 4),

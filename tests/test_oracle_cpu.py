@@ -280,6 +280,32 @@ def test_oracle_cluster_matches_golden(oracle, golden, cluster_case_list, name):
     assert cluster_summary(oracle.run_cluster(rows, cfgs, lb, hz)) == golden["clusters"][name]
 
 
+@pytest.fixture(scope="module")
+def reroute_case_list(oracle):
+    from catalog import reroute_cluster_cases
+    return {c[0]: c for c in reroute_cluster_cases(oracle.generate_bursty)}
+
+
+@pytest.mark.parametrize("name", ["rr_giant_2", "rr_pab0_4", "rr_pab30_3", "rr_count0_4",
+                                  "rr_off_pab0_4"])
+def test_oracle_reroute_matches_golden(oracle, golden, reroute_case_list, name):
+    """retry_reroute (cluster.cpp:222-237): a first rejection is routed once
+    more at the same instant; digests, routing and records equal the reference's."""
+    from backends import cluster_summary
+    _, rows, cfgs, lb, hz = reroute_case_list[name]
+    assert cluster_summary(oracle.run_cluster(rows, cfgs, lb, hz)) == golden["clusters"][name]
+
+
+def test_oracle_reroute_giant_prompt(oracle, reroute_case_list):
+    """test_cluster.cpp:225-250: request 2, rejected behind the giant prompts,
+    finishes on the other node; it is routed at most twice."""
+    _, rows, cfgs, lb, hz = reroute_case_list["rr_giant_2"]
+    out = oracle.run_cluster(rows, cfgs, lb, hz)
+    f = int(out.records["flags"][2])
+    assert f & _abi.REC_FINISHED and not f & _abi.REC_REJECTED
+    assert int(out.node_results["n_arrived"].sum()) <= len(rows) + 1
+
+
 def test_route_known_answers(oracle):
     """test_cluster.cpp:76-113 through a 2-node cluster's first decisions:
     pab_lb prefers the roomiest node that fits, ties go to the lowest id."""
