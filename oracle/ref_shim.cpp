@@ -453,6 +453,27 @@ int ref_event_log(const fb_trace* rows, const fb_instance* inst, const char* tmp
   }
 }
 
+// The reference's own load_event_log + replay_check (engine.cpp:290-393,
+// 453-520) of a JSONL file: the violations joined by '\n' into buf.
+int ref_replay_check(const char* path, char* buf, int64_t cap, int64_t* len_out,
+                     int64_t* n_violations) {
+  try {
+    const ReplayReport rep = replay_check(load_event_log(path));
+    std::string s;
+    for (const auto& v : rep.violations) {
+      s += v;
+      s += '\n';
+    }
+    *n_violations = static_cast<int64_t>(rep.violations.size());
+    *len_out = static_cast<int64_t>(s.size());
+    if (static_cast<int64_t>(s.size()) > cap) return fail(FB_ERR_CAPACITY, "buffer too small");
+    std::memcpy(buf, s.data(), s.size());
+    return FB_OK;
+  } catch (const std::exception& e) {
+    return map_exception(e);
+  }
+}
+
 // The reference's envelope-lead series (metrics.cpp:137-169) of one
 // instance: run_node, request_reports, envelope_lead_series(bucket).
 int ref_lead_series(const fb_trace* rows, const fb_instance* inst, int64_t bucket_us,

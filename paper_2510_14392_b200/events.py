@@ -78,3 +78,157 @@ def event_log_lines(rows, inst, result, counts, steps, entries, rejects, node_id
 
 def event_log_jsonl(rows, inst, result, counts, steps, entries, rejects, node_id: int = 0) -> str:
     return "".join(event_log_lines(rows, inst, result, counts, steps, entries, rejects, node_id))
+
+
+# ------------------------------------------------------------- replay check
+
+class EventLog:
+    """A parsed JSONL event log (EventLog, engine.h:60-72): events as dicts
+    with the reference's field names, plus node id and the incomplete flag."""
+
+    def __init__(self, events, node_id: int = 0, incomplete: bool = False):
+        self.events = events
+        self.node_id = node_id
+        self.incomplete = incomplete
+
+
+_KINDS = ("arrival", "admission_reject", "batch_start", "token_emit", "request_done",
+          "batch_end")
+
+
+def load_event_log(text: str) -> EventLog:
+    """load_event_log (engine.cpp:453-520) of a JSONL text: blank lines are
+    skipped, ``log_end`` sets node / incomplete, times are ms -> µs with
+    llround (time.h:30-32); an unknown kind or bad JSON raises ParseError."""
+    import json
+    from .batch import ms_to_us
+    from .fbgpu import ParseError
+    events = []
+    node, incomplete = 0, False
+    for line_no, line in enumerate(text.split("\n"), 1):
+        if not line.strip(" \t\r"):
+            continue
+        try:
+            j = json.loads(line)
+        except ValueError as ex:
+            raise ParseError(f"event log line {line_no}: {ex}") from None
+        kind = j.get("kind", "")
+        if kind == "log_end":
+            node = int(j.get("node", 0))
+            incomplete = int(j.get("incomplete", 0)) != 0
+            continue
+        if kind not in _KINDS:
+            raise ParseError(f"event log line {line_no}: unknown kind '{kind}'")
+        e = {"kind": kind, "t": ms_to_us(j.get("t_ms", 0.0))}
+        if kind in ("arrival", "admission_reject", "token_emit", "request_done"):
+            e["req_id"] = int(j.get("req_id", -1))
+        if kind == "arrival":
+            e["output_len"] = int(j.get("output_tokens", 0))
+        if kind in ("batch_start", "batch_end"):
+            e["step"] = int(j.get("step", -1))
+        if kind == "token_emit":
+            e["token_idx"] = int(j.get("token_idx", -1))
+        events.append(e)
+    return EventLog(events, node, incomplete)
+
+
+def replay_check(log: EventLog) -> list[str]:
+    """replay_check (engine.cpp:290-393): re-derives the log invariants --
+    monotone timestamps, batch bracketing and sequential step ids, token
+    indices consecutive from 0, request_done exactly at output_len, no
+    activity for rejected requests, every request settled in a complete log.
+    Returns the violation messages in the reference's wording and order
+    (the final unsettled-request scan walks requests in first-seen order;
+    the reference's hash-map order is unspecified, so compare that tail as a
+    set)."""
+    out = []
+
+    def violation(i, what):
+        out.append(f"event {i}: {what}")
+
+    reqs = {}  # id -> [arrived, rejected, done, expected_idx, output_len]
+
+    def req(i):
+        r = reqs.get(i)
+        if r is None:
+            r = reqs[i] = [False, False, False, 0, 0]
+        return r
+
+    last_t = None
+    in_batch = False
+    expected_step = 0
+    body = []
+    ev = log.events
+    for i, e in enumerate(ev):
+        if last_t is not None and e["t"] < last_t:
+            violation(i, "timestamp decreases")
+        last_t = e["t"] if last_t is None else max(last_t, e["t"])
+        k = e["kind"]
+        if k == "arrival":
+            r = req(e["req_id"])
+            if r[0]:
+                violation(i, "duplicate arrival")
+            r[0] = True
+            r[4] = e["output_len"]
+        elif k == "admission_reject":
+            r = req(e["req_id"])
+            if not r[0]:
+                violation(i, "reject before arrival")
+            if r[1]:
+                violation(i, "duplicate admission_reject")
+            if r[3] > 0 or r[2]:
+                violation(i, "reject after request activity")
+            r[1] = True
+        elif k == "batch_start":
+            if in_batch:
+                violation(i, "nested batch_start")
+            if e["step"] != expected_step:
+                violation(i, "non-sequential step id")
+            in_batch = True
+            body = []
+        elif k == "token_emit":
+            if not in_batch:
+                violation(i, "token_emit outside a batch")
+            body.append(i)
+            r = req(e["req_id"])
+            if not r[0]:
+                violation(i, "token_emit for unknown request")
+            if r[1]:
+                violation(i, "token_emit for rejected request")
+            if r[2]:
+                violation(i, "token_emit after request_done")
+            if e["token_idx"] != r[3]:
+                violation(i, f"token index {e['token_idx']} does not continue sequence "
+                             f"(expected {r[3]})")
+            if e["token_idx"] == r[3]:
+                r[3] = e["token_idx"] + 1
+        elif k == "request_done":
+            if not in_batch:
+                violation(i, "request_done outside a batch")
+            body.append(i)
+            r = req(e["req_id"])
+            if not r[0]:
+                violation(i, "request_done for unknown request")
+            if r[2]:
+                violation(i, "duplicate request_done")
+            if r[3] != r[4]:
+                violation(i, "request_done before all tokens emitted")
+            r[2] = True
+        elif k == "batch_end":
+            if not in_batch:
+                violation(i, "batch_end without batch_start")
+                continue
+            if e["step"] != expected_step:
+                violation(i, "batch_end step mismatch")
+            for bi in body:
+                if ev[bi]["t"] != e["t"]:
+                    violation(bi, "in-batch event timestamp differs from batch_end")
+            in_batch = False
+            expected_step += 1
+    if in_batch:
+        out.append("log ends inside an open batch")
+    if not log.incomplete:
+        for rid, r in reqs.items():
+            if r[0] and not r[1] and not r[2]:
+                out.append(f"request {rid} neither done nor rejected in a complete log")
+    return out

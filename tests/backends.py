@@ -348,6 +348,25 @@ class RefLib(_CpuLib):
                 raise RuntimeError(f"ref_event_log status {st}")
             return buf.raw[: n.value].decode()
 
+    def replay_check(self, jsonl: str, tmp_path: str) -> list[str]:
+        """The reference's load_event_log + replay_check of a JSONL text."""
+        fn = self.lib.ref_replay_check
+        fn.restype = C.c_int
+        with open(tmp_path, "w") as f:
+            f.write(jsonl)
+        n, nv = C.c_int64(0), C.c_int64(0)
+        cap = 1 << 16
+        while True:
+            buf = C.create_string_buffer(cap)
+            st = fn(tmp_path.encode(), buf, C.c_int64(cap), C.byref(n), C.byref(nv))
+            if st == _abi.FB_ERR_CAPACITY:
+                cap = n.value + 1
+                continue
+            if st:
+                raise RuntimeError(f"ref_replay_check status {st}: {self.lib.ref_last_error()}")
+            text = buf.raw[: n.value].decode()
+            return text.split("\n")[:-1] if text else []
+
     def lead_series(self, batch: Batch, i: int, bucket_us: int) -> np.ndarray:
         """The reference's envelope_lead_series (metrics.cpp:137-169) of instance i."""
         fn = self.lib.ref_lead_series

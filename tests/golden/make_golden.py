@@ -27,7 +27,7 @@ from backends import RefLib, cluster_summary  # noqa: E402
 from catalog import (SCENARIOS, TRACE_PROFILES, cluster_cases, reroute_cluster_cases,  # noqa: E402
                      rows_digest, summarize)
 from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views  # noqa: E402
-from tests_golden_cases import LEAD_CASES  # noqa: E402
+from tests_golden_cases import LEAD_CASES, REPLAY_MUTATIONS, replay_canonical  # noqa: E402
 from paper_2510_14392_b200.batch import ms_to_us  # noqa: E402
 
 
@@ -72,6 +72,14 @@ def main() -> None:
         gold["event_logs"][name] = [
             hashlib.sha256(ref.event_log(batch, i, "/tmp/_golden_ev.jsonl").encode()).hexdigest()
             for i in range(batch.n_instances)]
+    # the reference's replay_check on mutations of its own event log
+    batch = SCENARIOS["pab_overload"](ref.generate_bursty)
+    base = ref.event_log(batch, 0, "/tmp/_golden_ev.jsonl").rstrip("\n").split("\n")
+    gold["replay_check"] = {}
+    for name, fn in REPLAY_MUTATIONS.items():
+        v = replay_canonical(ref.replay_check("\n".join(fn(base)) + "\n", "/tmp/_golden_rc.jsonl"))
+        gold["replay_check"][name] = {"n": len(v), "head": v[:3],
+                                      "sha256": hashlib.sha256("\n".join(v).encode()).hexdigest()}
     gold["lead"] = {}
     for name, bucket_ms in LEAD_CASES.items():
         batch = SCENARIOS[name](ref.generate_bursty)

@@ -191,6 +191,21 @@ def test_gpu_event_logs_match_reference_jsonl(gpu, golden, name):
     assert got == golden["event_logs"][name]
 
 
+@pytest.mark.parametrize("name", ["pab_overload", "wide"])
+def test_gpu_event_logs_pass_replay_check(gpu, name):
+    """replay_check (engine.cpp:290-393) on the device-built event logs:
+    no violation in any instance."""
+    from paper_2510_14392_b200.events import event_log_jsonl, load_event_log, replay_check
+    batch = SCENARIOS[name](gpu.generate_bursty)
+    lo = _abi.LogOpts(40_000, 600_000, 5_000, 0)
+    out = gpu.run(batch, lo)
+    for i in range(batch.n_instances):
+        log = load_event_log(event_log_jsonl(batch.rows, batch.instance(i), out.results[i],
+                                             out.counts[i], out.steps[i], out.entries[i],
+                                             out.rejects[i]))
+        assert log.events and replay_check(log) == [], i
+
+
 def test_stepwise_api_matches_one_shot(gpu):
     """Node-style incremental driving (fb_arena_run with an event budget)."""
     batch = SCENARIOS["mixed"](gpu.generate_bursty)

@@ -262,6 +262,53 @@ def test_event_logs_from_plan_logs_match_reference_jsonl(oracle, golden, name):
     assert got == golden["event_logs"][name]
 
 
+@pytest.fixture(scope="module")
+def overload_log_lines(oracle):
+    from paper_2510_14392_b200.events import event_log_jsonl
+    batch = SCENARIOS["pab_overload"](oracle.generate_bursty)
+    lo = _abi.LogOpts(40_000, 600_000, 5_000, 0)
+    out = oracle.run(batch, lo, nthreads=4)
+    return [event_log_jsonl(batch.rows, batch.instance(i), out.results[i], out.counts[i],
+                            out.steps[i], out.entries[i], out.rejects[i])
+            for i in range(batch.n_instances)]
+
+
+def test_replay_check_clean_logs(overload_log_lines):
+    """Rebuilt event logs satisfy every replay_check invariant."""
+    from paper_2510_14392_b200.events import load_event_log, replay_check
+    for text in overload_log_lines:
+        log = load_event_log(text)
+        assert log.events and replay_check(log) == []
+
+
+@pytest.mark.parametrize("name", ["clean", "drop_first_token", "drop_first_batch_end",
+                                  "drop_first_arrival", "dup_arrival", "swap_2_3", "decrease_t",
+                                  "bad_token_idx", "reject_after_activity", "truncated_complete",
+                                  "done_early", "emit_outside", "unknown_request"])
+def test_replay_check_known_answers(golden, overload_log_lines, name):
+    """replay_check (engine.cpp:290-393) reports exactly the reference's
+    violations, in its order, on mutated copies of a log (golden.json holds
+    the reference's own answers on the same mutations)."""
+    from paper_2510_14392_b200.events import load_event_log, replay_check
+    from tests_golden_cases import REPLAY_MUTATIONS, replay_canonical
+    base = overload_log_lines[0].rstrip("\n").split("\n")
+    v = replay_canonical(replay_check(load_event_log("\n".join(REPLAY_MUTATIONS[name](base)))))
+    g = golden["replay_check"][name]
+    assert len(v) == g["n"] and v[:3] == g["head"]
+    assert hashlib.sha256("\n".join(v).encode()).hexdigest() == g["sha256"]
+
+
+def test_load_event_log_errors():
+    from paper_2510_14392_b200.events import load_event_log
+    from paper_2510_14392_b200.fbgpu import ParseError
+    with pytest.raises(ParseError):
+        load_event_log('{"t_ms":1.0,"kind":"teleport"}\n')
+    with pytest.raises(ParseError):
+        load_event_log('{"t_ms":1.0,\n')
+    log = load_event_log('\n  \n{"kind":"log_end","node":3,"incomplete":1}\n')
+    assert log.events == [] and log.node_id == 3 and log.incomplete
+
+
 # --------------------------------------------------------------- cluster
 
 @pytest.fixture(scope="module")
