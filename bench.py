@@ -155,7 +155,19 @@ def cpu_baseline(batch, n_threads: int, budget_s: float = 15.0) -> dict:
     steps, dt, n = best
     return {"value": steps / dt, "unit": UNIT, "cores": n_threads, "kind": kind,
             "sample": f"{n} of {n_total} C2 instances ({steps} instance-steps) in {dt:.2f} s, "
-                      f"{n_threads} threads, {os.cpu_count()} host CPUs"}
+                      f"{n_threads} threads, {os.cpu_count()} host CPUs",
+            "cpu_model": cpu_model()}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
@@ -388,6 +400,9 @@ def run_ours(args) -> None:
             line["c4"] = bench_c4(peak, peak_kind)
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(batch, os.cpu_count() or 1, args.ref_budget_s)
+            # the single-core figure beside the all-cores one
+            one = cpu_baseline(batch, 1, args.ref_budget_s / 3)
+            line["cpu_baseline"]["one_core"] = {"value": one["value"], "sample": one["sample"]}
         print(json.dumps(line), flush=True)
     arena.close()
     if ws > 1:
