@@ -1022,12 +1022,21 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
   constexpr int U = 4;
   int64_t mn[6] = {kInf, kInf, kInf, kInf, kInf, kInf};
   int64_t l_cnt = 0;
+  // the row indices of the next batch are loaded one batch ahead, so only the
+  // record loads' latency is exposed per batch (not index, then record)
+  int32_t rn[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    const int64_t p = p_lo + j * kWideThreads + threadIdx.x;
+    rn[j] = p < p_hi ? w.vl[p].x : -1;
+  }
   for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
     int32_t rr[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-      rr[j] = p < p_hi ? w.vl[p].x : -1;
+      rr[j] = rn[j];
+      const int64_t p = b0 + (U + j) * kWideThreads + threadIdx.x;
+      rn[j] = p < p_hi ? w.vl[p].x : -1;
     }
     int32_t prompt[U], pf[U], ni[U], seq[U];
     int64_t dl0[U], first[U], tpot[U];
