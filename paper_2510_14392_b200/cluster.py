@@ -215,6 +215,27 @@ def run_cluster_dist(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, dist,
     return merge_shards(parts, len(cfgs))
 
 
+def run_clusters(cases, device: int = 0) -> list[ClusterOutput]:
+    """Independent cluster simulations at once -- one one-rank shard per case,
+    each on its own stream, so their persistent cluster kernels (a few CTAs
+    each, bound by the per-epoch exchange latency) run side by side and a
+    sweep over seeds x rates x policies fills the GPU (replicas
+    amortise the epoch latency).  `cases` holds (rows, cfgs, lb, horizon_us);
+    the outputs equal run_cluster's case by case."""
+    shards = []
+    try:
+        for rows, cfgs, lb, hz in cases:
+            shards.append(ClusterShard(rows, cfgs, lb, hz, 0, 1, device))
+        for sh in shards:
+            sh.reset()
+        for sh in shards:
+            sh.launch()
+        return [merge_shards([sh.fetch(sh.wait())], len(c[1])) for sh, c in zip(shards, cases)]
+    finally:
+        for sh in shards:
+            sh.close()
+
+
 MODEL_7B = CostModel(5.0, 0.05, 0.0001)
 
 

@@ -320,6 +320,18 @@ def test_cluster_reroute_matches_golden(golden, gpu_reroute_cases, name):
     assert cluster_summary(out) == golden["clusters"][name]
 
 
+def test_clusters_side_by_side_match_golden(golden, gpu_cluster_cases, gpu_reroute_cases):
+    """run_clusters: concurrent shards (epoch-decomposed and serial reroute
+    engines mixed) give each case's golden run_cluster output."""
+    from backends import cluster_summary
+    from paper_2510_14392_b200.cluster import run_clusters
+    names = ["pab0_8", "count37_3", "rr_giant_2", "pab5000_8", "rr_pab30_3", "count0_8"]
+    cases = [(gpu_cluster_cases.get(n) or gpu_reroute_cases[n])[1:] for n in names]
+    outs = run_clusters(cases)
+    for n, out in zip(names, outs):
+        assert cluster_summary(out) == golden["clusters"][n], n
+
+
 def test_cluster_reroute_is_single_rank(fb):
     """The reroute engine replays the global loop on one GPU: a multi-rank
     shard with retry_reroute is a usage error, not a silent divergence."""

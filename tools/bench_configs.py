@@ -107,7 +107,39 @@ def main(which):
         report("C5 (64-node cluster, pab_lb, 11,694 requests)", steps, best, cpu,
                {"epochs": int(len(np.unique(rows.arrival_us))),
                 "cpu_note": "reference run_cluster is single-threaded by construction"})
+    if "c5x" in which:
+        # C5 replicas side by side (run_clusters): R seeds of the 64-node
+        # cluster, one shard + stream each; device time = first launch to last
+        # completion (host clock around launch-all / wait-all)
+        R = 16
+        cases = []
+        for i in range(R):
+            _, cfgs, lb, hz = cluster.c5()
+            cases.append((cluster.c5_rows(seed=5 + i), cfgs, lb, hz))
+        best, steps = 1e30, 0
+        for _ in range(3):
+            shards = [cluster.ClusterShard(r, c, l, h, 0, 1) for r, c, l, h in cases]
+            for sh in shards:
+                sh.reset()
+            t0 = time.perf_counter()
+            for sh in shards:
+                sh.launch()
+            for sh in shards:
+                sh.wait()
+            best = min(best, (time.perf_counter() - t0) * 1e3)
+            steps = sum(int(sh.fetch().node_results["steps"].sum()) for sh in shards)
+            for sh in shards:
+                sh.close()
+        cpu = None
+        if ref:
+            from concurrent.futures import ThreadPoolExecutor
+            t0 = time.perf_counter()
+            with ThreadPoolExecutor(min(R, NCPU)) as ex:
+                list(ex.map(lambda c: ref.run_cluster(*c), cases))
+            cpu = (steps / (time.perf_counter() - t0), min(R, NCPU))
+        report(f"C5 x{R} replicas side by side (run_clusters, 64 nodes each)", steps, best, cpu,
+               {"replicas": R, "cpu_note": "reference run_cluster, one replica per host thread"})
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c3", "c4", "c5"])
+    main(sys.argv[1:] or ["c1", "c3", "c4", "c5", "c5x"])
