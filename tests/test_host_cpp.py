@@ -1,0 +1,78 @@
+"""The C++ host API (paper_2510_14392_b200/host/fbsim_gpu.h): the reference's
+fbsim interfaces over the C ABI.  Driven through its test program
+(host/test_fbsim_gpu.cpp): host-only checks and loud failure without a GPU on
+CPU; the reference's known answers and byte-identical event logs on the GPU."""
+from __future__ import annotations
+
+import hashlib
+import os
+import subprocess
+
+import pytest
+
+from catalog import SCENARIOS
+from paper_2510_14392_b200.batch import Batch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "paper_2510_14392_b200", "host", "test_fbsim_gpu")
+
+
+def _run(*args, timeout=600):
+    if not os.path.exists(BIN):
+        pytest.fail("host/test_fbsim_gpu not built (run __graft_entry__.build())")
+    return subprocess.run([BIN, *args], capture_output=True, text=True, timeout=timeout)
+
+
+def _gpu_present() -> bool:
+    import torch
+    return torch.cuda.is_available()
+
+
+def test_host_api_without_gpu():
+    """Trace generation and the JSONL writer work on the host; every device
+    entry point throws CudaError (no CPU fallback)."""
+    if _gpu_present():
+        pytest.skip("a GPU is present: the no-device contract is checked on CPU hosts")
+    p = _run("nogpu")
+    assert p.returncode == 0, p.stderr
+
+
+@pytest.mark.gpu
+def test_host_api_known_answers():
+    """test_sched.cpp / test_engine.cpp / test_cluster.cpp known answers through
+    the C++ API: init budgets, plans, PAB 49009/44883/34883, the 6000 / 11020 /
+    16040 us timeline, the 49009 reject, chunking, routing, reroute."""
+    p = _run("kat")
+    assert p.returncode == 0, p.stdout + p.stderr
+
+
+def _instance_file(path, batch: Batch, i: int):
+    inst = batch.instance(i)
+    c = inst.cfg
+    s = c.scheduler
+    off, n = int(inst.trace_off), int(inst.n_req)
+    r = batch.rows
+    with open(path, "w") as f:
+        f.write(f"{inst.horizon_us} {s.policy} {s.token_budget} {s.max_chunk} "
+                f"{s.model.a_ms!r} {s.model.b_ms!r} {s.model.c_ms!r} "
+                f"{c.truth_model.a_ms!r} {c.truth_model.b_ms!r} {c.truth_model.c_ms!r} "
+                f"{c.noise_amplitude!r} {c.noise_seed} {c.global_ttft_us} {c.global_tpot_us} "
+                f"{c.max_active}\n{n}\n")
+        for k in range(off, off + n):
+            f.write(f"{r.arrival_us[k]} {r.prompt_len[k]} {r.output_len[k]} {r.ttft_us[k]} "
+                    f"{r.tpot_us[k]}\n")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pab_overload", "c1"])
+def test_host_api_event_logs_match_reference(golden, tmp_path, fb, name):
+    """run_node + save_event_log through the C++ API: byte-identical to the
+    reference's own writer (sha256 per instance, golden.json)."""
+    batch = SCENARIOS[name](fb.generate_bursty)
+    for i in range(batch.n_instances):
+        src, out = tmp_path / f"in{i}.txt", tmp_path / f"out{i}.jsonl"
+        _instance_file(src, batch, i)
+        p = _run("eventlog", str(src), str(out))
+        assert p.returncode == 0, p.stderr
+        got = hashlib.sha256(out.read_bytes()).hexdigest()
+        assert got == golden["event_logs"][name][i], (name, i)
