@@ -386,6 +386,78 @@ EventLog run_node(const Trace& trace, const EngineConfig& cfg, TimeUs horizon, i
   return run_nodes({&trace}, {cfg}, horizon, device)[0];
 }
 
+// -------------------------------------------------------------- NodeBatch
+
+struct NodeBatch::Impl {
+  Arena a;
+  std::vector<const Trace*> traces;
+  Rows rows;
+  std::vector<fb_instance> inst;
+  explicit Impl(int device) : a(device) {}
+};
+
+NodeBatch::NodeBatch(const std::vector<const Trace*>& traces,
+                     const std::vector<EngineConfig>& cfgs, TimeUs horizon, int device)
+    : impl_(nullptr) {
+  if (traces.size() != cfgs.size()) throw UsageError("NodeBatch: one config per trace");
+  Impl* m = new Impl(device);
+  try {
+    m->traces = traces;
+    for (size_t i = 0; i < traces.size(); ++i) {
+      fb_instance x{};
+      x.cfg = to_c(cfgs[i]);
+      x.trace_off = static_cast<int64_t>(m->rows.arrival.size());
+      x.n_req = static_cast<int64_t>(traces[i]->requests.size());
+      x.horizon_us = horizon;
+      m->inst.push_back(x);
+      m->rows.add(*traces[i]);
+    }
+    const fb_trace tr = m->rows.c();
+    check(fb_arena_load(m->a.a, &tr, m->inst.data(), static_cast<int64_t>(m->inst.size()),
+                        nullptr));
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  impl_ = m;
+}
+
+NodeBatch::~NodeBatch() { delete impl_; }
+
+std::int64_t NodeBatch::step(std::int64_t max_events) {
+  if (max_events < 1) throw UsageError("NodeBatch::step: max_events must be >= 1");
+  int64_t active = 0;
+  check(fb_arena_run(impl_->a.a, max_events, &active));
+  return active;
+}
+
+void NodeBatch::run() { check(fb_arena_run(impl_->a.a, 0, nullptr)); }
+
+std::vector<NodeSummary> NodeBatch::summaries() const {
+  std::vector<fb_instance_result> res(impl_->inst.size());
+  check(fb_arena_fetch_results(impl_->a.a, res.data()));
+  std::vector<NodeSummary> out;
+  for (const fb_instance_result& r : res) {
+    check(r.status);
+    out.push_back({r.steps, r.plan_digest, r.n_arrived, r.n_rejected, r.incomplete != 0});
+  }
+  return out;
+}
+
+std::vector<std::vector<RequestReport>> NodeBatch::reports() const {
+  std::vector<fb_record> rec(static_cast<size_t>(std::max<int64_t>(fb_arena_record_rows(impl_->a.a), 1)));
+  check(fb_arena_fetch_records(impl_->a.a, rec.data()));
+  std::vector<std::vector<RequestReport>> out;
+  for (size_t i = 0; i < impl_->traces.size(); ++i) {
+    const Trace& t = *impl_->traces[i];
+    std::vector<RequestReport> v;
+    for (size_t q = 0; q < t.requests.size(); ++q)
+      v.push_back(report_from_record(t.requests[q], rec[impl_->inst[i].trace_off + q]));
+    out.push_back(std::move(v));
+  }
+  return out;
+}
+
 // ----------------------------------------------------------------- reports
 
 double RequestReport::ttft_ms() const {
@@ -538,7 +610,8 @@ ClusterResult run_cluster(const Trace& trace, const std::vector<EngineConfig>& n
                        res.data(), rec.data(), route.data(), &inc, &out.device_ms));
   out.incomplete = inc != 0;
   for (size_t i = 0; i < nn; ++i)
-    out.nodes.push_back({res[i].steps, res[i].plan_digest, res[i].n_arrived, res[i].n_rejected});
+    out.nodes.push_back({res[i].steps, res[i].plan_digest, res[i].n_arrived, res[i].n_rejected,
+                         res[i].incomplete != 0});
   for (size_t q = 0; q < nr; ++q) {
     if (route[q] < 0) continue;
     const Request& r = trace.requests[q];

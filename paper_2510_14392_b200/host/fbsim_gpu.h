@@ -183,7 +183,38 @@ std::vector<EventLog> run_nodes(const std::vector<const Trace*>& traces,
                                 const std::vector<EngineConfig>& cfgs, TimeUs horizon,
                                 int device = 0);
 
+// The step machine, batched: many nodes (one per trace) resident on the
+// device, advanced together by step(max_events) -- max_events iterations of
+// each node's run_node event loop (engine.cpp:271-283: complete the step in
+// flight, enqueue the arrivals at t, begin_step) -- until every node is
+// quiescent.  reports() / summaries() read the current state at any point.
+struct NodeSummary;
+struct RequestReport;
+class NodeBatch {
+ public:
+  NodeBatch(const std::vector<const Trace*>& traces, const std::vector<EngineConfig>& cfgs,
+            TimeUs horizon, int device = 0);
+  ~NodeBatch();
+  NodeBatch(const NodeBatch&) = delete;
+  NodeBatch& operator=(const NodeBatch&) = delete;
+  // Returns the number of nodes still running (0: all quiescent).
+  std::int64_t step(std::int64_t max_events = 1);
+  void run();  // to quiescence
+  std::vector<NodeSummary> summaries() const;
+  // Per node, one RequestReport per request of its trace (in trace order).
+  std::vector<std::vector<RequestReport>> reports() const;
+
+ private:
+  struct Impl;
+  Impl* impl_;
+};
+
 // --------------------------------------------------------------- metrics.h
+struct NodeSummary {
+  std::uint64_t steps = 0, plan_digest = 0;  // steps_completed; rolling plan digest
+  std::int64_t n_arrived = 0, n_rejected = 0;
+  bool incomplete = false;
+};
 struct RequestReport {
   std::int64_t req_id = -1;
   TimeUs arrival = 0;
@@ -222,10 +253,7 @@ struct RoutingLogEntry {
   std::int64_t req_id = -1;
   int node = 0;  // the node the request was (last) routed to
 };
-struct NodeSummary {
-  std::uint64_t steps = 0, plan_digest = 0;
-  std::int64_t n_arrived = 0, n_rejected = 0;
-};
+
 struct ClusterResult {
   std::vector<RoutingLogEntry> routing;
   std::vector<RequestReport> reports;  // every routed request, by id

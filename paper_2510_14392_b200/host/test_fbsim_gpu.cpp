@@ -199,6 +199,30 @@ static int run_kat() {
     bad.requests.push_back(make_request(0, 0.0, 0, 3));  // prompt_len must be >= 1
     run_node(bad, node_config(Policy::kFairBatch), 1000);
   }));
+  // the step machine: one event-loop iteration per step() reaches the same
+  // state as a run to quiescence
+  {
+    NodeBatch nb({&t1, &t2, &t3},
+                 {node_config(Policy::kFairBatch), node_config(Policy::kFairBatchPab),
+                  node_config(Policy::kSarathi, 512, 256)},
+                 ms_to_us(60000.0));
+    int calls = 0;
+    while (nb.step(1) > 0) ++calls;
+    CHECK(calls >= 3);
+    NodeBatch all({&t1, &t2, &t3},
+                  {node_config(Policy::kFairBatch), node_config(Policy::kFairBatchPab),
+                   node_config(Policy::kSarathi, 512, 256)},
+                  ms_to_us(60000.0));
+    all.run();
+    const std::vector<NodeSummary> a = nb.summaries(), b2 = all.summaries();
+    CHECK(a.size() == 3 && a[0].steps == 3 && a[1].n_rejected == 1);
+    for (size_t i = 0; i < a.size(); ++i)
+      CHECK(a[i].plan_digest == b2[i].plan_digest && a[i].steps == b2[i].steps);
+    const auto rp = nb.reports();
+    CHECK(rp[0][0].finished && std::fabs(rp[0][0].ttft_ms() - 6.0) < 1e-12);
+    CHECK(rp[1][0].rejected && rp[1][1].finished);
+    CHECK(throws<UsageError>([&] { nb.step(0); }));
+  }
   CHECK(throws<ValidationError>([&] {  // Node ctor: validate_scheduler_config
     run_node(t1, node_config(Policy::kFairBatch, 100, 256), 1000);  // budget < max_chunk
   }));
