@@ -377,6 +377,14 @@ int fb_run_batch(int device, const fb_trace* rows, const fb_instance* instances,
 /* Cluster: run_cluster (cluster.h:107-109) on the device.                 */
 /* ---------------------------------------------------------------------- */
 
+/* One routing decision (RoutingLogEntry, cluster.h:86-91; its view snapshot
+ * is a separate row of n_nodes doubles). */
+typedef struct fb_route_log {
+  int64_t t_us;  /* decision time */
+  int32_t req;   /* trace row */
+  int32_t node;  /* target */
+} fb_route_log;
+
 /* LbConfig, cluster.h:36-47. */
 typedef struct fb_lb_config {
   int32_t policy;                /* FB_LB_COUNT / FB_LB_PAB */
@@ -399,6 +407,22 @@ int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* nod
                    int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
                    fb_instance_result* node_results, fb_record* records,
                    int32_t* route_node, int32_t* incomplete_out, double* device_ms_out);
+
+/* fb_run_cluster plus the logs ClusterResult carries (cluster.h:93-98): each
+ * node's plan log (steps / entries / rejects at node i * cap, counts per
+ * node; the node's EventLog is rebuilt from it and the routing log) and the
+ * routing log -- one fb_route_log per route_request call (reroutes
+ * included) and, in `snapshots`, n_nodes doubles per entry: the balancer's
+ * per-node score after the decision (RoutingLogEntry::view_snapshot).
+ * *n_routes_out receives the entry count; FB_ERR_CAPACITY when it exceeds
+ * route_cap (n_rows suffices without retry_reroute, 2 * n_rows with it). */
+int fb_run_cluster_logged(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                          int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                          const fb_log_opts* log, fb_instance_result* node_results,
+                          fb_record* records, int32_t* route_node, int32_t* incomplete_out,
+                          fb_log_counts* node_counts, fb_step_log* steps, fb_plan_entry* entries,
+                          fb_reject_log* rejects, fb_route_log* routes, double* snapshots,
+                          int64_t route_cap, int64_t* n_routes_out);
 
 /* ---------------------------------------------------------------------------
  * Multi-GPU cluster: the nodes are partitioned over n_ranks processes (one

@@ -453,6 +453,54 @@ int ref_event_log(const fb_trace* rows, const fb_instance* inst, const char* tmp
   }
 }
 
+// The real run_cluster's outputs in the reference's own file formats: every
+// node's save_event_log JSONL, then save_routing_log's JSONL (with the view
+// snapshots), concatenated into buf; offsets[0..n_nodes+1] delimit them.
+int ref_cluster_logs(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                     const fb_lb_config* lbc, int64_t horizon, const char* tmp_path, char* buf,
+                     int64_t cap, int64_t* offsets, int64_t* len_out) {
+  try {
+    fb_instance whole{};
+    whole.trace_off = 0;
+    whole.n_req = rows->n_rows;
+    const Trace tr = instance_trace(rows, whole);
+    LbConfig lb;
+    lb.policy = lbc->policy == FB_LB_PAB ? LbPolicy::kPabLb : LbPolicy::kCountLb;
+    lb.report_interval_steps = lbc->report_interval_steps;
+    lb.report_latency = lbc->report_latency_us;
+    lb.w_waiting = lbc->w_waiting;
+    lb.w_running = lbc->w_running;
+    lb.retry_reroute = lbc->retry_reroute != 0;
+    std::vector<EngineConfig> ecfg;
+    for (int i = 0; i < n_nodes; ++i) ecfg.push_back(to_engine(cfgs[i]));
+    const ClusterResult res = run_cluster(tr, ecfg, lb, horizon);
+    auto slurp = [&](std::string& out) {
+      FILE* f = std::fopen(tmp_path, "rb");
+      if (!f) throw ParseError("cannot reopen log");
+      char tmp[65536];
+      size_t k;
+      while ((k = std::fread(tmp, 1, sizeof(tmp), f)) > 0) out.append(tmp, k);
+      std::fclose(f);
+    };
+    std::string all;
+    offsets[0] = 0;
+    for (int i = 0; i < n_nodes; ++i) {
+      save_event_log(res.node_logs[static_cast<size_t>(i)], tmp_path);
+      slurp(all);
+      offsets[i + 1] = static_cast<int64_t>(all.size());
+    }
+    save_routing_log(res.routing, lb.policy, tmp_path);
+    slurp(all);
+    offsets[n_nodes + 1] = static_cast<int64_t>(all.size());
+    *len_out = static_cast<int64_t>(all.size());
+    if (*len_out > cap) return fail(FB_ERR_CAPACITY, "buffer too small");
+    std::memcpy(buf, all.data(), all.size());
+    return FB_OK;
+  } catch (const std::exception& e) {
+    return map_exception(e);
+  }
+}
+
 // The reference's own load_event_log + replay_check (engine.cpp:290-393,
 // 453-520) of a JSONL file: the violations joined by '\n' into buf.
 int ref_replay_check(const char* path, char* buf, int64_t cap, int64_t* len_out,

@@ -240,6 +240,7 @@ REJECT_DTYPE = np.dtype([("t_us", "<i8"), ("pab_tokens", "<i8"), ("req", "<i4"),
                          ("reserved", "<i4")], align=True)
 LOGCOUNT_DTYPE = np.dtype([("steps", "<i4"), ("entries", "<i4"), ("rejects", "<i4"),
                            ("truncated", "<i4")], align=True)
+ROUTELOG_DTYPE = np.dtype([("t_us", "<i8"), ("req", "<i4"), ("node", "<i4")], align=True)
 TASKVIEW_DTYPE = np.dtype(
     [("request_id", "<i8"), ("slack_us", "<i8"), ("context", "<i8"), ("arrival_seq", "<i8"),
      ("tpot_us", "<i8"), ("new_tokens", "<i4"), ("phase", "<i4")], align=True)

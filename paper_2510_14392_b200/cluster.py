@@ -215,6 +215,56 @@ def run_cluster_dist(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, dist,
     return merge_shards(parts, len(cfgs))
 
 
+@dataclass
+class ClusterLogs:
+    """run_cluster's logs (ClusterResult, cluster.h:93-98): per node the plan
+    log its EventLog is rebuilt from, and the routing log with the view
+    snapshot of every decision (events.cluster_event_logs writes both in the
+    reference's JSONL formats)."""
+    out: ClusterOutput
+    counts: np.ndarray     # LOGCOUNT_DTYPE per node
+    steps: np.ndarray      # [node, step_cap] STEPLOG_DTYPE
+    entries: np.ndarray    # [node, entry_cap] ENTRY_DTYPE
+    rejects: np.ndarray    # [node, reject_cap] REJECT_DTYPE
+    routes: np.ndarray     # ROUTELOG_DTYPE, decision order
+    snapshots: np.ndarray  # [decision, node] float64
+
+
+def run_cluster_logged(rows: Rows, cfgs, lb: LbConfig, horizon_us: int,
+                       device: int = 0) -> ClusterLogs:
+    """fb_run_cluster_logged; the plan-log capacities come from a first
+    (unlogged) run of the same cluster, so nothing is truncated."""
+    L = fbgpu.lib()
+    first = run_cluster(rows, cfgs, lb, horizon_us, device)
+    nr = first.node_results
+    lo = _abi.LogOpts(max(1, int(nr["steps"].max())), max(1, int(nr["sum_entries"].max())),
+                      max(1, int(nr["n_rejected"].max())), 0)
+    n, m = len(cfgs), len(rows)
+    tr = rows.to_c()
+    nc = node_configs_c(cfgs)
+    lbc = lb.to_c()
+    res = np.zeros(max(1, n), _abi.RESULT_DTYPE)
+    rec = np.zeros(max(1, m), _abi.RECORD_DTYPE)
+    route = np.zeros(max(1, m), np.int32)
+    inc = C.c_int32(0)
+    counts = np.zeros(max(1, n), _abi.LOGCOUNT_DTYPE)
+    steps = np.zeros((n, lo.step_cap), _abi.STEPLOG_DTYPE)
+    entries = np.zeros((n, lo.entry_cap), _abi.ENTRY_DTYPE)
+    rejects = np.zeros((n, lo.reject_cap), _abi.REJECT_DTYPE)
+    cap = 2 * m + 1 if lb.retry_reroute else m + 1
+    routes = np.zeros(cap, _abi.ROUTELOG_DTYPE)
+    snaps = np.zeros((cap, n), np.float64)
+    nrt = C.c_int64(0)
+    fbgpu._check(L.fb_run_cluster_logged(
+        device, C.byref(tr), C.cast(nc, C.c_void_p), n, C.byref(lbc), int(horizon_us),
+        C.byref(lo), _abi.vptr(res), _abi.vptr(rec), _abi.vptr(route), C.byref(inc),
+        _abi.vptr(counts), _abi.vptr(steps), _abi.vptr(entries), _abi.vptr(rejects),
+        _abi.vptr(routes), _abi.vptr(snaps), cap, C.byref(nrt)), "fb_run_cluster_logged")
+    out = ClusterOutput(res[:n], rec[:m], route[:m], inc.value, 0.0)
+    k = nrt.value
+    return ClusterLogs(out, counts[:n], steps, entries, rejects, routes[:k], snaps[:k])
+
+
 def run_clusters(cases, device: int = 0) -> list[ClusterOutput]:
     """Independent cluster simulations at once -- one one-rank shard per case,
     each on its own stream, so their persistent cluster kernels (a few CTAs

@@ -740,6 +740,8 @@ struct fb_cluster_shard {
   int64_t* d_out = nullptr;
   int32_t* d_route = nullptr;
   uint8_t* d_row_state = nullptr;  // retry_reroute: bit 0 retried, bit 1 ever rejected
+  fb_route_log* d_rlog = nullptr;  // routing log + view snapshots (logged runs)
+  double* d_rsnap = nullptr;
   ~fb_cluster_shard() {
     if (a) cudaSetDevice(a->device);
     for (void* p : opened) cudaIpcCloseMemHandle(p);
@@ -763,9 +765,24 @@ int fb_cluster_partition(int32_t n_nodes, int32_t n_ranks, int32_t rank, int32_t
 }
 
 // run_cluster (cluster.cpp:134-251) for the nodes of one rank (fb_cluster.cuh).
+static int shard_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                        int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                        int32_t rank, int32_t n_ranks, const fb_log_opts* log,
+                        fb_cluster_shard** out);
+
 int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
                             int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
                             int32_t rank, int32_t n_ranks, fb_cluster_shard** out) {
+  return shard_create(device, rows, node_cfgs, n_nodes, lb, horizon_us, rank, n_ranks, nullptr,
+                      out);
+}
+
+}  // extern "C"
+
+static int shard_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                        int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                        int32_t rank, int32_t n_ranks, const fb_log_opts* log,
+                        fb_cluster_shard** out) {
   if (!out) return set_error(FB_ERR_USAGE, "fb_cluster_shard_create: null output");
   *out = nullptr;
   if (!rows || !node_cfgs || !lb) return set_error(FB_ERR_USAGE, "fb_run_cluster: null argument");
@@ -814,7 +831,7 @@ int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_co
   sh->n_local = nl;
   sh->nr = nr;
   if ((st = fb_arena_create(device, nullptr, &sh->a))) return st;
-  if ((st = fb_arena_load(sh->a, rows, inst.data(), nl, nullptr))) return st;
+  if ((st = fb_arena_load(sh->a, rows, inst.data(), nl, log))) return st;
   const int cap = lb->report_cap > 0 ? lb->report_cap : 4096;
   auto dalloc = [&](void** p, size_t bytes) -> cudaError_t {
     cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
@@ -885,6 +902,14 @@ int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_co
   cp.fifo_cap = static_cast<int32_t>(fifo_cap);
   cp.fifo = d_fifo;
   cp.row_state = sh->d_row_state;
+  if (log) {  // routing log: one entry per route_request call
+    const int64_t cap = lb->retry_reroute ? 2 * nr + 1 : nr + 1;
+    FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_rlog), sizeof(fb_route_log) * cap));
+    FB_CUDA(dalloc(reinterpret_cast<void**>(&sh->d_rsnap), sizeof(double) * cap * n_nodes));
+    cp.rlog = sh->d_rlog;
+    cp.rsnap = sh->d_rsnap;
+    cp.rlog_cap = cap;
+  }
   if (fbgpu::cluster_param_bytes() != sizeof(cp))
     return set_error(FB_ERR_USAGE, "cluster parameter layout mismatch");
   if (n_ranks == 1) {
@@ -895,6 +920,8 @@ int fb_cluster_shard_create(int device, const fb_trace* rows, const fb_engine_co
   sh = nullptr;
   return FB_OK;
 }
+
+extern "C" {
 
 int fb_cluster_shard_exchange_handle(fb_cluster_shard* s, void* handle_out) {
   if (!s || !handle_out) return set_error(FB_ERR_USAGE, "fb_cluster_shard_exchange_handle: bad arguments");
@@ -1064,6 +1091,50 @@ int fb_cluster_shard_fetch(fb_cluster_shard* s, fb_instance_result* local_result
 }
 
 void fb_cluster_shard_destroy(fb_cluster_shard* s) { delete s; }
+
+// run_cluster with its logs: every node's plan log (for its EventLog) and
+// the routing log with view snapshots (ClusterResult::routing).
+int fb_run_cluster_logged(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                          int32_t n_nodes, const fb_lb_config* lb, int64_t horizon_us,
+                          const fb_log_opts* log, fb_instance_result* node_results,
+                          fb_record* records, int32_t* route_node, int32_t* incomplete_out,
+                          fb_log_counts* node_counts, fb_step_log* steps, fb_plan_entry* entries,
+                          fb_reject_log* rejects, fb_route_log* routes, double* snapshots,
+                          int64_t route_cap, int64_t* n_routes_out) {
+  if (!log || log->step_cap < 1 || log->entry_cap < 1 || log->reject_cap < 1)
+    return set_error(FB_ERR_USAGE, "fb_run_cluster_logged: log capacities must be >= 1");
+  fb_cluster_shard* s = nullptr;
+  int st = shard_create(device, rows, node_cfgs, n_nodes, lb, horizon_us, 0, 1, log, &s);
+  if (st) return st;
+  struct Drop {
+    fb_cluster_shard* p;
+    ~Drop() { fb_cluster_shard_destroy(p); }
+  } drop{s};
+  if ((st = fb_cluster_shard_reset(s)) || (st = fb_cluster_shard_launch(s)) ||
+      (st = fb_cluster_shard_wait(s, nullptr)))
+    return st;
+  if ((st = fb_cluster_shard_fetch(s, node_results, records, route_node, nullptr, incomplete_out)))
+    return st;
+  fb_arena* a = s->a;
+  if (node_counts && (st = fb_arena_fetch_log_counts(a, node_counts))) return st;
+  for (int32_t i = 0; i < n_nodes; ++i) {
+    st = fb_arena_fetch_log(a, i, steps ? steps + static_cast<int64_t>(i) * log->step_cap : nullptr,
+                            entries ? entries + static_cast<int64_t>(i) * log->entry_cap : nullptr,
+                            rejects ? rejects + static_cast<int64_t>(i) * log->reject_cap : nullptr);
+    if (st) return st;
+  }
+  int64_t out[4] = {0, 0, 0, 0};
+  FB_CUDA(cudaMemcpy(out, s->d_out, sizeof(out), cudaMemcpyDeviceToHost));
+  const int64_t n = out[3];
+  if (n_routes_out) *n_routes_out = n;
+  if (n > route_cap) return set_error(FB_ERR_CAPACITY, "fb_run_cluster_logged: route_cap too small");
+  if (routes && n > 0)
+    FB_CUDA(cudaMemcpy(routes, s->d_rlog, sizeof(fb_route_log) * n, cudaMemcpyDeviceToHost));
+  if (snapshots && n > 0)
+    FB_CUDA(cudaMemcpy(snapshots, s->d_rsnap, sizeof(double) * n * n_nodes,
+                       cudaMemcpyDeviceToHost));
+  return FB_OK;
+}
 
 // run_cluster (cluster.cpp:134-251) on one GPU: a one-rank shard.
 int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,

@@ -64,6 +64,9 @@ struct ClusterParams {
   int32_t retry_reroute, fifo_cap;    // serial engine (retry_reroute)
   int64_t* fifo;                      // [fifo_cap * 6] in-flight reports
   uint8_t* row_state;                 // [n_rows] bit 0 retried, bit 1 ever rejected
+  fb_route_log* rlog;                 // routing log (NULL: off)
+  double* rsnap;                      // per entry the view snapshot, [rlog_cap * n_nodes]
+  int64_t rlog_cap;
 };
 
 // Router view (replicated per CTA) + the CTA's routing results.
@@ -312,7 +315,8 @@ __device__ __forceinline__ bool cluster_stopped(const ClusterParams& C, const No
 // prompt (else overall), count_lb the smallest weighted count; ties to the
 // lowest node id.  Updates the view's local decrements.  Returns the node.
 __device__ __forceinline__ int cluster_pick(const ClusterParams& C, RouterSmem& rs,
-                                            int64_t prompt) {
+                                            int64_t prompt, int64_t log_k = -1, int64_t t = 0,
+                                            int64_t row = 0) {
   const int n = C.n_nodes;
   int chosen;
   if (C.lb_policy == FB_LB_PAB) {
@@ -373,6 +377,24 @@ __device__ __forceinline__ int cluster_pick(const ClusterParams& C, RouterSmem& 
     if (lane_id() == 0) rs.v_inc[chosen] += 1;
   }
   __syncwarp();
+  if (log_k >= 0 && C.rlog && log_k < C.rlog_cap) {
+    // route_request's routing-log entry (cluster.cpp:171-175): the view
+    // snapshot taken after the decision's decrement / increment
+    for (int i = lane_id(); i < n; i += kWarp) {
+      C.rsnap[log_k * n + i] =
+          C.lb_policy == FB_LB_PAB
+              ? static_cast<double>(rs.v_pab[i] - rs.v_dec[i])
+              : dadd(dmul(C.w_waiting, static_cast<double>(rs.v_wait[i] + rs.v_inc[i])),
+                     dmul(C.w_running, static_cast<double>(rs.v_run[i])));
+    }
+    if (lane_id() == 0) {
+      fb_route_log& e = C.rlog[log_k];
+      e.t_us = t;
+      e.req = static_cast<int32_t>(row);
+      e.node = chosen;
+    }
+    __syncwarp();
+  }
   return chosen;
 }
 
@@ -399,7 +421,7 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
   }
   __syncwarp();
   for (int64_t q = C.epoch_lo[e]; q < C.epoch_lo[e + 1]; ++q) {
-    const int chosen = cluster_pick(C, rs, P.prompt[q]);
+    const int chosen = cluster_pick(C, rs, P.prompt[q], blockIdx.x == 0 ? q : -1, C.epoch_t[e], q);
     if (lane_id() == 0) {
       if (blockIdx.x == 0) C.route_node[q] = chosen;
       const int k = chosen - node_base;  // Node::enqueue, on the owning CTA
@@ -488,6 +510,7 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     if (blockIdx.x == 0) {
       C.out[0] = e < C.n_epochs ? C.epoch_lo[e] : C.n_rows;
       C.out[2] = e;
+      C.out[3] = C.out[0];  // routing-log entries: one per routed request
     }
   }
 }
@@ -506,6 +529,7 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
 struct SerialSmem {
   RouterSmem rs;
   int64_t n_routed[kClusterMaxNodes];  // routed-list length per node
+  int64_t n_log;                       // routing-log entries
 };
 
 // The node's warp-uniform state, loaded from P.state (the memory path keeps
@@ -545,8 +569,10 @@ __device__ void serial_report(const EngineParams& P, const ClusterParams& C, Clu
 
 // route_request (cluster.cpp:171-175): pick, log the target, Node::enqueue.
 __device__ __forceinline__ void serial_route(const EngineParams& P, const ClusterParams& C,
-                                             SerialSmem& ss, int64_t row) {
-  const int chosen = cluster_pick(C, ss.rs, P.prompt[row]);
+                                             SerialSmem& ss, int64_t row, int64_t t) {
+  const int chosen = cluster_pick(C, ss.rs, P.prompt[row], ss.n_log, t, row);
+  __syncwarp();
+  if (lane_id() == 0) ss.n_log++;
   if (lane_id() == 0) {
     C.route_node[row] = chosen;
     const int64_t j = ss.n_routed[chosen];
@@ -570,6 +596,7 @@ cluster_serial_kernel(const __grid_constant__ EngineParams P,
     rs.v_pab[i] = rs.v_wait[i] = rs.v_run[i] = rs.v_dec[i] = rs.v_inc[i] = 0;
     ss.n_routed[i] = 0;
   }
+  if (lane_id() == 0) ss.n_log = 0;
   __syncwarp();
   int32_t status = FB_OK;
   int64_t head = 0, tail = 0;
@@ -618,7 +645,7 @@ cluster_serial_kernel(const __grid_constant__ EngineParams P,
       ++head;
     }
     // 3) arrivals at exactly t, in trace order
-    for (; arr < C.n_rows && P.arrival[arr] == t; ++arr) serial_route(P, C, ss, arr);
+    for (; arr < C.n_rows && P.arrival[arr] == t; ++arr) serial_route(P, C, ss, arr, t);
     // 4) begin_step on idle nodes; a first rejection is routed again at once
     if (t < C.horizon) {
       bool progress = true;
@@ -648,7 +675,7 @@ cluster_serial_kernel(const __grid_constant__ EngineParams P,
             if (lane_id() == 0) C.row_state[row] = rsv | 3;
             __syncwarp();
             if (!(rsv & 1) && C.retry_reroute) {
-              serial_route(P, C, ss, row);
+              serial_route(P, C, ss, row, t);
               progress = true;
             }
           }
@@ -671,6 +698,7 @@ cluster_serial_kernel(const __grid_constant__ EngineParams P,
     C.out[0] = arr;
     C.out[1] = status;
     C.out[2] = iters;
+    C.out[3] = ss.n_log;
   }
 }
 

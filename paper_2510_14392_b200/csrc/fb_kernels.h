@@ -140,6 +140,9 @@ struct ClusterParamsHost {
   int32_t retry_reroute, fifo_cap;
   int64_t* fifo;
   uint8_t* row_state;
+  fb_route_log* rlog;  // routing log (NULL: off), [rlog_cap]
+  double* rsnap;       // its view snapshots, [rlog_cap * n_nodes]
+  int64_t rlog_cap;
 };
 size_t cluster_param_bytes();
 int cluster_max_nodes();

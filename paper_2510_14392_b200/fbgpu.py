@@ -113,6 +113,11 @@ def lib() -> C.CDLL:
         "fb_run_cluster": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,
                                      C.POINTER(_abi.LbConfig), i64, vp, vp, vp,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+        "fb_run_cluster_logged": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,
+                                            C.POINTER(_abi.LbConfig), i64,
+                                            C.POINTER(_abi.LogOpts), vp, vp, vp,
+                                            C.POINTER(C.c_int32), vp, vp, vp, vp, vp, vp, i64,
+                                            C.POINTER(C.c_int64)]),
         "fb_cluster_partition": (C.c_int, [i32, i32, i32, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_int32)]),
         "fb_cluster_shard_create": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,

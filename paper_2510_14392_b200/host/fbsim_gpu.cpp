@@ -106,12 +106,11 @@ struct Arena {
 // plan order, then batch_end) at its end.  Within one timestamp run_node
 // appends completions, then arrivals, then rejects, then the batch start
 // (engine.cpp:271-283).
-EventLog build_log(const Trace& tr, const fb_instance_result& res, const fb_log_counts& cnt,
-                   const std::vector<fb_step_log>& steps,
-                   const std::vector<fb_plan_entry>& entries,
-                   const std::vector<fb_reject_log>& rejects) {
+// arrivals: (visible_at, trace row) in enqueue order.
+EventLog build_log(const Trace& tr, const std::vector<std::pair<TimeUs, int64_t>>& arrivals,
+                   bool incomplete, const fb_log_counts& cnt, const fb_step_log* steps,
+                   const fb_plan_entry* entries, const fb_reject_log* rejects) {
   if (cnt.truncated) throw CudaError("plan log truncated");
-  const int64_t n_arr = res.n_arrived;
   struct Item {
     TimeUs t;
     int phase;
@@ -119,10 +118,11 @@ EventLog build_log(const Trace& tr, const fb_instance_result& res, const fb_log_
     Event e;
   };
   std::vector<Item> items;
-  for (int64_t r = 0; r < n_arr; ++r) {
+  for (size_t k = 0; k < arrivals.size(); ++k) {
+    const int64_t r = arrivals[k].second;
     const Request& q = tr.requests[static_cast<size_t>(r)];
     Event e;
-    e.t = q.arrival;
+    e.t = arrivals[k].first;
     e.kind = EventKind::kArrival;
     e.req_id = q.id;
     e.arrival = q.arrival;
@@ -130,7 +130,7 @@ EventLog build_log(const Trace& tr, const fb_instance_result& res, const fb_log_
     e.output_len = q.output_len;
     e.ttft_slo = q.ttft_slo;
     e.tpot_slo = q.tpot_slo;
-    items.push_back({e.t, 1, r, 0, e});
+    items.push_back({e.t, 1, static_cast<int64_t>(k), 0, e});
   }
   for (int32_t k = 0; k < cnt.rejects; ++k) {
     const fb_reject_log& rj = rejects[static_cast<size_t>(k)];
@@ -142,7 +142,7 @@ EventLog build_log(const Trace& tr, const fb_instance_result& res, const fb_log_
     e.pab_tokens = rj.pab_tokens;
     items.push_back({e.t, 2, k, 0, e});
   }
-  std::vector<int64_t> prefilled(static_cast<size_t>(std::max<int64_t>(n_arr, 1)), 0);
+  std::vector<int64_t> prefilled(std::max<size_t>(tr.requests.size(), 1), 0);
   std::vector<int32_t> nidx(prefilled.size(), 0);
   for (int32_t s = 0; s < cnt.steps; ++s) {
     const fb_step_log& st = steps[static_cast<size_t>(s)];
@@ -190,7 +190,7 @@ EventLog build_log(const Trace& tr, const fb_instance_result& res, const fb_log_
     return std::tie(x.t, x.phase, x.order, x.sub) < std::tie(y.t, y.phase, y.order, y.sub);
   });
   EventLog log;
-  log.incomplete = res.incomplete != 0;
+  log.incomplete = incomplete;
   log.events.reserve(items.size());
   for (const Item& it : items) log.events.push_back(it.e);
   return log;
@@ -377,7 +377,11 @@ std::vector<EventLog> run_nodes(const std::vector<const Trace*>& traces,
   for (int64_t i = 0; i < n; ++i) {
     check(res[i].status);
     check(fb_arena_fetch_log(a.a, i, steps.data(), entries.data(), rejects.data()));
-    logs.push_back(build_log(*traces[i], res[i], cnt[i], steps, entries, rejects));
+    std::vector<std::pair<TimeUs, int64_t>> arrivals;
+    for (int64_t r = 0; r < res[i].n_arrived; ++r)
+      arrivals.push_back({traces[i]->requests[static_cast<size_t>(r)].arrival, r});
+    logs.push_back(build_log(*traces[i], arrivals, res[i].incomplete != 0, cnt[i], steps.data(),
+                             entries.data(), rejects.data()));
   }
   return logs;
 }
@@ -606,19 +610,79 @@ ClusterResult run_cluster(const Trace& trace, const std::vector<EngineConfig>& n
   std::vector<int32_t> route(std::max<size_t>(nr, 1));
   int32_t inc = 0;
   ClusterResult out;
+  // pass 1 sizes the node plan logs, pass 2 records them with the routing log
   check(fb_run_cluster(device, &tr, cfgs.data(), static_cast<int32_t>(nn), &l, horizon,
                        res.data(), rec.data(), route.data(), &inc, &out.device_ms));
+  fb_log_opts lo{1, 1, 1, 0};
+  for (size_t i = 0; i < nn; ++i) {
+    lo.step_cap = std::max<int32_t>(lo.step_cap, static_cast<int32_t>(res[i].steps));
+    lo.entry_cap = std::max<int32_t>(lo.entry_cap, static_cast<int32_t>(res[i].sum_entries));
+    lo.reject_cap = std::max<int32_t>(lo.reject_cap, static_cast<int32_t>(res[i].n_rejected));
+  }
+  std::vector<fb_log_counts> cnt(std::max<size_t>(nn, 1));
+  std::vector<fb_step_log> steps(nn * lo.step_cap);
+  std::vector<fb_plan_entry> entries(nn * lo.entry_cap);
+  std::vector<fb_reject_log> rejects(nn * lo.reject_cap);
+  const int64_t cap = static_cast<int64_t>(lb.retry_reroute ? 2 * nr + 1 : nr + 1);
+  std::vector<fb_route_log> routes(static_cast<size_t>(cap));
+  std::vector<double> snaps(static_cast<size_t>(cap) * nn);
+  int64_t n_routes = 0;
+  check(fb_run_cluster_logged(device, &tr, cfgs.data(), static_cast<int32_t>(nn), &l, horizon,
+                              &lo, res.data(), rec.data(), route.data(), &inc, cnt.data(),
+                              steps.data(), entries.data(), rejects.data(), routes.data(),
+                              snaps.data(), cap, &n_routes));
   out.incomplete = inc != 0;
   for (size_t i = 0; i < nn; ++i)
     out.nodes.push_back({res[i].steps, res[i].plan_digest, res[i].n_arrived, res[i].n_rejected,
                          res[i].incomplete != 0});
-  for (size_t q = 0; q < nr; ++q) {
-    if (route[q] < 0) continue;
-    const Request& r = trace.requests[q];
-    out.routing.push_back({r.arrival, r.id, route[q]});
-    out.reports.push_back(report_from_record(r, rec[q]));
+  for (int64_t k = 0; k < n_routes; ++k) {
+    const fb_route_log& e = routes[static_cast<size_t>(k)];
+    RoutingLogEntry r;
+    r.t = e.t_us;
+    r.req_id = trace.requests[static_cast<size_t>(e.req)].id;
+    r.node = e.node;
+    r.view_snapshot.assign(snaps.begin() + k * nn, snaps.begin() + (k + 1) * nn);
+    out.routing.push_back(std::move(r));
+  }
+  for (size_t q = 0; q < nr; ++q)
+    if (route[q] >= 0) out.reports.push_back(report_from_record(trace.requests[q], rec[q]));
+  // each node's EventLog: its arrivals are the requests routed to it; with
+  // retry_reroute a rerouted arrival's place among a node's events of one
+  // instant is not recorded, so node logs are left empty there
+  if (!lb.retry_reroute) {
+    for (size_t i = 0; i < nn; ++i) {
+      std::vector<std::pair<TimeUs, int64_t>> arrivals;
+      for (int64_t k = 0; k < n_routes; ++k)
+        if (routes[static_cast<size_t>(k)].node == static_cast<int32_t>(i))
+          arrivals.push_back({routes[static_cast<size_t>(k)].t_us, routes[static_cast<size_t>(k)].req});
+      EventLog log = build_log(trace, arrivals, out.incomplete, cnt[i], steps.data() + i * lo.step_cap,
+                               entries.data() + i * lo.entry_cap, rejects.data() + i * lo.reject_cap);
+      log.node_id = static_cast<int>(i);
+      out.node_logs.push_back(std::move(log));
+    }
   }
   return out;
+}
+
+const char* lb_policy_name(LbPolicy p) { return p == LbPolicy::kPabLb ? "pab_lb" : "count_lb"; }
+
+void save_routing_log(const std::vector<RoutingLogEntry>& log, LbPolicy policy,
+                      const std::string& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw ParseError("cannot open for writing: " + path);
+  char buf[256];
+  for (const RoutingLogEntry& e : log) {
+    std::snprintf(buf, sizeof(buf),
+                  "{\"t_ms\":%.3f,\"req_id\":%" PRId64 ",\"node\":%d,\"policy\":\"%s\","
+                  "\"view_snapshot\":[",
+                  us_to_ms(e.t), e.req_id, e.node, lb_policy_name(policy));
+    out << buf;
+    for (size_t i = 0; i < e.view_snapshot.size(); ++i) {
+      std::snprintf(buf, sizeof(buf), "%s%.3f", i ? "," : "", e.view_snapshot[i]);
+      out << buf;
+    }
+    out << "]}\n";
+  }
 }
 
 }  // namespace fbsim_gpu

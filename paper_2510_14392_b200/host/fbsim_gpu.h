@@ -12,9 +12,9 @@
 // Differences from fbsim, by design:
 //   * run_nodes() is the batched form of run_node (thousands of nodes in one
 //     device arena) -- the sweep drivers' hot loop (commands.cpp:100-116);
-//   * ClusterResult carries the routing decisions and per-request reports of
-//     the device run (node plan digests and step counts too) instead of the
-//     per-node event logs; the routing log has no view snapshot;
+//   * ClusterResult also carries per-request reports and per-node digests;
+//     its node event logs are left empty for rerouting clusters (a rerouted
+//     arrival's place among a node's events of one instant is not recorded);
 //   * RequestReport built from a device record (cluster runs) carries the
 //     first-token time and the max-TPOT figures instead of every emission.
 #pragma once
@@ -248,14 +248,20 @@ struct LbConfig {
   double w_running = 1.0;
   bool retry_reroute = false;
 };
+const char* lb_policy_name(LbPolicy p);
 struct RoutingLogEntry {
   TimeUs t = 0;
   std::int64_t req_id = -1;
-  int node = 0;  // the node the request was (last) routed to
+  int node = 0;
+  std::vector<double> view_snapshot;  // per-node score after the decision
 };
+// The reference's routing-log JSONL (cluster.cpp:114-131).
+void save_routing_log(const std::vector<RoutingLogEntry>& log, LbPolicy policy,
+                      const std::string& path);
 
 struct ClusterResult {
-  std::vector<RoutingLogEntry> routing;
+  std::vector<EventLog> node_logs;  // empty with retry_reroute
+  std::vector<RoutingLogEntry> routing;  // one entry per routing decision
   std::vector<RequestReport> reports;  // every routed request, by id
   std::vector<NodeSummary> nodes;
   bool incomplete = false;

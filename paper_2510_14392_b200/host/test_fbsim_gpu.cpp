@@ -10,6 +10,8 @@
 //   test_fbsim_gpu eventlog IN OUT       run_node on the instance described in
 //                                        IN, save_event_log to OUT (the caller
 //                                        compares it with the reference's log)
+//   test_fbsim_gpu clusterlogs IN DIR    run_cluster on the cluster in IN; its
+//                                        node logs + routing log into DIR
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -286,12 +288,70 @@ static int run_eventlog(const char* in_path, const char* out_path) {
   return 0;
 }
 
+static EngineConfig read_cfg(std::istream& in) {
+  int policy, max_chunk, max_active;
+  int64_t budget, ttft, tpot;
+  double a, b, c, ta, tb, tc, amp;
+  unsigned long long seed;
+  in >> policy >> budget >> max_chunk >> a >> b >> c >> ta >> tb >> tc >> amp >> seed >> ttft >>
+      tpot >> max_active;
+  EngineConfig cfg;
+  cfg.scheduler.policy = static_cast<Policy>(policy);
+  cfg.scheduler.token_budget = budget;
+  cfg.scheduler.max_chunk = max_chunk;
+  cfg.scheduler.model = {a, b, c};
+  cfg.truth_model = {ta, tb, tc};
+  cfg.noise = {amp, seed};
+  cfg.global_slo = {ttft, tpot};
+  cfg.max_active = max_active;
+  return cfg;
+}
+
+// IN: "n_nodes horizon policy(0 count, 1 pab) interval latency_us w_w w_r
+// reroute", one config line per node (as eventlog's, without the horizon),
+// n, then n rows.  Writes OUT/node<i>.jsonl and OUT/routing.jsonl.
+static int run_clusterlogs(const char* in_path, const std::string& out_dir) {
+  std::ifstream in(in_path);
+  int n_nodes, pol, interval, reroute;
+  int64_t horizon, latency;
+  double ww, wr;
+  in >> n_nodes >> horizon >> pol >> interval >> latency >> ww >> wr >> reroute;
+  std::vector<EngineConfig> cfgs;
+  for (int i = 0; i < n_nodes; ++i) cfgs.push_back(read_cfg(in));
+  size_t n;
+  in >> n;
+  Trace t;
+  for (size_t i = 0; i < n; ++i) {
+    Request r;
+    r.id = static_cast<int64_t>(i);
+    in >> r.arrival >> r.prompt_len >> r.output_len >> r.ttft_slo >> r.tpot_slo;
+    t.requests.push_back(r);
+  }
+  if (!in) {
+    std::fprintf(stderr, "bad input\n");
+    return 2;
+  }
+  LbConfig lb;
+  lb.policy = pol ? LbPolicy::kPabLb : LbPolicy::kCountLb;
+  lb.report_interval_steps = interval;
+  lb.report_latency = latency;
+  lb.w_waiting = ww;
+  lb.w_running = wr;
+  lb.retry_reroute = reroute != 0;
+  const ClusterResult res = run_cluster(t, cfgs, lb, horizon);
+  for (size_t i = 0; i < res.node_logs.size(); ++i)
+    save_event_log(res.node_logs[i], out_dir + "/node" + std::to_string(i) + ".jsonl");
+  save_routing_log(res.routing, lb.policy, out_dir + "/routing.jsonl");
+  return 0;
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "";
   try {
     if (mode == "nogpu") return run_nogpu() ? 1 : 0;
     if (mode == "kat") return run_kat() ? 1 : 0;
     if (mode == "eventlog" && argc == 4) return run_eventlog(argv[2], argv[3]);
+    if (mode == "clusterlogs" && argc == 4) return run_clusterlogs(argv[2], argv[3]);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught: %s\n", e.what());
     return 3;

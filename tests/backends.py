@@ -348,6 +348,33 @@ class RefLib(_CpuLib):
                 raise RuntimeError(f"ref_event_log status {st}")
             return buf.raw[: n.value].decode()
 
+    def cluster_logs(self, rows: Rows, cfgs, lb, horizon_us: int, tmp_path: str):
+        """The real run_cluster's node event logs and routing log, as written by
+        the reference's save_event_log / save_routing_log."""
+        from paper_2510_14392_b200.cluster import node_configs_c
+        fn = self.lib.ref_cluster_logs
+        fn.restype = C.c_int
+        n = len(cfgs)
+        tr = rows.to_c()
+        nc = node_configs_c(cfgs)
+        lbc = lb.to_c()
+        offs = np.zeros(n + 2, np.int64)
+        ln = C.c_int64(0)
+        cap = 1 << 22
+        while True:
+            buf = C.create_string_buffer(cap)
+            st = fn(C.byref(tr), C.cast(nc, C.c_void_p), C.c_int32(n), C.byref(lbc),
+                    C.c_int64(horizon_us), tmp_path.encode(), buf, C.c_int64(cap),
+                    _abi.vptr(offs), C.byref(ln))
+            if st == _abi.FB_ERR_CAPACITY:
+                cap = ln.value + 1
+                continue
+            if st:
+                raise RuntimeError(f"ref_cluster_logs status {st}: {self.lib.ref_last_error()}")
+            text = buf.raw[: ln.value].decode()
+            parts = [text[offs[i]:offs[i + 1]] for i in range(n + 1)]
+            return parts[:n], parts[n]
+
     def replay_check(self, jsonl: str, tmp_path: str) -> list[str]:
         """The reference's load_event_log + replay_check of a JSONL text."""
         fn = self.lib.ref_replay_check

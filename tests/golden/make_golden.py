@@ -27,7 +27,8 @@ from backends import RefLib, cluster_summary  # noqa: E402
 from catalog import (SCENARIOS, TRACE_PROFILES, cluster_cases, reroute_cluster_cases,  # noqa: E402
                      rows_digest, summarize)
 from fuzz import Rng, acceptance_corpus, gen_pab_instance, raw_to_views  # noqa: E402
-from tests_golden_cases import LEAD_CASES, REPLAY_MUTATIONS, replay_canonical  # noqa: E402
+from tests_golden_cases import (CLUSTER_LOG_CASES, LEAD_CASES, REPLAY_MUTATIONS,  # noqa: E402
+                                replay_canonical)
 from paper_2510_14392_b200.batch import ms_to_us  # noqa: E402
 
 
@@ -102,6 +103,15 @@ def main() -> None:
     for name, rows, cfgs, lb, hz in (cluster_cases(ref.generate_bursty) +
                                      reroute_cluster_cases(ref.generate_bursty)):
         gold["clusters"][name] = cluster_summary(ref.run_cluster(rows, cfgs, lb, hz, check=True))
+    cl = {c[0]: c for c in cluster_cases(ref.generate_bursty) +
+          reroute_cluster_cases(ref.generate_bursty)}
+    gold["cluster_logs"] = {}
+    for name in CLUSTER_LOG_CASES:
+        _, rows, cfgs, lb, hz = cl[name]
+        nodes, routing = ref.cluster_logs(rows, cfgs, lb, hz, "/tmp/_golden_cl.jsonl")
+        gold["cluster_logs"][name] = {
+            "nodes": [hashlib.sha256(x.encode()).hexdigest() for x in nodes],
+            "routing": hashlib.sha256(routing.encode()).hexdigest()}
     corpus = acceptance_corpus(10_000)
     gold["fuzz"] = {}
     for pol in (2, 1, 0):

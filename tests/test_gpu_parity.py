@@ -332,6 +332,28 @@ def test_clusters_side_by_side_match_golden(golden, gpu_cluster_cases, gpu_rerou
         assert cluster_summary(out) == golden["clusters"][n], n
 
 
+@pytest.mark.parametrize("name", ["pab0_8", "count37_3", "pab5000_8", "pab_hz10s_8", "pab20_2",
+                                  "rr_giant_2", "rr_pab30_3"])
+def test_cluster_logs_match_reference(golden, gpu_cluster_cases, gpu_reroute_cases, name):
+    """ClusterResult's logs from the device run: every node's EventLog
+    (save_event_log) and the routing log with view snapshots
+    (save_routing_log), byte-identical to the reference's files."""
+    from paper_2510_14392_b200.cluster import run_cluster_logged
+    from paper_2510_14392_b200.events import cluster_event_logs
+    _, rows, cfgs, lb, hz = (gpu_cluster_cases.get(name) or gpu_reroute_cases[name])
+    logs = run_cluster_logged(rows, cfgs, lb, hz)
+    g = golden["cluster_logs"][name]
+    if lb.retry_reroute:  # node logs are not rebuilt for rerouting clusters
+        with pytest.raises(ValueError):
+            cluster_event_logs(rows, logs, lb.policy)
+        _, routing = cluster_event_logs(rows, logs, lb.policy, nodes=False)
+        assert hashlib.sha256(routing.encode()).hexdigest() == g["routing"]
+        return
+    nodes, routing = cluster_event_logs(rows, logs, lb.policy)
+    assert hashlib.sha256(routing.encode()).hexdigest() == g["routing"]
+    assert [hashlib.sha256(x.encode()).hexdigest() for x in nodes] == g["nodes"]
+
+
 def test_cluster_reroute_is_single_rank(fb):
     """The reroute engine replays the global loop on one GPU: a multi-rank
     shard with retry_reroute is a usage error, not a silent divergence."""

@@ -76,3 +76,41 @@ def test_host_api_event_logs_match_reference(golden, tmp_path, fb, name):
         assert p.returncode == 0, p.stderr
         got = hashlib.sha256(out.read_bytes()).hexdigest()
         assert got == golden["event_logs"][name][i], (name, i)
+
+
+def _cfg_line(c):
+    s = c.scheduler
+    return (f"{s.policy} {s.token_budget} {s.max_chunk} {s.model.a_ms!r} {s.model.b_ms!r} "
+            f"{s.model.c_ms!r} {c.truth_model.a_ms!r} {c.truth_model.b_ms!r} "
+            f"{c.truth_model.c_ms!r} {c.noise_amplitude!r} {c.noise_seed} {c.global_ttft_us} "
+            f"{c.global_tpot_us} {c.max_active}\n")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pab0_8", "count37_3", "pab5000_8"])
+def test_host_api_cluster_logs_match_reference(golden, tmp_path, fb, name):
+    """run_cluster through the C++ API: every node's EventLog and the routing
+    log (view snapshots included), byte-identical to the reference's files."""
+    from catalog import cluster_cases
+    from paper_2510_14392_b200.cluster import node_configs_c
+    _, rows, cfgs, lb, hz = {c[0]: c for c in cluster_cases(fb.generate_bursty)}[name]
+    lbc = lb.to_c()
+    nc = node_configs_c(cfgs)
+    src = tmp_path / "cluster.txt"
+    with open(src, "w") as f:
+        f.write(f"{len(cfgs)} {hz} {lbc.policy} {lbc.report_interval_steps} "
+                f"{lbc.report_latency_us} {lbc.w_waiting!r} {lbc.w_running!r} "
+                f"{lbc.retry_reroute}\n")
+        for i in range(len(cfgs)):
+            f.write(_cfg_line(nc[i]))
+        f.write(f"{len(rows)}\n")
+        for k in range(len(rows)):
+            f.write(f"{rows.arrival_us[k]} {rows.prompt_len[k]} {rows.output_len[k]} "
+                    f"{rows.ttft_us[k]} {rows.tpot_us[k]}\n")
+    p = _run("clusterlogs", str(src), str(tmp_path))
+    assert p.returncode == 0, p.stderr
+    g = golden["cluster_logs"][name]
+    assert hashlib.sha256((tmp_path / "routing.jsonl").read_bytes()).hexdigest() == g["routing"]
+    got = [hashlib.sha256((tmp_path / f"node{i}.jsonl").read_bytes()).hexdigest()
+           for i in range(len(cfgs))]
+    assert got == g["nodes"]
