@@ -51,6 +51,30 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, i
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   EngineParams pp = p;
+  // One rank with at most kHwClusterMax CTAs: launch the grid as ONE
+  // thread-block cluster (co-scheduled on one GPC by construction) and use
+  // the hardware cluster barrier per epoch.  Otherwise a cooperative launch
+  // (every CTA co-resident) with the global-memory exchange barrier.
+  constexpr int kHwClusterMax = 8;  // portable cluster size
+  if (c.n_ranks == 1 && blocks <= kHwClusterMax && !std::getenv("FB_NO_HW_CLUSTER")) {
+    c.hw_cluster = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kWarp * c.warps_per_cta);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = blocks;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, cluster_kernel, pp, c);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();  // not schedulable as one cluster: fall back
+    c.hw_cluster = 0;
+  }
   void* args[] = {&pp, &c};
   // cooperative: every CTA must be co-resident for the epoch barrier
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cluster_kernel), dim3(blocks),

@@ -67,6 +67,8 @@ struct ClusterParams {
   fb_route_log* rlog;                 // routing log (NULL: off)
   double* rsnap;                      // per entry the view snapshot, [rlog_cap * n_nodes]
   int64_t rlog_cap;
+  int32_t hw_cluster;  // one rank, the whole grid is one thread-block cluster
+  int32_t pad_hw;
 };
 
 // Router view (replicated per CTA) + the CTA's routing results.
@@ -470,7 +472,15 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     const int64_t t_a = C.epoch_t[e];
     int32_t cmp = 0;
     if (owner) node_phase_a(P, C, nd, e, t_a, &cmp, &status);
-    if (!(ok = cluster_barrier(C, rs, e))) break;
+    if (C.hw_cluster) {
+      // the grid is one thread-block cluster: the hardware cluster barrier
+      // (release / acquire at cluster scope orders the report stores of
+      // every CTA before the reads) replaces the global-memory arrival count
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (!(ok = cluster_barrier(C, rs, e))) {
+      break;
+    }
     const NodeReport* all = xchg_reports(C.xbuf[C.rank], C.n_nodes, e);
     if (cluster_stopped(C, all, t_a)) break;
     if (warp == 0) cluster_route(P, C, rs, all, e, node_base);

@@ -143,6 +143,7 @@ struct ClusterParamsHost {
   fb_route_log* rlog;  // routing log (NULL: off), [rlog_cap]
   double* rsnap;       // its view snapshots, [rlog_cap * n_nodes]
   int64_t rlog_cap;
+  int32_t hw_cluster, pad_hw;  // set by launch_cluster
 };
 size_t cluster_param_bytes();
 int cluster_max_nodes();
