@@ -14,6 +14,11 @@
 
 namespace fbgpu {
 
+#ifndef FB_RANK_UNROLL
+#define FB_RANK_UNROLL 4  // 8: 36.2 ms, 16: 37.8 ms on C2 (code size)
+#endif
+constexpr int kRankUnroll = FB_RANK_UNROLL;
+
 // One live request held by one lane.
 struct TaskReg {
   int32_t r, seq, prompt, output, prefilled, nidx, take;
@@ -316,10 +321,10 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   if (!vis) key = ~uint64_t(0);
   int rank = 0;
   if (use32) {
-#pragma unroll 8
+#pragma unroll kRankUnroll
     for (int q = 0; q < A; ++q) rank += tile_shfl(k32, q) < k32;
   } else {
-#pragma unroll 8
+#pragma unroll kRankUnroll
     for (int q = 0; q < A; ++q) rank += tile_shfl(key, q) < key;
   }
   if (!vis) rank = lane;
