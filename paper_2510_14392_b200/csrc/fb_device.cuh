@@ -147,10 +147,10 @@ __device__ __forceinline__ uint64_t warp_xor_u64(uint64_t v) {
 
 // ------------------------------------------------------------- tile utils
 //
-// The warp engine simulates one node per *tile* of kTile lanes: a half-warp
-// in the engine kernel (two nodes advance per warp instruction when their
-// control flow agrees), a full warp in the cluster and pure-scheduler
-// kernels.  Every lane-collective on the per-node paths goes through these:
+// The warp engine simulates one node per *tile* of kTile lanes: a full warp
+// by default; FB_TILE = 16 builds half-warp tiles (two nodes advance per warp
+// instruction when their control flow agrees; bit-exact, slower on C2).
+// Every lane-collective on the per-node paths goes through these:
 // masks name only the tile, so the two tiles of a warp stay correct whether
 // they run converged or diverged.  Ballots / match results and lane indices
 // are tile-relative.

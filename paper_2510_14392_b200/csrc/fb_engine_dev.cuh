@@ -1,9 +1,9 @@
-// fb_engine_dev.cuh -- the warp engine's device code: one tile (kTile lanes;
-// a half-warp in the engine kernel, a full warp in the cluster and
-// pure-scheduler kernels) simulates one Node instance (engine.h:111-176):
-// task views, the memory-path begin/complete step, the register-resident
-// path (fb_engine_rr.cuh) and run_node's event loop.  Included by
-// fb_engine.cu (kTile = 16) and fb_cluster.cu (kTile = 32).
+// fb_engine_dev.cuh -- the warp engine's device code: one tile (kTile
+// lanes; a full warp by default, FB_TILE = 16 gives two nodes per warp)
+// simulates one Node instance (engine.h:111-176): task views, the
+// memory-path begin/complete step, the register-resident path
+// (fb_engine_rr.cuh) and run_node's event loop.  Included by fb_engine.cu
+// and fb_cluster.cu.
 #pragma once
 
 #include <cuda_runtime.h>
