@@ -169,7 +169,8 @@ typedef struct fb_reject_log {
   int64_t t_us;
   int64_t pab_tokens;
   int32_t req;
-  int32_t reserved;
+  int32_t step; /* steps the node began before this reject (the rejecting
+                   begin_step launches step `step`, if any) */
 } fb_reject_log;
 
 /* Plan-log capacities per instance; 0 disables logging. */
@@ -383,6 +384,8 @@ typedef struct fb_route_log {
   int64_t t_us;  /* decision time */
   int32_t req;   /* trace row */
   int32_t node;  /* target */
+  int32_t rej_before;   /* the target's admission rejects so far (-1: not recorded) */
+  int32_t steps_before; /* the target's steps begun so far (-1: not recorded) */
 } fb_route_log;
 
 /* LbConfig, cluster.h:36-47. */

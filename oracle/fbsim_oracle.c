@@ -522,7 +522,7 @@ static void orc_pull_arrivals(orc_node* nd, int64_t now) {
           rl->t_us = now;
           rl->pab_tokens = budget;
           rl->req = r;
-          rl->reserved = 0;
+          rl->step = (int32_t)nd->step_counter;
         } else if (nd->rejects) {
           nd->counts->truncated = 1;
         }

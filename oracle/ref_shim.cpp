@@ -204,7 +204,7 @@ int run_mirror(const fb_trace* rows, const fb_instance& inst,
           rl.t_us = e.t;
           rl.pab_tokens = e.pab_tokens;
           rl.req = static_cast<int32_t>(e.req_id);
-          rl.reserved = 0;
+          rl.step = static_cast<int32_t>(step);  // batch_starts logged before it
         } else {
           counts->truncated = 1;
         }

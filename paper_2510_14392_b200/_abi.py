@@ -140,7 +140,7 @@ class RejectLog(C.Structure):
         ("t_us", C.c_int64),
         ("pab_tokens", C.c_int64),
         ("req", C.c_int32),
-        ("reserved", C.c_int32),
+        ("step", C.c_int32),
     ]
 
 
@@ -237,10 +237,11 @@ STEPLOG_DTYPE = np.dtype(
      ("entry_off", "<i4"), ("n_entries", "<i4")], align=True)
 ENTRY_DTYPE = np.dtype([("req", "<i4"), ("new_tokens", "<i4")], align=True)
 REJECT_DTYPE = np.dtype([("t_us", "<i8"), ("pab_tokens", "<i8"), ("req", "<i4"),
-                         ("reserved", "<i4")], align=True)
+                         ("step", "<i4")], align=True)
 LOGCOUNT_DTYPE = np.dtype([("steps", "<i4"), ("entries", "<i4"), ("rejects", "<i4"),
                            ("truncated", "<i4")], align=True)
-ROUTELOG_DTYPE = np.dtype([("t_us", "<i8"), ("req", "<i4"), ("node", "<i4")], align=True)
+ROUTELOG_DTYPE = np.dtype([("t_us", "<i8"), ("req", "<i4"), ("node", "<i4"),
+                           ("rej_before", "<i4"), ("steps_before", "<i4")], align=True)
 TASKVIEW_DTYPE = np.dtype(
     [("request_id", "<i8"), ("slack_us", "<i8"), ("context", "<i8"), ("arrival_seq", "<i8"),
      ("tpot_us", "<i8"), ("new_tokens", "<i4"), ("phase", "<i4")], align=True)

@@ -318,7 +318,7 @@ __device__ __forceinline__ bool cluster_stopped(const ClusterParams& C, const No
 // lowest node id.  Updates the view's local decrements.  Returns the node.
 __device__ __forceinline__ int cluster_pick(const ClusterParams& C, RouterSmem& rs,
                                             int64_t prompt, int64_t log_k = -1, int64_t t = 0,
-                                            int64_t row = 0) {
+                                            int64_t row = 0, const DevState* states = nullptr) {
   const int n = C.n_nodes;
   int chosen;
   if (C.lb_policy == FB_LB_PAB) {
@@ -394,6 +394,10 @@ __device__ __forceinline__ int cluster_pick(const ClusterParams& C, RouterSmem& 
       e.t_us = t;
       e.req = static_cast<int32_t>(row);
       e.node = chosen;
+      // the target's log position at enqueue (serial engine: a rerouted
+      // arrival can fall between a node's events of one instant)
+      e.rej_before = states ? static_cast<int32_t>(states[chosen].n_rejected) : -1;
+      e.steps_before = states ? static_cast<int32_t>(states[chosen].step_counter) : -1;
     }
     __syncwarp();
   }
@@ -580,7 +584,7 @@ __device__ void serial_report(const EngineParams& P, const ClusterParams& C, Clu
 // route_request (cluster.cpp:171-175): pick, log the target, Node::enqueue.
 __device__ __forceinline__ void serial_route(const EngineParams& P, const ClusterParams& C,
                                              SerialSmem& ss, int64_t row, int64_t t) {
-  const int chosen = cluster_pick(C, ss.rs, P.prompt[row], ss.n_log, t, row);
+  const int chosen = cluster_pick(C, ss.rs, P.prompt[row], ss.n_log, t, row, P.state);
   __syncwarp();
   if (lane_id() == 0) ss.n_log++;
   if (lane_id() == 0) {

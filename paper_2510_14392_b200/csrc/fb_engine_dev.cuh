@@ -303,7 +303,7 @@ static __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
             rl.t_us = now;
             rl.pab_tokens = budget;
             rl.req = static_cast<int32_t>(r);
-            rl.reserved = 0;
+            rl.step = static_cast<int32_t>(w.S.step_counter);
           }
         }
       }

@@ -247,7 +247,7 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
           rl.t_us = now;
           rl.pab_tokens = budget;
           rl.req = static_cast<int32_t>(r);
-          rl.reserved = 0;
+          rl.step = static_cast<int32_t>(w.S.step_counter);
         }
       }
       if (P.log_on) {

@@ -937,7 +937,7 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
             rl.t_us = now;
             rl.pab_tokens = budget;
             rl.req = static_cast<int32_t>(r);
-            rl.reserved = 0;
+            rl.step = static_cast<int32_t>(w.S.step_counter);
             w.S.log_rejects++;
           } else {
             w.S.log_trunc = 1;

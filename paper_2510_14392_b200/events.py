@@ -78,20 +78,27 @@ def event_log_lines(rows, inst, result, counts, steps, entries, rejects, node_id
 
 def _node_lines(arrivals, prompt, output, arr_us, ttft, tpot, counts, steps, entries, rejects,
                 incomplete: bool, node_id: int):
-    """EventLog lines of one node whose arrivals are `arrivals` = [(t, row)]
-    in enqueue order; row-indexed request arrays."""
+    """EventLog lines of one cluster node.  `arrivals` = [(t, row, rej_before,
+    steps_before)] in enqueue order; the tags (-1: not recorded) place an
+    arrival among the node's begin_step events of the same instant -- after
+    the rejects and batch starts logged before it was enqueued (a rerouted
+    arrival can follow the node's own begin at that instant, cluster.cpp:
+    222-237).  Within one instant: the step completing (token_emit /
+    request_done in plan order, batch_end), then, ordered by (steps begun,
+    rejects logged): arrivals, rejects, the batch start."""
     if counts["truncated"]:
         raise ValueError("plan log truncated: raise the log capacities")
+    big = 1 << 62
     ev = []
-    for k, (t, r) in enumerate(arrivals):
-        ev.append((int(t), 1, k,
+    for k, (t, r, rc, sc) in enumerate(arrivals):
+        ev.append((int(t), 1, (int(sc), int(rc), 0, k),
                    '{"t_ms":%s,"kind":"arrival","req_id":%d,"arrival_ms":%s,"prompt_tokens":%d,'
                    '"output_tokens":%d,"ttft_slo_ms":%s,"tpot_slo_ms":%s}\n'
                    % (_ms(t), r, _ms(arr_us[r]), prompt[r], output[r], _ms(ttft[r]),
                       _ms(tpot[r]))))
-    for k in range(int(counts["rejects"])):
-        rj = rejects[k]
-        ev.append((int(rj["t_us"]), 2, k,
+    for j in range(int(counts["rejects"])):
+        rj = rejects[j]
+        ev.append((int(rj["t_us"]), 1, (int(rj["step"]), j, 1, 0),
                    '{"t_ms":%s,"kind":"admission_reject","req_id":%d,"prompt_tokens":%d,'
                    '"pab_tokens":%d}\n' % (_ms(rj["t_us"]), rj["req"], prompt[rj["req"]],
                                           rj["pab_tokens"])))
@@ -100,7 +107,7 @@ def _node_lines(arrivals, prompt, output, arr_us, ttft, tpot, counts, steps, ent
         st = steps[s]
         t0 = int(st["t_us"])
         t1 = t0 + int(st["duration_us"])
-        ev.append((t0, 3, s,
+        ev.append((t0, 1, (s, big, 2, 0),
                    '{"t_ms":%s,"kind":"batch_start","step":%d,"new_tokens":%d,'
                    '"context_tokens":%d,"predicted_ms":%.6f}\n'
                    % (_ms(t0), s, st["total_new"], st["total_ctx"], st["predicted_ms"])))
@@ -122,7 +129,7 @@ def _node_lines(arrivals, prompt, output, arr_us, ttft, tpot, counts, steps, ent
                     body.append('{"t_ms":%s,"kind":"request_done","req_id":%d}\n' % (_ms(t1), r))
         body.append('{"t_ms":%s,"kind":"batch_end","step":%d,"actual_ms":%.6f}\n'
                     % (_ms(t1), s, st["actual_ms"]))
-        ev.append((t1, 0, s, "".join(body)))
+        ev.append((t1, 0, (s,), "".join(body)))
     ev.sort(key=lambda x: (x[0], x[1], x[2]))
     lines = [x[3] for x in ev]
     lines.append('{"kind":"log_end","node":%d,"incomplete":%d}\n' % (node_id, 1 if incomplete else 0))
@@ -133,17 +140,14 @@ def cluster_event_logs(rows, logs, lb_policy: str, nodes: bool = True) -> tuple[
     """run_cluster's outputs in the reference's JSONL formats: every node's
     save_event_log (engine.cpp:395-451; arrivals = the requests routed to it,
     at their routing times) and save_routing_log (cluster.cpp:114-131, view
-    snapshots included).  `logs` is a cluster.ClusterLogs.  With
-    retry_reroute a rerouted arrival lands between a node's events of one
-    instant in an order the plan log does not record, so node logs are
-    refused there (ValueError; nodes=False returns the routing log only)."""
+    snapshots included).  `logs` is a cluster.ClusterLogs; nodes=False
+    returns the routing log only."""
     routes = logs.routes
     node_logs = []
-    if nodes and len(np.unique(routes["req"])) != len(routes):
-        raise ValueError("node event logs of a rerouting cluster are not rebuilt")
     for i in range(len(logs.counts) if nodes else 0):
         mine = routes[routes["node"] == i]
-        arrivals = list(zip(mine["t_us"].tolist(), mine["req"].tolist()))
+        arrivals = list(zip(mine["t_us"].tolist(), mine["req"].tolist(),
+                            mine["rej_before"].tolist(), mine["steps_before"].tolist()))
         node_logs.append("".join(_node_lines(
             arrivals, rows.prompt_len, rows.output_len, rows.arrival_us, rows.ttft_us,
             rows.tpot_us, logs.counts[i], logs.steps[i], logs.entries[i], logs.rejects[i],

@@ -101,28 +101,37 @@ struct Arena {
   Arena& operator=(const Arena&) = delete;
 };
 
-// One node's EventLog from its plan log: arrivals, rejects and batch starts
-// at their times; the completions of a step (token_emit / request_done in
-// plan order, then batch_end) at its end.  Within one timestamp run_node
-// appends completions, then arrivals, then rejects, then the batch start
-// (engine.cpp:271-283).
-// arrivals: (visible_at, trace row) in enqueue order.
-EventLog build_log(const Trace& tr, const std::vector<std::pair<TimeUs, int64_t>>& arrivals,
-                   bool incomplete, const fb_log_counts& cnt, const fb_step_log* steps,
+// One node's EventLog from its plan log.  At one instant the step
+// completing comes first (token_emit / request_done in plan order,
+// batch_end); then arrivals, rejects and the batch start ordered by (steps
+// begun, rejects logged) -- an arrival tagged with its node's counts at
+// enqueue falls after the events logged before it (a rerouted arrival can
+// follow the node's own begin_step of that instant, cluster.cpp:222-237);
+// untagged arrivals (-1) precede the instant's begin_step (run_node,
+// engine.cpp:271-283).
+struct Arrival {
+  TimeUs t;
+  int64_t row;
+  int64_t rej_before, steps_before;
+};
+
+EventLog build_log(const Trace& tr, const std::vector<Arrival>& arrivals, bool incomplete,
+                   const fb_log_counts& cnt, const fb_step_log* steps,
                    const fb_plan_entry* entries, const fb_reject_log* rejects) {
   if (cnt.truncated) throw CudaError("plan log truncated");
+  constexpr int64_t kBig = int64_t(1) << 62;
   struct Item {
     TimeUs t;
-    int phase;
-    int64_t order, sub;
+    int cls;
+    int64_t a, b, c, d;
     Event e;
   };
   std::vector<Item> items;
   for (size_t k = 0; k < arrivals.size(); ++k) {
-    const int64_t r = arrivals[k].second;
-    const Request& q = tr.requests[static_cast<size_t>(r)];
+    const Arrival& ar = arrivals[k];
+    const Request& q = tr.requests[static_cast<size_t>(ar.row)];
     Event e;
-    e.t = arrivals[k].first;
+    e.t = ar.t;
     e.kind = EventKind::kArrival;
     e.req_id = q.id;
     e.arrival = q.arrival;
@@ -130,22 +139,22 @@ EventLog build_log(const Trace& tr, const std::vector<std::pair<TimeUs, int64_t>
     e.output_len = q.output_len;
     e.ttft_slo = q.ttft_slo;
     e.tpot_slo = q.tpot_slo;
-    items.push_back({e.t, 1, static_cast<int64_t>(k), 0, e});
+    items.push_back({e.t, 1, ar.steps_before, ar.rej_before, 0, static_cast<int64_t>(k), e});
   }
-  for (int32_t k = 0; k < cnt.rejects; ++k) {
-    const fb_reject_log& rj = rejects[static_cast<size_t>(k)];
+  for (int32_t j = 0; j < cnt.rejects; ++j) {
+    const fb_reject_log& rj = rejects[j];
     Event e;
     e.t = rj.t_us;
     e.kind = EventKind::kAdmissionReject;
     e.req_id = tr.requests[static_cast<size_t>(rj.req)].id;
     e.prompt_len = tr.requests[static_cast<size_t>(rj.req)].prompt_len;
     e.pab_tokens = rj.pab_tokens;
-    items.push_back({e.t, 2, k, 0, e});
+    items.push_back({e.t, 1, rj.step, j, 1, 0, e});
   }
   std::vector<int64_t> prefilled(std::max<size_t>(tr.requests.size(), 1), 0);
   std::vector<int32_t> nidx(prefilled.size(), 0);
   for (int32_t s = 0; s < cnt.steps; ++s) {
-    const fb_step_log& st = steps[static_cast<size_t>(s)];
+    const fb_step_log& st = steps[s];
     const TimeUs t0 = st.t_us, t1 = st.t_us + st.duration_us;
     Event b;
     b.t = t0;
@@ -154,10 +163,10 @@ EventLog build_log(const Trace& tr, const std::vector<std::pair<TimeUs, int64_t>
     b.new_tokens = st.total_new;
     b.context_tokens = st.total_ctx;
     b.predicted_ms = st.predicted_ms;
-    items.push_back({t0, 3, s, 0, b});
+    items.push_back({t0, 1, s, kBig, 2, 0, b});
     int64_t sub = 0;
     for (int32_t k = 0; k < st.n_entries; ++k) {
-      const fb_plan_entry& pe = entries[static_cast<size_t>(st.entry_off + k)];
+      const fb_plan_entry& pe = entries[st.entry_off + k];
       const Request& q = tr.requests[static_cast<size_t>(pe.req)];
       bool emit = true;
       if (prefilled[pe.req] < q.prompt_len) {
@@ -170,13 +179,13 @@ EventLog build_log(const Trace& tr, const std::vector<std::pair<TimeUs, int64_t>
       e.kind = EventKind::kTokenEmit;
       e.req_id = q.id;
       e.token_idx = nidx[pe.req]++;
-      items.push_back({t1, 0, s, sub++, e});
+      items.push_back({t1, 0, s, sub++, 0, 0, e});
       if (nidx[pe.req] >= q.output_len) {
         Event d;
         d.t = t1;
         d.kind = EventKind::kRequestDone;
         d.req_id = q.id;
-        items.push_back({t1, 0, s, sub++, d});
+        items.push_back({t1, 0, s, sub++, 0, 0, d});
       }
     }
     Event end;
@@ -184,10 +193,10 @@ EventLog build_log(const Trace& tr, const std::vector<std::pair<TimeUs, int64_t>
     end.kind = EventKind::kBatchEnd;
     end.step = s;
     end.actual_ms = st.actual_ms;
-    items.push_back({t1, 0, s, sub++, end});
+    items.push_back({t1, 0, s, sub++, 0, 0, end});
   }
   std::stable_sort(items.begin(), items.end(), [](const Item& x, const Item& y) {
-    return std::tie(x.t, x.phase, x.order, x.sub) < std::tie(y.t, y.phase, y.order, y.sub);
+    return std::tie(x.t, x.cls, x.a, x.b, x.c, x.d) < std::tie(y.t, y.cls, y.a, y.b, y.c, y.d);
   });
   EventLog log;
   log.incomplete = incomplete;
@@ -377,9 +386,9 @@ std::vector<EventLog> run_nodes(const std::vector<const Trace*>& traces,
   for (int64_t i = 0; i < n; ++i) {
     check(res[i].status);
     check(fb_arena_fetch_log(a.a, i, steps.data(), entries.data(), rejects.data()));
-    std::vector<std::pair<TimeUs, int64_t>> arrivals;
+    std::vector<Arrival> arrivals;
     for (int64_t r = 0; r < res[i].n_arrived; ++r)
-      arrivals.push_back({traces[i]->requests[static_cast<size_t>(r)].arrival, r});
+      arrivals.push_back({traces[i]->requests[static_cast<size_t>(r)].arrival, r, -1, -1});
     logs.push_back(build_log(*traces[i], arrivals, res[i].incomplete != 0, cnt[i], steps.data(),
                              entries.data(), rejects.data()));
   }
@@ -646,20 +655,19 @@ ClusterResult run_cluster(const Trace& trace, const std::vector<EngineConfig>& n
   }
   for (size_t q = 0; q < nr; ++q)
     if (route[q] >= 0) out.reports.push_back(report_from_record(trace.requests[q], rec[q]));
-  // each node's EventLog: its arrivals are the requests routed to it; with
-  // retry_reroute a rerouted arrival's place among a node's events of one
-  // instant is not recorded, so node logs are left empty there
-  if (!lb.retry_reroute) {
-    for (size_t i = 0; i < nn; ++i) {
-      std::vector<std::pair<TimeUs, int64_t>> arrivals;
-      for (int64_t k = 0; k < n_routes; ++k)
-        if (routes[static_cast<size_t>(k)].node == static_cast<int32_t>(i))
-          arrivals.push_back({routes[static_cast<size_t>(k)].t_us, routes[static_cast<size_t>(k)].req});
-      EventLog log = build_log(trace, arrivals, out.incomplete, cnt[i], steps.data() + i * lo.step_cap,
-                               entries.data() + i * lo.entry_cap, rejects.data() + i * lo.reject_cap);
-      log.node_id = static_cast<int>(i);
-      out.node_logs.push_back(std::move(log));
+  // each node's EventLog: its arrivals are the requests routed to it, at
+  // their routing times
+  for (size_t i = 0; i < nn; ++i) {
+    std::vector<Arrival> arrivals;
+    for (int64_t k = 0; k < n_routes; ++k) {
+      const fb_route_log& e = routes[static_cast<size_t>(k)];
+      if (e.node == static_cast<int32_t>(i))
+        arrivals.push_back({e.t_us, e.req, e.rej_before, e.steps_before});
     }
+    EventLog log = build_log(trace, arrivals, out.incomplete, cnt[i], steps.data() + i * lo.step_cap,
+                             entries.data() + i * lo.entry_cap, rejects.data() + i * lo.reject_cap);
+    log.node_id = static_cast<int>(i);
+    out.node_logs.push_back(std::move(log));
   }
   return out;
 }

@@ -13,8 +13,6 @@
 //   * run_nodes() is the batched form of run_node (thousands of nodes in one
 //     device arena) -- the sweep drivers' hot loop (commands.cpp:100-116);
 //   * ClusterResult also carries per-request reports and per-node digests;
-//     its node event logs are left empty for rerouting clusters (a rerouted
-//     arrival's place among a node's events of one instant is not recorded);
 //   * RequestReport built from a device record (cluster runs) carries the
 //     first-token time and the max-TPOT figures instead of every emission.
 #pragma once
@@ -260,7 +258,7 @@ void save_routing_log(const std::vector<RoutingLogEntry>& log, LbPolicy policy,
                       const std::string& path);
 
 struct ClusterResult {
-  std::vector<EventLog> node_logs;  // empty with retry_reroute
+  std::vector<EventLog> node_logs;
   std::vector<RoutingLogEntry> routing;  // one entry per routing decision
   std::vector<RequestReport> reports;  // every routed request, by id
   std::vector<NodeSummary> nodes;

@@ -343,12 +343,6 @@ def test_cluster_logs_match_reference(golden, gpu_cluster_cases, gpu_reroute_cas
     _, rows, cfgs, lb, hz = (gpu_cluster_cases.get(name) or gpu_reroute_cases[name])
     logs = run_cluster_logged(rows, cfgs, lb, hz)
     g = golden["cluster_logs"][name]
-    if lb.retry_reroute:  # node logs are not rebuilt for rerouting clusters
-        with pytest.raises(ValueError):
-            cluster_event_logs(rows, logs, lb.policy)
-        _, routing = cluster_event_logs(rows, logs, lb.policy, nodes=False)
-        assert hashlib.sha256(routing.encode()).hexdigest() == g["routing"]
-        return
     nodes, routing = cluster_event_logs(rows, logs, lb.policy)
     assert hashlib.sha256(routing.encode()).hexdigest() == g["routing"]
     assert [hashlib.sha256(x.encode()).hexdigest() for x in nodes] == g["nodes"]

@@ -87,13 +87,16 @@ def _cfg_line(c):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["pab0_8", "count37_3", "pab5000_8"])
+@pytest.mark.parametrize("name", ["pab0_8", "count37_3", "pab5000_8", "rr_giant_2", "rr_pab30_3"])
 def test_host_api_cluster_logs_match_reference(golden, tmp_path, fb, name):
     """run_cluster through the C++ API: every node's EventLog and the routing
-    log (view snapshots included), byte-identical to the reference's files."""
-    from catalog import cluster_cases
+    log (view snapshots included), byte-identical to the reference's files --
+    with retry_reroute too."""
+    from catalog import cluster_cases, reroute_cluster_cases
     from paper_2510_14392_b200.cluster import node_configs_c
-    _, rows, cfgs, lb, hz = {c[0]: c for c in cluster_cases(fb.generate_bursty)}[name]
+    cases = {c[0]: c for c in cluster_cases(fb.generate_bursty) +
+             reroute_cluster_cases(fb.generate_bursty)}
+    _, rows, cfgs, lb, hz = cases[name]
     lbc = lb.to_c()
     nc = node_configs_c(cfgs)
     src = tmp_path / "cluster.txt"
