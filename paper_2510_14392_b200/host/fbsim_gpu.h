@@ -269,4 +269,51 @@ struct ClusterResult {
 ClusterResult run_cluster(const Trace& trace, const std::vector<EngineConfig>& node_cfgs,
                           const LbConfig& lb, TimeUs horizon, int device = 0);
 
+// ------------------------------------------------- metrics.h / scenario.h
+struct PercentileRow {
+  double p50 = 0.0, p95 = 0.0, p99 = 0.0;
+  std::size_t count = 0;
+};
+PercentileRow percentiles(std::vector<double> values);  // nearest rank, metrics.cpp:118-135
+struct ScenarioReport {                                  // metrics.h:74-88
+  std::string name;
+  std::size_t total_requests = 0, rejected = 0, finished = 0, good = 0;
+  double slo_violation_rate = 0.0, offered_rps = 0.0, effective_rps = 0.0;
+  PercentileRow ttft_ms, max_tpot_ms, max_tpot_alt_ms;
+};
+// scenario_report (metrics.cpp:171-205) over the arrived requests' reports.
+ScenarioReport scenario_report(const std::vector<RequestReport>& reports, double offered_rps,
+                               const std::string& name, bool alt_tpot = false);
+
+struct Scenario {  // scenario.h:31-61
+  std::string name = "scenario";
+  std::string trace_file, trace_format = "jsonl";
+  bool bursty = false;
+  BurstProfile burst;
+  TimeUs burst_horizon = 0;
+  std::int64_t max_requests = 0;
+  double scale = 1.0;
+  SloTargets slo;
+  SchedulerConfig scheduler;
+  CostModel truth;
+  double noise_amplitude = 0.0;
+  int nodes = 1;
+  LbConfig lb;
+  TimeUs horizon = 0;
+  std::uint64_t seed = 0;
+  std::string out_dir = "out";
+  std::int32_t max_active = 0;
+  TimeUs lead_bucket = 1000000;
+  bool alt_tpot = false;
+};
+// load_scenario / scenario_from_json (scenario.cpp:77-222, 280-289): the
+// JSON schema with unknown-key rejection; ConfigError on any violation,
+// ValidationError for an invalid scheduler configuration.
+Scenario load_scenario(const std::string& path);
+Scenario scenario_from_json(const std::string& text);
+Trace materialize_trace(const Scenario& sc);      // scenario.cpp:298-308
+EngineConfig engine_config(const Scenario& sc);   // scenario.cpp:310-319
+// run_scenario (commands.cpp:59-85) without the file writers.
+ScenarioReport run_scenario(const Scenario& sc, int device = 0);
+
 }  // namespace fbsim_gpu

@@ -345,6 +345,27 @@ static int run_clusterlogs(const char* in_path, const std::string& out_dir) {
   return 0;
 }
 
+// run_scenario on a scenario file; one line of report fields.
+static int run_scenario_file(const char* path) {
+  try {
+    const ScenarioReport r = run_scenario(load_scenario(path));
+    std::printf("{\"name\":\"%s\",\"total\":%zu,\"rejected\":%zu,\"finished\":%zu,"
+                "\"good\":%zu,\"offered\":%.17g,\"effective\":%.17g,\"violation\":%.17g,"
+                "\"ttft\":[%.17g,%.17g,%.17g,%zu],\"tpot\":[%.17g,%.17g,%.17g,%zu]}\n",
+                r.name.c_str(), r.total_requests, r.rejected, r.finished, r.good, r.offered_rps,
+                r.effective_rps, r.slo_violation_rate, r.ttft_ms.p50, r.ttft_ms.p95, r.ttft_ms.p99,
+                r.ttft_ms.count, r.max_tpot_ms.p50, r.max_tpot_ms.p95, r.max_tpot_ms.p99,
+                r.max_tpot_ms.count);
+  } catch (const ConfigError& e) {
+    std::fprintf(stderr, "config error: %s\n", e.what());
+    return 1;  // commands.h:30-33
+  } catch (const ValidationError& e) {
+    std::fprintf(stderr, "validation error: %s\n", e.what());
+    return 2;
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "";
   try {
@@ -352,6 +373,7 @@ int main(int argc, char** argv) {
     if (mode == "kat") return run_kat() ? 1 : 0;
     if (mode == "eventlog" && argc == 4) return run_eventlog(argv[2], argv[3]);
     if (mode == "clusterlogs" && argc == 4) return run_clusterlogs(argv[2], argv[3]);
+    if (mode == "scenario" && argc == 3) return run_scenario_file(argv[2]);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught: %s\n", e.what());
     return 3;

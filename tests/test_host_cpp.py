@@ -117,3 +117,57 @@ def test_host_api_cluster_logs_match_reference(golden, tmp_path, fb, name):
     got = [hashlib.sha256((tmp_path / f"node{i}.jsonl").read_bytes()).hexdigest()
            for i in range(len(cfgs))]
     assert got == g["nodes"]
+
+
+def _scenario(nodes: int, policy: str) -> dict:
+    return {
+        "name": f"cpp_{policy}_{nodes}",
+        "trace": {"bursty": {"base_rate": 2.0 * nodes, "burst_rate": 8.0 * nodes,
+                             "burst_duration_ms": 1000, "idle_duration_ms": 2000,
+                             "prompt_mean": 892, "prompt_p90": 1776, "output_mean": 120,
+                             "output_p90": 260, "seed": 7, "horizon_ms": 20000},
+                  "scale": 1.5},
+        "slo": {"ttft_ms": 500, "tpot_ms": 50},
+        "scheduler": {"policy": policy, "token_budget": 2048},
+        "cost_model": {"truth": {"a_ms": 5.0, "b_ms_per_token": 0.05,
+                                 "c_ms_per_context_token": 0.0001},
+                       "noise_amplitude": 0.03},
+        "cluster": {"nodes": nodes, "policy": "pab_lb"},
+        "run": {"horizon_ms": 3600000, "seed": 42},
+    }
+
+
+def test_host_scenario_config_errors(tmp_path):
+    """Schema violations are ConfigError (exit 1) before any device work --
+    unknown keys, missing sections, bad policies (scenario.cpp:77-222)."""
+    import json
+    bad = _scenario(1, "fairbatch")
+    bad["run"]["horizon"] = 5
+    for j in (bad, {k: v for k, v in _scenario(1, "fairbatch").items() if k != "slo"},
+              dict(_scenario(1, "fairbatch"), scheduler={"policy": "fifo"})):
+        f = tmp_path / "bad.json"
+        f.write_text(json.dumps(j))
+        p = _run("scenario", str(f))
+        assert p.returncode == 1 and "config error" in p.stderr, (p.returncode, p.stderr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nodes,policy", [(1, "fairbatch"), (1, "fairbatch_pab"), (4, "fairbatch_pab")])
+def test_host_scenario_matches_python(tmp_path, fb, nodes, policy):
+    """load_scenario + run_scenario through the C++ API report exactly what
+    the Python driver (pinned against the reference's acceptance criteria)
+    reports for the same scenario file."""
+    import json
+    from paper_2510_14392_b200.scenario import load_scenario, run_scenario
+    f = tmp_path / "sc.json"
+    f.write_text(json.dumps(_scenario(nodes, policy)))
+    p = _run("scenario", str(f))
+    assert p.returncode == 0, p.stderr
+    got = json.loads(p.stdout.strip().splitlines()[-1])
+    rep = run_scenario(load_scenario(str(f)))
+    assert got["total"] == rep.total_requests and got["good"] == rep.good
+    assert got["rejected"] == rep.rejected and got["finished"] == rep.finished
+    assert got["offered"] == rep.offered_rps and got["effective"] == rep.effective_rps
+    assert got["ttft"] == [rep.ttft.p50, rep.ttft.p95, rep.ttft.p99, rep.ttft.count]
+    assert got["tpot"] == [rep.max_tpot.p50, rep.max_tpot.p95, rep.max_tpot.p99,
+                           rep.max_tpot.count]
