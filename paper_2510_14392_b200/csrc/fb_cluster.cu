@@ -100,6 +100,15 @@ cudaError_t launch_cluster_serial(const EngineParams& p, const ClusterParamsHost
   return cudaGetLastError();
 }
 
+#ifdef FB_CLUSTER_PROF
+extern "C" int fb_debug_cluster_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_cluster_prof, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(g_cluster_prof, z, sizeof(z));
+  return static_cast<int>(cudaDeviceSynchronize());
+}
+#endif
+
 // ------------------------------------------------- pure scheduler kernels
 
 __device__ __forceinline__ Scratch set_scratch(unsigned char* smem_warp, unsigned char* g,

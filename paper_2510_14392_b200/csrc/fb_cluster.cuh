@@ -45,6 +45,10 @@ struct __align__(16) NodeReport {
   int32_t bz;     // node busy when the global clock reaches t_a
 };
 
+#ifdef FB_CLUSTER_PROF
+__device__ unsigned long long g_cluster_prof[8];
+#endif
+
 struct ClusterParams {
   int32_t n_nodes, lb_policy, interval, report_cap;
   int64_t latency, horizon, n_rows, n_epochs;
@@ -73,6 +77,10 @@ struct ClusterParams {
 
 // Router view (replicated per CTA) + the CTA's routing results.
 struct RouterSmem {
+  // one thread-block cluster (hw_cluster): every node's NodeReport of epoch
+  // e is stored straight into every CTA's slot e&1 (distributed shared
+  // memory), so the routers read their reports from local shared memory
+  NodeReport xrep[2][kClusterMaxNodes];
   int64_t v_t[kClusterMaxNodes], v_pab[kClusterMaxNodes], v_wait[kClusterMaxNodes];
   int64_t v_run[kClusterMaxNodes], v_dec[kClusterMaxNodes], v_inc[kClusterMaxNodes];
   int32_t v_has[kClusterMaxNodes];
@@ -263,7 +271,8 @@ __device__ __forceinline__ void node_begin(const EngineParams& P, ClusterNode& n
 // Phase A for one node: events before t_a, the completion at t_a, and the
 // NodeReport of epoch e stored into every rank's exchange buffer.
 __device__ void node_phase_a(const EngineParams& P, const ClusterParams& C, ClusterNode& nd,
-                             int64_t e, int64_t t_a, int32_t* cmp_out, int32_t* status) {
+                             RouterSmem& rs, int64_t e, int64_t t_a, int32_t* cmp_out,
+                             int32_t* status) {
   Inst& w = nd.w;
   while (w.S.busy && w.S.step_end < t_a) {
     const int64_t t = w.S.step_end;
@@ -292,13 +301,41 @@ __device__ void node_phase_a(const EngineParams& P, const ClusterParams& C, Clus
     ++h;
   }
   nd.rep_head = h;
-  // lane p stores the 32-byte report into rank p's buffer
-  if (lane_id() < C.n_ranks) {
+  if (C.hw_cluster) {
+    // lane p stores the report into CTA p's shared memory (DSMEM)
+    if (lane_id() < C.total_ctas) {
+      const uint32_t local = static_cast<uint32_t>(
+          __cvta_generic_to_shared(&rs.xrep[e & 1][C.node_lo + w.id]));
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                   : "=r"(remote) : "r"(local), "r"(static_cast<uint32_t>(lane_id())));
+      const int4* v = reinterpret_cast<const int4*>(&nr);
+      const int4 a = v[0], b = v[1];
+      asm volatile("st.shared::cluster.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(remote), "r"(a.x),
+                   "r"(a.y), "r"(a.z), "r"(a.w) : "memory");
+      asm volatile("st.shared::cluster.v4.s32 [%0+16], {%1, %2, %3, %4};" ::"r"(remote), "r"(b.x),
+                   "r"(b.y), "r"(b.z), "r"(b.w) : "memory");
+    }
+  } else if (lane_id() < C.n_ranks) {  // lane p stores into rank p's buffer
     NodeReport* dst = xchg_reports(C.xbuf[lane_id()], C.n_nodes, e) + C.node_lo + w.id;
     *dst = nr;
     if (C.n_ranks > 1) __threadfence_system();
   }
   __syncwarp();
+}
+
+// The 32-byte report of node i: from this CTA's shared memory (hw_cluster)
+// or from the exchange buffer in L2.
+__device__ __forceinline__ void load_report(const NodeReport* all, int i, bool local, int4& a,
+                                            int4& b) {
+  const int4* rp = reinterpret_cast<const int4*>(all + i);
+  if (local) {
+    a = rp[0];
+    b = rp[1];
+  } else {
+    a = __ldcg(rp);
+    b = __ldcg(rp + 1);
+  }
 }
 
 // Horizon rule (cluster.cpp:191-192): at t_a >= horizon the global loop only
@@ -308,7 +345,11 @@ __device__ __forceinline__ bool cluster_stopped(const ClusterParams& C, const No
                                                 int64_t t_a) {
   if (t_a < C.horizon) return false;
   int mine = 0;
-  for (int i = threadIdx.x; i < C.n_nodes; i += blockDim.x) mine |= __ldcg(&all[i].bz);
+  for (int i = threadIdx.x; i < C.n_nodes; i += blockDim.x) {
+    int4 a, b;
+    load_report(all, i, C.hw_cluster != 0, a, b);
+    mine |= b.w;  // bz
+  }
   return __syncthreads_or(mine) == 0;
 }
 
@@ -410,8 +451,8 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
   const int n = C.n_nodes;
   for (int i = lane_id(); i < n; i += kWarp) {
     // the whole 32-byte report in two 16-byte loads (one round trip)
-    const int4* rp = reinterpret_cast<const int4*>(all + i);
-    const int4 a = __ldcg(rp), b = __ldcg(rp + 1);
+    int4 a, b;
+    load_report(all, i, C.hw_cluster != 0, a, b);
     if (b.z) {  // fresh
       const int64_t t = (static_cast<int64_t>(a.y) << 32) | static_cast<uint32_t>(a.x);
       if (!(rs.v_has[i] && t < rs.v_t[i])) {
@@ -472,10 +513,19 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
   __syncthreads();
   int64_t e = 0;
   bool ok = true;
+#ifdef FB_CLUSTER_PROF
+  uint64_t pt0 = global_ns(), pacc[6] = {0, 0, 0, 0, 0, 0};
+  // [0] phase A (own node), [1] barrier wait, [2] report read + stop test,
+  // [3] routing, [4] phase C (own node), [5] epochs
+#define CPT(k) { const uint64_t n_ = global_ns(); pacc[k] += n_ - pt0; pt0 = n_; }
+#else
+#define CPT(k)
+#endif
   for (; e < C.n_epochs; ++e) {
     const int64_t t_a = C.epoch_t[e];
     int32_t cmp = 0;
-    if (owner) node_phase_a(P, C, nd, e, t_a, &cmp, &status);
+    if (owner) node_phase_a(P, C, nd, rs, e, t_a, &cmp, &status);
+    CPT(0)
     if (C.hw_cluster) {
       // the grid is one thread-block cluster: the hardware cluster barrier
       // (release / acquire at cluster scope orders the report stores of
@@ -485,10 +535,14 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     } else if (!(ok = cluster_barrier(C, rs, e))) {
       break;
     }
-    const NodeReport* all = xchg_reports(C.xbuf[C.rank], C.n_nodes, e);
+    CPT(1)
+    const NodeReport* all =
+        C.hw_cluster ? rs.xrep[e & 1] : xchg_reports(C.xbuf[C.rank], C.n_nodes, e);
     if (cluster_stopped(C, all, t_a)) break;
+    CPT(2)
     if (warp == 0) cluster_route(P, C, rs, all, e, node_base);
     __syncthreads();
+    CPT(3)
     if (owner && (rs.got[warp] || cmp)) {  // Node::enqueue (visible at t_a), begin_step(t_a)
       Inst& w = nd.w;
       w.S.arr = rs.n_routed[warp];
@@ -497,7 +551,14 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     }
     __syncwarp();
     if (owner && lane_id() == 0) rs.got[warp] = 0;
+    CPT(4)
   }
+#ifdef FB_CLUSTER_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int k = 0; k < 5; ++k) g_cluster_prof[k] += pacc[k];
+    g_cluster_prof[5] += e;
+  }
+#endif
   if (owner) {
     Inst& w = nd.w;
     if (ok) {  // all arrivals routed (or the loop stopped): run to quiescence
