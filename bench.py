@@ -223,6 +223,32 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
                 "k1_views_achieved": k1_ach, "k1_views_frac": k1_ach / peak}}
 
 
+def bench_c5(reps: int = 3) -> dict:
+    """Secondary line item: BASELINE config 5, the 64-node cluster (one GPU;
+    the grid is one thread-block cluster), next to the reference's
+    single-threaded run_cluster on this host."""
+    from paper_2510_14392_b200 import cluster
+    rows, cfgs, lb, hz = cluster.c5()
+    best, out = 1e30, None
+    for _ in range(reps):
+        out = cluster.run_cluster(rows, cfgs, lb, hz)
+        best = min(best, out.device_ms)
+    steps = int(out.node_results["steps"].sum())
+    line = {"workload": "C5: 64-node cluster, pab_lb, 11,694 requests, 11,690 dispatch epochs",
+            "value": steps / (best / 1000.0), "unit": "node-steps/s", "ms_per_pass": best,
+            "node_steps": steps}
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from backends import REF_SO, RefLib
+    if os.path.exists(REF_SO):
+        t0 = time.perf_counter()
+        RefLib().run_cluster(rows, cfgs, lb, hz)
+        dt = time.perf_counter() - t0
+        line["cpu_reference"] = {"value": steps / dt, "unit": "node-steps/s", "cores": 1,
+                                 "kind": "reference",
+                                 "sample": f"the whole C5 run_cluster in {dt:.2f} s (sequential)"}
+    return line
+
+
 def run_reference(args) -> None:
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -398,6 +424,7 @@ def run_ours(args) -> None:
         }
         if ws == 1 and not args.no_c4:
             line["c4"] = bench_c4(peak, peak_kind)
+            line["c5"] = bench_c5()
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(batch, os.cpu_count() or 1, args.ref_budget_s)
             # the single-core figure beside the all-cores one
