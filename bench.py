@@ -113,15 +113,19 @@ def measured_peak_hbm() -> tuple[float, str]:
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """DRAM bytes per engine launch from the committed ncu --set full summary."""
+def ncu_summary() -> dict:
+    """The committed ncu --set full summary of the engine kernel."""
     path = os.path.join(ROOT, "profiles", "engine_ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+            return json.load(f)
     except (OSError, ValueError):
-        return None
+        return {}
+
+
+def ncu_traffic():
+    """DRAM bytes per engine launch from the committed ncu --set full summary."""
+    return ncu_summary().get("dram_bytes_per_launch")
 
 
 def cpu_baseline(batch, n_threads: int, budget_s: float = 15.0) -> dict:
@@ -412,7 +416,11 @@ def run_ours(args) -> None:
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
                          "kernel": "engine_kernel", "kernel_ms": eng,
-                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
+                         "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
+                         # the working set is L2-resident: the binding limit is
+                         # instruction issue (ncu, profiles/engine_ncu_summary.json)
+                         "issue_active_pct": ncu_summary().get("issue_active_pct"),
+                         "l2_hit_rate_pct": ncu_summary().get("lts_hit_rate_pct")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": pipe_ms,
                     "mode": "pipelined: 2 arenas, step k+1 upload overlaps step k run",
