@@ -345,6 +345,41 @@ static int run_clusterlogs(const char* in_path, const std::string& out_dir) {
   return 0;
 }
 
+// IN: K, then K instance blocks in eventlog's format.  NodeBatch over all
+// of them; prints per instance "steps digest n_rejected" (hex digest).
+static int run_batch_digests(const char* in_path) {
+  std::ifstream in(in_path);
+  size_t k;
+  in >> k;
+  std::vector<Trace> traces(k);
+  std::vector<EngineConfig> cfgs;
+  TimeUs horizon = 0;
+  for (size_t i = 0; i < k; ++i) {
+    in >> horizon;
+    cfgs.push_back(read_cfg(in));
+    size_t n;
+    in >> n;
+    for (size_t j = 0; j < n; ++j) {
+      Request r;
+      r.id = static_cast<int64_t>(j);
+      in >> r.arrival >> r.prompt_len >> r.output_len >> r.ttft_slo >> r.tpot_slo;
+      traces[i].requests.push_back(r);
+    }
+  }
+  if (!in) {
+    std::fprintf(stderr, "bad input\n");
+    return 2;
+  }
+  std::vector<const Trace*> tp;
+  for (const Trace& t : traces) tp.push_back(&t);
+  NodeBatch nb(tp, cfgs, horizon);
+  nb.run();
+  for (const NodeSummary& s : nb.summaries())
+    std::printf("%llu %016llx %lld\n", static_cast<unsigned long long>(s.steps),
+                static_cast<unsigned long long>(s.plan_digest), static_cast<long long>(s.n_rejected));
+  return 0;
+}
+
 // run_scenario on a scenario file; one line of report fields.
 static int run_scenario_file(const char* path) {
   try {
@@ -374,6 +409,7 @@ int main(int argc, char** argv) {
     if (mode == "eventlog" && argc == 4) return run_eventlog(argv[2], argv[3]);
     if (mode == "clusterlogs" && argc == 4) return run_clusterlogs(argv[2], argv[3]);
     if (mode == "scenario" && argc == 3) return run_scenario_file(argv[2]);
+    if (mode == "batch" && argc == 3) return run_batch_digests(argv[2]);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught: %s\n", e.what());
     return 3;

@@ -171,3 +171,36 @@ def test_host_scenario_matches_python(tmp_path, fb, nodes, policy):
     assert got["ttft"] == [rep.ttft.p50, rep.ttft.p95, rep.ttft.p99, rep.ttft.count]
     assert got["tpot"] == [rep.max_tpot.p50, rep.max_tpot.p95, rep.max_tpot.p99,
                            rep.max_tpot.count]
+
+
+@pytest.mark.gpu
+def test_host_node_batch_matches_arena(tmp_path, fb):
+    """NodeBatch (the C++ step machine over many nodes) on C2 instances: every
+    instance's step count, plan digest and reject count equal the Python
+    arena's (which the oracle and golden fixtures pin)."""
+    from paper_2510_14392_b200 import workloads
+    batch = workloads.c2_batch(n_seeds=24, seed0=300)
+    hz = {int(batch.instance(i).horizon_us) for i in range(batch.n_instances)}
+    assert len(hz) == 1
+    src = tmp_path / "batch.txt"
+    r = batch.rows
+    with open(src, "w") as f:
+        f.write(f"{batch.n_instances}\n")
+        for i in range(batch.n_instances):
+            inst = batch.instance(i)
+            off, n = int(inst.trace_off), int(inst.n_req)
+            f.write(f"{inst.horizon_us}\n" + _cfg_line(inst.cfg) + f"{n}\n")
+            for k in range(off, off + n):
+                f.write(f"{r.arrival_us[k]} {r.prompt_len[k]} {r.output_len[k]} {r.ttft_us[k]} "
+                        f"{r.tpot_us[k]}\n")
+    p = _run("batch", str(src))
+    assert p.returncode == 0, p.stderr
+    got = [ln.split() for ln in p.stdout.strip().splitlines()]
+    a = fb.Arena(0)
+    a.load(batch)
+    a.run()
+    res = a.results()
+    a.close()
+    want = [[str(int(x["steps"])), "%016x" % int(x["plan_digest"]), str(int(x["n_rejected"]))]
+            for x in res]
+    assert got == want
