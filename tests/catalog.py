@@ -197,6 +197,11 @@ def reroute_cluster_cases(gen):
         cfgs = [engine_config("fairbatch_pab", 2048, MODEL, 500, 50) for _ in range(nn)]
         out.append((name, rows_o, cfgs, LbConfig(pol, 1, lat, retry_reroute=True),
                     ms_to_us(3.6e6)))
+    # noise, max_active and a report interval of 2 under rerouting
+    cfgs = [engine_config("fairbatch_pab", 2048, MODEL, 500, 50, noise_amplitude=0.04,
+                          noise_seed=11 + i, max_active=(0, 12, 0, 20)[i]) for i in range(4)]
+    out.append(("rr_mixed_4", rows_o, cfgs, LbConfig("pab_lb", 2, 10.0, retry_reroute=True),
+                ms_to_us(3.6e6)))
     # the same overload without rerouting (rejected requests stay rejected)
     cfgs = [engine_config("fairbatch_pab", 2048, MODEL, 500, 50) for _ in range(4)]
     out.append(("rr_off_pab0_4", rows_o, cfgs, LbConfig("pab_lb", 1, 0.0), ms_to_us(3.6e6)))

@@ -309,7 +309,7 @@ def gpu_reroute_cases(fb):
 
 
 @pytest.mark.parametrize("name", ["rr_giant_2", "rr_pab0_4", "rr_pab30_3", "rr_count0_4",
-                                  "rr_off_pab0_4"])
+                                  "rr_mixed_4", "rr_off_pab0_4"])
 def test_cluster_reroute_matches_golden(golden, gpu_reroute_cases, name):
     """retry_reroute (cluster.cpp:222-237) on the serial cluster engine:
     digests, routing (last target) and merged records equal the reference's."""
@@ -333,7 +333,7 @@ def test_clusters_side_by_side_match_golden(golden, gpu_cluster_cases, gpu_rerou
 
 
 @pytest.mark.parametrize("name", ["pab0_8", "count37_3", "pab5000_8", "pab_hz10s_8", "pab20_2",
-                                  "rr_giant_2", "rr_pab30_3"])
+                                  "rr_giant_2", "rr_pab30_3", "rr_mixed_4"])
 def test_cluster_logs_match_reference(golden, gpu_cluster_cases, gpu_reroute_cases, name):
     """ClusterResult's logs from the device run: every node's EventLog
     (save_event_log) and the routing log with view snapshots

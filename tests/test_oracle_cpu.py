@@ -334,7 +334,7 @@ def reroute_case_list(oracle):
 
 
 @pytest.mark.parametrize("name", ["rr_giant_2", "rr_pab0_4", "rr_pab30_3", "rr_count0_4",
-                                  "rr_off_pab0_4"])
+                                  "rr_mixed_4", "rr_off_pab0_4"])
 def test_oracle_reroute_matches_golden(oracle, golden, reroute_case_list, name):
     """retry_reroute (cluster.cpp:222-237): a first rejection is routed once
     more at the same instant; digests, routing and records equal the reference's."""

@@ -106,4 +106,4 @@ def replay_canonical(violations):
 # run_cluster cases whose node event logs and routing log (save_event_log /
 # save_routing_log) are pinned byte for byte.
 CLUSTER_LOG_CASES = ("pab0_8", "count37_3", "pab5000_8", "pab_hz10s_8", "pab20_2", "rr_giant_2",
-                     "rr_pab30_3")
+                     "rr_pab30_3", "rr_mixed_4")
