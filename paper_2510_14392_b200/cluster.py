@@ -273,9 +273,19 @@ def run_clusters(cases, device: int = 0) -> list[ClusterOutput]:
     amortise the epoch latency).  `cases` holds (rows, cfgs, lb, horizon_us);
     the outputs equal run_cluster's case by case."""
     shards = []
+    L = fbgpu.lib()
     try:
         for rows, cfgs, lb, hz in cases:
             shards.append(ClusterShard(rows, cfgs, lb, hz, 0, 1, device))
+        # one-cluster grids only while they all fit the device at once (more
+        # would run in waves): otherwise every shard takes the cooperative grid
+        fit = C.c_int32(0)
+        fbgpu._check(L.fb_cluster_max_hw_clusters(device, max(len(c[1]) for c in cases),
+                                                  C.byref(fit)), "fb_cluster_max_hw_clusters")
+        if len(cases) > fit.value:
+            for sh in shards:
+                fbgpu._check(L.fb_cluster_shard_allow_hw_cluster(sh._h, 0),
+                             "fb_cluster_shard_allow_hw_cluster")
         for sh in shards:
             sh.reset()
         for sh in shards:

@@ -733,6 +733,7 @@ struct fb_cluster_shard {
   int64_t nr = 0;
   int blocks = 0;
   bool connected = false, launched = false;
+  bool allow_hw = true;  // one thread-block cluster when the grid fits one
   fbgpu::ClusterParamsHost cp{};
   std::vector<void*> bufs;    // device allocations
   std::vector<void*> opened;  // CUDA-IPC peer mappings
@@ -923,6 +924,22 @@ static int shard_create(int device, const fb_trace* rows, const fb_engine_config
 
 extern "C" {
 
+int fb_cluster_shard_allow_hw_cluster(fb_cluster_shard* s, int32_t allow) {
+  if (!s) return set_error(FB_ERR_USAGE, "fb_cluster_shard_allow_hw_cluster: null shard");
+  s->allow_hw = allow != 0;
+  return FB_OK;
+}
+
+int fb_cluster_max_hw_clusters(int device, int32_t n_nodes, int32_t* out) {
+  if (!out || n_nodes < 1) return set_error(FB_ERR_USAGE, "fb_cluster_max_hw_clusters: bad arguments");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return set_error(FB_ERR_CUDA, "no CUDA device available (the product path has no CPU fallback)");
+  FB_CUDA(cudaSetDevice(device));
+  *out = fbgpu::cluster_max_hw_clusters(n_nodes);
+  return FB_OK;
+}
+
 int fb_cluster_shard_exchange_handle(fb_cluster_shard* s, void* handle_out) {
   if (!s || !handle_out) return set_error(FB_ERR_USAGE, "fb_cluster_shard_exchange_handle: bad arguments");
   static_assert(sizeof(cudaIpcMemHandle_t) == FB_IPC_HANDLE_BYTES, "IPC handle size");
@@ -998,7 +1015,7 @@ int fb_cluster_shard_launch(fb_cluster_shard* s) {
   if (s->cp.retry_reroute) {
     FB_CUDA(fbgpu::launch_cluster_serial(s->a->params(0), s->cp, q));
   } else {
-    FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q));
+    FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q, s->allow_hw));
   }
   FB_CUDA(cudaEventRecord(s->a->ev1, q));
   s->launched = true;

@@ -40,8 +40,35 @@ size_t cluster_smem_bytes(int warps_per_cta) {
          static_cast<size_t>(warps_per_cta) * kSmemSlots * kScratchBytesPerSlot;
 }
 
+int cluster_max_hw_clusters(int n_nodes) {
+  const int wpc = cluster_warps_per_cta(n_nodes, 1);
+  const int blocks = (n_nodes + wpc - 1) / wpc;
+  if (blocks > 8) return 0;
+  const size_t smem = cluster_smem_bytes(wpc);
+  if (cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kWarp * wpc);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = blocks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, cluster_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, int blocks,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool allow_hw) {
   static_assert(sizeof(ClusterParamsHost) == sizeof(ClusterParams), "cluster params layout");
   ClusterParams c;
   std::memcpy(&c, &ch, sizeof(c));
@@ -56,7 +83,7 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, i
   // the hardware cluster barrier per epoch.  Otherwise a cooperative launch
   // (every CTA co-resident) with the global-memory exchange barrier.
   constexpr int kHwClusterMax = 8;  // portable cluster size
-  if (c.n_ranks == 1 && blocks <= kHwClusterMax && !std::getenv("FB_NO_HW_CLUSTER")) {
+  if (allow_hw && c.n_ranks == 1 && blocks <= kHwClusterMax && !std::getenv("FB_NO_HW_CLUSTER")) {
     c.hw_cluster = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);

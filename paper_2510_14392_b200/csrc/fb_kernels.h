@@ -154,8 +154,11 @@ int cluster_warps_per_cta(int n_nodes, int n_ranks);
 size_t cluster_smem_bytes(int warps_per_cta);
 cudaError_t launch_cluster_serial(const EngineParams& p, const ClusterParamsHost& c,
                                   cudaStream_t st);
+// allow_hw: a one-rank grid of <= 8 CTAs may run as one thread-block cluster.
 cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& c, int blocks,
-                           cudaStream_t st);
+                           cudaStream_t st, bool allow_hw = true);
+// How many one-cluster grids of an n_nodes cluster fit the device at once.
+int cluster_max_hw_clusters(int n_nodes);
 // Warp engine, then the grid-wide wide engine; `between` (may be null) is
 // recorded between the two launches.
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g,

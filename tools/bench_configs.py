@@ -3,6 +3,7 @@ reference CPU code on this host.  Prints one JSON object per config.
 
     python tools/bench_configs.py [c1 c3 c4 c5]
 """
+import ctypes as C
 import json
 import os
 import sys
@@ -119,7 +120,10 @@ def main(which):
         best, steps = 1e30, 0
         for _ in range(3):
             shards = [cluster.ClusterShard(r, c, l, h, 0, 1) for r, c, l, h in cases]
-            for sh in shards:
+            fit = C.c_int32(0)
+            fbgpu.lib().fb_cluster_max_hw_clusters(0, len(cases[0][1]), C.byref(fit))
+            for sh in shards:  # as run_clusters: one-cluster grids only if all fit
+                fbgpu.lib().fb_cluster_shard_allow_hw_cluster(sh._h, int(R <= fit.value))
                 sh.reset()
             t0 = time.perf_counter()
             for sh in shards:
