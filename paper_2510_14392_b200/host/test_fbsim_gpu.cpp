@@ -380,6 +380,39 @@ static int run_batch_digests(const char* in_path) {
   return 0;
 }
 
+// IN as for `batch` (all instances share the horizon); run_nodes over all of
+// them, each log written with save_event_log to DIR/out<i>.jsonl.
+static int run_eventlogs(const char* in_path, const std::string& out_dir) {
+  std::ifstream in(in_path);
+  size_t k;
+  in >> k;
+  std::vector<Trace> traces(k);
+  std::vector<EngineConfig> cfgs;
+  TimeUs horizon = 0;
+  for (size_t i = 0; i < k; ++i) {
+    in >> horizon;
+    cfgs.push_back(read_cfg(in));
+    size_t n;
+    in >> n;
+    for (size_t j = 0; j < n; ++j) {
+      Request r;
+      r.id = static_cast<int64_t>(j);
+      in >> r.arrival >> r.prompt_len >> r.output_len >> r.ttft_slo >> r.tpot_slo;
+      traces[i].requests.push_back(r);
+    }
+  }
+  if (!in) {
+    std::fprintf(stderr, "bad input\n");
+    return 2;
+  }
+  std::vector<const Trace*> tp;
+  for (const Trace& t : traces) tp.push_back(&t);
+  const std::vector<EventLog> logs = run_nodes(tp, cfgs, horizon);
+  for (size_t i = 0; i < logs.size(); ++i)
+    save_event_log(logs[i], out_dir + "/out" + std::to_string(i) + ".jsonl");
+  return 0;
+}
+
 // run_scenario on a scenario file; one line of report fields.
 static int run_scenario_file(const char* path) {
   try {
@@ -410,6 +443,7 @@ int main(int argc, char** argv) {
     if (mode == "clusterlogs" && argc == 4) return run_clusterlogs(argv[2], argv[3]);
     if (mode == "scenario" && argc == 3) return run_scenario_file(argv[2]);
     if (mode == "batch" && argc == 3) return run_batch_digests(argv[2]);
+    if (mode == "eventlogs" && argc == 4) return run_eventlogs(argv[2], argv[3]);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught: %s\n", e.what());
     return 3;

@@ -66,16 +66,38 @@ def _instance_file(path, batch: Batch, i: int):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["pab_overload", "c1"])
 def test_host_api_event_logs_match_reference(golden, tmp_path, fb, name):
-    """run_node + save_event_log through the C++ API: byte-identical to the
+    """run_node on the single-instance path and run_nodes batched, each log
+    written with save_event_log through the C++ API: byte-identical to the
     reference's own writer (sha256 per instance, golden.json)."""
     batch = SCENARIOS[name](fb.generate_bursty)
-    for i in range(batch.n_instances):
-        src, out = tmp_path / f"in{i}.txt", tmp_path / f"out{i}.jsonl"
-        _instance_file(src, batch, i)
-        p = _run("eventlog", str(src), str(out))
+    src = tmp_path / "in0.txt"  # run_node on instance 0 (one process)
+    _instance_file(src, batch, 0)
+    p = _run("eventlog", str(src), str(tmp_path / "single.jsonl"))
+    assert p.returncode == 0, p.stderr
+    assert hashlib.sha256((tmp_path / "single.jsonl").read_bytes()).hexdigest() == \
+        golden["event_logs"][name][0]
+    hz = {int(batch.instance(i).horizon_us) for i in range(batch.n_instances)}
+    groups = {h: [i for i in range(batch.n_instances) if int(batch.instance(i).horizon_us) == h]
+              for h in hz}
+    r = batch.rows
+    for h, idx in groups.items():  # run_nodes per horizon group
+        src = tmp_path / f"batch{h}.txt"
+        with open(src, "w") as f:
+            f.write(f"{len(idx)}\n")
+            for i in idx:
+                inst = batch.instance(i)
+                off, n = int(inst.trace_off), int(inst.n_req)
+                f.write(f"{inst.horizon_us}\n" + _cfg_line(inst.cfg) + f"{n}\n")
+                for k in range(off, off + n):
+                    f.write(f"{r.arrival_us[k]} {r.prompt_len[k]} {r.output_len[k]} "
+                            f"{r.ttft_us[k]} {r.tpot_us[k]}\n")
+        out = tmp_path / f"logs{h}"
+        out.mkdir()
+        p = _run("eventlogs", str(src), str(out))
         assert p.returncode == 0, p.stderr
-        got = hashlib.sha256(out.read_bytes()).hexdigest()
-        assert got == golden["event_logs"][name][i], (name, i)
+        for j, i in enumerate(idx):
+            got = hashlib.sha256((out / f"out{j}.jsonl").read_bytes()).hexdigest()
+            assert got == golden["event_logs"][name][i], (name, i)
 
 
 def _cfg_line(c):
