@@ -177,6 +177,7 @@ __device__ __forceinline__ unsigned tile_match_any(unsigned v) {
   return __match_any_sync(tile_mask(), v) >> tile_base();
 }
 __device__ __forceinline__ unsigned tile_lanemask_lt() { return (1u << tile_lane()) - 1u; }
+__device__ __forceinline__ unsigned tile_or(unsigned v) { return __reduce_or_sync(tile_mask(), v); }
 template <typename T>
 __device__ __forceinline__ T tile_shfl(T v, int src) {
   return __shfl_sync(tile_mask(), v, src, kTile);

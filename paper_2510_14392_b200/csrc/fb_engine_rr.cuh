@@ -14,6 +14,9 @@
 
 namespace fbgpu {
 
+#ifndef FB_RANK_REUSE
+#define FB_RANK_REUSE 1  // C1 77.7 -> 74.9 ms, C2 35.55 -> 35.27 ms (tools/ab_time.py)
+#endif
 #ifndef FB_RANK_UNROLL
 #define FB_RANK_UNROLL 4  // 8: 36.2 ms, 16: 37.8 ms on C2 (code size)
 #endif
@@ -22,6 +25,7 @@ constexpr int kRankUnroll = FB_RANK_UNROLL;
 // One live request held by one lane.
 struct TaskReg {
   int32_t r, seq, prompt, output, prefilled, nidx, take;
+  int32_t rk;  // rank in the previous step's slack order, -1 unknown
   uint32_t flags;
   int64_t dl0;  // arrival + ttft_slo (TTFT deadline)
   int64_t tpot;
@@ -37,6 +41,7 @@ __device__ __forceinline__ void permute_task(TaskReg& t, int src) {
   t.prefilled = tile_shfl(t.prefilled, src);
   t.nidx = tile_shfl(t.nidx, src);
   t.take = tile_shfl(t.take, src);
+  t.rk = tile_shfl(t.rk, src);
   t.flags = tile_shfl(t.flags, src);
   t.dl0 = tile_shfl(t.dl0, src);
   t.tpot = tile_shfl(t.tpot, src);
@@ -58,6 +63,7 @@ __device__ __forceinline__ void fresh_task(const EngineParams& P, const Inst& w,
   t.prefilled = 0;
   t.nidx = 0;
   t.take = 0;
+  t.rk = -1;
   t.flags = 0;
   t.first = -1;
   t.maxtp = 0.0;
@@ -84,6 +90,7 @@ __device__ __forceinline__ void load_task(const EngineParams& P, const Inst& w, 
   const int64_t row = w.toff + v.x;
   t.r = v.x;
   t.take = v.y;
+  t.rk = -1;
   t.prompt = P.prompt[row];
   t.output = P.output[row];
   t.dl0 = P.arrival[row] + P.ttft[row];
@@ -153,6 +160,11 @@ __device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, Task
   if (P.lead_bucket > 0) lead_step(P, w, now, emit, fin, t.r, t.output);
   const unsigned finm = tile_ballot(fin);
   if (finm) {  // order-preserving removal from active_ (engine.cpp:228-229)
+#if FB_RANK_REUSE
+    // previous-order ranks stay dense over the remaining tasks
+    const unsigned gone = tile_or(fin && t.rk >= 0 ? 1u << t.rk : 0u);
+    if (t.rk >= 0) t.rk -= __popc(gone & ((1u << t.rk) - 1u));
+#endif
     const unsigned keep = tile_ballot(live && !fin);
     const int nk = __popc(keep);
     const int src = lane < nk ? static_cast<int>(__fns(keep, 0, lane + 1)) : lane;
@@ -302,34 +314,75 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   // prefill-first keys (group, seq) fit in 32 bits; fair-batching keys use
   // their high half when it is distinct across the visible tasks (the order of
   // distinct high halves is the order of the full keys).
-  uint64_t key;
-  uint32_t k32;
-  bool use32;
+#if FB_RANK_REUSE
+  // The previous step's order is usually still sorted (every admitted decode
+  // advances by one tpot, every prefill by the same clock): when the visible
+  // tasks carry dense previous ranks 0..A-1 and the keys increase along them,
+  // those ranks ARE the sort (keys are unique).  Otherwise rank by counting.
+  uint64_t key_r;
   if (fair) {
     const uint64_t g = (v.decode && v.slack < urgency) ? 0 : (!v.decode ? 1 : 2);
-    key = (g << 62) | (static_cast<uint64_t>(v.slack + kPackSlack) << 22) |
-          static_cast<uint64_t>(t.seq);
-    k32 = vis ? static_cast<uint32_t>(key >> 32) : 0xffffffffu;  // visible hi <= 0xbfffffff
-    const unsigned same = tile_match_any(k32);
-    use32 = tile_all(!vis || same == (1u << lane));
+    key_r = (g << 62) | (static_cast<uint64_t>(v.slack + kPackSlack) << 22) |
+            static_cast<uint64_t>(t.seq);
   } else {
     const uint32_t g = policy == FB_POLICY_SARATHI ? (v.decode ? 0u : 1u) : 0u;
-    key = (static_cast<uint64_t>(g) << 62) | static_cast<uint64_t>(t.seq);
-    k32 = vis ? ((g << 30) | static_cast<uint32_t>(t.seq)) : 0xffffffffu;
-    use32 = true;
+    key_r = (static_cast<uint64_t>(g) << 62) | static_cast<uint64_t>(t.seq);
   }
-  if (!vis) key = ~uint64_t(0);
-  int rank = 0;
-  if (use32) {
-#pragma unroll kRankUnroll
-    for (int q = 0; q < A; ++q) rank += tile_shfl(k32, q) < k32;
+  if (!vis) key_r = ~uint64_t(0);
+  const bool rk_ok = !vis || (t.rk >= 0 && t.rk < A);
+  const unsigned rk_bits = tile_or(vis && rk_ok ? 1u << t.rk : 0u);
+  bool reuse = tile_all(rk_ok) && rk_bits == (A == 32 ? ~0u : (1u << A) - 1u);
+  if (reuse) {
+    s.order[vis ? t.rk : lane] = lane;
+    tile_sync();
+    const int nx = vis && t.rk + 1 < A ? s.order[t.rk + 1] : lane;
+    const uint64_t kn = tile_shfl(key_r, nx);
+    reuse = tile_all(!vis || t.rk + 1 >= A || key_r < kn);
+  }
+  int rank;
+  if (reuse) {
+    rank = vis ? t.rk : lane;
   } else {
-#pragma unroll kRankUnroll
-    for (int q = 0; q < A; ++q) rank += tile_shfl(key, q) < key;
+#endif
+  uint64_t key;
+    uint32_t k32;
+    bool use32;
+    if (fair) {
+      const uint64_t g = (v.decode && v.slack < urgency) ? 0 : (!v.decode ? 1 : 2);
+      key = (g << 62) | (static_cast<uint64_t>(v.slack + kPackSlack) << 22) |
+            static_cast<uint64_t>(t.seq);
+      k32 = vis ? static_cast<uint32_t>(key >> 32) : 0xffffffffu;  // visible hi <= 0xbfffffff
+      const unsigned same = tile_match_any(k32);
+      use32 = tile_all(!vis || same == (1u << lane));
+    } else {
+      const uint32_t g = policy == FB_POLICY_SARATHI ? (v.decode ? 0u : 1u) : 0u;
+      key = (static_cast<uint64_t>(g) << 62) | static_cast<uint64_t>(t.seq);
+      k32 = vis ? ((g << 30) | static_cast<uint32_t>(t.seq)) : 0xffffffffu;
+      use32 = true;
+    }
+    if (!vis) key = ~uint64_t(0);
+#if FB_RANK_REUSE
+    rank = 0;
+#else
+    int rank = 0;
+#endif
+    if (use32) {
+  #pragma unroll kRankUnroll
+      for (int q = 0; q < A; ++q) rank += tile_shfl(k32, q) < k32;
+    } else {
+  #pragma unroll kRankUnroll
+      for (int q = 0; q < A; ++q) rank += tile_shfl(key, q) < key;
+    }
+    if (!vis) rank = lane;
+#if FB_RANK_REUSE
+    tile_sync();  // the reuse check read s.order
+#endif
+    s.order[rank] = lane;
+    tile_sync();
+#if FB_RANK_REUSE
   }
-  if (!vis) rank = lane;
-  s.order[rank] = lane;
-  tile_sync();
+  t.rk = vis ? rank : -1;
+#endif
   const int pk = s.order[lane];  // view position at sorted rank `lane` (k < A)
 
   // K3: sorted costs (sched.cpp:142-144) -> shared scratch -> greedy scan
