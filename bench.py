@@ -26,6 +26,9 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# 32 hardware work queues: the C5 replica item runs 16 cluster simulations
+# on their own streams (must be set before the CUDA context exists)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
@@ -128,39 +131,89 @@ def ncu_traffic():
     return ncu_summary().get("dram_bytes_per_launch")
 
 
-def cpu_baseline(batch, n_threads: int, budget_s: float = 15.0) -> dict:
-    """The reference's own CPU run_node + request_reports (oracle/_ref, the
-    unmodified library) on a bounded sample of the same instances, all host
-    threads; falls back to the C oracle port when the reference was not built."""
+def ref_lib():
+    """The reference's own CPU implementation (oracle/_ref, compiled unmodified
+    from /root/reference), else the C oracle port (kind "port")."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from backends import REF_SO, OracleLib, RefLib
-
     if os.path.exists(REF_SO):
-        lib, kind = RefLib(), "reference"
-        runner = lambda b: lib.run_node_batch(b, nthreads=n_threads)  # noqa: E731
-    else:
-        lib, kind = OracleLib(), "port"
-        runner = lambda b: lib.run(b, nthreads=n_threads)  # noqa: E731
-    # probe with a few instances, then size the sample to ~budget_s
+        return RefLib(), "reference"
+    return OracleLib(), "port"
+
+
+def ref_batch_runner(lib, kind, n_threads):
+    if kind == "reference":
+        return lambda b: lib.run_node_batch(b, nthreads=n_threads)  # stock run_node
+    return lambda b: lib.run(b, nthreads=n_threads)
+
+
+def cpu_baseline(batch, n_threads: int, budget_s: float = 15.0, lib=None) -> dict:
+    """The reference's own CPU run_node + request_reports (oracle/_ref) on the
+    same instances with `n_threads` host threads: the whole batch when it fits
+    `budget_s`, else an evenly strided sample sized to it.  Returns the line
+    plus the run's outputs (`_out`, `_sel`) for the parity check."""
+    if lib is None:
+        lib = ref_lib()
+    lib, kind = lib
+    runner = ref_batch_runner(lib, kind, n_threads)
     n_total = batch.n_instances
     take = min(n_total, max(2 * n_threads, 64))
-    best = None
     while True:
         sel = list(range(0, n_total, max(1, n_total // take)))[:take]
-        sub = batch.subset(sel)
+        sub = batch if len(sel) == n_total else batch.subset(sel)
         t0 = time.perf_counter()
         out = runner(sub)
         dt = time.perf_counter() - t0
         steps = int(out.results["steps"].sum())
-        best = (steps, dt, len(sel))
         if dt >= budget_s / 3 or take >= n_total:
             break
         take = min(n_total, int(take * max(2.0, (budget_s / 2) / max(dt, 1e-3))))
-    steps, dt, n = best
     return {"value": steps / dt, "unit": UNIT, "cores": n_threads, "kind": kind,
-            "sample": f"{n} of {n_total} C2 instances ({steps} instance-steps) in {dt:.2f} s, "
+            "sample": f"{len(sel)} of {n_total} instances ({steps} instance-steps) in {dt:.2f} s, "
                       f"{n_threads} threads, {os.cpu_count()} host CPUs",
-            "cpu_model": cpu_model()}
+            "cpu_model": cpu_model(), "_out": out, "_sel": sel}
+
+
+def live_parity(gpu_res, gpu_rec, batch, out, sel) -> dict:
+    """Per-instance step / arrival / reject counts, incomplete flags and the
+    per-request records of the GPU run against the reference's stock
+    run_node + request_reports on the same instances."""
+    keys = ("steps", "n_arrived", "n_rejected", "incomplete")
+    off = batch.record_offsets()
+    g = gpu_res[sel]
+    ok = {k: bool(np.array_equal(g[k].astype(np.int64), out.results[k].astype(np.int64)))
+          for k in keys}
+    rec = np.concatenate([gpu_rec[off[i]:off[i + 1]] for i in sel]) if sel else gpu_rec[:0]
+    ok["records"] = bool(rec.tobytes() == out.records.tobytes())
+    return {"instances": len(sel), "equal": all(ok.values()), "fields": ok,
+            "against": "reference run_node + request_reports (oracle/_ref), live on this host"}
+
+
+def fixture_parity(name: str, batch, res, rec=None) -> dict:
+    """Per-instance plan digests (every step's batch composition, chunk sizes
+    and step times) against the committed reference fixture
+    tests/golden/full_size.json (made by tests/golden/make_golden_full.py from
+    oracle/_ref, checked against the real run_node)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from full_size import CONFIGS, canonical_results, chunk_digests
+    with open(os.path.join(ROOT, "tests", "golden", "full_size.json")) as f:
+        gold = json.load(f)[name]
+    chunk = CONFIGS[name]["chunk"]
+    if rec is not None:
+        got = chunk_digests(batch, res, rec, chunk)
+        rec_eq = got["records_sha256"] == gold["records_sha256"]
+    else:
+        import hashlib
+        can = canonical_results(res)
+        got = {"results_sha256": [hashlib.sha256(can[c:c + chunk].tobytes()).hexdigest()
+                                  for c in range(0, len(res), chunk)],
+               "total_steps": int(res["steps"].sum())}
+        rec_eq = None
+    eq = got["results_sha256"] == gold["results_sha256"]
+    return {"fixture": f"tests/golden/full_size.json:{name}", "instances": len(res),
+            "plan_digests_equal": bool(eq), "records_equal": rec_eq,
+            "total_steps": got["total_steps"], "reference_total_steps": gold["total_steps"],
+            "equal": bool(eq and rec_eq is not False and got["total_steps"] == gold["total_steps"])}
 
 
 def cpu_model() -> str:
@@ -174,12 +227,14 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
+def bench_c4(peak: float, peak_kind: str, reps: int = 3, cpu: bool = True) -> dict:
     """Secondary line item: BASELINE config 4 (decode-heavy, 64 nodes x 120k
     requests, > 77k visible tasks per step), the only configuration whose
     per-step working set exceeds L2, so the one whose slack/selection passes
     are HBM-bound.  Runs on the grid-wide wide engine; roofline over the
-    whole pass (both engine kernels, device events)."""
+    whole pass (both engine kernels, device events).  Parity: plan digests
+    against the reference fixture; with `cpu`, the reference's run_node on
+    all 64 instances with every host thread (measured, and compared)."""
     from paper_2510_14392_b200 import fbgpu, workloads
     batch = workloads.c4_batch(n_inst=64)
     arena = fbgpu.Arena(0)
@@ -196,6 +251,7 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
         wide.append(g)
         phases.append(arena.wide_phases()[0])
     r = arena.results()
+    rec = arena.records()
     arena.close()
     ph = {k: statistics.median(p[k] for p in phases) for k in phases[0]}
     # the slack/selection kernels proper: K1 views (envelope slack, key
@@ -211,7 +267,7 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
               + 64 * r["n_arrived"].sum())
     ms = statistics.median(tot)
     ach = alg / (ms / 1000.0) / 1e9
-    return {"workload": "C4: decode-heavy, 64 nodes x 120,000 requests, horizon 1.5 s",
+    line = {"workload": "C4: decode-heavy, 64 nodes x 120,000 requests, horizon 1.5 s",
             "value": steps / (ms / 1000.0), "unit": UNIT, "ms_per_pass": ms,
             "wide_engine_ms": statistics.median(wide), "instance_steps": steps,
             "mean_visible": float(r["sum_visible"].sum()) / max(steps, 1),
@@ -224,13 +280,24 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3) -> dict:
                 "bound": "hbm", "achieved": sel_ach, "peak": peak, "unit": "GB/s",
                 "frac": sel_ach / peak, "phases": "K1 views + K2a histogram + K2b gather",
                 "alg_bytes": sel_bytes, "ms": sel_ms,
-                "k1_views_achieved": k1_ach, "k1_views_frac": k1_ach / peak}}
+                "k1_views_achieved": k1_ach, "k1_views_frac": k1_ach / peak},
+            "parity": {"fixture": fixture_parity("c4_full", batch, r, rec)}}
+    if cpu:
+        lib = ref_lib()
+        nt = os.cpu_count() or 1
+        cb = cpu_baseline(batch, nt, budget_s=1e9, lib=lib)  # all 64 instances
+        out, sel = cb.pop("_out"), cb.pop("_sel")
+        line["cpu_reference"] = cb
+        line["parity"]["live"] = live_parity(r, rec, batch, out, sel)
+    return line
 
 
-def bench_c5(reps: int = 3) -> dict:
+def bench_c5(reps: int = 3, cpu: bool = True, n_rep: int = 16) -> dict:
     """Secondary line item: BASELINE config 5, the 64-node cluster (one GPU;
-    the grid is one thread-block cluster), next to the reference's
-    single-threaded run_cluster on this host."""
+    the grid is one thread-block cluster), next to the reference's own
+    single-threaded run_cluster on this host; plus `n_rep` copies side by
+    side (replicas, the multi-simulation throughput form) next to the
+    reference running the same copies on every host thread."""
     from paper_2510_14392_b200 import cluster
     rows, cfgs, lb, hz = cluster.c5()
     best, out = 1e30, None
@@ -241,29 +308,143 @@ def bench_c5(reps: int = 3) -> dict:
     line = {"workload": "C5: 64-node cluster, pab_lb, 11,694 requests, 11,690 dispatch epochs",
             "value": steps / (best / 1000.0), "unit": "node-steps/s", "ms_per_pass": best,
             "node_steps": steps}
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from backends import REF_SO, RefLib
-    if os.path.exists(REF_SO):
+    # replicas: one launch per copy on its own stream, all copies at once
+    cases = [(rows, cfgs, lb, hz)] * n_rep
+    cluster.run_clusters(cases)
+    t_rep = []
+    for _ in range(reps):
         t0 = time.perf_counter()
-        RefLib().run_cluster(rows, cfgs, lb, hz)
+        outs = cluster.run_clusters(cases)
+        t_rep.append(time.perf_counter() - t0)
+    rep_steps = sum(int(o.node_results["steps"].sum()) for o in outs)
+    line["replicas"] = {"copies": n_rep, "value": rep_steps / min(t_rep), "unit": "node-steps/s",
+                        "ms_per_pass": 1000.0 * min(t_rep),
+                        "timing": "host wall clock around run_clusters (upload, all launches, "
+                                  "fetch)"}
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from backends import REF_SO, RefLib, cluster_summary
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        gold = json.load(f)["clusters"]["c5_pab0_64"]
+    line["parity"] = {"fixture": {"fixture": "tests/golden/golden.json:clusters.c5_pab0_64",
+                                  "equal": cluster_summary(out) == gold and
+                                  all(cluster_summary(o) == gold for o in outs)}}
+    if cpu and os.path.exists(REF_SO):
+        ref = RefLib()
+        t0 = time.perf_counter()
+        res1, rec1 = ref.run_cluster_stock(rows, cfgs, lb, hz, 1, 1, records=True)
         dt = time.perf_counter() - t0
         line["cpu_reference"] = {"value": steps / dt, "unit": "node-steps/s", "cores": 1,
                                  "kind": "reference",
-                                 "sample": f"the whole C5 run_cluster in {dt:.2f} s (sequential)"}
+                                 "sample": f"the whole C5 run_cluster in {dt:.2f} s "
+                                           "(sequential by construction)"}
+        keys = ("steps", "n_arrived", "n_rejected", "incomplete")
+        line["parity"]["live"] = {
+            "equal": bool(all(np.array_equal(res1[0][k].astype(np.int64),
+                                             out.node_results[k].astype(np.int64)) for k in keys)
+                          and rec1.tobytes() == out.records.tobytes()),
+            "against": "reference run_cluster (stock) + request_reports, live on this host"}
+        nt = min(n_rep, os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        ref.run_cluster_stock(rows, cfgs, lb, hz, n_rep, nt)
+        dt = time.perf_counter() - t0
+        line["replicas"]["cpu_reference"] = {
+            "value": rep_steps / dt, "unit": "node-steps/s", "cores": nt, "kind": "reference",
+            "sample": f"{n_rep} copies of run_cluster on {nt} threads in {dt:.2f} s"}
     return line
 
 
+def bench_c3(ws: int, rank: int, dev: int, stream, reps: int = 3) -> dict:
+    """BASELINE config 3, the capacity-search grid, at its stated size:
+    65,536 instances (64 trace seeds x 16 scales x 16 SLO pairs x 4
+    policies), dealt round-robin over the ranks (strong scaling: the total is
+    fixed).  Device time per pass, max over ranks; per-instance results
+    gathered to every rank over NCCL and checked against the reference
+    fixture (plan digests of all 65,536 instances; records too at N=1)."""
+    import torch
+    from paper_2510_14392_b200 import dist as fdist
+    from paper_2510_14392_b200 import fbgpu, workloads
+    batch = workloads.c3_batch(shard=rank, n_shards=ws)
+    arena = fbgpu.Arena(dev, stream=stream.cuda_stream)
+    arena.load(batch)
+    arena.run()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _barrier(ws)
+        a.record(stream)
+        arena.reset()
+        arena.run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    res = arena.results()
+    rec = arena.records() if ws == 1 else None
+    arena.close()
+    t = torch.tensor([statistics.median(ms), float(res["steps"].sum())], dtype=torch.float64,
+                     device="cuda")
+    if ws > 1:
+        tmax = t[:1].clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
+        t = torch.cat([tmax, tsum])
+        idx = np.asarray(fdist.shard_indices(65536, rank, ws), np.int64)
+        res = fdist.gather_results(res, idx, 65536, torch.distributed, device="cuda")
+    max_ms, steps = float(t[0].item()), float(t[1].item())
+    line = {"workload": "C3: balanced bursty trace, 64 seeds x 16 scales x 16 (TTFT, TPOT) SLO "
+                        "pairs x 4 policies = 65,536 instances",
+            "value": steps / (max_ms / 1000.0), "unit": UNIT, "ms_per_pass": max_ms,
+            "instance_steps": steps, "n_gpus": ws, "scaling": "strong",
+            "instances_per_gpu": batch.n_instances}
+    if rank == 0:  # at N=1 `batch` is the whole grid; at N>1 results only
+        line["parity"] = {"fixture": fixture_parity("c3_full", batch, res, rec)}
+    return line
+
+
+def _barrier(ws: int) -> None:
+    import torch
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+
+def repo_so_loaded() -> list[str]:
+    """The repo's product libraries mapped into this process."""
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f
+                           if ln.rstrip().endswith(".so") and "paper_2510_14392_b200" in ln})
+    except OSError:
+        return []
+
+
 def run_reference(args) -> None:
+    """The reference arm: the reference's own CPU implementation (oracle/_ref:
+    stock run_node + request_reports, compiled unmodified from /root/reference)
+    on the C2 workload, all host threads.  Inputs are generated with the
+    reference's own generate_bursty / scale_trace, so nothing of the product
+    (libfbgpu.so) is loaded into this process.  Under torchrun only rank 0
+    runs."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     from paper_2510_14392_b200 import workloads
-    batch = workloads.c2_batch(n_seeds=SEEDS_PER_GPU)
+    lib = ref_lib()
+    ref, kind = lib
+
+    def scale(rows, f):
+        from paper_2510_14392_b200.batch import Rows
+        return Rows(ref.scale_trace(rows.arrival_us, f), rows.prompt_len, rows.output_len,
+                    rows.ttft_us, rows.tpot_us)
+    batch = workloads.c2_batch(n_seeds=SEEDS_PER_GPU, gen=ref.generate_bursty, scale=scale)
     n_threads = os.cpu_count() or 1
     vals = []
     cb = None
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(batch, n_threads, budget_s=args.ref_budget_s)
+        r = cpu_baseline(batch, n_threads, budget_s=args.ref_budget_s, lib=lib)
+        r.pop("_out"), r.pop("_sel")
         if i >= args.warmup:
             vals.append(r["value"])
             cb = r
@@ -273,14 +454,18 @@ def run_reference(args) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "int64+fp64", "data": "synthetic",
             "config": workload_config(1), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
-                             "sample": cb["sample"]},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": cb["sample"], "cpu_model": cb["cpu_model"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "inputs": "generate_bursty / scale_trace of the reference library",
+            "repo_so_loaded": repo_so_loaded()}
     print(json.dumps(line), flush=True)
 
 
 def run_ours(args) -> None:
     import torch
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -300,10 +485,7 @@ def run_ours(args) -> None:
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
 
     def barrier():
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
+        _barrier(ws)
 
     # warm-up (full passes)
     for _ in range(args.warmup):
@@ -311,6 +493,7 @@ def run_ours(args) -> None:
         arena.run()
     torch.cuda.synchronize()
     res = arena.results()
+    rec0 = arena.records()
     steps_per_pass = int(res["steps"].sum())
     assert (res["status"] == 0).all() and (res["incomplete"] == 0).all()
     # algorithmic bytes per engine launch: 32 A + 64 E + 64 N_arr
@@ -335,9 +518,13 @@ def run_ours(args) -> None:
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     n = torch.tensor([steps_per_pass * args.steps], dtype=torch.float64, device="cuda")
+    per_rank = torch.tensor([float(steps_per_pass)], dtype=torch.float64, device="cuda")
+    rank_steps = [per_rank]
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(n, op=torch.distributed.ReduceOp.SUM)
+        rank_steps = [torch.empty_like(per_rank) for _ in range(ws)]
+        torch.distributed.all_gather(rank_steps, per_rank)
     max_ms = float(t.item())
     all_steps = float(n.item())
     value = all_steps / (max_ms / 1000.0)
@@ -348,9 +535,8 @@ def run_ours(args) -> None:
     # per-instance results and per-request records into a pinned buffer
     batch.pin()
     rec_out = fbgpu.pinned_empty(arena.record_rows(), _abi.RECORD_DTYPE)
-    rows = batch.rows
     import ctypes as C
-    h2d = rows.nbytes + C.sizeof(_abi.Instance) * batch.n_instances
+    h2d = batch.rows.nbytes + C.sizeof(_abi.Instance) * batch.n_instances
     # (a) serial: one arena, each step load -> run -> fetch
     e2e_ms = []
     for k in range(max(1, min(args.steps, 5))):
@@ -408,6 +594,9 @@ def run_ours(args) -> None:
     serial_ms, pipe_ms = float(te[0].item()), float(te[1].item())
     e2e_value = (all_steps / args.steps) / (pipe_ms / 1000.0)
     e2e_serial = (all_steps / args.steps) / (serial_ms / 1000.0)
+    arena.close()
+
+    c3 = None if args.no_c3 else bench_c3(ws, rank, dev, stream)
 
     if rank == 0:
         peak, peak_kind = measured_peak_hbm()
@@ -419,6 +608,7 @@ def run_ours(args) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "int64+fp64", "data": "synthetic",
             "config": workload_config(ws),
             "instance_steps_per_pass": all_steps / args.steps,
+            "instance_steps_per_rank": [float(x.item()) for x in rank_steps],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
                          "kernel": "engine_kernel", "kernel_ms": eng,
@@ -436,19 +626,75 @@ def run_ours(args) -> None:
             # (CTA-wide engine; exits at once when no instance escalated)
             "gpu_launches": 3 * args.steps,
             "clocks": clocks.summary(),
+            # rank 0's shard is seeds 0..2047, the fixture's batch
+            "parity": {"fixture": fixture_parity("c2_full", batch, res, rec0)},
         }
+        if c3 is not None:
+            line["c3"] = c3
         if ws == 1 and not args.no_c4:
-            line["c4"] = bench_c4(peak, peak_kind)
-            line["c5"] = bench_c5()
+            line["c4"] = bench_c4(peak, peak_kind, cpu=not args.no_cpu_baseline)
+            line["c5"] = bench_c5(cpu=not args.no_cpu_baseline)
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(batch, os.cpu_count() or 1, args.ref_budget_s)
+            # the reference on the whole C2 batch (all host threads): the
+            # CPU baseline and a live parity check of every instance
+            lib = ref_lib()
+            cb = cpu_baseline(batch, os.cpu_count() or 1, args.ref_budget_s, lib=lib)
+            out, sel = cb.pop("_out"), cb.pop("_sel")
+            line["parity"]["live"] = live_parity(res, rec0, batch, out, sel)
+            line["cpu_baseline"] = cb
             # the single-core figure beside the all-cores one
-            one = cpu_baseline(batch, 1, args.ref_budget_s / 3)
+            one = cpu_baseline(batch, 1, args.ref_budget_s / 3, lib=lib)
             line["cpu_baseline"]["one_core"] = {"value": one["value"], "sample": one["sample"]}
+        line["parity"]["equal"] = all(v.get("equal", True) for v in line["parity"].values()
+                                      if isinstance(v, dict))
         print(json.dumps(line), flush=True)
-    arena.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def relaunch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args) -> None:
+    """CPU dry run of the multi-rank plumbing (tests/test_dist_cpu.py): gloo
+    instead of NCCL, no device work.  Each rank builds its C2 and C3 shards,
+    and the same reductions as the GPU run produce the line's n_gpus,
+    per-rank steps (here: instances) and the gathered C3 coverage."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    dist.init_process_group("gloo")
+    from paper_2510_14392_b200 import _abi, workloads
+    from paper_2510_14392_b200 import dist as fdist
+    c2 = workloads.c2_batch(n_seeds=args.dry_seeds, seed0=rank * args.dry_seeds)
+    c3 = workloads.c3_batch(n_seeds=1, shard=rank, n_shards=ws)
+    per = torch.tensor([float(c2.n_instances)], dtype=torch.float64)
+    parts = [torch.empty_like(per) for _ in range(ws)]
+    dist.all_gather(parts, per)
+    res = np.zeros(c3.n_instances, _abi.RESULT_DTYPE)
+    res["steps"] = [c3.instance(i).n_req for i in range(c3.n_instances)]
+    res["plan_digest"] = np.asarray(fdist.shard_indices(1024, rank, ws), np.uint64)
+    idx = np.asarray(fdist.shard_indices(1024, rank, ws), np.int64)
+    allres = fdist.gather_results(res, idx, 1024, dist)
+    if rank == 0:
+        print(json.dumps({"n_gpus": ws, "dry_run": True,
+                          "instances_per_rank": [float(p.item()) for p in parts],
+                          "c3_gathered_in_order": bool(np.array_equal(
+                              allres["plan_digest"], np.arange(1024, dtype=np.uint64))),
+                          "c3_instances": int(len(allres))}), flush=True)
+    dist.destroy_process_group()
 
 
 def main() -> None:
@@ -458,11 +704,20 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c4", action="store_true", help="skip the config-4 line item")
+    ap.add_argument("--no-c4", action="store_true", help="skip the config-4/5 line items")
+    ap.add_argument("--no-c3", action="store_true", help="skip the config-3 line item")
     ap.add_argument("--ref-budget-s", type=float, default=15.0)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU-only check of the multi-rank launcher and reductions (gloo)")
+    ap.add_argument("--dry-seeds", type=int, default=4)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)
 

@@ -264,7 +264,13 @@ typedef struct fb_plan_entry_id {
  * device.  Set s owns tasks[set_off[s] .. set_off[s+1]).  Entries of set s are
  * written at entries[set_off[s] ...] (a plan never has more entries than
  * tasks) and plans[s].entry_off/n_entries describe them.  Empty sets are a
- * UsageError for the fair-batching policies (sched.cpp:91-93). */
+ * UsageError for the fair-batching policies (sched.cpp:91-93).
+ * Any task set the reference's form_batch takes gives the same plan,
+ * including zero-token tasks (fair batching's `consider`, sched.cpp:141-150,
+ * admits them as {id, 0} whenever c*ctx <= time_budget, even once the token
+ * budget is spent) and negative contexts.  Stricter than the reference:
+ * new_tokens < 0, |slack_us| >= 2^61 and, for the fair-batching policies,
+ * b <= 0 (the chunk size divides by b) are ValidationErrors. */
 int fb_form_batch(int device, const fb_task_view* tasks, const int64_t* set_off,
                   const fb_scheduler_config* cfgs, int64_t n_sets,
                   fb_plan_entry_id* entries, fb_batch_plan* plans);

@@ -714,4 +714,59 @@ int ref_run_node_batch(const fb_trace* rows, const fb_instance* inst,
   return status.load();
 }
 
+// The reference's own run_cluster (cluster.cpp:134-251), unmirrored, for
+// timing: n_rep independent copies of one cluster case (the C5 replica
+// baseline) on a std::thread pool, one copy per task.  Fills each copy's
+// node steps / arrivals / rejects (counted from the node logs) and
+// incomplete flag; records of copy 0 when `records` is non-NULL.
+int ref_run_cluster_stock(const fb_trace* rows, const fb_engine_config* cfgs, int32_t n_nodes,
+                          const fb_lb_config* lbc, int64_t horizon, int32_t n_rep,
+                          fb_instance_result* node_results, fb_record* records, int nthreads) {
+  fb_instance whole{};
+  whole.trace_off = 0;
+  whole.n_req = rows->n_rows;
+  const Trace tr = instance_trace(rows, whole);
+  LbConfig lb;
+  lb.policy = lbc->policy == FB_LB_PAB ? LbPolicy::kPabLb : LbPolicy::kCountLb;
+  lb.report_interval_steps = lbc->report_interval_steps;
+  lb.report_latency = lbc->report_latency_us;
+  lb.w_waiting = lbc->w_waiting;
+  lb.w_running = lbc->w_running;
+  lb.retry_reroute = lbc->retry_reroute != 0;
+  std::vector<EngineConfig> ecfg;
+  for (int i = 0; i < n_nodes; ++i) ecfg.push_back(to_engine(cfgs[i]));
+  std::atomic<int> next{0};
+  std::atomic<int> status{FB_OK};
+  auto worker = [&]() {
+    for (;;) {
+      const int k = next.fetch_add(1);
+      if (k >= n_rep) return;
+      try {
+        const ClusterResult res = run_cluster(tr, ecfg, lb, horizon);
+        for (int i = 0; i < n_nodes; ++i) {
+          fb_instance_result& r = node_results[static_cast<int64_t>(k) * n_nodes + i];
+          std::memset(&r, 0, sizeof(r));
+          for (const auto& e : res.node_logs[static_cast<size_t>(i)].events) {
+            if (e.kind == EventKind::kBatchStart) r.steps++;
+            if (e.kind == EventKind::kArrival) r.n_arrived++;
+            if (e.kind == EventKind::kAdmissionReject) r.n_rejected++;
+          }
+          r.incomplete = res.incomplete ? 1 : 0;
+        }
+        if (records && k == 0) fill_records(res.node_logs, tr, records);
+      } catch (const std::exception& e) {
+        status = map_exception(e);
+      }
+    }
+  };
+  if (nthreads <= 1) {
+    worker();
+  } else {
+    std::vector<std::thread> th;
+    for (int k = 0; k < nthreads; ++k) th.emplace_back(worker);
+    for (auto& x : th) x.join();
+  }
+  return status.load();
+}
+
 }  // extern "C"

@@ -1,8 +1,9 @@
-"""B200-native FairBatching per-iteration scheduling hot path (fbsim drop-in)."""
-import os as _os
+"""B200-native FairBatching per-iteration scheduling hot path (fbsim drop-in).
 
-# Independent simulations run side by side on their own streams (sweeps,
-# cluster replicas): with the default 8 hardware work queues, kernels on more
-# than 8 streams serialise into waves.  Takes effect if set before the
-# process creates its CUDA context.
-_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+Importing the package changes no process state.  Independent simulations run
+side by side on their own streams (cluster replicas in `cluster.run_clusters`,
+sweeps): with the driver's default 8 hardware work queues, kernels on more
+than 8 streams serialise into waves, so entry points that launch many
+simulations at once (bench.py, tests/conftest.py) set
+CUDA_DEVICE_MAX_CONNECTIONS=32 before the process creates its CUDA context.
+"""

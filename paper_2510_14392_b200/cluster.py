@@ -272,6 +272,9 @@ def run_clusters(cases, device: int = 0) -> list[ClusterOutput]:
     sweep over seeds x rates x policies fills the GPU (replicas
     amortise the epoch latency).  `cases` holds (rows, cfgs, lb, horizon_us);
     the outputs equal run_cluster's case by case."""
+    cases = list(cases)
+    if not cases:
+        return []
     shards = []
     L = fbgpu.lib()
     try:

@@ -171,6 +171,7 @@ form_batch_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restr
     }
     const Scratch s = set_scratch(my, gscratch, off, n);
     ViewAcc acc;
+    bool unusual = false;
     for (int64_t p = lane_id(); p < n; p += kWarp) {
       const fb_task_view t = tasks[off + p];
       const bool decode = t.phase == FB_PHASE_DECODE;
@@ -180,9 +181,12 @@ form_batch_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restr
       s.nw[p] = t.new_tokens | (decode ? static_cast<int32_t>(kDecodeBit) : 0);
       s.req[p] = static_cast<int32_t>(p);
       acc.add(decode, t.slack_us, t.tpot_us);
+      unusual |= t.new_tokens == 0 || t.context < 0;
     }
     __syncwarp();
     acc.reduce();
+    // consider's early exit is proven only for new >= 1 and c*ctx >= 0
+    const bool exits_ok = !__any_sync(kFull, unusual) && cfg.model.c_ms >= 0.0;
     FormCfg f;
     f.policy = cfg.policy;
     f.max_chunk = cfg.max_chunk;
@@ -191,7 +195,7 @@ form_batch_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restr
     f.b = cfg.model.b_ms;
     f.c = cfg.model.c_ms;
     const int Ai = static_cast<int>(n);
-    const FormOut o = form_batch_warp(s, Ai, acc, f, /*seq_unique=*/false);
+    const FormOut o = form_batch_warp<true>(s, Ai, acc, f, /*seq_unique=*/false, exits_ok);
     int run = 0;
     for (int k0 = 0; k0 < Ai; k0 += kWarp) {
       const int k = k0 + lane_id();
@@ -200,8 +204,9 @@ form_batch_kernel(const fb_task_view* __restrict__ tasks, const int64_t* __restr
         p = s.order[k];
         tk = s.take[k];
       }
-      const unsigned m = __ballot_sync(kFull, tk > 0);
-      if (tk > 0) {
+      const bool adm = k < Ai && admitted_take<true>(tk);
+      const unsigned m = __ballot_sync(kFull, adm);
+      if (adm) {
         fb_plan_entry_id e;
         e.request_id = tasks[off + p].request_id;
         e.new_tokens = tk;
@@ -235,6 +240,7 @@ __global__ void init_time_budget_kernel(const fb_task_view* __restrict__ tasks,
     const int64_t off = set_off[set];
     const int64_t n = set_off[set + 1] - off;
     ViewAcc acc;
+    bool unusual = false;
     for (int64_t p = lane_id(); p < n; p += kWarp) {
       const fb_task_view t = tasks[off + p];
       acc.add(t.phase == FB_PHASE_DECODE, t.slack_us, t.tpot_us);

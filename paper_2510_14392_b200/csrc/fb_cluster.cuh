@@ -506,6 +506,15 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
   if (threadIdx.x == 0) rs.abort = 0;
   int32_t status = FB_OK;
   ClusterNode nd;
+  if (C.hw_cluster) {
+    // distributed shared memory may be written only once every CTA of the
+    // cluster is known to be running: one cluster barrier before the first
+    // remote report store (the initial report below)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
   if (owner) {
     cluster_node_init(P, C, il, my, nd);
     node_report(P, C, nd, 0, &status);  // initial report (cluster.cpp:198)

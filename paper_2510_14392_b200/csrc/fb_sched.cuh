@@ -158,14 +158,19 @@ __device__ __forceinline__ void gather_sorted(const Scratch& s, int A, double b,
 // (sched.cpp:129-166).  Skipped tasks never mutate the budgets, and the
 // budgets only shrink, so the pass stops exactly when neither branch can
 // admit anything any more (token_budget <= 0, or time_budget < 0 since
-// b > 0 and c*ctx >= 0).
+// b > 0 and c*ctx >= 0).  That early exit needs every task to carry
+// new >= 1 and c*ctx >= 0 -- always true for the engines' views; the pure
+// scheduler (fb_form_batch) passes `exits_ok` = false for sets holding a
+// zero-token task (which `consider` admits as {id, 0} whenever
+// c*ctx <= time_budget, even at token_budget 0) or a negative context.
 __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
-                                               double init_ms, const FormCfg& f) {
+                                               double init_ms, const FormCfg& f,
+                                               bool exits_ok = true) {
   if (tile_lane() == 0) {
     double tb = dsub(init_ms, f.a);
     int64_t tok = f.token_budget;
     for (int k = 0; k < A; ++k) {
-      if (tok <= 0 || tb < 0.0) break;
+      if (exits_ok && (tok <= 0 || tb < 0.0)) break;
       const double tc = s.tcost[k];
       const double cc = s.ccost[k];
       const int64_t nv = static_cast<int64_t>(static_cast<uint32_t>(s.khi[k]) & 0x7fffffffu);
@@ -238,9 +243,22 @@ __device__ __forceinline__ void scan_prefill_first(const Scratch& s, int A,
 // Whole K2+K3 pipeline after K1 filled s.{slack,seq,ctx,nw} for [0, A) and
 // acc holds the reduced K1 accumulators.  Leaves s.order / s.take (sorted) and
 // s.seq (sorted context) for the caller's bookkeeping.
+//
+// Admission marks: on the engine paths every task has new >= 1, so an
+// admitted entry has take >= 1 and take == 0 means "not admitted".  The pure
+// scheduler (kExact) also takes arbitrary task sets, where fair batching
+// admits zero-token entries {id, 0}: there take == -1 means "not admitted"
+// and every take >= 0 is a plan entry (`admitted_take`).
+template <bool kExact = false>
+__device__ __forceinline__ bool admitted_take(int32_t take) {
+  return kExact ? take >= 0 : take > 0;
+}
+
+template <bool kExact = false>
 __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
                                                    const ViewAcc& acc,
-                                                   const FormCfg& f, bool seq_unique) {
+                                                   const FormCfg& f, bool seq_unique,
+                                                   bool exits_ok = true) {
   FormOut out;
   out.init_ms = 0.0;
   const bool fair = f.policy == FB_POLICY_FAIRBATCH || f.policy == FB_POLICY_FAIRBATCH_PAB;
@@ -255,8 +273,12 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
   const bool packed = make_keys(s, A, f.policy, urgency, seq_unique);
   rank_order(s, A, packed);
   gather_sorted(s, A, f.b, f.c);
+  if (kExact) {
+    for (int k = tile_lane(); k < A; k += kTile) s.take[k] = -1;
+    tile_sync();
+  }
   if (fair) {
-    scan_fairbatch(s, A, out.init_ms, f);
+    scan_fairbatch(s, A, out.init_ms, f, exits_ok);
   } else if (f.policy == FB_POLICY_SARATHI) {
     scan_sarathi(s, A, acc.n_dec, f);
   } else {
@@ -267,7 +289,7 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
   int64_t tn = 0, tc = 0;
   for (int k = tile_lane(); k < A; k += kTile) {
     const int32_t tk = s.take[k];
-    if (tk > 0) {
+    if (admitted_take<kExact>(tk)) {
       e++;
       tn += tk;
       tc += s.seq[k];

@@ -7,6 +7,12 @@ generate_bursty (workload.cpp:244-298), identical for CPU and GPU runs.
   C3  request-rate x SLO x policy grid, 65,536 instances
   C4  decode-heavy, 120,000 live requests per instance
   C5  64-node cluster (load-estimation dispatch) -- see cluster.py
+
+Every builder takes an optional `gen(profile, horizon_us) -> Rows` (default:
+the product's fbgpu.generate_bursty) and `scale(rows, factor) -> Rows`
+(default: Rows.scaled), so the reference arm of bench.py and the golden
+fixtures build the identical batches with the reference's own generator
+(tests/backends.py RefLib) without loading libfbgpu.so.
 """
 from __future__ import annotations
 
@@ -25,15 +31,23 @@ def qwen_profile(seed: int, ttft_ms: float = 500.0, tpot_ms: float = 50.0):
                                ttft_ms, tpot_ms)
 
 
-def c1_rows() -> Rows:
+def _gen(gen):
+    return fbgpu.generate_bursty if gen is None else gen
+
+
+def _scale(scale):
+    return (lambda rows, f: rows.scaled(f)) if scale is None else scale
+
+
+def c1_rows(gen=None) -> Rows:
     """C1: pure Poisson 4 rps, seed 33, 250 s -> 931 requests."""
     p = fbgpu.burst_profile(4.0, 4.0, 1500.0, 3500.0, 892.0, 1776.0, 377.0, 742.0, 33)
-    return fbgpu.generate_bursty(p, ms_to_us(250_000.0))
+    return _gen(gen)(p, ms_to_us(250_000.0))
 
 
-def c1_batch(policies=("fairbatch",)) -> Batch:
+def c1_batch(policies=("fairbatch",), gen=None) -> Batch:
     b = Batch()
-    rows = c1_rows()
+    rows = c1_rows(gen)
     off = b.add_rows(rows)
     budgets = {"fairbatch": 2048, "fairbatch_pab": 2048, "sarathi": 512, "prefill_first": 8192}
     for pol in policies:
@@ -42,12 +56,14 @@ def c1_batch(policies=("fairbatch",)) -> Batch:
     return b
 
 
-def c2_batch(n_seeds: int = 2048, seed0: int = 0) -> Batch:
+def c2_batch(n_seeds: int = 2048, seed0: int = 0, gen=None, scale=None, stride: int = 1) -> Batch:
     """C2: qwen_profile(seed) x1.5 over 40 s, seeds x {sarathi 512, fairbatch 2048}.
-    Both policies of a seed share the same trace rows."""
+    Both policies of a seed share the same trace rows.  `stride` > 1 takes
+    every stride-th seed of the range (bounded CPU samples of the same sweep)."""
     b = Batch()
-    for s in range(seed0, seed0 + n_seeds):
-        rows = fbgpu.generate_bursty(qwen_profile(s), ms_to_us(40_000.0)).scaled(1.5)
+    gen, scale = _gen(gen), _scale(scale)
+    for s in range(seed0, seed0 + n_seeds, stride):
+        rows = scale(gen(qwen_profile(s), ms_to_us(40_000.0)), 1.5)
         off = b.add_rows(rows)
         rps = rows.offered_rps()
         b.add_instance(engine_config("sarathi", 512, MODEL_7B, 500, 50), off, len(rows),
@@ -66,7 +82,7 @@ C3_POLICIES = (("prefill_first", 8192), ("sarathi", 512), ("fairbatch", 2048),
 
 def c3_batch(n_seeds: int = 64, scales=C3_SCALES, ttfts=C3_TTFT, tpots=C3_TPOT,
              policies=C3_POLICIES, horizon_ms: float = 40_000.0, shard: int = 0,
-             n_shards: int = 1) -> Batch:
+             n_shards: int = 1, seed0: int = 0, gen=None, scale=None) -> Batch:
     """C3: the "balanced" shape (acceptance.cpp:347) over a 40 s horizon,
     16 scales x 4 TTFT x 4 TPOT x 4 policies x 64 seeds = 65,536 instances
     (SURVEY §8d lists 16 seeds, which gives 16,384; BASELINE.json names
@@ -74,13 +90,14 @@ def c3_batch(n_seeds: int = 64, scales=C3_SCALES, ttfts=C3_TTFT, tpots=C3_TPOT,
     SLOs are stamped per request and used as global_slo (scenario.cpp:142-143).
     Instances are dealt round-robin to `n_shards` shards (multi-GPU)."""
     b = Batch()
+    gen, scale = _gen(gen), _scale(scale)
     idx = 0
-    for seed in range(n_seeds):
-        base = fbgpu.generate_bursty(
+    for seed in range(seed0, seed0 + n_seeds):
+        base = gen(
             fbgpu.burst_profile(2.0, 6.0, 1000.0, 2000.0, 892.0, 1776.0, 377.0, 742.0, 7 + seed),
             ms_to_us(horizon_ms))
         for sc in scales:
-            scaled = base.scaled(sc)
+            scaled = scale(base, sc)
             for tt in ttfts:
                 for tp in tpots:
                     rows = scaled.with_slo(ms_to_us(tt), ms_to_us(tp))

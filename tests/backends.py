@@ -330,6 +330,27 @@ class RefLib(_CpuLib):
             raise RuntimeError(f"ref_run_cluster status {st}: {self.lib.ref_last_error()}")
         return ClusterOutput(res[:n], rec[:len(rows)], route[:len(rows)], inc.value)
 
+    def run_cluster_stock(self, rows: Rows, cfgs, lb, horizon_us: int, n_rep: int = 1,
+                          nthreads: int = 1, records: bool = False):
+        """The reference's own run_cluster, unmirrored (timing baseline):
+        n_rep copies on a thread pool.  Per-node results [n_rep, n_nodes]
+        (steps / n_arrived / n_rejected / incomplete) and copy 0's records."""
+        from paper_2510_14392_b200.cluster import node_configs_c
+        fn = self.lib.ref_run_cluster_stock
+        fn.restype = C.c_int
+        n = len(cfgs)
+        tr = rows.to_c()
+        nc = node_configs_c(cfgs)
+        lbc = lb.to_c()
+        res = np.zeros((n_rep, n), _abi.RESULT_DTYPE)
+        rec = np.zeros(max(1, len(rows)), _abi.RECORD_DTYPE) if records else None
+        st = fn(C.byref(tr), C.cast(nc, C.c_void_p), C.c_int32(n), C.byref(lbc),
+                C.c_int64(horizon_us), C.c_int32(n_rep), _abi.vptr(res), _abi.vptr(rec),
+                C.c_int(nthreads))
+        if st:
+            raise RuntimeError(f"ref_run_cluster_stock status {st}: {self.lib.ref_last_error()}")
+        return res, (rec[:len(rows)] if records else None)
+
     def event_log(self, batch: Batch, i: int, tmp_path: str) -> str:
         """The reference's save_event_log JSONL of instance i."""
         fn = self.lib.ref_event_log

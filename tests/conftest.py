@@ -7,6 +7,8 @@ import sys
 import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+# side-by-side simulations (run_clusters) on more than 8 streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 ROOT = os.path.dirname(HERE)
 for p in (ROOT, HERE):
     if p not in sys.path:

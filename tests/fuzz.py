@@ -152,3 +152,29 @@ def fb_config(token_budget=8192, policy=_abi.POLICY_FAIRBATCH, max_chunk=None):
     """test_sched.cpp:46-53."""
     return _abi.SchedulerConfig(policy, token_budget if max_chunk is None else max_chunk,
                                 token_budget, _abi.CostModel(5.0, 0.01, 0.0001))
+
+
+def degenerate_corpus(n: int = 5_000, seed: int = 77_001, max_tasks: int = 40):
+    """Task sets outside what the engines produce, for the pure scheduler
+    boundary (fb_form_batch vs form_batch, sched.cpp:129-246): zero-token
+    tasks (which fair batching's `consider` admits as {id, 0} whenever
+    c*ctx <= time_budget, even once the token budget is spent), negative
+    contexts, tiny token budgets and c = 0.  List of (views, cfg), the
+    policy cycling prefill_first / sarathi / fairbatch / fairbatch_pab."""
+    rng = Rng(seed)
+    out = []
+    for i in range(n):
+        raw, cfg, now = gen_instance(rng, max_tasks)
+        for t in raw:
+            if rng.next_double() < 0.25:
+                t["new"] = 0
+            if rng.next_double() < 0.1:
+                t["ctx"] = -rng.uniform_int(1, 5000)
+        budget = (1, 2, 8, 64, 256, 2048)[rng.uniform_int(0, 5)]
+        cfg.token_budget = budget
+        cfg.max_chunk = max(1, budget // (1 + rng.uniform_int(0, 3)))
+        if rng.next_double() < 0.2:
+            cfg.model.c_ms = 0.0
+        cfg.policy = i % 4
+        out.append((raw_to_views(raw, now), cfg))
+    return out

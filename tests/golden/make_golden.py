@@ -118,6 +118,8 @@ def main() -> None:
         for _, cfg in corpus:
             cfg.policy = pol
         gold["fuzz"][f"acceptance_policy{pol}"] = plans_digest(ref, corpus)
+    from fuzz import degenerate_corpus
+    gold["fuzz"]["degenerate_77001"] = plans_digest(ref, degenerate_corpus())
     gold["fuzz"]["pab_424242"] = hashlib.sha256(
         np.asarray(pab_values(ref), np.int64).tobytes()).hexdigest()
     with open(os.path.join(HERE, "golden.json"), "w") as f:

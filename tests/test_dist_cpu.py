@@ -160,3 +160,40 @@ def test_cluster_partition_matches_abi():
                 assert (lo.value, nl.value) == partition(n, w, r)
                 seen.extend(range(lo.value, lo.value + nl.value))
             assert seen == list(range(n))
+
+
+def _bench(*args, timeout=600):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], cwd=root,
+                         env=env, capture_output=True, text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_launches_n_ranks(world):
+    """`python bench.py --gpus N` outside torchrun starts N ranks itself
+    (torch.distributed.run on 127.0.0.1); here with gloo and no device work:
+    every rank builds its C2 shard, the line reports n_gpus == N with one
+    per-rank figure each, and the C3 results gathered from the interleaved
+    shards come back in global instance order."""
+    line = _bench("--gpus", str(world), "--dry-run")
+    assert line["n_gpus"] == world
+    assert line["instances_per_rank"] == [8.0] * world
+    assert line["c3_gathered_in_order"] and line["c3_instances"] == 1024
+
+
+def test_bench_reference_arm_loads_no_product_code():
+    """The reference arm builds its inputs with the reference's own generator
+    and runs the reference's run_node: libfbgpu.so is never mapped."""
+    line = _bench("--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-budget-s", "1")
+    assert line["impl"] == "reference"
+    assert line["repo_so_loaded"] == []
+    assert line["value"] > 0 and line["e2e"]["value"] == line["value"]

@@ -130,6 +130,18 @@ def test_acceptance_corpus_plans_match_golden(oracle, golden, corpus, policy):
     assert h.hexdigest() == golden["fuzz"][f"acceptance_policy{policy}"]
 
 
+def test_degenerate_corpus_plans_match_golden(oracle, golden):
+    """Zero-token tasks, negative contexts, tiny budgets, c = 0: the
+    restatement's `consider` equals the reference's plans (fixture)."""
+    from fuzz import degenerate_corpus
+    h = hashlib.sha256()
+    for v, cfg in degenerate_corpus():
+        plan, e = oracle.form_batch(v, cfg)
+        h.update(plan.tobytes())
+        h.update(e.tobytes())
+    assert h.hexdigest() == golden["fuzz"]["degenerate_77001"]
+
+
 def test_pab_fuzz_matches_golden(oracle, golden):
     rng = Rng(424242)
     vals = []
