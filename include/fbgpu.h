@@ -492,6 +492,71 @@ int fb_cluster_shard_fetch(fb_cluster_shard* s, fb_instance_result* local_result
                            int32_t* incomplete);
 void fb_cluster_shard_destroy(fb_cluster_shard* s);
 
+/* ---------------------------------------------------------------------- */
+/* Interactive node set: the Node surface (engine.h:111-176) of n nodes,   */
+/* batched, for an external dispatcher (the upper-level load balancer).    */
+/* ---------------------------------------------------------------------- */
+/* Every call acts on all nodes at once (one warp per node); node state stays
+ * in HBM between calls.  Requests are the rows of the trace given at
+ * creation (request_id = row); a dispatcher routes rows to nodes with
+ * fb_nodes_enqueue.  Driving the calls in run_cluster's order
+ * (cluster.cpp:134-251) reproduces run_cluster exactly
+ * (cluster.py run_cluster_host, tests/test_gpu_parity.py). */
+
+typedef struct fb_nodes fb_nodes;
+
+/* Node queries (engine.h:119-139). */
+typedef struct fb_node_state {
+  int64_t step_end;        /* Node::step_end (valid when busy) */
+  int64_t waiting;         /* Node::waiting_count */
+  int64_t running;         /* Node::running_count */
+  int64_t steps_completed; /* Node::steps_completed */
+  int32_t busy;            /* Node::busy */
+  int32_t has_live;        /* Node::has_live_requests */
+} fb_node_state;
+
+/* Node(i, cfgs[i]) for i < n_nodes (engine.cpp:83-90 validation), over the
+ * trace `rows`; the nodes begin no step at or after horizon_us.  reports:
+ * NULL, or the metric-report hook of run_cluster -- an initial report at 0
+ * and make_report (cluster.cpp:50-58: waiting, running, and current_pab when
+ * policy == FB_LB_PAB) after every report_interval_steps-th complete_step,
+ * delivered report_latency_us later (fb_nodes_advance). */
+int fb_nodes_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                    int32_t n_nodes, int64_t horizon_us, const fb_lb_config* reports,
+                    fb_nodes** out);
+void fb_nodes_destroy(fb_nodes* h);
+int32_t fb_nodes_count(const fb_nodes* h);
+/* Step-to-time: every node completes its in-flight steps ending before t and
+ * begins its next ones at their end times (no dispatcher input can reach a
+ * node between the dispatcher's calls), then completes a step ending at
+ * exactly t -- but begins none at t (that waits for fb_nodes_begin, after
+ * routing).  delivered[i] (may be NULL): node i's newest report with
+ * emitted_at + latency <= t (fresh = 1 when one arrived since the last
+ * call), and busy = node busy when the clock reached t. */
+int fb_nodes_advance(fb_nodes* h, int64_t t, fb_node_report* delivered);
+/* Node::enqueue(rows[row[k]], t) (engine.cpp:92-105) for k < n, in order:
+ * visible at the node's next begin_step (at or after t).  t is the
+ * dispatcher's current time (the only form run_cluster uses). */
+int fb_nodes_enqueue(fb_nodes* h, int64_t t, const int32_t* node, const int64_t* row, int64_t n);
+/* Node::begin_step(t) (engine.cpp:153-202) on every idle node of
+ * [node_lo, node_hi): PAB admission of its visible arrivals, batch
+ * formation, launch.  Rejected rows collect for fb_nodes_drain_rejects. */
+int fb_nodes_begin(fb_nodes* h, int64_t t, int32_t node_lo, int32_t node_hi);
+/* Node::drain_rejects (engine.h:143-145) of every node, in node order:
+ * (node, row) pairs; *n_out = count (FB_ERR_CAPACITY when cap is smaller,
+ * nothing drained). */
+int fb_nodes_drain_rejects(fb_nodes* h, int32_t* node_out, int64_t* row_out, int64_t cap,
+                           int64_t* n_out);
+/* Node::current_pab(now) (engine.cpp:123-125) of every node. */
+int fb_nodes_current_pab(fb_nodes* h, int64_t now, int64_t* pab_out);
+int fb_nodes_state(fb_nodes* h, fb_node_state* out);
+/* Per-node results (steps, plan digest, counters; incomplete = any node
+ * still live -- OR in the dispatcher's own unrouted arrivals), per-row
+ * records of the node each row was last routed to (rejected only if never
+ * served, metrics.cpp:96-98) and that node (-1: never routed). */
+int fb_nodes_fetch(fb_nodes* h, fb_instance_result* node_results, fb_record* records,
+                   int32_t* node_of_row, int32_t* incomplete_out);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -1170,6 +1170,240 @@ int fb_run_cluster(int device, const fb_trace* rows, const fb_engine_config* nod
 
 }  // extern "C"
 
+// ------------------------------------------------ interactive node set
+
+struct fb_nodes {
+  fb_cluster_shard* sh = nullptr;
+  int64_t* d_rep_ht = nullptr;
+  int64_t* d_rej = nullptr;
+  int64_t* d_nrej = nullptr;
+  int64_t* d_out = nullptr;
+  int32_t* d_status = nullptr;
+  int32_t* d_enode = nullptr;
+  int64_t* d_erow = nullptr;
+  int64_t ecap = 0, rej_cap = 0;
+  bool reports = false;
+  std::vector<int64_t> h_out;
+  ~fb_nodes() {
+    if (sh) cudaSetDevice(sh->a->device);
+    for (void* p : {static_cast<void*>(d_rep_ht), static_cast<void*>(d_rej),
+                    static_cast<void*>(d_nrej), static_cast<void*>(d_out),
+                    static_cast<void*>(d_status), static_cast<void*>(d_enode),
+                    static_cast<void*>(d_erow)})
+      if (p) cudaFree(p);
+    fb_cluster_shard_destroy(sh);
+  }
+};
+
+namespace {
+
+// One node-set op over nodes [lo, hi); out (n x 6 int64) fetched when wanted.
+int nodes_op(fb_nodes* h, int32_t op, int64_t t, int32_t lo, int32_t hi, bool fetch_out) {
+  fb_cluster_shard* s = h->sh;
+  FB_CUDA(cudaSetDevice(s->a->device));
+  cudaStream_t q = s->a->stream;
+  fbgpu::NodesIoHost io{};
+  io.op = op;
+  io.lo = lo;
+  io.hi = hi;
+  io.reports = h->reports ? 1 : 0;
+  io.t = t;
+  io.rep_ht = h->d_rep_ht;
+  io.rej = h->d_rej;
+  io.n_rej = h->d_nrej;
+  io.rej_cap = h->rej_cap;
+  io.out = h->d_out;
+  io.status = h->d_status;
+  FB_CUDA(fbgpu::launch_nodes(s->a->params(0), s->cp, io, q));
+  int32_t status = 0;
+  FB_CUDA(cudaMemcpyAsync(&status, h->d_status, sizeof(status), cudaMemcpyDeviceToHost, q));
+  if (fetch_out)
+    FB_CUDA(cudaMemcpyAsync(h->h_out.data(), h->d_out, sizeof(int64_t) * 6 * s->n_nodes,
+                            cudaMemcpyDeviceToHost, q));
+  FB_CUDA(cudaStreamSynchronize(q));
+  if (status == FB_ERR_CAPACITY)
+    return set_error(FB_ERR_CAPACITY, "fb_nodes: report FIFO or reject list overflow");
+  if (status != FB_OK) return set_error(status, "fb_nodes: device error");
+  return FB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fb_nodes_create(int device, const fb_trace* rows, const fb_engine_config* node_cfgs,
+                    int32_t n_nodes, int64_t horizon_us, const fb_lb_config* reports,
+                    fb_nodes** out) {
+  if (!out) return set_error(FB_ERR_USAGE, "fb_nodes_create: null output");
+  *out = nullptr;
+  fb_lb_config lb{};
+  if (reports) {
+    lb = *reports;
+  } else {
+    lb.policy = FB_LB_COUNT;
+    lb.report_interval_steps = 0;
+  }
+  // routed lists sized for one re-enqueue of every row, and the per-row
+  // "ever rejected" state of request_reports (metrics.cpp:96-98)
+  lb.retry_reroute = 1;
+  fb_cluster_shard* sh = nullptr;
+  int st = shard_create(device, rows, node_cfgs, n_nodes, &lb, horizon_us, 0, 1, nullptr, &sh);
+  if (st) return st;
+  fb_nodes* h = new fb_nodes();
+  h->sh = sh;
+  struct Drop {
+    fb_nodes*& p;
+    ~Drop() { delete p; }
+  } drop{h};
+  if ((st = fb_cluster_shard_reset(sh))) return st;
+  h->reports = reports != nullptr;
+  h->rej_cap = sh->nr + 1;
+  h->h_out.assign(static_cast<size_t>(6) * n_nodes, 0);
+  const size_t n = static_cast<size_t>(n_nodes);
+  FB_CUDA(cudaMalloc(&h->d_rep_ht, sizeof(int64_t) * 2 * n));
+  FB_CUDA(cudaMalloc(&h->d_rej, sizeof(int64_t) * h->rej_cap * n));
+  FB_CUDA(cudaMalloc(&h->d_nrej, sizeof(int64_t) * n));
+  FB_CUDA(cudaMalloc(&h->d_out, sizeof(int64_t) * 6 * n));
+  FB_CUDA(cudaMalloc(&h->d_status, sizeof(int32_t)));
+  cudaStream_t q = sh->a->stream;
+  FB_CUDA(cudaMemsetAsync(h->d_rep_ht, 0, sizeof(int64_t) * 2 * n, q));
+  FB_CUDA(cudaMemsetAsync(h->d_nrej, 0, sizeof(int64_t) * n, q));
+  FB_CUDA(cudaMemsetAsync(h->d_status, 0, sizeof(int32_t), q));
+  // initial reports so a dispatcher has a view before the first boundary
+  if ((st = nodes_op(h, fbgpu::kNodesInitOp, 0, 0, n_nodes, false))) return st;
+  *out = h;
+  h = nullptr;
+  return FB_OK;
+}
+
+void fb_nodes_destroy(fb_nodes* h) { delete h; }
+
+int32_t fb_nodes_count(const fb_nodes* h) { return h ? h->sh->n_nodes : 0; }
+
+int fb_nodes_advance(fb_nodes* h, int64_t t, fb_node_report* delivered) {
+  if (!h) return set_error(FB_ERR_USAGE, "fb_nodes_advance: null handle");
+  int st = nodes_op(h, fbgpu::kNodesAdvanceOp, t, 0, h->sh->n_nodes, delivered != nullptr);
+  if (st || !delivered) return st;
+  for (int32_t i = 0; i < h->sh->n_nodes; ++i) {
+    const int64_t* o = h->h_out.data() + 6 * static_cast<size_t>(i);
+    delivered[i].emitted_at = o[0];
+    delivered[i].pab_tokens = o[1];
+    delivered[i].waiting = static_cast<int32_t>(o[2]);
+    delivered[i].running = static_cast<int32_t>(o[3]);
+    delivered[i].fresh = static_cast<int32_t>(o[4]);
+    delivered[i].busy = static_cast<int32_t>(o[5]);
+  }
+  return FB_OK;
+}
+
+int fb_nodes_enqueue(fb_nodes* h, int64_t t, const int32_t* node, const int64_t* row, int64_t n) {
+  if (!h) return set_error(FB_ERR_USAGE, "fb_nodes_enqueue: null handle");
+  if (n < 0 || (n > 0 && (!node || !row))) return set_error(FB_ERR_USAGE, "fb_nodes_enqueue: bad arrays");
+  if (n == 0) return FB_OK;
+  fb_cluster_shard* s = h->sh;
+  for (int64_t k = 0; k < n; ++k) {
+    if (node[k] < 0 || node[k] >= s->n_nodes)
+      return set_error(FB_ERR_USAGE, "fb_nodes_enqueue: node out of range");
+    if (row[k] < 0 || row[k] >= s->nr)
+      return set_error(FB_ERR_USAGE, "fb_nodes_enqueue: trace row out of range");
+  }
+  FB_CUDA(cudaSetDevice(s->a->device));
+  cudaStream_t q = s->a->stream;
+  if (n > h->ecap) {
+    FB_CUDA(cudaStreamSynchronize(q));
+    if (h->d_enode) cudaFree(h->d_enode);
+    if (h->d_erow) cudaFree(h->d_erow);
+    h->d_enode = nullptr;
+    h->d_erow = nullptr;
+    h->ecap = 0;
+    FB_CUDA(cudaMalloc(&h->d_enode, sizeof(int32_t) * n));
+    FB_CUDA(cudaMalloc(&h->d_erow, sizeof(int64_t) * n));
+    h->ecap = n;
+  }
+  FB_CUDA(cudaMemcpyAsync(h->d_enode, node, sizeof(int32_t) * n, cudaMemcpyHostToDevice, q));
+  FB_CUDA(cudaMemcpyAsync(h->d_erow, row, sizeof(int64_t) * n, cudaMemcpyHostToDevice, q));
+  FB_CUDA(fbgpu::launch_nodes_enqueue(s->a->params(0), s->cp, t, h->d_enode, h->d_erow, n,
+                                      h->d_status, q));
+  int32_t status = 0;
+  FB_CUDA(cudaMemcpyAsync(&status, h->d_status, sizeof(status), cudaMemcpyDeviceToHost, q));
+  FB_CUDA(cudaStreamSynchronize(q));
+  if (status) return set_error(FB_ERR_CAPACITY, "fb_nodes_enqueue: a node's routed list is full");
+  return FB_OK;
+}
+
+int fb_nodes_begin(fb_nodes* h, int64_t t, int32_t node_lo, int32_t node_hi) {
+  if (!h) return set_error(FB_ERR_USAGE, "fb_nodes_begin: null handle");
+  if (node_lo < 0 || node_hi > h->sh->n_nodes || node_lo > node_hi)
+    return set_error(FB_ERR_USAGE, "fb_nodes_begin: bad node range");
+  return nodes_op(h, fbgpu::kNodesBeginOp, t, node_lo, node_hi, false);
+}
+
+int fb_nodes_drain_rejects(fb_nodes* h, int32_t* node_out, int64_t* row_out, int64_t cap,
+                           int64_t* n_out) {
+  if (!h || !n_out) return set_error(FB_ERR_USAGE, "fb_nodes_drain_rejects: bad arguments");
+  fb_cluster_shard* s = h->sh;
+  FB_CUDA(cudaSetDevice(s->a->device));
+  cudaStream_t q = s->a->stream;
+  const int32_t n = s->n_nodes;
+  std::vector<int64_t> cnt(static_cast<size_t>(n));
+  FB_CUDA(cudaMemcpyAsync(cnt.data(), h->d_nrej, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, q));
+  FB_CUDA(cudaStreamSynchronize(q));
+  int64_t total = 0;
+  for (int64_t c : cnt) total += c;
+  *n_out = total;
+  if (total == 0) return FB_OK;
+  if (total > cap || !node_out || !row_out)
+    return set_error(FB_ERR_CAPACITY, "fb_nodes_drain_rejects: output too small");
+  int64_t k = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (cnt[i] == 0) continue;
+    FB_CUDA(cudaMemcpyAsync(row_out + k, h->d_rej + static_cast<int64_t>(i) * h->rej_cap,
+                            sizeof(int64_t) * cnt[i], cudaMemcpyDeviceToHost, q));
+    for (int64_t j = 0; j < cnt[i]; ++j) node_out[k + j] = i;
+    k += cnt[i];
+  }
+  FB_CUDA(cudaMemsetAsync(h->d_nrej, 0, sizeof(int64_t) * n, q));
+  FB_CUDA(cudaStreamSynchronize(q));
+  return FB_OK;
+}
+
+int fb_nodes_current_pab(fb_nodes* h, int64_t now, int64_t* pab_out) {
+  if (!h || !pab_out) return set_error(FB_ERR_USAGE, "fb_nodes_current_pab: bad arguments");
+  int st = nodes_op(h, fbgpu::kNodesPabOp, now, 0, h->sh->n_nodes, true);
+  if (st) return st;
+  for (int32_t i = 0; i < h->sh->n_nodes; ++i) pab_out[i] = h->h_out[6 * static_cast<size_t>(i)];
+  return FB_OK;
+}
+
+int fb_nodes_state(fb_nodes* h, fb_node_state* out) {
+  if (!h || !out) return set_error(FB_ERR_USAGE, "fb_nodes_state: bad arguments");
+  int st = nodes_op(h, fbgpu::kNodesStateOp, 0, 0, h->sh->n_nodes, true);
+  if (st) return st;
+  for (int32_t i = 0; i < h->sh->n_nodes; ++i) {
+    const int64_t* o = h->h_out.data() + 6 * static_cast<size_t>(i);
+    out[i].busy = static_cast<int32_t>(o[0]);
+    out[i].step_end = o[1];
+    out[i].waiting = o[2];
+    out[i].running = o[3];
+    out[i].steps_completed = o[4];
+    out[i].has_live = static_cast<int32_t>(o[5]);
+  }
+  return FB_OK;
+}
+
+int fb_nodes_fetch(fb_nodes* h, fb_instance_result* node_results, fb_record* records,
+                   int32_t* node_of_row, int32_t* incomplete_out) {
+  if (!h) return set_error(FB_ERR_USAGE, "fb_nodes_fetch: null handle");
+  int st = nodes_op(h, fbgpu::kNodesFinishOp, 0, 0, h->sh->n_nodes, false);
+  if (st) return st;
+  fb_cluster_shard* s = h->sh;
+  const int64_t routed_all[1] = {s->nr};  // trace arrivals are the dispatcher's business
+  FB_CUDA(cudaMemcpy(s->d_out, routed_all, sizeof(int64_t), cudaMemcpyHostToDevice));
+  return fb_cluster_shard_fetch(s, node_results, records, node_of_row, nullptr, incomplete_out);
+}
+
+}  // extern "C"
+
 // ------------------------------------------------ pure scheduler surface
 
 namespace {

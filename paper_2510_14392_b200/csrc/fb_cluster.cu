@@ -127,6 +127,31 @@ cudaError_t launch_cluster_serial(const EngineParams& p, const ClusterParamsHost
   return cudaGetLastError();
 }
 
+cudaError_t launch_nodes(const EngineParams& p, const ClusterParamsHost& ch, const NodesIoHost& ih,
+                         cudaStream_t st) {
+  static_assert(sizeof(NodesIoHost) == sizeof(NodesIo), "node-set io layout");
+  ClusterParams c;
+  std::memcpy(&c, &ch, sizeof(c));
+  NodesIo io;
+  std::memcpy(&io, &ih, sizeof(io));
+  const size_t smem = static_cast<size_t>(kClusterMaxWarps) * kSmemSlots * kScratchBytesPerSlot;
+  cudaError_t e = cudaFuncSetAttribute(nodes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int blocks = (c.n_local + kClusterMaxWarps - 1) / kClusterMaxWarps;
+  if (blocks > 0) nodes_kernel<<<blocks, kWarp * kClusterMaxWarps, smem, st>>>(p, c, io);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nodes_enqueue(const EngineParams& p, const ClusterParamsHost& ch, int64_t t,
+                                 const int32_t* node, const int64_t* row, int64_t n,
+                                 int32_t* status, cudaStream_t st) {
+  ClusterParams c;
+  std::memcpy(&c, &ch, sizeof(c));
+  nodes_enqueue_kernel<<<1, 32, 0, st>>>(p, c, t, node, row, n, status);
+  return cudaGetLastError();
+}
+
 #ifdef FB_CLUSTER_PROF
 extern "C" int fb_debug_cluster_prof(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_cluster_prof, sizeof(unsigned long long) * 8);

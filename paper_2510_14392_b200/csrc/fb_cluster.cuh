@@ -786,4 +786,165 @@ cluster_serial_kernel(const __grid_constant__ EngineParams P,
   }
 }
 
+// ------------------------------------------------------ interactive node set
+//
+// fb_nodes_*: the Node surface (engine.h:111-176) of n nodes at once, driven
+// one host call at a time by an external dispatcher (e.g. run_cluster's loop,
+// cluster.cpp:134-251, on the host).  Between calls every node's state lives
+// in global memory (the memory path for every step, like the serial engine);
+// one warp per node per call.
+
+enum NodesOp : int32_t {
+  kNodesInit = 0,     // initial report at t = 0 (cluster.cpp:178)
+  kNodesAdvance = 1,  // events before t, the completion at t, newest delivered report
+  kNodesBegin = 2,    // begin_step(t) on the idle nodes of [lo, hi), collect rejects
+  kNodesPab = 3,      // current_pab(t)
+  kNodesState = 4,    // busy / step_end / waiting / running / steps / live
+  kNodesFinish = 5,   // done + incomplete flags for the result fetch
+};
+
+struct NodesIo {
+  int32_t op, lo, hi, reports;  // reports: emit make_report (cluster.cpp:50-58)
+  int64_t t;
+  int64_t* rep_ht;    // [n * 2] report FIFO head / tail per node
+  int64_t* rej;       // [n * rej_cap] rows rejected since the last drain
+  int64_t* n_rej;     // [n]
+  int64_t rej_cap;
+  int64_t* out;       // [n * 6] per-node output of the op
+  int32_t* status;
+};
+
+__global__ void __launch_bounds__(kWarp * kClusterMaxWarps)
+nodes_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ ClusterParams C,
+             const __grid_constant__ NodesIo io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x / kWarp;
+  const int i = blockIdx.x * kClusterMaxWarps + warp;
+  if (i >= C.n_local || i < io.lo || i >= io.hi) return;
+  unsigned char* my = smem_raw + static_cast<size_t>(warp) * kSmemSlots * kScratchBytesPerSlot;
+  ClusterNode nd;
+  cluster_node_init(P, C, i, my, nd);
+  nd.rep_head = io.rep_ht[2 * i];
+  nd.rep_tail = io.rep_ht[2 * i + 1];
+  Inst& w = nd.w;
+  int32_t status = FB_OK;
+  int64_t* o = io.out + static_cast<int64_t>(i) * 6;
+  const int64_t t = io.t;
+  auto complete = [&]() {  // Node::complete_step + the boundary report
+    const int64_t te = w.S.step_end;
+    w.S.t_last = te;
+    complete_step(P, w);
+    if (io.reports && C.interval > 0 && w.S.step_counter % static_cast<uint64_t>(C.interval) == 0)
+      node_report(P, C, nd, te, &status);
+  };
+  if (io.op == kNodesInit) {
+    if (io.reports) node_report(P, C, nd, 0, &status);
+  } else if (io.op == kNodesAdvance) {
+    while (w.S.busy && w.S.step_end < t) {  // the node's own events before t
+      const int64_t te = w.S.step_end;
+      complete();
+      if (te < w.horizon && (w.S.pulled < w.S.arr || w.S.n_live > 0)) {
+        w.S.t_last = te;
+        begin_step(P, w, te);
+        w.S.paths |= kPathMemory;
+      }
+    }
+    const int32_t bz = w.S.busy != 0;
+    if (bz && w.S.step_end == t) complete();  // begin at t waits for the dispatcher
+    // the newest report delivered by t (FIFO per node, constant latency)
+    int64_t h = nd.rep_head, rt = -1, rp = 0, rw = 0, rr = 0, fresh = 0;
+    while (h < nd.rep_tail) {
+      const int64_t* r = C.rep + (w.id * C.report_cap + h % C.report_cap) * 4;
+      if (r[0] + C.latency > t) break;
+      rt = r[0];
+      rp = r[1];
+      rw = r[2];
+      rr = r[3];
+      fresh = 1;
+      ++h;
+    }
+    nd.rep_head = h;
+    if (lane_id() == 0) {
+      o[0] = rt;
+      o[1] = rp;
+      o[2] = rw;
+      o[3] = rr;
+      o[4] = fresh;
+      o[5] = bz;
+    }
+  } else if (io.op == kNodesBegin) {
+    if (!w.S.busy) {
+      const int64_t p0 = w.S.pulled, rej0 = w.S.n_rejected;
+      if (w.S.pulled < w.S.arr || w.S.n_live > 0) {
+        w.S.t_last = t;
+        begin_step(P, w, t);
+        w.S.paths |= kPathMemory;
+      }
+      if (w.S.n_rejected != rej0) {
+        // drain_rejects' contents: the pulled rows flagged rejected, in pull
+        // order (a row flagged at an earlier visit was drained then)
+        int64_t n = io.n_rej[i];
+        for (int64_t q = p0; q < w.S.pulled; ++q) {
+          const int64_t row = w.routed[q];
+          if (!(P.flags[w.roff + row] & FB_REC_REJECTED)) continue;
+          if (lane_id() == 0) {
+            if (n < io.rej_cap) io.rej[static_cast<int64_t>(i) * io.rej_cap + n] = row;
+            C.row_state[row] |= 2;  // ever rejected (metrics.cpp:96-98)
+          }
+          ++n;
+        }
+        if (lane_id() == 0) io.n_rej[i] = n;
+        if (n > io.rej_cap) status = FB_ERR_CAPACITY;
+      }
+    }
+  } else if (io.op == kNodesPab) {
+    const int64_t pab = node_pab(P, nd, t);  // Node::current_pab (engine.cpp:123-125)
+    if (lane_id() == 0) o[0] = pab;
+  } else if (io.op == kNodesState) {
+    if (lane_id() == 0) {
+      o[0] = w.S.busy;
+      o[1] = w.S.step_end;
+      o[2] = w.S.n_live - w.S.n_active;  // waiting_count (engine.h:133-135)
+      o[3] = w.S.n_active;               // running_count
+      o[4] = static_cast<int64_t>(w.S.step_counter);  // steps_completed
+      o[5] = (w.S.pulled < w.S.arr || w.S.n_live > 0) ? 1 : 0;  // has_live_requests
+    }
+  } else if (io.op == kNodesFinish) {
+    w.S.done = 1;
+    w.S.incomplete = (w.S.busy || w.S.pulled < w.S.arr || w.S.n_live > 0) ? 1 : 0;
+  }
+  __syncwarp();
+  if (lane_id() == 0) {
+    P.state[i] = w.S;
+    io.rep_ht[2 * i] = nd.rep_head;
+    io.rep_ht[2 * i + 1] = nd.rep_tail;
+    if (status != FB_OK) atomicExch(io.status, status);
+  }
+}
+
+// Node::enqueue(r, t) (engine.cpp:92-105) for (node, row) pairs in order:
+// the row joins the node's routed list (pending until its next begin_step).
+__global__ void nodes_enqueue_kernel(const __grid_constant__ EngineParams P,
+                                     const __grid_constant__ ClusterParams C, int64_t t,
+                                     const int32_t* node, const int64_t* row, int64_t n,
+                                     int32_t* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int64_t k = 0; k < n; ++k) {
+    const int i = node[k];
+    DevState& st = P.state[i];
+    const int64_t j = st.arr;
+    if (j >= C.route_stride) {
+      *status = FB_ERR_CAPACITY;
+      return;
+    }
+    C.routed[static_cast<int64_t>(i) * C.route_stride + j] = static_cast<int32_t>(row[k]);
+    // a row routed here again after a rejection starts unrejected (the
+    // record keeps "ever rejected" in row_state)
+    P.flags[P.inst[i].rec_off + row[k]] &= ~static_cast<uint32_t>(FB_REC_REJECTED);
+    st.arr = j + 1;
+    st.t_last = t;
+    C.route_node[row[k]] = i;
+  }
+}
+
 }  // namespace fbgpu

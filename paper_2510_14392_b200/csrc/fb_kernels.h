@@ -159,6 +159,24 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& c, in
                            cudaStream_t st, bool allow_hw = true);
 // How many one-cluster grids of an n_nodes cluster fit the device at once.
 int cluster_max_hw_clusters(int n_nodes);
+// Interactive node set (fb_nodes_*, fb_cluster.cuh): ops and NodesIo.
+constexpr int32_t kNodesInitOp = 0, kNodesAdvanceOp = 1, kNodesBeginOp = 2, kNodesPabOp = 3,
+                  kNodesStateOp = 4, kNodesFinishOp = 5;
+struct NodesIoHost {
+  int32_t op, lo, hi, reports;
+  int64_t t;
+  int64_t* rep_ht;
+  int64_t* rej;
+  int64_t* n_rej;
+  int64_t rej_cap;
+  int64_t* out;
+  int32_t* status;
+};
+cudaError_t launch_nodes(const EngineParams& p, const ClusterParamsHost& c, const NodesIoHost& io,
+                         cudaStream_t st);
+cudaError_t launch_nodes_enqueue(const EngineParams& p, const ClusterParamsHost& c, int64_t t,
+                                 const int32_t* node, const int64_t* row, int64_t n,
+                                 int32_t* status, cudaStream_t st);
 // Warp engine, then the grid-wide wide engine; `between` (may be null) is
 // recorded between the two launches.
 cudaError_t launch_engine(const EngineParams& p, const EngineGeometry& g,

@@ -297,7 +297,13 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
   }
   out.n_entries = static_cast<int32_t>(__reduce_add_sync(tile_mask(), static_cast<uint32_t>(e)));
   out.total_new = tile_sum_small(tn);
-  out.total_ctx = tile_sum_small(tc);
+  if (kExact) {  // arbitrary (possibly negative) contexts: full 64-bit sum
+#pragma unroll
+    for (int o = kTile / 2; o > 0; o >>= 1) tc += tile_shfl_xor(tc, o);
+    out.total_ctx = tc;
+  } else {
+    out.total_ctx = tile_sum_small(tc);
+  }
   out.predicted_ms = out.n_entries == 0 ? 0.0 : predict_ms(f.a, f.b, f.c, out.total_new, out.total_ctx);
   return out;
 }
