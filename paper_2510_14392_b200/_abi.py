@@ -224,6 +224,9 @@ def _np_dtype(struct):
 
 NODE_REPORT_DTYPE = np.dtype([("emitted_at", "<i8"), ("pab_tokens", "<i8"), ("waiting", "<i4"),
                               ("running", "<i4"), ("fresh", "<i4"), ("busy", "<i4")])  # fb_node_report
+NODE_STATE_DTYPE = np.dtype([("step_end", "<i8"), ("waiting", "<i8"), ("running", "<i8"),
+                             ("steps_completed", "<i8"), ("busy", "<i4"),
+                             ("has_live", "<i4")])  # fb_node_state
 RECORD_DTYPE = np.dtype(
     [("first_emit_us", "<i8"), ("max_tpot_ms", "<f8"), ("max_tpot_alt_ms", "<f8"),
      ("tokens_emitted", "<i4"), ("flags", "<u4")], align=True)

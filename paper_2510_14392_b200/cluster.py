@@ -12,6 +12,7 @@ nodes).
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -265,7 +266,7 @@ def run_cluster_logged(rows: Rows, cfgs, lb: LbConfig, horizon_us: int,
     return ClusterLogs(out, counts[:n], steps, entries, rejects, routes[:k], snaps[:k])
 
 
-def run_clusters(cases, device: int = 0) -> list[ClusterOutput]:
+def run_clusters(cases, device: int = 0, span: dict | None = None) -> list[ClusterOutput]:
     """Independent cluster simulations at once -- one one-rank shard per case,
     each on its own stream, so their persistent cluster kernels (a few CTAs
     each, bound by the per-epoch exchange latency) run side by side and a
@@ -291,12 +292,280 @@ def run_clusters(cases, device: int = 0) -> list[ClusterOutput]:
                              "fb_cluster_shard_allow_hw_cluster")
         for sh in shards:
             sh.reset()
+        t0 = time.perf_counter()
         for sh in shards:
             sh.launch()
-        return [merge_shards([sh.fetch(sh.wait())], len(c[1])) for sh, c in zip(shards, cases)]
+        done = [sh.wait() for sh in shards]
+        if span is not None:  # host clock from the first launch to the last completion
+            span["ms"] = (time.perf_counter() - t0) * 1000.0
+        return [merge_shards([sh.fetch(d)], len(c[1])) for sh, d, c in zip(shards, done, cases)]
     finally:
         for sh in shards:
             sh.close()
+
+
+class NodeSet:
+    """fb_nodes_*: n Node objects (engine.h:111-176) on the device, driven one
+    call at a time by a host dispatcher.  Requests are rows of `rows`
+    (request_id = row).  `reports`: None, or the LbConfig whose report hook
+    (initial report, make_report every report_interval_steps completions,
+    delivered report_latency_ms later) the nodes run."""
+
+    def __init__(self, rows: Rows, cfgs, horizon_us: int, reports: LbConfig | None = None,
+                 device: int = 0):
+        L = fbgpu.lib()
+        self._L = L
+        self.n = len(cfgs)
+        self.n_rows = len(rows)
+        self._tr = rows.to_c()
+        nc = node_configs_c(cfgs)
+        lbc = reports.to_c() if reports is not None else None
+        h = C.c_void_p()
+        fbgpu._check(L.fb_nodes_create(device, C.byref(self._tr), C.cast(nc, C.c_void_p), self.n,
+                                       int(horizon_us), C.byref(lbc) if lbc is not None else None,
+                                       C.byref(h)), "fb_nodes_create")
+        self._h = h
+        self._rep = np.zeros(self.n, _abi.NODE_REPORT_DTYPE)
+        self._pab = np.zeros(self.n, np.int64)
+        self._st = np.zeros(self.n, _abi.NODE_STATE_DTYPE)
+
+    def close(self) -> None:
+        if self._h:
+            self._L.fb_nodes_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def advance(self, t: int) -> np.ndarray:
+        """Step to time t; per node the newest report delivered by t."""
+        fbgpu._check(self._L.fb_nodes_advance(self._h, int(t), _abi.vptr(self._rep)),
+                     "fb_nodes_advance")
+        return self._rep
+
+    def enqueue(self, t: int, nodes, rows) -> None:
+        nd = np.ascontiguousarray(nodes, np.int32)
+        rw = np.ascontiguousarray(rows, np.int64)
+        fbgpu._check(self._L.fb_nodes_enqueue(self._h, int(t), _abi.vptr(nd), _abi.vptr(rw),
+                                              len(nd)), "fb_nodes_enqueue")
+
+    def begin(self, t: int, lo: int = 0, hi: int | None = None) -> None:
+        fbgpu._check(self._L.fb_nodes_begin(self._h, int(t), lo, self.n if hi is None else hi),
+                     "fb_nodes_begin")
+
+    def drain_rejects(self):
+        """[(node, row)] rejected since the last drain, in node order."""
+        n = C.c_int64(0)
+        st = self._L.fb_nodes_drain_rejects(self._h, None, None, 0, C.byref(n))
+        if st == _abi.FB_OK and n.value == 0:
+            return []
+        nodes = np.zeros(n.value, np.int32)
+        rows = np.zeros(n.value, np.int64)
+        fbgpu._check(self._L.fb_nodes_drain_rejects(self._h, _abi.vptr(nodes), _abi.vptr(rows),
+                                                    n.value, C.byref(n)),
+                     "fb_nodes_drain_rejects")
+        return list(zip(nodes.tolist(), rows.tolist()))
+
+    def current_pab(self, now: int) -> np.ndarray:
+        fbgpu._check(self._L.fb_nodes_current_pab(self._h, int(now), _abi.vptr(self._pab)),
+                     "fb_nodes_current_pab")
+        return self._pab.copy()
+
+    def state(self) -> np.ndarray:
+        fbgpu._check(self._L.fb_nodes_state(self._h, _abi.vptr(self._st)), "fb_nodes_state")
+        return self._st.copy()
+
+    def fetch(self) -> ClusterOutput:
+        res = np.zeros(self.n, _abi.RESULT_DTYPE)
+        rec = np.zeros(max(1, self.n_rows), _abi.RECORD_DTYPE)
+        route = np.zeros(max(1, self.n_rows), np.int32)
+        inc = C.c_int32(0)
+        fbgpu._check(self._L.fb_nodes_fetch(self._h, _abi.vptr(res), _abi.vptr(rec),
+                                            _abi.vptr(route), C.byref(inc)), "fb_nodes_fetch")
+        return ClusterOutput(res, rec[:self.n_rows], route[:self.n_rows], inc.value)
+
+
+class HostRouter:
+    """The dispatcher's ClusterView (cluster.h:55-73) with apply_report and
+    route (cluster.cpp:60-112), on the host."""
+
+    def __init__(self, n: int, lb: LbConfig):
+        self.lb = lb
+        self.has = [False] * n
+        self.t = [-1] * n
+        self.pab = [0] * n
+        self.wait = [0] * n
+        self.run = [0] * n
+        self.dec = [0] * n
+        self.inc = [0] * n
+
+    def apply(self, i: int, emitted_at: int, pab: int, waiting: int, running: int) -> None:
+        if self.has[i] and emitted_at < self.t[i]:
+            return
+        self.has[i] = True
+        self.t[i] = emitted_at
+        self.pab[i] = pab
+        self.wait[i] = waiting
+        self.run[i] = running
+        self.dec[i] = 0
+        self.inc[i] = 0
+
+    def route(self, prompt: int) -> int:
+        n = len(self.pab)
+        chosen = -1
+        if self.lb.policy == "pab_lb":
+            eff = [self.pab[i] - self.dec[i] for i in range(n)]
+            for i in range(n):
+                if eff[i] >= prompt and (chosen < 0 or eff[i] > eff[chosen]):
+                    chosen = i
+            if chosen < 0:
+                for i in range(n):
+                    if chosen < 0 or eff[i] > eff[chosen]:
+                        chosen = i
+            self.dec[chosen] += prompt
+        else:
+            best = 0.0
+            for i in range(n):
+                score = (self.lb.w_waiting * float(self.wait[i] + self.inc[i])
+                         + self.lb.w_running * float(self.run[i]))
+                if chosen < 0 or score < best:
+                    chosen, best = i, score
+            self.inc[chosen] += 1
+        return chosen
+
+
+def run_cluster_host(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, device: int = 0,
+                     dist=None) -> ClusterOutput:
+    """run_cluster (cluster.cpp:134-251) driven from the host over the
+    interactive node set: the dispatcher (HostRouter) sees only delivered
+    reports, routes with Node::enqueue and reroutes drained rejects -- the
+    batched Node surface an external upper-level dispatcher uses.
+
+    Without retry_reroute the loop visits the dispatch epochs (distinct
+    arrival times; the nodes advance on their own in between, SURVEY §8e);
+    with it, every global event time, and begin_step runs node by node so a
+    rerouted request can wake a later node at the same instant.
+
+    `dist` (a torch.distributed group): the nodes are partitioned over the
+    ranks (`partition`, one GPU each).  Per dispatch epoch the ranks
+    all-gather their nodes' 32-byte load reports (the north star's per-epoch
+    allgather of load estimates); routing is replicated on every rank, each
+    rank enqueues the requests routed to its own nodes.  With retry_reroute
+    the owner of node i broadcasts node i's rejects after its begin_step, so
+    every rank reroutes them identically.  Every rank returns the whole
+    cluster's output."""
+    rank, world = (dist.get_rank(), dist.get_world_size()) if dist is not None else (0, 1)
+    n = len(cfgs)
+    lo, nl = partition(n, world, rank)
+    owner = np.zeros(n, np.int64)
+    for r in range(world):
+        a, k = partition(n, world, r)
+        owner[a:a + k] = r
+    nodes = NodeSet(rows, cfgs[lo:lo + nl], horizon_us, lb, device)
+    if dist is not None:
+        import torch
+        cap = max(partition(n, world, r)[1] for r in range(world))
+    try:
+        view = HostRouter(n, lb)
+        arrival = rows.arrival_us
+        prompt = rows.prompt_len
+        n_rows = len(rows)
+        kinf = np.iinfo(np.int64).max
+        arr = 0
+        retried = set()
+        route = np.full(n_rows, -1, np.int32)
+
+        def all_reports(local):
+            if dist is None:
+                return local
+            buf = np.zeros(cap, _abi.NODE_REPORT_DTYPE)
+            buf[:nl] = local
+            t = torch.from_numpy(buf.view(np.int64).copy())
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t)
+            return np.concatenate([p.numpy().view(_abi.NODE_REPORT_DTYPE)[:partition(n, world, r)[1]]
+                                   for r, p in enumerate(parts)])
+
+        def enqueue(t, targets, qrows):
+            targets = np.asarray(targets, np.int64)
+            qrows = np.asarray(qrows, np.int64)
+            route[qrows] = targets
+            mine = (targets >= lo) & (targets < lo + nl)
+            nodes.enqueue(t, targets[mine] - lo, qrows[mine])
+
+        def global_min_step_end():
+            st = nodes.state()
+            busy = st["busy"] != 0
+            m = int(st["step_end"][busy].min()) if busy.any() else kinf
+            if dist is not None:
+                v = torch.tensor([m], dtype=torch.int64)
+                dist.all_reduce(v, op=dist.ReduceOp.MIN)
+                m = int(v.item())
+            return m
+
+        while True:
+            t = global_min_step_end() if lb.retry_reroute else kinf
+            if arr < n_rows:
+                t = min(t, int(arrival[arr]))
+            if t == kinf:
+                break
+            rep = all_reports(nodes.advance(t))
+            if not rep["busy"].any() and t >= horizon_us:
+                break
+            for i in np.nonzero(rep["fresh"])[0]:
+                r = rep[i]
+                view.apply(int(i), int(r["emitted_at"]), int(r["pab_tokens"]), int(r["waiting"]),
+                           int(r["running"]))
+            q0 = arr
+            targets = []
+            while arr < n_rows and arrival[arr] == t:
+                targets.append(view.route(int(prompt[arr])))
+                arr += 1
+            enqueue(t, targets, np.arange(q0, arr))
+            if t >= horizon_us:
+                continue
+            if not lb.retry_reroute:
+                nodes.begin(t)
+                continue
+            progress = True
+            while progress:
+                progress = False
+                for i in range(n):
+                    rej = []
+                    if owner[i] == rank:
+                        nodes.begin(t, i - lo, i - lo + 1)
+                        rej = [row for _, row in nodes.drain_rejects()]
+                    if dist is not None:
+                        box = [rej]
+                        dist.broadcast_object_list(box, src=int(owner[i]))
+                        rej = box[0]
+                    for row in rej:
+                        if row not in retried:
+                            retried.add(row)
+                            enqueue(t, [view.route(int(prompt[row]))], [row])
+                            progress = True
+        nodes.advance(kinf)  # in-flight steps finish; no step begins past the horizon
+        local = nodes.fetch()
+        if dist is None:
+            parts = [(lo, local)]
+        else:
+            parts = [None] * world
+            dist.all_gather_object(parts, (lo, local))
+        res = np.concatenate([o.node_results for _, o in sorted(parts, key=lambda x: x[0])])
+        rec = np.zeros(n_rows, _abi.RECORD_DTYPE)
+        rec["first_emit_us"] = -1
+        for plo, o in parts:
+            pn = len(o.node_results)
+            own = (route >= plo) & (route < plo + pn)
+            rec[own] = o.records[own]
+        inc = int(arr < n_rows or any(o.incomplete for _, o in parts))
+        res["incomplete"] = inc
+        return ClusterOutput(res, rec, route, inc)
+    finally:
+        nodes.close()
 
 
 MODEL_7B = CostModel(5.0, 0.05, 0.0001)

@@ -361,9 +361,11 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   // scanned once, validating and computing the per-range facts together.
   std::vector<int64_t> rec_off(static_cast<size_t>(n_instances) + 1, 0);
   std::vector<int64_t> tpot_u(static_cast<size_t>(n_instances), -1);
+  std::vector<char> wide_ok(static_cast<size_t>(n_instances), 0);
   std::vector<double> key(static_cast<size_t>(n_instances), 0.0);
   struct RangeFacts {
     int64_t tpot_u;
+    bool wide_ok;  // the wide engine's 16-byte view records can hold every row
     double key;
   };
   std::unordered_map<std::string, RangeFacts> memo;
@@ -392,16 +394,20 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
       RangeFacts f;
       // a uniform tpot_slo makes init_time_budget's min over tasks a constant
       f.tpot_u = in.n_req > 0 ? rows->tpot_us[in.trace_off] : -1;
+      f.wide_ok = in.n_req < (int64_t(1) << 22);
       // work-queue order key: predicted steps ~ max of arrival/a + output_len
       f.key = 0.0;
       for (int64_t r = in.trace_off; r < in.trace_off + in.n_req; ++r) {
         if (rows->tpot_us[r] != f.tpot_u) f.tpot_u = -1;
+        if (rows->arrival_us[r] >= (int64_t(1) << 40) || rows->ttft_us[r] >= (int64_t(1) << 40))
+          f.wide_ok = false;
         const double v = static_cast<double>(rows->arrival_us[r]) / a_us + rows->output_len[r];
         if (v > f.key) f.key = v;
       }
       it = memo.emplace(std::move(mk), f).first;
     }
     tpot_u[i] = it->second.tpot_u;
+    wide_ok[i] = it->second.wide_ok ? 1 : 0;
     key[i] = it->second.key;
     rec_off[i + 1] = rec_off[i] + in.n_req;
   }
@@ -457,7 +463,8 @@ int fb_arena_load(fb_arena* a, const fb_trace* rows, const fb_instance* instance
   std::vector<unsigned char> hinst(static_cast<size_t>(n_instances) * fbgpu::dev_inst_bytes());
   for (int64_t i = 0; i < n_instances; ++i)
     fbgpu::pack_instance(instances[i], rec_off[i], i * lo.step_cap, i * lo.entry_cap,
-                         i * lo.reject_cap, tpot_u[i], hinst.data() + i * fbgpu::dev_inst_bytes());
+                         i * lo.reject_cap, tpot_u[i], wide_ok[i] != 0,
+                         hinst.data() + i * fbgpu::dev_inst_bytes());
   // Work queues (see EngineParams): cost = predicted steps x the policy's
   // relative per-step cost (fair batching ranks slack keys, PAB also folds
   // admission terms).  Scheduling only, no semantic effect.

@@ -484,6 +484,9 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
   }
 }
 
+// One CTA per SM: measured, two per SM (<= 128 registers) packs a cluster's
+// 8 CTAs onto 4 SMs -- C5 233 ms instead of 185 ms, and 33 side-by-side
+// copies 485 ms (16.6 M node-steps/s) against 16 copies in 217 ms.
 __global__ void __launch_bounds__(kWarp * kClusterMaxWarps, 1)
 cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ ClusterParams C) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -834,8 +837,13 @@ nodes_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ Clu
     const int64_t te = w.S.step_end;
     w.S.t_last = te;
     complete_step(P, w);
-    if (io.reports && C.interval > 0 && w.S.step_counter % static_cast<uint64_t>(C.interval) == 0)
+    if (io.reports && C.interval > 0 &&
+        w.S.step_counter % static_cast<uint64_t>(C.interval) == 0) {
+      // a full FIFO whose head is delivered by t loses nothing by dropping
+      // it: this newer report is delivered by t as well and supersedes it
+      if (nd.rep_tail - nd.rep_head >= C.report_cap && te + C.latency <= t) nd.rep_head++;
       node_report(P, C, nd, te, &status);
+    }
   };
   if (io.op == kNodesInit) {
     if (io.reports) node_report(P, C, nd, 0, &status);

@@ -260,7 +260,8 @@ struct DevInst {
   int64_t n_req;
   int64_t log_step_off, log_entry_off, log_reject_off;
   int64_t tpot_uniform;  // every row's tpot_slo when they are all equal, else -1
-  int32_t policy, max_chunk, max_active, pad;
+  int32_t policy, max_chunk, max_active;
+  int32_t wide_ok;  // may escalate to the wide engine: n_req < 2^22, arrival + ttft < 2^41
 };
 
 // Mutable per-instance step-machine state (Node's scalars, engine.h:156-175).

@@ -201,7 +201,7 @@ WideGridSizes wide_grid_sizes(const EngineGeometry& g, int64_t n_rec) {
 
 void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
                    int64_t log_entry_off, int64_t log_reject_off, int64_t tpot_uniform,
-                   void* out) {
+                   bool wide_ok, void* out) {
   DevInst d;
   std::memset(&d, 0, sizeof(d));
   const fb_engine_config& c = in.cfg;
@@ -227,6 +227,7 @@ void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
   d.policy = c.scheduler.policy;
   d.max_chunk = c.scheduler.max_chunk;
   d.max_active = c.max_active;
+  d.wide_ok = wide_ok ? 1 : 0;
   std::memcpy(out, &d, sizeof(d));
 }
 

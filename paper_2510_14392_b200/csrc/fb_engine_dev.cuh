@@ -530,7 +530,7 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   }
   if (!w.S.busy && t < w.horizon) {
     const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
-    if (upcoming > kEscalateLive) {  // hand over to the wide engine
+    if (upcoming > kEscalateLive && w.I->wide_ok) {  // hand over to the wide engine
       if (c.rr) rr_spill(P, w, c.tk);
       w.S.pending_begin = 1;
       w.S.escalated = 1;

@@ -104,6 +104,7 @@ size_t dev_state_bytes();
 // assigned by the caller).
 void pack_instance(const fb_instance& in, int64_t rec_off, int64_t log_step_off,
                    int64_t log_entry_off, int64_t log_reject_off, int64_t tpot_uniform,
+                   bool wide_ok,
                    void* out);
 // Host decode of a DevState into fb_instance_result.
 void unpack_state(const void* state, fb_instance_result* out);

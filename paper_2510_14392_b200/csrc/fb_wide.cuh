@@ -66,20 +66,49 @@ struct WideSmem {
   int32_t ibcast[8];
 };
 
-// Per-instance global scratch (72 bytes per request slot, see Scratch).
+// Between K2a and K2b the window arrays (owner-phase only) hold the
+// selection bin of each view of the CTA's range, as uint16.
+constexpr int64_t kWgBinCap =
+    static_cast<int64_t>(offsetof(WideSmem, hist) - offsetof(WideSmem, wkey)) / 2;
+static_assert(kSelBins <= 65536, "bins must fit uint16");
+__device__ __forceinline__ uint16_t* wg_bins(WideSmem& sm) {
+  return reinterpret_cast<uint16_t*>(sm.wkey);
+}
+
 // Per-request view record of an escalated node (request index r): the
 // K1-relevant progress, mirrored from the SoA arena at escalation and kept
-// in step by pull / complete, so K1 reads one 32-byte record per view (two
-// 16-byte loads) instead of seven gathers.
+// in step by pull / complete, so K1 reads one 16-byte record per view (one
+// vector load) instead of seven gathers.  Everything K1 derives a view from
+// (build_task_views, engine.cpp:51-81; slack, slo.h:45-61):
+//   anchor  = min(first token, arrival + ttft_slo) once token 0 is out, else
+//             arrival + ttft_slo  -- fixed from the first token on
+//   slack   = anchor + tpot_slo * next_idx - now   (prefill: next_idx = 0)
+//   context = prefilled (prefill) or prompt + next_idx (decode)
+// Packing needs anchor < 2^41 and seq < 2^22: DevInst::wide_ok (host-checked
+// arrival, ttft_slo < 2^40 and n_req < 2^22; anchor <= arrival + ttft_slo).
 struct __align__(16) WRec {
-  int64_t dl0;    // arrival + ttft_slo (slo.h:45-61 anchor)
-  int64_t first;  // time of token 0, -1 none
-  int32_t prompt, prefilled, nidx, seq;
+  int64_t anc_seq;  // anchor << 22 | seq
+  int32_t ctx;      // context tokens
+  int32_t nid;      // next_idx | decode << 31
 };
+constexpr int64_t kWRecSeqMask = (int64_t(1) << 22) - 1;
+
+__device__ __forceinline__ WRec make_wrec(int64_t dl0, int64_t first, int32_t prompt,
+                                          int32_t prefilled, int32_t nidx, int32_t seq) {
+  const bool decode = prefilled >= prompt;
+  const int64_t anchor = (first >= 0 && first < dl0) ? first : dl0;
+  WRec r;
+  r.anc_seq = (anchor << 22) | (static_cast<int64_t>(static_cast<uint32_t>(seq)) & kWRecSeqMask);
+  r.ctx = decode ? prompt + nidx : prefilled;
+  r.nid = static_cast<int32_t>(static_cast<uint32_t>(nidx) | (decode ? 0x80000000u : 0u));
+  return r;
+}
+
+// Per-instance global scratch (kScratchBytesPerSlot per request slot).
 
 // Per-instance global scratch (kScratchBytesPerSlot per request slot).
 struct WideScratch {
-  WRec* rec;       // [r] view records
+  WRec* rec;       // [r] view records (16 of the slot's first 32 bytes)
   uint64_t* klow;  // [p] decode<<63 | (slack+2^39)<<22 | seq   (stem of the key)
   int2* vtmp;      // reorder buffer / PAB terms
   int32_t* mark;   // [p] admitted-waiting flag
@@ -95,6 +124,50 @@ __device__ __forceinline__ WideScratch wide_scratch(const EngineParams& P, const
   s.vtmp = reinterpret_cast<int2*>(base + 40 * n);
   s.mark = reinterpret_cast<int32_t*>(base + 48 * n);
   return s;
+}
+
+// ------------------------------------------------------ L2 residency
+//
+// One iteration streams every beginning node's views once (K1: row index +
+// 32-byte record, ~200 MB at C4) and writes the 8-byte key stems (~40 MB)
+// that K2a reads back.  The records and row indices are marked evict_first
+// and the stems evict_last, so the stems stay in the 126 MB L2 between K1
+// and K2a instead of being written back and re-read from HBM.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int4 ld_stream_v4(const int4* a, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* a, uint64_t pol) {
+  int32_t r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(r)
+               : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_keep_u64(uint64_t* a, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t ld_keep_u64(const uint64_t* a, uint64_t pol) {
+  uint64_t r;
+  asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+  asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(a));
 }
 
 // ------------------------------------------------------ block primitives
@@ -834,9 +907,8 @@ __device__ void wide_complete(const EngineParams& P, Inst& w, WideSmem& sm) {
         lfin += fin ? P.output[row] : 0;
       }
       WRec& rec = ws.rec[v.x];  // keep the view record in step
-      rec.prefilled = pf;
-      rec.nidx = P.nidx[g];
-      rec.first = P.first[g];
+      rec = make_wrec(P.arrival[row] + P.ttft[row], P.first[g], prompt, pf, P.nidx[g],
+                      static_cast<int32_t>(rec.anc_seq & kWRecSeqMask));
       w.vl[p] = make_int2(fin ? -1 : v.x, 0);
       any |= fin;
     }
@@ -878,7 +950,7 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
     for (int64_t j = threadIdx.x; j < k; j += kWideThreads) {
       const int64_t r = arrival_row(w, w.S.pulled + j);
       P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter + j);
-      ws.rec[r].seq = static_cast<int32_t>(w.S.seq_counter + j);
+      ws.rec[r].anc_seq = (ws.rec[r].anc_seq & ~kWRecSeqMask) | (w.S.seq_counter + j);
       w.vl[w.S.n_live + j] = make_int2(static_cast<int>(r), 0);
     }
     __syncthreads();
@@ -918,7 +990,7 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
           vis = (w.S.n_live - w.S.n_active) < slots;
         }
         P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter);
-        ws.rec[r].seq = static_cast<int32_t>(w.S.seq_counter);
+        ws.rec[r].anc_seq = (ws.rec[r].anc_seq & ~kWRecSeqMask) | w.S.seq_counter;
         w.vl[w.S.n_live] = make_int2(static_cast<int>(r), 0);
         w.S.seq_counter++;
         w.S.n_live++;
@@ -1019,51 +1091,63 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
                                               int64_t (&r)[kK1Vals], WideSmem& sm) {
   const WideScratch ws = wide_scratch(P, w);
   const int64_t tpu = w.I->tpot_uniform;
+  const uint64_t pol_stream = l2_evict_first_policy();
+  const uint64_t pol_keep = l2_evict_last_policy();
+  const int32_t* vrow = reinterpret_cast<const int32_t*>(w.vl);  // .x of {row, take}
   constexpr int U = 4;
   int64_t mn[6] = {kInf, kInf, kInf, kInf, kInf, kInf};
   int64_t l_cnt = 0;
-  // the row indices of the next batch are loaded one batch ahead, so only the
-  // record loads' latency is exposed per batch (not index, then record)
-  int32_t rn[U];
+  // The row indices are loaded two batches ahead and the records of the
+  // next batch prefetched into L2 one batch ahead (prefetches hold no
+  // registers), so each batch's record loads hit L2 instead of waiting on
+  // HBM behind their row index.
+  int32_t rn[U], rn2[U];
 #pragma unroll
   for (int j = 0; j < U; ++j) {
     const int64_t p = p_lo + j * kWideThreads + threadIdx.x;
-    rn[j] = p < p_hi ? w.vl[p].x : -1;
+    rn[j] = p < p_hi ? ld_stream_s32(vrow + 2 * p, pol_stream) : -1;
+    const int64_t p2 = p + U * kWideThreads;
+    rn2[j] = p2 < p_hi ? ld_stream_s32(vrow + 2 * p2, pol_stream) : -1;
   }
+#pragma unroll
+  for (int j = 0; j < U; ++j)
+    if (rn[j] >= 0) prefetch_l2(ws.rec + rn[j]);
   for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
     int32_t rr[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       rr[j] = rn[j];
-      const int64_t p = b0 + (U + j) * kWideThreads + threadIdx.x;
-      rn[j] = p < p_hi ? w.vl[p].x : -1;
+      rn[j] = rn2[j];
+      const int64_t p = b0 + (2 * U + j) * kWideThreads + threadIdx.x;
+      rn2[j] = p < p_hi ? ld_stream_s32(vrow + 2 * p, pol_stream) : -1;
     }
-    int32_t prompt[U], pf[U], ni[U], seq[U];
-    int64_t dl0[U], first[U], tpot[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (rn[j] >= 0) prefetch_l2(ws.rec + rn[j]);
+    int4 rc[U];
+    int64_t tpot[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (rr[j] < 0) continue;
-      const int4* rp = reinterpret_cast<const int4*>(ws.rec + rr[j]);
-      const int4 a = rp[0], b = rp[1];
-      dl0[j] = (static_cast<int64_t>(static_cast<uint32_t>(a.y)) << 32) | static_cast<uint32_t>(a.x);
-      first[j] = (static_cast<int64_t>(static_cast<uint32_t>(a.w)) << 32) | static_cast<uint32_t>(a.z);
-      prompt[j] = b.x;
-      pf[j] = b.y;
-      ni[j] = b.z;
-      seq[j] = b.w;
+      rc[j] = ld_stream_v4(reinterpret_cast<const int4*>(ws.rec + rr[j]), pol_stream);
       tpot[j] = tpu >= 0 ? tpu : P.tpot[w.toff + rr[j]];
     }
+    int32_t seq[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (rr[j] < 0) continue;
       const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-      const bool decode = pf[j] >= prompt[j];
-      const int64_t anchor = (first[j] >= 0 && first[j] < dl0[j]) ? first[j] : dl0[j];
-      const int64_t slack = anchor + tpot[j] * static_cast<int64_t>(ni[j]) - now;
-      const int64_t ctx = decode ? static_cast<int64_t>(prompt[j]) + ni[j] : pf[j];
-      if (static_cast<uint32_t>(seq[j]) >= static_cast<uint32_t>(kPackSeq)) l_cnt |= int64_t(1) << 40;
+      const int64_t as = (static_cast<int64_t>(static_cast<uint32_t>(rc[j].y)) << 32) |
+                         static_cast<uint32_t>(rc[j].x);
+      seq[j] = static_cast<int32_t>(as & kWRecSeqMask);
+      const bool decode = rc[j].w < 0;
+      const int64_t ni = rc[j].w & 0x7fffffff;
+      const int64_t slack = (as >> 22) + tpot[j] * ni - now;
+      const int64_t ctx = rc[j].z;
       const uint64_t sl = fair ? static_cast<uint64_t>(slack + kPackSlack) : 0;
-      ws.klow[p] = (decode ? (uint64_t(1) << 63) : 0) | (sl << 22) | static_cast<uint64_t>(seq[j]);
+      st_keep_u64(ws.klow + p,
+                  (decode ? (uint64_t(1) << 63) : 0) | (sl << 22) | static_cast<uint64_t>(seq[j]),
+                  pol_keep);
       if (fair && (slack < -kPackSlack || slack >= kPackSlack)) l_cnt |= int64_t(1) << 40;
       const int64_t ord = fair ? static_cast<int64_t>((sl << 22) | static_cast<uint64_t>(seq[j]))
                                : seq[j];  // selection ordinal
@@ -1498,14 +1582,8 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
         for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) {
           ws.mark[q] = 0;
           const int64_t g = w.roff + q, row = w.toff + q;
-          WRec r;
-          r.dl0 = P.arrival[row] + P.ttft[row];  // slo.h:45-61 anchor
-          r.first = P.first[g];
-          r.prompt = P.prompt[row];
-          r.prefilled = P.prefilled[g];
-          r.nidx = P.nidx[g];
-          r.seq = P.seq[g];
-          ws.rec[q] = r;
+          ws.rec[q] = make_wrec(P.arrival[row] + P.ttft[row], P.first[g], P.prompt[row],
+                                P.prefilled[g], P.nidx[g], P.seq[g]);
         }
         for (int64_t q = threadIdx.x; q < w.S.n_active; q += kWideThreads) w.vl[q].y = 0;
         __syncthreads();
@@ -1896,18 +1974,26 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
         for (int k = threadIdx.x; k < kSelBins; k += kWideThreads) sm.hist[k] = 0;
         __syncthreads();
+        // each view's bin is kept in shared memory for K2b (index = the
+        // view's offset in this CTA's range; beyond kWgBinCap K2b recomputes)
+        const int64_t sb0 = s_v0[t] - my_lo;
+        const uint64_t pol_keep = l2_evict_last_policy();
         constexpr int U = 8;
         for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
           uint64_t kl[U];
 #pragma unroll
           for (int j = 0; j < U; ++j) {
             const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-            kl[j] = p < p_hi ? __ldcg(ws.klow + p) : 0;
+            kl[j] = p < p_hi ? ld_keep_u64(ws.klow + p, pol_keep) : 0;
           }
 #pragma unroll
           for (int j = 0; j < U; ++j) {
             const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-            if (p < p_hi) atomicAdd(&sm.hist[sel_bin(kl[j], sv.policy, sv.urgency, sv.sb)], 1u);
+            if (p < p_hi) {
+              const int bin = sel_bin(kl[j], sv.policy, sv.urgency, sv.sb);
+              atomicAdd(&sm.hist[bin], 1u);
+              if (sb0 + p < kWgBinCap) wg_bins(sm)[sb0 + p] = static_cast<uint16_t>(bin);
+            }
           }
         }
         __syncthreads();
@@ -1983,27 +2069,32 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
         int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
         int32_t* ncand = &slots[t].ncand;
-        constexpr int U = 8;
-        for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads * U) {
-          uint64_t kl[U];
-#pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-            kl[j] = p < p_hi ? __ldcg(ws.klow + p) : 0;
-          }
-#pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const int64_t p = b0 + j * kWideThreads + threadIdx.x;
-            const bool sel = p < p_hi && sel_bin(kl[j], sv.policy, sv.urgency, sv.sb) <= bmax;
-            const unsigned m = __ballot_sync(kFull, sel);
-            int base = 0;
-            if (m && lane_id() == 0) base = atomicAdd(ncand, __popc(m));
-            base = __shfl_sync(kFull, base, 0);
-            if (sel) {
-              const int slot = base + __popc(m & lanemask_lt());
-              ck[slot] = kl[j];  // key stem; the owner derives bin and key
-              cp[slot] = static_cast<int32_t>(p);
+        // the bins K2a left in shared memory: only the selected views' stems
+        // are read again (a window's worth per node, not every view)
+        const int64_t sb0 = s_v0[t] - my_lo;
+        const uint16_t* bins = wg_bins(sm);
+        for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads) {
+          const int64_t p = b0 + threadIdx.x;
+          bool sel = false;
+          uint64_t kl = 0;
+          if (p < p_hi) {
+            if (sb0 + p < kWgBinCap) {
+              sel = static_cast<int>(bins[sb0 + p]) <= bmax;
+              if (sel) kl = __ldcg(ws.klow + p);
+            } else {
+              kl = __ldcg(ws.klow + p);
+              sel = sel_bin(kl, sv.policy, sv.urgency, sv.sb) <= bmax;
             }
+          }
+          const unsigned m = __ballot_sync(kFull, sel);
+          if (m == 0) continue;
+          int base = 0;
+          if (lane_id() == 0) base = atomicAdd(ncand, __popc(m));
+          base = __shfl_sync(kFull, base, 0);
+          if (sel) {
+            const int slot = base + __popc(m & lanemask_lt());
+            ck[slot] = kl;  // key stem; the owner derives bin and key
+            cp[slot] = static_cast<int32_t>(p);
           }
         }
       }

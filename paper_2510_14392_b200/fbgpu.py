@@ -134,6 +134,17 @@ def lib() -> C.CDLL:
         "fb_cluster_shard_wait": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "fb_cluster_shard_fetch": (C.c_int, [vp, vp, vp, vp, pi64, C.POINTER(C.c_int32)]),
         "fb_cluster_shard_destroy": (None, [vp]),
+        "fb_nodes_create": (C.c_int, [C.c_int, C.POINTER(_abi.Trace), vp, i32,
+                                      i64, C.POINTER(_abi.LbConfig), C.POINTER(vp)]),
+        "fb_nodes_destroy": (None, [vp]),
+        "fb_nodes_count": (i32, [vp]),
+        "fb_nodes_advance": (C.c_int, [vp, i64, vp]),
+        "fb_nodes_enqueue": (C.c_int, [vp, i64, vp, vp, i64]),
+        "fb_nodes_begin": (C.c_int, [vp, i64, i32, i32]),
+        "fb_nodes_drain_rejects": (C.c_int, [vp, vp, vp, i64, pi64]),
+        "fb_nodes_current_pab": (C.c_int, [vp, i64, vp]),
+        "fb_nodes_state": (C.c_int, [vp, vp]),
+        "fb_nodes_fetch": (C.c_int, [vp, vp, vp, vp, C.POINTER(C.c_int32)]),
         "fb_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
         "fb_host_free": (C.c_int, [vp]),
     }

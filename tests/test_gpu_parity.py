@@ -622,3 +622,65 @@ def test_lead_capacity_overflow_reported(fb, gpu):
     a.run()
     assert all(s is None for s in a.lead())
     a.close()
+
+
+# ------------------------------------------------------------ interactive node set
+
+@pytest.mark.parametrize("name", ["pab0_8", "count0_8", "count37_3", "pab5000_8", "pab_hz10s_8",
+                                  "pab20_2", "c5_pab0_64", "rr_giant_2", "rr_pab30_3",
+                                  "rr_count0_4", "rr_mixed_4", "rr_off_pab0_4"])
+def test_host_dispatcher_over_node_set_matches_golden(golden, gpu_cluster_cases,
+                                                      gpu_reroute_cases, name):
+    """run_cluster's loop (cluster.cpp:134-251) on the host, over the batched
+    Node surface (fb_nodes_*: advance / enqueue / begin / drain_rejects with
+    the report hook): routing, per-node plan digests and records equal the
+    reference's run_cluster -- including retry_reroute, where the host
+    visits every event time and begins node by node."""
+    from backends import cluster_summary
+    from paper_2510_14392_b200.cluster import run_cluster_host
+    _, rows, cfgs, lb, hz = (gpu_cluster_cases.get(name) or gpu_reroute_cases[name])
+    out = run_cluster_host(rows, cfgs, lb, hz)
+    assert cluster_summary(out) == golden["clusters"][name]
+
+
+def test_node_set_queries(fb, gpu_cluster_cases):
+    """current_pab / state / drain_rejects against the same nodes' reports,
+    visiting every global event time (step ends and arrivals): a node that
+    completes at t reports at t, and its PAB / waiting / running queried at t
+    equal the report."""
+    from paper_2510_14392_b200.cluster import HostRouter, NodeSet
+    _, rows, cfgs, lb, hz = gpu_cluster_cases["pab0_8"]
+    ns = NodeSet(rows, cfgs, hz, lb)
+    view = HostRouter(len(cfgs), lb)
+    checked, arr = 0, 0
+    try:
+        for _ in range(1500):
+            st = ns.state()
+            busy = st["busy"] != 0
+            t = int(st["step_end"][busy].min()) if busy.any() else 1 << 62
+            t = min(t, int(rows.arrival_us[arr]))
+            rep = ns.advance(t)
+            st = ns.state()
+            pab = ns.current_pab(t)
+            for i in range(len(cfgs)):
+                assert st["busy"][i] == 0 or st["step_end"][i] > t
+                if rep["fresh"][i]:
+                    view.apply(i, int(rep["emitted_at"][i]), int(rep["pab_tokens"][i]),
+                               int(rep["waiting"][i]), int(rep["running"][i]))
+                    if rep["emitted_at"][i] == t:  # completed and reported at this instant
+                        assert pab[i] == rep["pab_tokens"][i]
+                        assert (st["waiting"][i], st["running"][i]) == (rep["waiting"][i],
+                                                                        rep["running"][i])
+                        checked += 1
+            q = arr
+            while arr < len(rows) and rows.arrival_us[arr] == t:
+                arr += 1
+            ns.enqueue(t, [view.route(int(rows.prompt_len[k])) for k in range(q, arr)],
+                       np.arange(q, arr))
+            ns.begin(t)
+        assert checked > 100
+        assert isinstance(ns.drain_rejects(), list)
+        with pytest.raises(fb.UsageError):
+            ns.enqueue(0, [len(cfgs)], [0])
+    finally:
+        ns.close()
