@@ -1405,7 +1405,9 @@ int fb_nodes_fetch(fb_nodes* h, fb_instance_result* node_results, fb_record* rec
   if (st) return st;
   fb_cluster_shard* s = h->sh;
   const int64_t routed_all[1] = {s->nr};  // trace arrivals are the dispatcher's business
-  FB_CUDA(cudaMemcpy(s->d_out, routed_all, sizeof(int64_t), cudaMemcpyHostToDevice));
+  FB_CUDA(cudaMemcpyAsync(s->d_out, routed_all, sizeof(int64_t), cudaMemcpyHostToDevice,
+                          s->a->stream));
+  FB_CUDA(cudaStreamSynchronize(s->a->stream));
   return fb_cluster_shard_fetch(s, node_results, records, node_of_row, nullptr, incomplete_out);
 }
 

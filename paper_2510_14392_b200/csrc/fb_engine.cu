@@ -131,6 +131,14 @@ extern "C" int fb_debug_wide_prof(unsigned long long* out, int reset) {
   }
   return static_cast<int>(cudaDeviceSynchronize());
 }
+extern "C" int fb_debug_sub_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_sub_prof, sizeof(unsigned long long) * 256 * 8);
+  if (reset) {
+    static unsigned long long z[256 * 8] = {};
+    cudaMemcpyToSymbol(g_sub_prof, z, sizeof(z));
+  }
+  return static_cast<int>(cudaDeviceSynchronize());
+}
 extern "C" int fb_debug_cta_prof(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_cta_prof, sizeof(unsigned long long) * 256 * 4);
   if (reset) {

@@ -26,6 +26,7 @@ namespace fbgpu {
 #ifdef FB_WIDE_PROF
 __device__ unsigned long long g_wide_prof[24];
 __device__ unsigned long long g_cta_prof[256][4];  // per CTA busy clocks: K1, hist, gather, owner
+__device__ unsigned long long g_sub_prof[256][8];   // per CTA sub-phase clocks (SPROF)
 #define WPROF_START long long wp_t_ = clock64();
 #define WPROF(slot)                                                               \
   if (threadIdx.x == 0) {                                                         \
@@ -1866,13 +1867,20 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     atomicAdd(&g_wide_prof[slot], static_cast<unsigned long long>(n_ - gp_t));         \
     gp_t = n_;                                                                         \
   }
-#define CPROF_START long long cp_t_ = clock64();
+#define CPROF_START long long cp_t_ = clock64(); long long sp_t_ = cp_t_;
+#define SPROF(k)                                                                       \
+  if (threadIdx.x == 0) {                                                              \
+    const long long n_ = clock64();                                                    \
+    g_sub_prof[blockIdx.x][k] += n_ - sp_t_;                                           \
+    sp_t_ = n_;                                                                        \
+  }
 #define CPROF(k)                                                                       \
   if (threadIdx.x == 0) g_cta_prof[blockIdx.x][k] += clock64() - cp_t_;
 #else
 #define GPROF(slot)
 #define CPROF_START
 #define CPROF(k)
+#define SPROF(k)
 #endif
   for (;;) {
     // ---- owner: advance to the next begin_step
@@ -1974,6 +1982,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
         for (int k = threadIdx.x; k < kSelBins; k += kWideThreads) sm.hist[k] = 0;
         __syncthreads();
+        SPROF(0)
         // each view's bin is kept in shared memory for K2b (index = the
         // view's offset in this CTA's range; beyond kWgBinCap K2b recomputes)
         const int64_t sb0 = s_v0[t] - my_lo;
@@ -1997,6 +2006,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
           }
         }
         __syncthreads();
+        SPROF(1)
         // Flush only up to this segment's own crossing bin (the first whose
         // cumulative count exceeds a window): the node's global crossing bin
         // can only come earlier (counts only add), so every bin up to it is
@@ -2027,6 +2037,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
           if (v && c0 + k <= cross) atomicAdd(gh + c0 + k, v);
         }
         __syncthreads();
+        SPROF(2)
         // the CTA that completes the node's histogram picks its window once
         if (threadIdx.x == 0) {
           __threadfence();
@@ -2047,6 +2058,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
           }
         }
         __syncthreads();
+        SPROF(3)
       }
       CPROF(1)
     }
@@ -2073,6 +2085,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         // are read again (a window's worth per node, not every view)
         const int64_t sb0 = s_v0[t] - my_lo;
         const uint16_t* bins = wg_bins(sm);
+        SPROF(4)
         for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads) {
           const int64_t p = b0 + threadIdx.x;
           bool sel = false;
@@ -2098,6 +2111,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
           }
         }
       }
+      SPROF(5)
       CPROF(2)
     }
     wg_barrier(P.wg.bar, ++gen);
