@@ -1097,7 +1097,7 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
   const int32_t* vrow = reinterpret_cast<const int32_t*>(w.vl);  // .x of {row, take}
   constexpr int U = 4;
   int64_t mn[6] = {kInf, kInf, kInf, kInf, kInf, kInf};
-  int64_t l_cnt = 0;
+  int64_t l_cnt = 0, l_views = 0;
   // The row indices are loaded two batches ahead and the records of the
   // next batch prefetched into L2 one batch ahead (prefetches hold no
   // registers), so each batch's record loads hit L2 instead of waiting on
@@ -1138,6 +1138,7 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
     for (int j = 0; j < U; ++j) {
       if (rr[j] < 0) continue;
       const int64_t p = b0 + j * kWideThreads + threadIdx.x;
+      ++l_views;
       const int64_t as = (static_cast<int64_t>(static_cast<uint32_t>(rc[j].y)) << 32) |
                          static_cast<uint32_t>(rc[j].x);
       seq[j] = static_cast<int32_t>(as & kWRecSeqMask);
@@ -1164,12 +1165,15 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
       }
     }
   }
-  block_min_n<6>(mn, sm);
-  const int64_t cnt = block_sum(l_cnt, sm);
+  // warp-level reductions only: the warps fold into the node's global row
+  // with atomics (no CTA barrier per view range)
 #pragma unroll
-  for (int q = 0; q < 6; ++q) r[q] = mn[q];
-  r[6] = kInf;
-  r[7] = cnt;
+  for (int q = 0; q < 6; ++q) r[q] = warp_min_i64(mn[q]);
+  r[6] = warp_sum_small(l_views);
+  int64_t c = l_cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  r[7] = c;
 }
 
 // Combines K1 partials (elementwise min of [0,7), sum of [7]).
@@ -1547,6 +1551,10 @@ __device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w,
     my->begin = 1;
     my->policy = w.policy;
     my->ncand = 0;
+    int64_t* row = P.wg.partial + static_cast<int64_t>(blockIdx.x) * kK1Vals;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) row[k] = kInf;
+    row[7] = 0;
     my->k1_done = 0;
     my->hist_done = 0;
     my->bmax = -2;
@@ -1937,19 +1945,24 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const bool fair = sv.policy == FB_POLICY_FAIRBATCH || sv.policy == FB_POLICY_FAIRBATCH_PAB;
         int64_t r[kK1Vals];
         wide_k1_views(P, wv, a - s_v0[t], z - s_v0[t], sv.now, fair, r, sm);
-        if (threadIdx.x == 0) {
-          int64_t* part =
-              P.wg.partial + (static_cast<int64_t>(blockIdx.x) * n_slots + t) * kK1Vals;
+        // each warp folds its reductions into the node's row (P.wg.partial
+        // row t, reset by the owner at publish); the warp that completes the
+        // node's view count derives init budget, urgency and selection bins
+        if (lane_id() == 0 && r[6] > 0) {
+          int64_t* row = P.wg.partial + static_cast<int64_t>(t) * kK1Vals;
 #pragma unroll
-          for (int k = 0; k < kK1Vals; ++k) part[k] = r[k];
-          // the CTA that completes the node's views combines everyone's
-          // partials once (init budget, urgency, selection bins)
+          for (int k = 0; k < 6; ++k)
+            if (r[k] != kInf)
+              atomicMin(reinterpret_cast<long long*>(row + k), static_cast<long long>(r[k]));
+          atomicAdd(reinterpret_cast<unsigned long long*>(row + 7),
+                    static_cast<unsigned long long>(r[7]));
           __threadfence();
-          const unsigned long long seg = static_cast<unsigned long long>(z - a);
+          const unsigned long long seg = static_cast<unsigned long long>(r[6]);
           if (atomicAdd(&slots[t].k1_done, seg) + seg == static_cast<unsigned long long>(sv.A)) {
             __threadfence();
             int64_t acc[kK1Vals];
-            wg_combine(P, sp, t, acc);
+#pragma unroll
+            for (int k = 0; k < kK1Vals; ++k) acc[k] = __ldcg(row + k);
             const WideStep ss = wide_step(acc, sv.A, sv.policy);
             volatile WideSlot* vs = slots + t;
 #pragma unroll
@@ -2082,34 +2095,38 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
         int32_t* ncand = &slots[t].ncand;
         // the bins K2a left in shared memory: only the selected views' stems
-        // are read again (a window's worth per node, not every view)
+        // are read again (a window's worth per node, not every view).  Count
+        // this CTA's selected views, reserve their slots with one atomic,
+        // then write them (any order: the owner sorts the window).
         const int64_t sb0 = s_v0[t] - my_lo;
         const uint16_t* bins = wg_bins(sm);
         SPROF(4)
-        for (int64_t b0 = p_lo; b0 < p_hi; b0 += kWideThreads) {
-          const int64_t p = b0 + threadIdx.x;
-          bool sel = false;
-          uint64_t kl = 0;
-          if (p < p_hi) {
-            if (sb0 + p < kWgBinCap) {
-              sel = static_cast<int>(bins[sb0 + p]) <= bmax;
-              if (sel) kl = __ldcg(ws.klow + p);
-            } else {
-              kl = __ldcg(ws.klow + p);
-              sel = sel_bin(kl, sv.policy, sv.urgency, sv.sb) <= bmax;
-            }
-          }
-          const unsigned m = __ballot_sync(kFull, sel);
-          if (m == 0) continue;
-          int base = 0;
-          if (lane_id() == 0) base = atomicAdd(ncand, __popc(m));
-          base = __shfl_sync(kFull, base, 0);
+        int cnt = 0;
+        for (int64_t p = p_lo + threadIdx.x; p < p_hi; p += kWideThreads) {
+          const bool sel = sb0 + p < kWgBinCap
+                               ? static_cast<int>(bins[sb0 + p]) <= bmax
+                               : sel_bin(__ldcg(ws.klow + p), sv.policy, sv.urgency, sv.sb) <= bmax;
+          cnt += sel;
+        }
+        int tot;
+        int slot = block_excl_sum(cnt, tot, sm);
+        if (tot == 0) continue;
+        if (threadIdx.x == 0) sm.ibcast[7] = atomicAdd(ncand, tot);
+        __syncthreads();
+        slot += sm.ibcast[7];
+        for (int64_t p = p_lo + threadIdx.x; cnt > 0 && p < p_hi; p += kWideThreads) {
+          const uint64_t kl = sb0 + p < kWgBinCap ? 0 : __ldcg(ws.klow + p);
+          const bool sel = sb0 + p < kWgBinCap
+                               ? static_cast<int>(bins[sb0 + p]) <= bmax
+                               : sel_bin(kl, sv.policy, sv.urgency, sv.sb) <= bmax;
           if (sel) {
-            const int slot = base + __popc(m & lanemask_lt());
-            ck[slot] = kl;  // key stem; the owner derives bin and key
+            ck[slot] = sb0 + p < kWgBinCap ? __ldcg(ws.klow + p) : kl;  // key stem
             cp[slot] = static_cast<int32_t>(p);
+            ++slot;
+            --cnt;
           }
         }
+        __syncthreads();
       }
       SPROF(5)
       CPROF(2)
