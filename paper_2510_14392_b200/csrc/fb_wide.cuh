@@ -1763,7 +1763,7 @@ __device__ __forceinline__ void wg_window(const EngineParams& P, int t, int64_t 
 // merge sort is cheaper.
 constexpr int64_t kBinRankWork = int64_t(1) << 20;
 __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int policy,
-                            const WideStep& ss, WideSmem& sm) {
+                            const WideStep& ss, const uint64_t* klow, WideSmem& sm) {
   const uint32_t* gh = P.wg.hist + static_cast<size_t>(t) * kSelBins;
   uint32_t* start = sm.hist;                                // [bin] first slot
   uint32_t* cur = reinterpret_cast<uint32_t*>(sm.wcc);      // [bin] fill cursor
@@ -1797,7 +1797,7 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
   const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
   if (rank_work > kBinRankWork) {
     for (int k = threadIdx.x; k < K; k += kWideThreads) {
-      sm.wkey[k] = wide_key(__ldcg(ck + k), policy, ss.urgency);
+      sm.wkey[k] = wide_key(__ldcg(klow + __ldcg(cp + k)), policy, ss.urgency);
       sm.wpos[k] = __ldcg(cp + k);
     }
     __syncthreads();
@@ -1808,7 +1808,7 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
   for (int q = 0; q < kWideWin / kWideThreads; ++q) {
     const int k = threadIdx.x + q * kWideThreads;
     if (k < K) {
-      const uint64_t kl = __ldcg(ck + k);
+      const uint64_t kl = __ldcg(klow + __ldcg(cp + k));
       const int b = sel_bin(kl, policy, ss.urgency, ss.sb);
       const uint32_t dst = atomicAdd(&cur[b], 1u);
       tkey[dst] = wide_key(kl, policy, ss.urgency);
@@ -2114,13 +2114,12 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         if (threadIdx.x == 0) sm.ibcast[7] = atomicAdd(ncand, tot);
         __syncthreads();
         slot += sm.ibcast[7];
+        // positions only: the owner reads the window's stems itself
         for (int64_t p = p_lo + threadIdx.x; cnt > 0 && p < p_hi; p += kWideThreads) {
-          const uint64_t kl = sb0 + p < kWgBinCap ? 0 : __ldcg(ws.klow + p);
           const bool sel = sb0 + p < kWgBinCap
                                ? static_cast<int>(bins[sb0 + p]) <= bmax
-                               : sel_bin(kl, sv.policy, sv.urgency, sv.sb) <= bmax;
+                               : sel_bin(__ldcg(ws.klow + p), sv.policy, sv.urgency, sv.sb) <= bmax;
           if (sel) {
-            ck[slot] = sb0 + p < kWgBinCap ? __ldcg(ws.klow + p) : kl;  // key stem
             cp[slot] = static_cast<int32_t>(p);
             ++slot;
             --cnt;
@@ -2151,7 +2150,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       if (bmax >= 0) {
         K0 = vs->ncand;
         WPROF(0)
-        wg_bin_sort(P, t, K0, bmax, w.policy, ss, sm);
+        wg_bin_sort(P, t, K0, bmax, w.policy, ss, wide_scratch(P, w).klow, sm);
         WPROF(1)
       } else {
         all0 = false;
