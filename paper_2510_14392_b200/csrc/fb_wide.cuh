@@ -1815,56 +1815,20 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
       tpos[dst] = __ldcg(cp + k);
     }
   }
-  // Rank within bins (keys are unique), balanced over the CTA: one work item
-  // = (key i of bin b, a chunk of 64 of b's keys), n_b * ceil(n_b / 64) items
-  // for a bin of n_b keys, so a bin crowded by slack ties is shared by many
-  // threads instead of each of its keys' threads scanning the whole bin.
-  uint32_t* istart = reinterpret_cast<uint32_t*>(sm.wcx);  // [bin] first item
-  uint32_t* rnk = sm.wnw;                                   // [slot] rank in its bin
-  int litems = 0;
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int n = static_cast<int>(hv[k]);
-    litems += n * ((n + 63) >> 6);
-  }
-  int total_items;
-  int irun = block_excl_sum(litems, total_items, sm);
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    istart[c0 + k] = static_cast<uint32_t>(irun);
-    const int n = static_cast<int>(hv[k]);
-    irun += n * ((n + 63) >> 6);
-  }
-  for (int k = threadIdx.x; k < K; k += kWideThreads) rnk[k] = 0;
-  __syncthreads();
-  for (int it = threadIdx.x; it < total_items; it += kWideThreads) {
-    int lo = 0, hi = bmax;  // the last bin whose first item is <= it
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (static_cast<int>(istart[mid]) <= it) lo = mid; else hi = mid - 1;
-    }
-    const int b0 = static_cast<int>(start[lo]);
-    const int n = static_cast<int>(cur[lo]) - b0;
-    const int chunks = (n + 63) >> 6;
-    const int local = it - static_cast<int>(istart[lo]);
-    const int i = local / chunks, c = local - (local / chunks) * chunks;
-    const uint64_t x = tkey[b0 + i];
-    const int q0 = b0 + c * 64, q1 = q0 + 64 < b0 + n ? q0 + 64 : b0 + n;
-    int cnt = 0;
-    for (int q = q0; q < q1; ++q) cnt += tkey[q] < x;
-    if (cnt) atomicAdd(&rnk[b0 + i], static_cast<uint32_t>(cnt));
-  }
   __syncthreads();
   for (int k = threadIdx.x; k < K; k += kWideThreads) {
+    const uint64_t x = tkey[k];
     // bin of slot k: the last bin whose start is <= k (binary search)
     int lo = 0, hi = bmax;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (static_cast<int>(start[mid]) <= k) lo = mid; else hi = mid - 1;
     }
-    const int dst = static_cast<int>(start[lo]) + static_cast<int>(rnk[k]);
-    sm.wkey[dst] = tkey[k];
-    sm.wpos[dst] = tpos[k];
+    const int b0 = static_cast<int>(start[lo]), b1 = static_cast<int>(cur[lo]);
+    int rank = 0;
+    for (int q = b0; q < b1; ++q) rank += tkey[q] < x;
+    sm.wkey[b0 + rank] = x;
+    sm.wpos[b0 + rank] = tpos[k];
   }
   __syncthreads();
 }
