@@ -324,6 +324,10 @@ int fb_arena_last_run_split_ms(fb_arena* arena, float* warp_ms, float* wide_ms);
  * {owner advance, K1 views, K2a histogram, K2b gather, owner finish};
  * *iterations (may be NULL) = lockstep iterations. */
 int fb_arena_wide_phases(fb_arena* arena, double* ms_out, int64_t* iterations);
+/* Selection path counts of the last run's grid-wide wide engine: node steps
+ * whose window K1 gathered itself (fused candidate window) and node steps
+ * that took the K2a / K2b passes. */
+int fb_arena_wide_selection(fb_arena* arena, int64_t* fused_steps, int64_t* k2_steps);
 
 int fb_arena_fetch_results(fb_arena* arena, fb_instance_result* out);
 /* Records for instance rows: out has sum over instances of n_req rows, in

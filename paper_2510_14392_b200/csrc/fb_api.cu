@@ -557,6 +557,18 @@ int fb_arena_wide_phases(fb_arena* a, double* ms_out, int64_t* iterations) {
   return FB_OK;
 }
 
+int fb_arena_wide_selection(fb_arena* a, int64_t* fused_steps, int64_t* k2_steps) {
+  if (!a || !a->loaded || !fused_steps || !k2_steps)
+    return set_error(FB_ERR_USAGE, "fb_arena_wide_selection");
+  FB_CUDA(cudaSetDevice(a->device));
+  unsigned long long h[16] = {};
+  FB_CUDA(cudaMemcpyAsync(h, a->wg_bar.p, sizeof(h), cudaMemcpyDeviceToHost, a->stream));
+  FB_CUDA(cudaStreamSynchronize(a->stream));
+  *fused_steps = static_cast<int64_t>(h[14]);
+  *k2_steps = static_cast<int64_t>(h[15]);
+  return FB_OK;
+}
+
 int fb_arena_synchronize(fb_arena* a) {
   if (!a) return set_error(FB_ERR_USAGE, "null arena");
   FB_CUDA(cudaSetDevice(a->device));

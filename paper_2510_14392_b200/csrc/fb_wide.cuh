@@ -297,119 +297,132 @@ __device__ __forceinline__ uint64_t wide_key(uint64_t klow, int policy, int64_t 
   return seq;
 }
 
-// Ascending sort of sm.wkey / sm.wpos [0, K) (keys unique; K <= kWideWin).
-// Each warp sorts a run of 128 elements in registers (4 consecutive per lane:
-// bitonic network, in-thread strides 1-2, shuffle strides 4-64, no barrier),
-// then four merge-path rounds double the runs (128 -> 2048): every thread
-// finds where its 4 outputs start by a binary search on the two input runs
-// (co-rank) and merges them sequentially.  Padding keys (~0) sort last.
-constexpr int kPerT = kWideWin / kWideThreads;  // 4
-constexpr int kRun = kWarp * kPerT;             // 128
-__device__ __forceinline__ void bitonic_cx(uint64_t& a, int32_t& pa, uint64_t b, int32_t pb,
-                                           bool take_min) {
-  const bool sw = take_min ? (b < a) : (b > a);
-  if (sw) {
-    a = b;
-    pa = pb;
-  }
+// Branch-free bitonic sort of sm.wkey / sm.wpos [0, K) (keys unique, K <=
+// kWideWin; padding keys ~0 sort last), at the smallest size N = 512 * PER
+// (PER = 1, 2, 4 elements per thread) that holds K.  Element e = warp *
+// 32 * PER + lane * PER + q lives in register q of its lane: compare-
+// exchange distances below PER are in-thread, up to a warp's run (32 * PER)
+// lane shuffles, longer ones go through shared memory (one barrier per
+// distance).  Every exchange is a mask select, never a branch, and every
+// stage is unrolled at compile time (the earlier loop-form merge sort
+// compiled to divergent branches per element: 15 us for any K; this one
+// 9 us at N = 2048, tools/micro/sortbench.cu).
+__device__ __forceinline__ uint64_t msel64(uint64_t m, uint64_t x, uint64_t y) {
+  return (x & m) | (y & ~m);
 }
-__device__ void wide_sort_window(int K, WideSmem& sm) {
-  static_assert(kPerT == 4 && kWideWin == kRun * kWideWarps, "sort layout");
-  uint64_t k[kPerT];
-  int32_t v[kPerT];
-  const int e0 = threadIdx.x * kPerT;  // global element index of k[0]
-  const int l0 = lane_id() * kPerT;    // index inside the warp's run
+__device__ __forceinline__ int32_t msel32(uint32_t m, int32_t x, int32_t y) {
+  return static_cast<int32_t>((static_cast<uint32_t>(x) & m) | (static_cast<uint32_t>(y) & ~m));
+}
+// keys unique (padding ~0 only meets padding): b < a <=> !(a < b)
+__device__ __forceinline__ void cx_sel(uint64_t& a, int32_t& pa, uint64_t b, int32_t pb,
+                                       bool take_min) {
+  const uint32_t pick = 0u - static_cast<uint32_t>((b < a) == take_min);
+  const uint64_t pick64 = 0ull - static_cast<uint64_t>(pick & 1u);
+  a = msel64(pick64, b, a);
+  pa = msel32(pick, pb, pa);
+}
+__device__ __forceinline__ void cx_pair(uint64_t& a, int32_t& pa, uint64_t& b, int32_t& pb,
+                                        bool asc) {
+  const uint32_t sw = 0u - static_cast<uint32_t>((b < a) == asc);
+  const uint64_t sw64 = 0ull - static_cast<uint64_t>(sw & 1u);
+  const uint64_t lo = msel64(sw64, b, a), hi = msel64(sw64, a, b);
+  const int32_t plo = msel32(sw, pb, pa), phi = msel32(sw, pa, pb);
+  a = lo;
+  b = hi;
+  pa = plo;
+  pb = phi;
+}
+template <int PER, int KK, int J>
+__device__ __forceinline__ void bsort_reg_stages(uint64_t (&k)[PER], int32_t (&v)[PER], int e0) {
+  if constexpr (J >= PER) {
 #pragma unroll
-  for (int q = 0; q < kPerT; ++q) {
+    for (int q = 0; q < PER; ++q) {
+      const int e = e0 + q;
+      const uint64_t b = __shfl_xor_sync(kFull, k[q], J / PER);
+      const int32_t pb = __shfl_xor_sync(kFull, v[q], J / PER);
+      cx_sel(k[q], v[q], b, pb, ((e & J) == 0) == ((e & KK) == 0));
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      if ((q & J) != 0) continue;
+      cx_pair(k[q], v[q], k[q + J], v[q + J], ((e0 + q) & KK) == 0);
+    }
+  }
+  if constexpr (J > 1) bsort_reg_stages<PER, KK, J / 2>(k, v, e0);
+}
+template <int PER, int KK, int J>
+__device__ __forceinline__ void bsort_smem_stages(uint64_t* key, int32_t* pos) {
+#pragma unroll
+  for (int h = 0; h < PER / 2 + (PER == 1 ? 1 : 0); ++h) {
+    const int pid = threadIdx.x + h * kWideThreads;  // pair index
+    if (PER == 1 && pid >= kWideThreads / 2) break;
+    const int e = (pid / J) * (2 * J) + (pid % J);
+    uint64_t a = key[e], b = key[e + J];
+    int32_t pa = pos[e], pb = pos[e + J];
+    cx_pair(a, pa, b, pb, (e & KK) == 0);
+    key[e] = a;
+    pos[e] = pa;
+    key[e + J] = b;
+    pos[e + J] = pb;
+  }
+  __syncthreads();
+  if constexpr (J / 2 >= kWarp * PER) bsort_smem_stages<PER, KK, J / 2>(key, pos);
+}
+template <int PER, int KK>
+__device__ __forceinline__ void bsort_merge(uint64_t (&k)[PER], int32_t (&v)[PER], int e0,
+                                            WideSmem& sm) {
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    sm.wkey[e0 + q] = k[q];
+    sm.wpos[e0 + q] = v[q];
+  }
+  __syncthreads();
+  bsort_smem_stages<PER, KK, KK / 2>(sm.wkey, sm.wpos);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    k[q] = sm.wkey[e0 + q];
+    v[q] = sm.wpos[e0 + q];
+  }
+  bsort_reg_stages<PER, KK, kWarp * PER / 2>(k, v, e0);
+  if constexpr (KK < kWideThreads * PER) bsort_merge<PER, KK * 2>(k, v, e0, sm);
+}
+template <int PER, int KK>
+__device__ __forceinline__ void bsort_runs(uint64_t (&k)[PER], int32_t (&v)[PER], int e0) {
+  bsort_reg_stages<PER, KK, KK / 2>(k, v, e0);
+  if constexpr (KK < kWarp * PER) bsort_runs<PER, KK * 2>(k, v, e0);
+}
+template <int PER>
+__device__ void wide_bitonic_sort_n(int K, WideSmem& sm) {
+  static_assert(kWideThreads * PER <= kWideWin, "sort size");
+  uint64_t k[PER];
+  int32_t v[PER];
+  const int e0 = threadIdx.x * PER;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
     const int e = e0 + q;
     k[q] = e < K ? sm.wkey[e] : ~uint64_t(0);
     v[q] = e < K ? sm.wpos[e] : -1;
   }
-  // 1. warp runs of 128, ascending
-  for (int kk = 2; kk <= kRun; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= kPerT) {
-        const int lm = j / kPerT;
+  __syncthreads();  // every thread read its elements before the first smem stage
+  bsort_runs<PER, 2>(k, v, e0);
+  bsort_merge<PER, 2 * kWarp * PER>(k, v, e0, sm);
 #pragma unroll
-        for (int q = 0; q < kPerT; ++q) {
-          const int e = l0 + q;
-          const uint64_t b = __shfl_xor_sync(kFull, k[q], lm);
-          const int32_t pb = __shfl_xor_sync(kFull, v[q], lm);
-          const bool asc = (e & kk) == 0, lower = (e & j) == 0;
-          bitonic_cx(k[q], v[q], b, pb, lower == asc);
-        }
-      } else {
-        auto cx = [&](uint64_t& a, int32_t& pa, uint64_t& b, int32_t& pb, int e) {
-          const bool asc = (e & kk) == 0;
-          if ((a > b) == asc) {
-            const uint64_t tk = a;
-            a = b;
-            b = tk;
-            const int32_t tv = pa;
-            pa = pb;
-            pb = tv;
-          }
-        };
-        if (j == 2) {
-          cx(k[0], v[0], k[2], v[2], l0);
-          cx(k[1], v[1], k[3], v[3], l0 + 1);
-        } else {
-          cx(k[0], v[0], k[1], v[1], l0);
-          cx(k[2], v[2], k[3], v[3], l0 + 2);
-        }
-      }
+  for (int q = 0; q < PER; ++q) {
+    if (e0 + q < K) {
+      sm.wkey[e0 + q] = k[q];
+      sm.wpos[e0 + q] = v[q];
     }
-  }
-  uint64_t* src = sm.wkey;
-  int32_t* spos = sm.wpos;
-  uint64_t* dst = reinterpret_cast<uint64_t*>(sm.wtc);
-  int32_t* dpos = sm.wtake;
-#pragma unroll
-  for (int q = 0; q < kPerT; ++q) {
-    src[e0 + q] = k[q];
-    spos[e0 + q] = v[q];
   }
   __syncthreads();
-  // 2. merge-path rounds
-  for (int L = kRun; L < kWideWin; L <<= 1) {
-    const int g0 = (e0 / (2 * L)) * (2 * L);  // this pair of runs
-    const int i = e0 - g0;                    // first output inside the pair
-    const uint64_t* A = src + g0;
-    const uint64_t* B = A + L;
-    // co-rank: a + b = i with A[a-1] < B[b] and B[b-1] < A[a]
-    int lo = i > L ? i - L : 0, hi = i < L ? i : L;
-    while (lo < hi) {
-      const int a = (lo + hi) >> 1;
-      if (A[a] < B[i - a - 1]) lo = a + 1; else hi = a;
-    }
-    int a = lo, b = i - lo;
-#pragma unroll
-    for (int q = 0; q < kPerT; ++q) {
-      const bool takeA = b >= L || (a < L && A[a] < B[b]);
-      if (takeA) {
-        dst[e0 + q] = A[a];
-        dpos[e0 + q] = spos[g0 + a];
-        ++a;
-      } else {
-        dst[e0 + q] = B[b];
-        dpos[e0 + q] = spos[g0 + L + b];
-        ++b;
-      }
-    }
-    __syncthreads();
-    uint64_t* t = src;
-    src = dst;
-    dst = t;
-    int32_t* tp = spos;
-    spos = dpos;
-    dpos = tp;
-  }
-  if (src != sm.wkey) {
-    for (int e = threadIdx.x; e < K; e += kWideThreads) {
-      sm.wkey[e] = src[e];
-      sm.wpos[e] = spos[e];
-    }
-    __syncthreads();
+}
+__device__ void wide_bitonic_sort(int K, WideSmem& sm) {
+  if (K <= kWideThreads) {
+    wide_bitonic_sort_n<1>(K, sm);
+  } else if (K <= 2 * kWideThreads) {
+    wide_bitonic_sort_n<2>(K, sm);
+  } else {
+    wide_bitonic_sort_n<4>(K, sm);
   }
 }
 
@@ -492,7 +505,7 @@ __device__ int wide_select(const WideScratch& ws, int A, bool has_lo, uint64_t l
   }
   __syncthreads();
   const int K = sm.ibcast[4];
-  wide_sort_window(K, sm);
+  wide_bitonic_sort(K, sm);
   return K;
 }
 
@@ -624,7 +637,7 @@ __device__ int wide_select_binned(const WideScratch& ws, int A, bool has_lo, uin
   }
   __syncthreads();
   const int K = sm.ibcast[4];
-  wide_sort_window(K, sm);
+  wide_bitonic_sort(K, sm);
   if (threadIdx.x == 0) sm.ibcast[1] = all;
   __syncthreads();
   return K;
@@ -1055,6 +1068,74 @@ __device__ void wide_pull(const EngineParams& P, Inst& w, int64_t now, const Wid
 // and n_dec | (keys outside the packed range << 40) in [7] (summed).
 constexpr int kK1Vals = 8;
 
+// Fused candidate window.  K1 can select the window itself: with ordinal
+// thresholds (Td, Tp) published by the owner, a view is a candidate iff its
+// ordinal is below the threshold of its phase (decode: Td, prefill: Tp), and
+// K1 gathers the candidates' positions while it streams the views.  Whatever
+// the thresholds, the candidates are exactly the smallest keys -- a window,
+// as the K2 passes would select it -- iff every candidate key is below every
+// other key.  The thresholds are built per group of the threshold key so
+// that this holds by construction except for the one quantity K1 itself
+// reduces: the urgency, which splits fair batching's decodes into groups 0
+// and 2.  wide_fused_ok checks the decode threshold against the true
+// urgency ordinal.  When it fails, or the candidates overflow the window,
+// the node takes the K2a / K2b passes as before.  The thresholds are a prediction from the node's
+// previous step (WidePred): the boundary key its scan reached plus a margin,
+// kept as an absolute deadline so it stays put while `now` advances.
+struct WidePred {
+  int32_t valid;  // 0: no prediction (first wide step of a node)
+  int32_t g;      // group of the threshold key
+  int64_t d;      // fair batching: threshold deadline (slack + now); else 0
+  int64_t seq;    // threshold seq (fair: tie-break inside the deadline)
+  int64_t urgency;  // the step's urgency (fair), predicts the next one
+};
+
+// Ordinal thresholds (Td, Tp) for a step at `now` from the prediction.
+__device__ __forceinline__ void wide_thresholds(const WidePred& pr, int policy, int64_t now,
+                                                int64_t& td, int64_t& tp, bool& on) {
+  td = 0;
+  tp = 0;
+  on = pr.valid != 0;
+  if (!on) return;
+  const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
+  constexpr int64_t kOrdMax = int64_t(1) << 62;
+  int64_t ord;
+  if (fair) {
+    int64_t sl = pr.d - now + kPackSlack;
+    if (sl < 0) {  // below every packed key: no candidates
+      on = false;
+      return;
+    }
+    ord = sl >= 2 * kPackSlack ? (2 * kPackSlack) << 22 : (sl << 22) | pr.seq;
+    const int64_t u = pr.urgency < -kPackSlack
+                          ? -kPackSlack
+                          : (pr.urgency > kPackSlack ? kPackSlack : pr.urgency);
+    const int64_t uord = (u + kPackSlack) << 22;
+    if (pr.g == 0) {
+      td = ord;
+    } else if (pr.g == 1) {
+      td = uord;
+      tp = ord;
+    } else {
+      td = ord;
+      tp = kOrdMax;
+    }
+  } else {
+    ord = pr.seq;
+    if (policy == FB_POLICY_SARATHI) {
+      if (pr.g == 0) {
+        td = ord;
+      } else {
+        td = kOrdMax;
+        tp = ord;
+      }
+    } else {
+      td = ord;
+      tp = ord;
+    }
+  }
+}
+
 struct WideStep {
   int64_t A, n_dec, min_tpot, min_dec, ctx_min, urgency;
   double init_ms;
@@ -1089,7 +1170,9 @@ __device__ __forceinline__ Inst wide_view_ctx(const EngineParams& P, int64_t ins
 // r[].
 __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst& w, int64_t p_lo,
                                               int64_t p_hi, int64_t now, bool fair,
-                                              int64_t (&r)[kK1Vals], WideSmem& sm) {
+                                              int64_t (&r)[kK1Vals], WideSmem& sm, bool fused,
+                                              int64_t td, int64_t tp, int32_t* ncand,
+                                              int32_t* cpos) {
   const WideScratch ws = wide_scratch(P, w);
   const int64_t tpu = w.I->tpot_uniform;
   const uint64_t pol_stream = l2_evict_first_policy();
@@ -1134,6 +1217,7 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
       tpot[j] = tpu >= 0 ? tpu : P.tpot[w.toff + rr[j]];
     }
     int32_t seq[U];
+    unsigned cmask = 0;  // candidates of this batch (bit j)
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (rr[j] < 0) continue;
@@ -1155,6 +1239,7 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
                                : seq[j];  // selection ordinal
       mn[0] = tpot[j] < mn[0] ? tpot[j] : mn[0];
       mn[1] = ctx < mn[1] ? ctx : mn[1];
+      if (ord < (decode ? td : tp)) cmask |= 1u << j;
       if (decode) {
         l_cnt++;
         mn[2] = ord < mn[2] ? ord : mn[2];
@@ -1162,6 +1247,23 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
       } else {
         mn[4] = ord < mn[4] ? ord : mn[4];
         mn[5] = -ord < mn[5] ? -ord : mn[5];
+      }
+    }
+    // candidate gather: one slot reservation per warp and batch
+    if (fused && __any_sync(kFull, cmask != 0)) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const bool cand = (cmask >> j) & 1u;
+        const unsigned m = __ballot_sync(kFull, cand);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          int base = 0;
+          if (lane_id() == leader) base = atomicAdd(ncand, __popc(m));
+          base = __shfl_sync(kFull, base, leader);
+          const int slot = base + __popc(m & lanemask_lt());
+          if (cand && slot < kWideWin)
+            cpos[slot] = static_cast<int32_t>(b0 + j * kWideThreads + threadIdx.x);
+        }
       }
     }
   }
@@ -1174,16 +1276,6 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   r[7] = c;
-}
-
-// Combines K1 partials (elementwise min of [0,7), sum of [7]).
-__device__ __forceinline__ void wide_k1_combine(int64_t (&acc)[kK1Vals], const int64_t* part) {
-#pragma unroll
-  for (int q = 0; q < 7; ++q) {
-    const int64_t v = __ldcg(part + q);  // written by other CTAs: read from L2
-    acc[q] = v < acc[q] ? v : acc[q];
-  }
-  acc[7] += __ldcg(part + 7);
 }
 
 // init_time_budget (sched.cpp:90-106), urgency bound (sched.cpp:111-113) and
@@ -1233,6 +1325,22 @@ __device__ __forceinline__ WideStep wide_step(const int64_t (&mn)[kK1Vals], int6
   return s;
 }
 
+// Whether K1's candidates are a window that fits.  Fair batching: group 0
+// threshold -> the candidates are the decodes below Td, a prefix of group 0
+// iff Td <= the urgency ordinal U; group 1 -> all decodes below Td = the
+// predicted U plus the prefills below Tp: groups 0 and a prefix of 1 iff Td
+// == U; group 2 -> decodes below Td and every prefill: iff Td >= U.  Sarathi
+// and prefill-first thresholds are prefixes by construction (seq order).
+__device__ __forceinline__ bool wide_fused_ok(const WideStep& ss, int policy, int g, int64_t td,
+                                              int ncand) {
+  if (ss.bad || ncand <= 0 || ncand > kWideWin) return false;
+  if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
+    const int64_t uord = ss.sb.urg;
+    return g == 0 ? td <= uord : (g == 1 ? td == uord : td >= uord);
+  }
+  return true;
+}
+
 // Pull (engine.cpp:127-151) and the visible count; 0 means no step.
 __device__ int64_t wide_prepare(const EngineParams& P, Inst& w, int64_t now, WideSmem& sm) {
   w.S.paths |= kPathWide;
@@ -1244,7 +1352,7 @@ __device__ int64_t wide_prepare(const EngineParams& P, Inst& w, int64_t now, Wid
 // smallest keys; all of them when all0) is already sorted in sm.wkey /
 // sm.wpos; K0 < 0: select it here.
 __device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const WideStep& ss,
-                            int K0, bool all0, WideSmem& sm) {
+                            int K0, bool all0, WideSmem& sm, WidePred& pred) {
   const DevInst* I = w.I;
   const WideScratch ws = wide_scratch(P, w);
   WPROF_START
@@ -1285,6 +1393,7 @@ __device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const W
   uint64_t lo = 0;
   uint64_t esum = 0;
   int E_before = 0, Ew_before = 0;
+  int64_t seen_before = 0;  // keys of the earlier windows (all considered)
   int64_t l_pmax = -1;  // last view position of an admitted waiting task
   const bool log_on = P.log_on != 0;
   const int64_t entry_base = I->log_entry_off + w.S.log_entries;
@@ -1303,7 +1412,7 @@ __device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const W
       all = K < kWideWin;
     }
     WPROF(2)
-    WPROF_COUNT(9, 1)
+    WPROF_COUNT(20, 1)
     if (K == 0) break;
     for (int k = threadIdx.x; k < K; k += kWideThreads) {
       const View v = load_view(P, w, sm.wpos[k], now);
@@ -1360,7 +1469,55 @@ __device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const W
     }
     __syncthreads();
     WPROF(5)
-    if (done || all) break;
+    if (done || all) {
+      // the next step's candidate thresholds (WidePred): the boundary key the
+      // scan reached plus a margin of 5/4 of the keys of its group it took
+      // (+64).  Past the window's end the margin is extrapolated from the
+      // deadline (or seq) density of those keys, so the prediction can grow.
+      if (threadIdx.x == 0)
+        sm.ibcast[2] = done ? static_cast<int>(st.n_seen - seen_before) - 1 : K - 1;
+      __syncthreads();
+      int kb = sm.ibcast[2];
+      kb = kb < 0 ? 0 : (kb > K - 1 ? K - 1 : kb);
+      const uint64_t gb = sm.wkey[kb] >> 62;
+      int c = 0;
+      for (int k = threadIdx.x; k <= kb; k += kWideThreads) c += (sm.wkey[k] >> 62) == gb;
+      const int m_gb = static_cast<int>(block_sum(c, sm));
+      if (threadIdx.x == 0) {
+        constexpr uint64_t kLow = (uint64_t(1) << 62) - 1;
+        const int margin = m_gb + m_gb / 4 + 64;
+        pred.valid = 1;
+        pred.urgency = urgency;
+        const int R = kb + margin < K - 1 ? kb + margin : K - 1;
+        const uint64_t kr = sm.wkey[R];
+        if (kb + margin <= K - 1 || (kr >> 62) != gb) {
+          const int64_t ord = static_cast<int64_t>(kr & kLow);
+          pred.g = static_cast<int32_t>(kr >> 62);
+          pred.seq = ord & kWRecSeqMask;
+          pred.d = fair ? (ord >> 22) - kPackSlack + now : 0;
+        } else {
+          // the window ends inside group gb: extrapolate over [f, kb]
+          const int f = kb - m_gb + 1 > 0 ? kb - m_gb + 1 : 0;
+          const int n = kb - f;
+          const int64_t ob = static_cast<int64_t>(sm.wkey[kb] & kLow);
+          const int64_t of = static_cast<int64_t>(sm.wkey[f] & kLow);
+          const int64_t sb = ob & kWRecSeqMask, sf = of & kWRecSeqMask;
+          pred.g = static_cast<int32_t>(gb);
+          const int64_t db = fair ? (ob >> 22) - kPackSlack + now : 0;
+          const int64_t df = fair ? (of >> 22) - kPackSlack + now : 0;
+          if (fair && n > 0 && db > df) {
+            pred.d = db + ((db - df) * margin + n - 1) / n;
+            pred.seq = 0;
+          } else {
+            int64_t sq = n > 0 && sb > sf ? sb + ((sb - sf) * margin + n - 1) / n : sb + margin;
+            pred.d = db;
+            pred.seq = sq > kWRecSeqMask ? kWRecSeqMask : sq;
+          }
+        }
+      }
+      break;
+    }
+    seen_before += K;
     has_lo = true;
     lo = sm.wkey[K - 1];
     __syncthreads();
@@ -1482,13 +1639,16 @@ struct WideSlot {
   int64_t urgency;
   SelBins sb;
   int32_t bmax, all;     // window: last bin, holds every key
+  // fused candidate window: thresholds published by the owner, result of K1
+  int64_t td, tp;
+  int32_t fused, fok, fg, pad2;  // fg: group of the threshold key
 };
 
 // What a helper CTA needs of a slot, read from L2 (the slot is written by
 // another CTA).
 struct WgView {
-  int64_t inst, A, now, urgency;
-  int32_t policy, bmax;
+  int64_t inst, A, now, urgency, td, tp;
+  int32_t policy, bmax, fused, fok, fg;
   SelBins sb;
 };
 __device__ __forceinline__ WgView wg_view(const WideSlot* s) {
@@ -1500,6 +1660,11 @@ __device__ __forceinline__ WgView wg_view(const WideSlot* s) {
   o.policy = v->policy;
   o.urgency = v->urgency;
   o.bmax = v->bmax;
+  o.td = v->td;
+  o.tp = v->tp;
+  o.fused = v->fused;
+  o.fok = v->fok;
+  o.fg = v->fg;
 #pragma unroll
   for (int g = 0; g < 3; ++g) {
     o.sb.lo[g] = v->sb.lo[g];
@@ -1540,7 +1705,7 @@ __device__ __forceinline__ void wg_release(const EngineParams& P, Inst& w, bool&
 
 // Owner: publishes a beginning node to the grid.
 __device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w, int64_t A,
-                                           int64_t now, WideSlot* my) {
+                                           int64_t now, WideSlot* my, const WidePred& pred) {
   uint32_t* hist = P.wg.hist + static_cast<size_t>(blockIdx.x) * kSelBins;
   for (int q = threadIdx.x; q < kSelBins; q += kWideThreads) hist[q] = 0;
   if (threadIdx.x == 0) {
@@ -1553,8 +1718,16 @@ __device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w,
     my->ncand = 0;
     int64_t* row = P.wg.partial + static_cast<int64_t>(blockIdx.x) * kK1Vals;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) row[k] = kInf;
+    for (int k = 0; k < kK1Vals; ++k) row[k] = kInf;
     row[7] = 0;
+    int64_t td, tp;
+    bool on;
+    wide_thresholds(pred, w.policy, now, td, tp, on);
+    my->td = td;
+    my->tp = tp;
+    my->fused = on ? 1 : 0;
+    my->fg = pred.g;
+    my->fok = 0;
     my->k1_done = 0;
     my->hist_done = 0;
     my->bmax = -2;
@@ -1564,7 +1737,7 @@ __device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w,
 // Owner: runs the node's event loop until it must form a batch (returns
 // true, slot published) or the slot has no node left (returns false).
 __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& ev,
-                           WideSlot* my, WideSmem& sm) {
+                           WideSlot* my, WideSmem& sm, WidePred& pred) {
   for (;;) {
     if (!have) {
       if (threadIdx.x == 0) sm.bcast[0] = static_cast<int64_t>(atomicAdd(&P.work[2], 1ull));
@@ -1584,6 +1757,9 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
       if (w.S.done) continue;
       have = true;
       ev = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) pred.valid = 0;  // a new node: no prediction yet
+      __syncthreads();
       if (w.S.pending_begin) {
         // escalation: admitted-waiting marks all-zero, in-flight takes cleared
         // (the warp engine's memory path leaves consumed takes behind)
@@ -1600,7 +1776,7 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
         const int64_t now = w.S.t_last;
         const int64_t A = wide_prepare(P, w, now, sm);
         if (A > 0) {
-          wg_publish(P, w, A, now, my);
+          wg_publish(P, w, A, now, my, pred);
           return true;
         }
       }
@@ -1643,7 +1819,7 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
     if (!w.S.busy && t < w.horizon) {
       const int64_t A = wide_prepare(P, w, t, sm);
       if (A > 0) {
-        wg_publish(P, w, A, t, my);
+        wg_publish(P, w, A, t, my, pred);
         return true;
       }
     }
@@ -1699,24 +1875,6 @@ struct WgSplit {
     return b;
   }
 };
-
-// Combined K1 reductions of slot t: the partials of every CTA whose range
-// meets the slot (read from L2).
-__device__ __forceinline__ void wg_combine(const EngineParams& P, const WgSplit& sp, int t,
-                                           int64_t (&acc)[kK1Vals]) {
-#pragma unroll
-  for (int k = 0; k < 7; ++k) acc[k] = kInf;
-  acc[7] = 0;
-  const int64_t a = sp.v0[t], z = sp.v0[t + 1];
-  if (z <= a) return;
-  const int b0 = sp.cta_of(a), b1 = sp.cta_of(z - 1);
-  for (int b = b0; b <= b1; ++b) {
-    const int64_t lo = sp.lo(b) > a ? sp.lo(b) : a;
-    const int64_t hi = sp.lo(b + 1) < z ? sp.lo(b + 1) : z;
-    if (hi <= lo) continue;
-    wide_k1_combine(acc, P.wg.partial + (static_cast<int64_t>(b) * sp.n_slots + t) * kK1Vals);
-  }
-}
 
 // The window of slot t from its global histogram: last bin whose inclusive
 // count fits (-1: the first nonempty bin overflows), and whether it holds
@@ -1801,7 +1959,7 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
       sm.wpos[k] = __ldcg(cp + k);
     }
     __syncthreads();
-    wide_sort_window(K, sm);
+    wide_bitonic_sort(K, sm);
     return;
   }
 #pragma unroll
@@ -1848,9 +2006,11 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
   Inst& s_w = *reinterpret_cast<Inst*>(s_wbuf);
   __shared__ int s_have;
   __shared__ int64_t s_ev;
+  __shared__ WidePred s_pred;  // the owned node's candidate-window prediction
   if (threadIdx.x == 0) {
     s_have = 0;
     s_ev = 0;
+    s_pred.valid = 0;
   }
   __syncthreads();
   uint64_t gen = 0;
@@ -1897,7 +2057,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       Inst w = s_w;
       bool have = s_have != 0;
       int64_t ev = s_ev;
-      wg_advance(P, w, have, ev, my, sm);
+      wg_advance(P, w, have, ev, my, sm, s_pred);
       __syncthreads();
       if (threadIdx.x == 0) {
         s_w = w;
@@ -1944,7 +2104,8 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const Inst wv = wide_view_ctx(P, sv.inst);
         const bool fair = sv.policy == FB_POLICY_FAIRBATCH || sv.policy == FB_POLICY_FAIRBATCH_PAB;
         int64_t r[kK1Vals];
-        wide_k1_views(P, wv, a - s_v0[t], z - s_v0[t], sv.now, fair, r, sm);
+        wide_k1_views(P, wv, a - s_v0[t], z - s_v0[t], sv.now, fair, r, sm, sv.fused != 0, sv.td,
+                      sv.tp, &slots[t].ncand, P.wg.cpos + static_cast<size_t>(t) * kWideWin);
         // each warp folds its reductions into the node's row (P.wg.partial
         // row t, reset by the owner at publish); the warp that completes the
         // node's view count derives init budget, urgency and selection bins
@@ -1974,6 +2135,11 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
               vs->sb.sh[g] = ss.sb.sh[g];
             }
             vs->sb.urg = ss.sb.urg;
+            const int nc = atomicAdd(&slots[t].ncand, 0);
+            const bool ok = sv.fused != 0 && wide_fused_ok(ss, sv.policy, sv.fg, sv.td, nc);
+            vs->fok = ok ? 1 : 0;
+            atomicAdd(&P.wg.bar[ok ? 14 : 15], 1ull);
+            if (!ok) vs->ncand = 0;  // K2b gathers the window instead
           }
         }
       }
@@ -1982,6 +2148,15 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
     wg_barrier(P.wg.bar, ++gen);
     GPROF(13)
     phase(1);
+    // the K2 passes only for nodes whose candidates are not a window (every
+    // CTA reads the same slots after the barrier: the same decision)
+    int need = 0;
+    if (threadIdx.x < n_slots) {
+      const volatile WideSlot* sl = slots + threadIdx.x;
+      need = sl->inst >= 0 && sl->begin && !sl->fok;
+    }
+    const bool need_k2 = __syncthreads_or(need) != 0;
+    if (need_k2) {
     // ---- K2a: histogram of the selection bins
     {
       CPROF_START
@@ -1990,6 +2165,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const int64_t z = s_v0[t + 1] < my_hi ? s_v0[t + 1] : my_hi;
         if (z <= a) continue;
         const WgView sv = wg_view(slots + t);
+        if (sv.fok) continue;
         const Inst wv = wide_view_ctx(P, sv.inst);
         const WideScratch ws = wide_scratch(P, wv);
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
@@ -2087,7 +2263,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         if (z <= a) continue;
         const WgView sv = wg_view(slots + t);
         const int bmax = sv.bmax;
-        if (bmax < 0) continue;
+        if (sv.fok || bmax < 0) continue;
         const Inst wv = wide_view_ctx(P, sv.inst);
         const WideScratch ws = wide_scratch(P, wv);
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
@@ -2131,6 +2307,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       CPROF(2)
     }
     wg_barrier(P.wg.bar, ++gen);
+    }  // need_k2
     GPROF(15)
     phase(3);
     // ---- owner: the rest of begin_step
@@ -2147,7 +2324,23 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       const int bmax = vs->bmax;
       bool all0 = vs->all != 0;
       int K0 = -1;
-      if (bmax >= 0) {
+      if (vs->fok) {  // K1 gathered the window: its keys, sorted
+        K0 = vs->ncand;
+        all0 = K0 == vs->A;
+        const uint64_t* klow = wide_scratch(P, w).klow;
+        const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
+        WPROF(0)
+        for (int k = threadIdx.x; k < K0; k += kWideThreads) {
+          const int32_t pos = __ldcg(cp + k);
+          sm.wkey[k] = wide_key(__ldcg(klow + pos), w.policy, ss.urgency);
+          sm.wpos[k] = pos;
+        }
+        __syncthreads();
+        WPROF(21)
+        wide_bitonic_sort(K0, sm);
+        WPROF(1)
+        WPROF_COUNT(18, K0)
+      } else if (bmax >= 0) {
         K0 = vs->ncand;
         WPROF(0)
         wg_bin_sort(P, t, K0, bmax, w.policy, ss, wide_scratch(P, w).klow, sm);
@@ -2155,7 +2348,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       } else {
         all0 = false;
       }
-      wide_finish(P, w, vs->now, ss, K0, all0, sm);
+      wide_finish(P, w, vs->now, ss, K0, all0, sm, s_pred);
       __syncthreads();
       if (w.S.done) wg_release(P, w, have);
       if (threadIdx.x == 0) {

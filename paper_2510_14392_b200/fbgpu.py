@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         "fb_arena_last_run_ms": (C.c_int, [vp, C.POINTER(C.c_float)]),
         "fb_arena_last_run_split_ms": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
         "fb_arena_wide_phases": (C.c_int, [vp, C.POINTER(C.c_double), pi64]),
+        "fb_arena_wide_selection": (C.c_int, [vp, pi64, pi64]),
         "fb_arena_fetch_results": (C.c_int, [vp, vp]),
         "fb_arena_fetch_records": (C.c_int, [vp, vp]),
         "fb_arena_fetch_summaries": (C.c_int, [vp, vp]),
@@ -377,6 +378,14 @@ class Arena:
         _check(self._lib.fb_arena_wide_phases(self._h, ms, C.byref(it)), "fb_arena_wide_phases")
         names = ("owner_advance", "k1_views", "k2_hist", "k2_gather", "owner_finish_cta0")
         return dict(zip(names, list(ms))), it.value
+
+    def wide_selection(self) -> dict:
+        """Node steps of the last run whose window K1 gathered itself (fused)
+        and node steps that took the K2a / K2b passes."""
+        f, k = C.c_int64(0), C.c_int64(0)
+        _check(self._lib.fb_arena_wide_selection(self._h, C.byref(f), C.byref(k)),
+               "fb_arena_wide_selection")
+        return {"fused": f.value, "k2": k.value}
 
     def results(self) -> np.ndarray:
         out = np.zeros(max(1, self.n_instances), _abi.RESULT_DTYPE)

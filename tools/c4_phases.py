@@ -25,4 +25,4 @@ r = a.results()
 h = hashlib.sha1(r.tobytes()).hexdigest()[:12]
 med = {k: statistics.median(p[k] for p in ph) for k in ph[0]}
 print(f"{os.environ.get('FBGPU_LIB', 'default')}: {statistics.median(tot):.3f} ms "
-      + " ".join(f"{k}={v:.3f}" for k, v in med.items()) + f" digest {h}")
+      + " ".join(f"{k}={v:.3f}" for k, v in med.items()) + f" digest {h} {a.wide_selection()}")
