@@ -1172,7 +1172,7 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
                                               int64_t p_hi, int64_t now, bool fair,
                                               int64_t (&r)[kK1Vals], WideSmem& sm, bool fused,
                                               int64_t td, int64_t tp, int32_t* ncand,
-                                              int32_t* cpos) {
+                                              int32_t* cpos, uint64_t* ckey) {
   const WideScratch ws = wide_scratch(P, w);
   const int64_t tpu = w.I->tpot_uniform;
   const uint64_t pol_stream = l2_evict_first_policy();
@@ -1217,6 +1217,7 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
       tpot[j] = tpu >= 0 ? tpu : P.tpot[w.toff + rr[j]];
     }
     int32_t seq[U];
+    uint64_t stem[U];
     unsigned cmask = 0;  // candidates of this batch (bit j)
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -1231,9 +1232,10 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
       const int64_t slack = (as >> 22) + tpot[j] * ni - now;
       const int64_t ctx = rc[j].z;
       const uint64_t sl = fair ? static_cast<uint64_t>(slack + kPackSlack) : 0;
-      st_keep_u64(ws.klow + p,
-                  (decode ? (uint64_t(1) << 63) : 0) | (sl << 22) | static_cast<uint64_t>(seq[j]),
-                  pol_keep);
+      stem[j] = (decode ? (uint64_t(1) << 63) : 0) | (sl << 22) | static_cast<uint64_t>(seq[j]);
+      // a fused node keeps only its candidates' stems (ckey); the others
+      // are written for the K2 passes
+      if (!fused) st_keep_u64(ws.klow + p, stem[j], pol_keep);
       if (fair && (slack < -kPackSlack || slack >= kPackSlack)) l_cnt |= int64_t(1) << 40;
       const int64_t ord = fair ? static_cast<int64_t>((sl << 22) | static_cast<uint64_t>(seq[j]))
                                : seq[j];  // selection ordinal
@@ -1261,8 +1263,10 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
           if (lane_id() == leader) base = atomicAdd(ncand, __popc(m));
           base = __shfl_sync(kFull, base, leader);
           const int slot = base + __popc(m & lanemask_lt());
-          if (cand && slot < kWideWin)
+          if (cand && slot < kWideWin) {
             cpos[slot] = static_cast<int32_t>(b0 + j * kWideThreads + threadIdx.x);
+            ckey[slot] = stem[j];
+          }
         }
       }
     }
@@ -1276,6 +1280,16 @@ __device__ __forceinline__ void wide_k1_views(const EngineParams& P, const Inst&
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
   r[7] = c;
+}
+
+// The key stems of view positions [p_lo, p_hi) (K1's view code, stems only):
+// a fused node whose candidates were not a window needs them for the K2
+// passes or a later window.  Out of line: the rare path.
+__device__ __noinline__ void wide_write_stems(const EngineParams& P, const Inst& w, int64_t p_lo,
+                                              int64_t p_hi, int64_t now, bool fair, WideSmem& sm) {
+  int64_t r[kK1Vals];
+  wide_k1_views(P, w, p_lo, p_hi, now, fair, r, sm, false, 0, 0, nullptr, nullptr, nullptr);
+  __syncthreads();
 }
 
 // init_time_budget (sched.cpp:90-106), urgency bound (sched.cpp:111-113) and
@@ -1352,7 +1366,7 @@ __device__ int64_t wide_prepare(const EngineParams& P, Inst& w, int64_t now, Wid
 // smallest keys; all of them when all0) is already sorted in sm.wkey /
 // sm.wpos; K0 < 0: select it here.
 __device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const WideStep& ss,
-                            int K0, bool all0, WideSmem& sm, WidePred& pred) {
+                            int K0, bool all0, WideSmem& sm, WidePred& pred, bool stems) {
   const DevInst* I = w.I;
   const WideScratch ws = wide_scratch(P, w);
   WPROF_START
@@ -1402,6 +1416,10 @@ __device__ void wide_finish(const EngineParams& P, Inst& w, int64_t now, const W
     int K = K0;
     bool all = all0;
     K0 = -1;
+    if (K < 0 && !stems) {  // a later window of a fused node: its stems first
+      wide_write_stems(P, w, 0, A64, now, fair, sm);
+      stems = true;
+    }
     if (K < 0) {
       K = wide_select_binned(ws, A, has_lo, lo, policy, urgency, sb, sm);
       all = sm.ibcast[1] != 0;
@@ -2105,7 +2123,8 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const bool fair = sv.policy == FB_POLICY_FAIRBATCH || sv.policy == FB_POLICY_FAIRBATCH_PAB;
         int64_t r[kK1Vals];
         wide_k1_views(P, wv, a - s_v0[t], z - s_v0[t], sv.now, fair, r, sm, sv.fused != 0, sv.td,
-                      sv.tp, &slots[t].ncand, P.wg.cpos + static_cast<size_t>(t) * kWideWin);
+                      sv.tp, &slots[t].ncand, P.wg.cpos + static_cast<size_t>(t) * kWideWin,
+                      P.wg.ckey + static_cast<size_t>(t) * kWideWin);
         // each warp folds its reductions into the node's row (P.wg.partial
         // row t, reset by the owner at publish); the warp that completes the
         // node's view count derives init budget, urgency and selection bins
@@ -2169,6 +2188,10 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const Inst wv = wide_view_ctx(P, sv.inst);
         const WideScratch ws = wide_scratch(P, wv);
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
+        if (sv.fused) {  // K1 kept only candidate stems: write them all now
+          const bool fair = sv.policy == FB_POLICY_FAIRBATCH || sv.policy == FB_POLICY_FAIRBATCH_PAB;
+          wide_write_stems(P, wv, p_lo, p_hi, sv.now, fair, sm);
+        }
         for (int k = threadIdx.x; k < kSelBins; k += kWideThreads) sm.hist[k] = 0;
         __syncthreads();
         SPROF(0)
@@ -2327,13 +2350,12 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       if (vs->fok) {  // K1 gathered the window: its keys, sorted
         K0 = vs->ncand;
         all0 = K0 == vs->A;
-        const uint64_t* klow = wide_scratch(P, w).klow;
+        const uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
         const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
         WPROF(0)
         for (int k = threadIdx.x; k < K0; k += kWideThreads) {
-          const int32_t pos = __ldcg(cp + k);
-          sm.wkey[k] = wide_key(__ldcg(klow + pos), w.policy, ss.urgency);
-          sm.wpos[k] = pos;
+          sm.wkey[k] = wide_key(__ldcg(ck + k), w.policy, ss.urgency);
+          sm.wpos[k] = __ldcg(cp + k);
         }
         __syncthreads();
         WPROF(21)
@@ -2348,7 +2370,7 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       } else {
         all0 = false;
       }
-      wide_finish(P, w, vs->now, ss, K0, all0, sm, s_pred);
+      wide_finish(P, w, vs->now, ss, K0, all0, sm, s_pred, vs->fok == 0);
       __syncthreads();
       if (w.S.done) wg_release(P, w, have);
       if (threadIdx.x == 0) {
