@@ -169,8 +169,15 @@ __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
   if (tile_lane() == 0) {
     double tb = dsub(init_ms, f.a);
     int64_t tok = f.token_budget;
+    // b_lo = RD(b (1 - 2^-52)): x < b_lo gives fl(x / b) < 1, so a chunk of
+    // x = tb - cc budget floors to 0 tokens (no division needed), and with
+    // every task's new >= 1 and c*ctx >= 0 (exits_ok) each task costs at
+    // least b, so tb < b_lo admits nothing more: the exact stop (it implies
+    // the reference's implicit tb < 0 one).
+    const bool bpos = f.b > 0.0;
+    const double b_lo = bpos ? __dmul_rd(f.b, 1.0 - 0x1p-52) : 0.0;
     for (int k = 0; k < A; ++k) {
-      if (exits_ok && (tok <= 0 || tb < 0.0)) break;
+      if (exits_ok && (tok <= 0 || tb < 0.0 || tb < b_lo)) break;
       const double tc = s.tcost[k];
       const double cc = s.ccost[k];
       const int64_t nv = static_cast<int64_t>(static_cast<uint32_t>(s.khi[k]) & 0x7fffffffu);
@@ -179,7 +186,9 @@ __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
         tb = dsub(tb, tc);
         tok -= nv;
       } else if (tok > 0 && cc <= tb) {
-        const double lim = ddiv(dsub(tb, cc), f.b);
+        const double x = dsub(tb, cc);
+        if (bpos && x < b_lo) continue;  // floor(min(tok, x / b)) == 0
+        const double lim = ddiv(x, f.b);
         const double dt = static_cast<double>(tok);
         const double cp_real = lim < dt ? lim : dt;  // std::min(dt, lim)
         const int64_t cp = static_cast<int64_t>(floor(cp_real));
