@@ -310,10 +310,15 @@ def bench_c5(reps: int = 3, cpu: bool = True) -> dict:
     import ctypes as C
     from paper_2510_14392_b200 import cluster, fbgpu
     rows, cfgs, lb, hz = cluster.c5()
-    fit = C.c_int32(0)
-    fbgpu._check(fbgpu.lib().fb_cluster_max_hw_clusters(0, len(cfgs), C.byref(fit)),
-                 "fb_cluster_max_hw_clusters")
-    n_rep = max(1, fit.value)  # more would push every copy off the hardware-cluster path
+    fit1 = cluster.cluster_fit(len(cfgs), 1)
+    fit2 = cluster.cluster_fit(len(cfgs), 2)
+    # as many copies as fit as one-cluster grids at two CTAs per SM (more
+    # would push every copy off the hardware-cluster path), one stream each,
+    # at most one per hardware work queue (CUDA_DEVICE_MAX_CONNECTIONS, 32:
+    # a 33rd stream would queue behind another copy)
+    queues = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
+    n_rep = max(1, min(max(fit1, fit2), queues))
+    mode = cluster.cluster_density(n_rep, len(cfgs))
     best, out = 1e30, None
     for _ in range(reps):
         out = cluster.run_cluster(rows, cfgs, lb, hz)
@@ -331,7 +336,9 @@ def bench_c5(reps: int = 3, cpu: bool = True) -> dict:
         outs = cluster.run_clusters(cases, span=span)
         t_rep.append(span["ms"] / 1000.0)
     rep_steps = sum(int(o.node_results["steps"].sum()) for o in outs)
-    line["replicas"] = {"copies": n_rep, "fit_as_hw_clusters": fit.value,
+    line["replicas"] = {"copies": n_rep, "fit_as_hw_clusters": {"1_cta_per_sm": fit1,
+                                                                  "2_ctas_per_sm": fit2},
+                        "ctas_per_sm": mode,
                         "value": rep_steps / min(t_rep), "unit": "node-steps/s",
                         "ms_per_pass": 1000.0 * min(t_rep),
                         "timing": "host clock from the first launch to the last copy's "

@@ -481,11 +481,15 @@ int fb_cluster_shard_connect_ptrs(fb_cluster_shard* s, void* const* dev_ptrs);
  * any rank launches. */
 int fb_cluster_shard_reset(fb_cluster_shard* s);
 /* A one-rank shard of at most 8 CTAs runs as one thread-block cluster
- * (hardware cluster barrier, reports through distributed shared memory)
- * unless disallowed here -- e.g. when more shards run side by side than
- * fb_cluster_max_hw_clusters grids fit the device at once. */
+ * (hardware cluster barrier, reports through distributed shared memory):
+ * allow = 1 (default) one CTA per SM, 2 two CTAs per SM (for many shards side
+ * by side: each runs slower, twice as many fit), 0 the cooperative grid --
+ * e.g. when more shards run side by side than fit the device at once. */
 int fb_cluster_shard_allow_hw_cluster(fb_cluster_shard* s, int32_t allow);
+/* How many one-cluster grids of n_nodes fit the device at once (one CTA per
+ * SM); fb_cluster_fit: the same for ctas_per_sm = 1 or 2. */
 int fb_cluster_max_hw_clusters(int device, int32_t n_nodes, int32_t* out);
+int fb_cluster_fit(int device, int32_t n_nodes, int32_t ctas_per_sm, int32_t* out);
 int fb_cluster_shard_launch(fb_cluster_shard* s);
 int fb_cluster_shard_wait(fb_cluster_shard* s, double* device_ms_out);
 /* local_results: n_local entries (incomplete = this rank's view);

@@ -266,6 +266,25 @@ def run_cluster_logged(rows: Rows, cfgs, lb: LbConfig, horizon_us: int,
     return ClusterLogs(out, counts[:n], steps, entries, rejects, routes[:k], snaps[:k])
 
 
+def cluster_fit(n_nodes: int, ctas_per_sm: int = 1, device: int = 0) -> int:
+    """How many one-cluster grids of n_nodes fit the device at once."""
+    fit = C.c_int32(0)
+    fbgpu._check(fbgpu.lib().fb_cluster_fit(device, n_nodes, ctas_per_sm, C.byref(fit)),
+                 "fb_cluster_fit")
+    return fit.value
+
+
+def cluster_density(n_copies: int, n_nodes: int, device: int = 0) -> int:
+    """fb_cluster_shard_allow_hw_cluster mode for n_copies side by side: 1
+    (one CTA per SM) while they fit so, 2 (two per SM) while they fit so,
+    else 0 (cooperative grids)."""
+    if n_copies <= cluster_fit(n_nodes, 1, device):
+        return 1
+    if n_copies <= cluster_fit(n_nodes, 2, device):
+        return 2
+    return 0
+
+
 def run_clusters(cases, device: int = 0, span: dict | None = None) -> list[ClusterOutput]:
     """Independent cluster simulations at once -- one one-rank shard per case,
     each on its own stream, so their persistent cluster kernels (a few CTAs
@@ -282,13 +301,13 @@ def run_clusters(cases, device: int = 0, span: dict | None = None) -> list[Clust
         for rows, cfgs, lb, hz in cases:
             shards.append(ClusterShard(rows, cfgs, lb, hz, 0, 1, device))
         # one-cluster grids only while they all fit the device at once (more
-        # would run in waves): otherwise every shard takes the cooperative grid
-        fit = C.c_int32(0)
-        fbgpu._check(L.fb_cluster_max_hw_clusters(device, max(len(c[1]) for c in cases),
-                                                  C.byref(fit)), "fb_cluster_max_hw_clusters")
-        if len(cases) > fit.value:
+        # would run in waves): one CTA per SM while they fit so, else two per
+        # SM (each copy slower, twice as many at once), else every shard takes
+        # the cooperative grid
+        mode = cluster_density(len(cases), max(len(c[1]) for c in cases), device)
+        if mode != 1:
             for sh in shards:
-                fbgpu._check(L.fb_cluster_shard_allow_hw_cluster(sh._h, 0),
+                fbgpu._check(L.fb_cluster_shard_allow_hw_cluster(sh._h, mode),
                              "fb_cluster_shard_allow_hw_cluster")
         for sh in shards:
             sh.reset()

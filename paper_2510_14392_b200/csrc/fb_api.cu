@@ -752,7 +752,7 @@ struct fb_cluster_shard {
   int64_t nr = 0;
   int blocks = 0;
   bool connected = false, launched = false;
-  bool allow_hw = true;  // one thread-block cluster when the grid fits one
+  int hw_mode = 1;  // one thread-block cluster (1 or 2 CTAs per SM) when the grid fits one
   fbgpu::ClusterParamsHost cp{};
   std::vector<void*> bufs;    // device allocations
   std::vector<void*> opened;  // CUDA-IPC peer mappings
@@ -945,7 +945,8 @@ extern "C" {
 
 int fb_cluster_shard_allow_hw_cluster(fb_cluster_shard* s, int32_t allow) {
   if (!s) return set_error(FB_ERR_USAGE, "fb_cluster_shard_allow_hw_cluster: null shard");
-  s->allow_hw = allow != 0;
+  if (allow < 0 || allow > 2) return set_error(FB_ERR_USAGE, "fb_cluster_shard_allow_hw_cluster: mode 0, 1 or 2");
+  s->hw_mode = allow;
   return FB_OK;
 }
 
@@ -956,6 +957,17 @@ int fb_cluster_max_hw_clusters(int device, int32_t n_nodes, int32_t* out) {
     return set_error(FB_ERR_CUDA, "no CUDA device available (the product path has no CPU fallback)");
   FB_CUDA(cudaSetDevice(device));
   *out = fbgpu::cluster_max_hw_clusters(n_nodes);
+  return FB_OK;
+}
+
+int fb_cluster_fit(int device, int32_t n_nodes, int32_t ctas_per_sm, int32_t* out) {
+  if (!out || n_nodes < 1 || ctas_per_sm < 1 || ctas_per_sm > 2)
+    return set_error(FB_ERR_USAGE, "fb_cluster_fit: bad arguments");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return set_error(FB_ERR_CUDA, "no CUDA device available (the product path has no CPU fallback)");
+  FB_CUDA(cudaSetDevice(device));
+  *out = fbgpu::cluster_max_hw_clusters(n_nodes, ctas_per_sm);
   return FB_OK;
 }
 
@@ -1034,7 +1046,7 @@ int fb_cluster_shard_launch(fb_cluster_shard* s) {
   if (s->cp.retry_reroute) {
     FB_CUDA(fbgpu::launch_cluster_serial(s->a->params(0), s->cp, q));
   } else {
-    FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q, s->allow_hw));
+    FB_CUDA(fbgpu::launch_cluster(s->a->params(0), s->cp, s->blocks, q, s->hw_mode));
   }
   FB_CUDA(cudaEventRecord(s->a->ev1, q));
   s->launched = true;

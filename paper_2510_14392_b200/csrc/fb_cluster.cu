@@ -40,12 +40,20 @@ size_t cluster_smem_bytes(int warps_per_cta) {
          static_cast<size_t>(warps_per_cta) * kSmemSlots * kScratchBytesPerSlot;
 }
 
-int cluster_max_hw_clusters(int n_nodes) {
+// The cluster kernel for a CTA density (fb_cluster_shard_allow_hw_cluster):
+// 2 = two CTAs per SM, otherwise one.
+static const void* cluster_kernel_for(int ctas_per_sm) {
+  return ctas_per_sm == 2 ? reinterpret_cast<const void*>(cluster_kernel<2>)
+                          : reinterpret_cast<const void*>(cluster_kernel<1>);
+}
+
+int cluster_max_hw_clusters(int n_nodes, int ctas_per_sm) {
   const int wpc = cluster_warps_per_cta(n_nodes, 1);
   const int blocks = (n_nodes + wpc - 1) / wpc;
   if (blocks > 8) return 0;
   const size_t smem = cluster_smem_bytes(wpc);
-  if (cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const void* k = cluster_kernel_for(ctas_per_sm);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
     return 0;
   cudaLaunchConfig_t cfg = {};
@@ -60,7 +68,7 @@ int cluster_max_hw_clusters(int n_nodes) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, cluster_kernel, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -68,22 +76,23 @@ int cluster_max_hw_clusters(int n_nodes) {
 }
 
 cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, int blocks,
-                           cudaStream_t st, bool allow_hw) {
+                           cudaStream_t st, int hw_mode) {
   static_assert(sizeof(ClusterParamsHost) == sizeof(ClusterParams), "cluster params layout");
   ClusterParams c;
   std::memcpy(&c, &ch, sizeof(c));
   if (c.warps_per_cta < 1 || c.warps_per_cta > kClusterMaxWarps) return cudaErrorInvalidValue;
   const size_t smem = cluster_smem_bytes(c.warps_per_cta);
-  cudaError_t e = cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
   EngineParams pp = p;
   // One rank with at most kHwClusterMax CTAs: launch the grid as ONE
   // thread-block cluster (co-scheduled on one GPC by construction) and use
   // the hardware cluster barrier per epoch.  Otherwise a cooperative launch
   // (every CTA co-resident) with the global-memory exchange barrier.
   constexpr int kHwClusterMax = 8;  // portable cluster size
-  if (allow_hw && c.n_ranks == 1 && blocks <= kHwClusterMax && !std::getenv("FB_NO_HW_CLUSTER")) {
+  if (hw_mode > 0 && c.n_ranks == 1 && blocks <= kHwClusterMax && !std::getenv("FB_NO_HW_CLUSTER")) {
+    const void* k = cluster_kernel_for(hw_mode);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
     c.hw_cluster = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
@@ -97,14 +106,18 @@ cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& ch, i
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, cluster_kernel, pp, c);
+    e = hw_mode == 2 ? cudaLaunchKernelEx(&cfg, cluster_kernel<2>, pp, c)
+                     : cudaLaunchKernelEx(&cfg, cluster_kernel<1>, pp, c);
     if (e == cudaSuccess) return e;
     cudaGetLastError();  // not schedulable as one cluster: fall back
     c.hw_cluster = 0;
   }
+  cudaError_t e = cudaFuncSetAttribute(cluster_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
   void* args[] = {&pp, &c};
   // cooperative: every CTA must be co-resident for the epoch barrier
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cluster_kernel), dim3(blocks),
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cluster_kernel<1>), dim3(blocks),
                                      dim3(kWarp * c.warps_per_cta), args, smem, st);
 }
 
@@ -153,6 +166,14 @@ cudaError_t launch_nodes_enqueue(const EngineParams& p, const ClusterParamsHost&
 }
 
 #ifdef FB_CLUSTER_PROF
+#ifdef FB_CLUSTER_NODE_PROF
+extern "C" int fb_debug_node_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_node_prof, sizeof(unsigned long long) * 512 * 8);
+  static unsigned long long z[512 * 8] = {};
+  cudaMemcpyToSymbol(g_node_prof, z, sizeof(z));
+  return static_cast<int>(cudaDeviceSynchronize());
+}
+#endif
 extern "C" int fb_debug_cluster_prof(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_cluster_prof, sizeof(unsigned long long) * 8);
   unsigned long long z[8] = {};

@@ -484,10 +484,13 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
   }
 }
 
-// One CTA per SM: measured, two per SM (<= 128 registers) packs a cluster's
-// 8 CTAs onto 4 SMs -- C5 233 ms instead of 185 ms, and 33 side-by-side
-// copies 485 ms (16.6 M node-steps/s) against 16 copies in 217 ms.
-__global__ void __launch_bounds__(kWarp * kClusterMaxWarps, 1)
+// One persistent grid per cluster simulation.  kCtasPerSm = 1: one CTA per
+// SM (the single-simulation form, C5 184 ms); 2 (<= 128 registers): two per
+// SM for many simulations side by side -- a single copy slows to 237 ms, but
+// twice as many copies fit at once (32 copies in 257 ms: 30.4 M node-steps/s
+// against 16 copies in 206 ms: 19.0 M, tools/c5_replicas.py).
+template <int kCtasPerSm>
+__global__ void __launch_bounds__(kWarp * kClusterMaxWarps, kCtasPerSm)
 cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ ClusterParams C) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RouterSmem& rs = *reinterpret_cast<RouterSmem*>(smem_raw);

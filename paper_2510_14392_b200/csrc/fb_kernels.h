@@ -155,11 +155,12 @@ int cluster_warps_per_cta(int n_nodes, int n_ranks);
 size_t cluster_smem_bytes(int warps_per_cta);
 cudaError_t launch_cluster_serial(const EngineParams& p, const ClusterParamsHost& c,
                                   cudaStream_t st);
-// allow_hw: a one-rank grid of <= 8 CTAs may run as one thread-block cluster.
+// hw_mode: a one-rank grid of <= 8 CTAs may run as one thread-block cluster,
+// with one (1) or two (2) CTAs per SM; 0 = cooperative grid.
 cudaError_t launch_cluster(const EngineParams& p, const ClusterParamsHost& c, int blocks,
-                           cudaStream_t st, bool allow_hw = true);
+                           cudaStream_t st, int hw_mode = 1);
 // How many one-cluster grids of an n_nodes cluster fit the device at once.
-int cluster_max_hw_clusters(int n_nodes);
+int cluster_max_hw_clusters(int n_nodes, int ctas_per_sm = 1);
 // Interactive node set (fb_nodes_*, fb_cluster.cuh): ops and NodesIo.
 constexpr int32_t kNodesInitOp = 0, kNodesAdvanceOp = 1, kNodesBeginOp = 2, kNodesPabOp = 3,
                   kNodesStateOp = 4, kNodesFinishOp = 5;

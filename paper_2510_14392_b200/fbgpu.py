@@ -131,6 +131,7 @@ def lib() -> C.CDLL:
         "fb_cluster_shard_reset": (C.c_int, [vp]),
         "fb_cluster_shard_allow_hw_cluster": (C.c_int, [vp, i32]),
         "fb_cluster_max_hw_clusters": (C.c_int, [C.c_int, i32, C.POINTER(C.c_int32)]),
+        "fb_cluster_fit": (C.c_int, [C.c_int, i32, i32, C.POINTER(C.c_int32)]),
         "fb_cluster_shard_launch": (C.c_int, [vp]),
         "fb_cluster_shard_wait": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "fb_cluster_shard_fetch": (C.c_int, [vp, vp, vp, vp, pi64, C.POINTER(C.c_int32)]),

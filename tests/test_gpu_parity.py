@@ -360,11 +360,12 @@ def test_clusters_side_by_side_match_golden(golden, gpu_cluster_cases, gpu_rerou
 
 def test_clusters_cooperative_fallback_match_golden(fb, golden, gpu_cluster_cases, monkeypatch):
     """The cooperative-grid path (global-memory epoch barrier) that runs when
-    a one-cluster launch is not possible: forced with FB_NO_HW_CLUSTER, and
-    reached by run_clusters with more replicas than fit as hardware clusters."""
+    a one-cluster launch is not possible (forced with FB_NO_HW_CLUSTER), and
+    the two-CTAs-per-SM cluster kernel run_clusters takes for more replicas
+    than fit at one CTA per SM."""
     import ctypes as C
     from backends import cluster_summary
-    from paper_2510_14392_b200.cluster import run_cluster, run_clusters
+    from paper_2510_14392_b200.cluster import cluster_density, cluster_fit, run_cluster, run_clusters
     assert run_clusters([]) == []
     monkeypatch.setenv("FB_NO_HW_CLUSTER", "1")
     for n in ("c5_pab0_64", "pab5000_8", "count37_3"):
@@ -374,9 +375,13 @@ def test_clusters_cooperative_fallback_match_golden(fb, golden, gpu_cluster_case
     fit = C.c_int32(0)
     fb._check(fb.lib().fb_cluster_max_hw_clusters(0, 64, C.byref(fit)), "max_hw_clusters")
     assert 1 <= fit.value <= 64
+    fit1, fit2 = cluster_fit(64, 1), cluster_fit(64, 2)
+    assert fit1 == fit.value and fit2 >= fit1
     case = gpu_cluster_cases["c5_pab0_64"][1:]
-    outs = run_clusters([case] * (fit.value + 1))
-    assert len(outs) == fit.value + 1
+    # one copy more than fit at one CTA per SM: every copy at two per SM
+    assert cluster_density(fit1 + 1, 64) == (2 if fit1 + 1 <= fit2 else 0)
+    outs = run_clusters([case] * (fit1 + 1))
+    assert len(outs) == fit1 + 1
     for out in outs:
         assert cluster_summary(out) == golden["clusters"]["c5_pab0_64"]
 
