@@ -152,6 +152,7 @@ __device__ bool cluster_barrier(const ClusterParams& C, RouterSmem& rs, int64_t 
 struct ClusterNode {
   Inst w;
   TaskReg tk;
+  Steady sd;
   bool rr;
   int64_t rep_head, rep_tail;
 };
@@ -173,6 +174,7 @@ __device__ __forceinline__ void cluster_node_init(const EngineParams& P, const C
   w.vl = P.vlist + w.roff;
   w.smem = smem_warp;
   nd.tk = TaskReg{};
+  nd.sd.ok = false;
   nd.rr = false;
   nd.rep_head = nd.rep_tail = 0;
 }
@@ -234,7 +236,7 @@ __device__ __forceinline__ void node_complete(const EngineParams& P, const Clust
   const int64_t t = w.S.step_end;
   w.S.t_last = t;
   if (nd.rr) {
-    complete_rr(P, w, nd.tk);
+    complete_rr(P, w, nd.tk, nd.sd);
   } else {
     complete_step(P, w);
   }
@@ -251,12 +253,13 @@ __device__ __forceinline__ void node_begin(const EngineParams& P, ClusterNode& n
     nd.rr = false;
   } else if (!nd.rr && upcoming <= kWarp) {
     rr_load(P, w, nd.tk);
+    nd.sd.ok = false;
     nd.rr = true;
     w.S.paths |= kPathRegister;
   }
   if (nd.rr) {
     const Scratch s = carve_scratch(w.smem, kSmemSlots);
-    if (begin_rr(P, w, nd.tk, t, s) < 0) {  // keys outside the packed range
+    if (begin_rr(P, w, nd.tk, t, s, nd.sd) < 0) {  // keys outside the packed range
       rr_spill(P, w, nd.tk);
       nd.rr = false;
       begin_step(P, w, t);

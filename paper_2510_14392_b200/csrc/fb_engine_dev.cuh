@@ -468,6 +468,7 @@ namespace fbgpu {
 // Per-instance loop state of run_node's event loop.
 struct RunCtx {
   TaskReg tk;
+  Steady sd;         // repeated-plan state of the register path
   bool rr;           // live requests held in registers (fb_engine_rr.cuh)
   int64_t next_arr;  // arrival time of the next trace row
   int64_t ev;        // events processed in this launch
@@ -475,6 +476,7 @@ struct RunCtx {
 
 __device__ __forceinline__ void run_begin(const EngineParams& P, const Inst& w, RunCtx& c) {
   c.tk = TaskReg{};
+  c.sd.ok = false;
   c.rr = false;
   c.next_arr = w.S.arr < w.nreq ? P.arrival[w.toff + w.S.arr] : kInf;
   c.ev = 0;
@@ -519,7 +521,7 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   w.S.t_last = t;
   if (w.S.busy && t_step == t) {
     if (c.rr) {
-      complete_rr(P, w, c.tk);
+      complete_rr(P, w, c.tk, c.sd);
     } else {
       complete_step(P, w);
     }
@@ -545,11 +547,12 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
       c.rr = false;
     } else if (!c.rr && upcoming <= kTile) {
       rr_load(P, w, c.tk);
+      c.sd.ok = false;
       c.rr = true;
       w.S.paths |= kPathRegister;
     }
     if (c.rr) {
-      if (begin_rr(P, w, c.tk, t, s) < 0) {  // keys outside the packed range
+      if (begin_rr(P, w, c.tk, t, s, c.sd) < 0) {  // keys outside the packed range
         rr_spill(P, w, c.tk);
         c.rr = false;
         begin_step(P, w, t);
