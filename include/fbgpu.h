@@ -335,8 +335,17 @@ int fb_arena_fetch_results(fb_arena* arena, fb_instance_result* out);
 int fb_arena_fetch_records(fb_arena* arena, fb_record* out);
 int64_t fb_arena_record_rows(const fb_arena* arena);
 int fb_arena_fetch_log_counts(fb_arena* arena, fb_log_counts* out);
-/* Per instance, which device engine paths ran: FB_PATH_* bits. */
-enum { FB_PATH_REGISTER = 1u, FB_PATH_MEMORY = 2u, FB_PATH_WIDE = 4u };
+/* Per instance, which device engine paths ran: FB_PATH_* bits (REPEAT_*:
+ * repeated-plan steps -- the previous plan admitted every visible task as a
+ * one-token decode and nothing entered or left -- on the register / memory
+ * path). */
+enum {
+  FB_PATH_REGISTER = 1u,
+  FB_PATH_MEMORY = 2u,
+  FB_PATH_WIDE = 4u,
+  FB_PATH_REPEAT_REGISTER = 8u,
+  FB_PATH_REPEAT_MEMORY = 16u
+};
 int fb_arena_fetch_paths(fb_arena* arena, uint32_t* out);
 /* Copies instance i's logs; buffers sized by the log caps (NULL skips). */
 int fb_arena_fetch_log(fb_arena* arena, int64_t instance, fb_step_log* steps,

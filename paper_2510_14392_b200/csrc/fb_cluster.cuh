@@ -152,7 +152,6 @@ __device__ bool cluster_barrier(const ClusterParams& C, RouterSmem& rs, int64_t 
 struct ClusterNode {
   Inst w;
   TaskReg tk;
-  Steady sd;
   bool rr;
   int64_t rep_head, rep_tail;
 };
@@ -174,7 +173,7 @@ __device__ __forceinline__ void cluster_node_init(const EngineParams& P, const C
   w.vl = P.vlist + w.roff;
   w.smem = smem_warp;
   nd.tk = TaskReg{};
-  nd.sd.ok = false;
+  w.sd.ok = false;
   nd.rr = false;
   nd.rep_head = nd.rep_tail = 0;
 }
@@ -236,7 +235,7 @@ __device__ __forceinline__ void node_complete(const EngineParams& P, const Clust
   const int64_t t = w.S.step_end;
   w.S.t_last = t;
   if (nd.rr) {
-    complete_rr(P, w, nd.tk, nd.sd);
+    complete_rr(P, w, nd.tk);
   } else {
     complete_step(P, w);
   }
@@ -250,16 +249,17 @@ __device__ __forceinline__ void node_begin(const EngineParams& P, ClusterNode& n
   const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
   if (nd.rr && upcoming > kWarp) {
     rr_spill(P, w, nd.tk);
+    w.sd.ok = false;
     nd.rr = false;
   } else if (!nd.rr && upcoming <= kWarp) {
     rr_load(P, w, nd.tk);
-    nd.sd.ok = false;
+    w.sd.ok = false;
     nd.rr = true;
     w.S.paths |= kPathRegister;
   }
   if (nd.rr) {
     const Scratch s = carve_scratch(w.smem, kSmemSlots);
-    if (begin_rr(P, w, nd.tk, t, s, nd.sd) < 0) {  // keys outside the packed range
+    if (begin_rr(P, w, nd.tk, t, s) < 0) {  // keys outside the packed range
       rr_spill(P, w, nd.tk);
       nd.rr = false;
       begin_step(P, w, t);

@@ -284,7 +284,8 @@ struct DevState {
   uint32_t paths;         // engine paths used: 1 register, 2 warp-memory, 4 CTA-wide
   int32_t pad2;
 };
-constexpr uint32_t kPathRegister = 1u, kPathMemory = 2u, kPathWide = 4u;
+constexpr uint32_t kPathRegister = 1u, kPathMemory = 2u, kPathWide = 4u, kPathRepeatRegister = 8u,
+                   kPathRepeatMemory = 16u;
 
 // Per-request mutable state, structure of arrays indexed by rec_off + row.
 struct DevReq {

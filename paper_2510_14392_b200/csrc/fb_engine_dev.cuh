@@ -34,6 +34,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+#ifndef FB_STEADY
+#define FB_STEADY 1
+#endif
+
+// Warp-uniform record of the node's last plan, for repeated-plan steps: `ok`
+// when that plan admitted every visible task as a one-token decode (E == A ==
+// total_new) and nothing has entered or left the node since (no arrival
+// pulled, no request finished).  Then the visible set, its sorted order and
+// the plan entries repeat exactly -- see steady_fits.
+struct Steady {
+  bool ok;
+  int32_t E;        // plan size == visible count
+  uint64_t esum;    // XOR of the entries' digests (idx, request, 1)
+  int64_t tctx;     // the plan's total context
+  int64_t min_dec;  // the plan's minimum decode slack (fair batching)
+  int64_t now;      // the plan's begin time
+};
+
 // Warp-uniform view of one instance while a warp owns it.
 struct Inst {
   int64_t id;
@@ -44,7 +62,9 @@ struct Inst {
   int32_t policy, max_active;
   int2* vl;
   unsigned char* smem;  // this warp's shared scratch
+  Steady sd;            // repeated-plan state (false whenever a warp takes the node)
 };
+
 
 // Trace row of the q-th request that reached this node (run_node: the trace
 // itself; cluster nodes: the router's append order).
@@ -230,7 +250,10 @@ static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w
     if (tile_lane() == 0 && (ne || nf)) lead_account(P, w.id, t, ne, nf);
   }
   tile_sync();
-  if (any_fin) compact_vlist(w);
+  if (any_fin) {
+    w.sd.ok = false;
+    compact_vlist(w);
+  }
   w.S.busy = 0;
 }
 
@@ -322,11 +345,112 @@ static __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
   w.S.pulled = w.S.arr;
 }
 
+
+__device__ __forceinline__ void steady_record(Steady& sd, const Inst& w, bool all_decode_whole,
+                                              int E, uint64_t esum, int64_t tctx,
+                                              int64_t min_dec, int64_t now) {
+  const bool fair = w.policy == FB_POLICY_FAIRBATCH || w.policy == FB_POLICY_FAIRBATCH_PAB;
+  sd.ok = all_decode_whole && (!fair || w.I->tpot_uniform >= 0);
+  sd.E = E;
+  sd.esum = esum;
+  sd.tctx = tctx;
+  sd.min_dec = min_dec;
+  sd.now = now;
+}
+
+// A repeated-plan step: begin_step at `now` when the previous plan (begun at
+// sd.now, ending exactly at now) admitted all A visible tasks as one-token
+// decodes and no request has entered or left the node since.  The plan is
+// the same one again:
+//  * order -- every task is a decode.  Sarathi / prefill-first order by seq
+//    alone.  Fair batching orders by (group, slack, seq) with group 0 iff
+//    slack < urgency, i.e. by (slack, seq); with one tpot every decode's
+//    slack moved by the same tpot - (now - sd.now), so the order is unchanged
+//    and the minimum decode slack moved by that amount;
+//  * admission -- sarathi admits every decode (sched.cpp:180-183);
+//    prefill-first does while A <= token_budget (sched.cpp:214-224); fair
+//    batching admits everything whole when the all-fit test of begin_rr holds,
+//    here evaluated on an upper bound of the cost sum: with b > 0, c >= 0
+//    (validated on input) and one new token per task, sum_i fl(b + fl(c
+//    ctx_i)) <= (1 + 2^-53)^2 (A b + c sum ctx) <= RU(RU(RU(A b) + RU(c sum
+//    ctx)) (1 + 2^-51)); when the bound fails the caller takes the full path;
+//  * totals -- total_new = A, total_ctx = previous + A (every decode's
+//    context grew by its one emitted token), the entry digests repeat.
+// Returns false (nothing modified) when the full path must decide.
+__device__ __forceinline__ bool steady_fits(const Inst& w, const Steady& sd, int64_t now, int A,
+                                            double& init_ms, int64_t& min_dec) {
+  const DevInst* I = w.I;
+  const int policy = w.policy;
+  init_ms = 0.0;
+  min_dec = 0;
+  if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
+    const int64_t tpot_u = I->tpot_uniform;
+    min_dec = sd.min_dec + tpot_u - (now - sd.now);
+    init_ms = us_to_ms(min_dec > tpot_u ? min_dec : tpot_u);
+    const double tb0 = dsub(init_ms, I->sa);
+    if (!(tb0 >= 0.0 && A <= I->token_budget)) return false;
+    const double s_up = __dmul_ru(__dadd_ru(__dmul_ru(static_cast<double>(A), I->sb),
+                                            __dmul_ru(I->sc, static_cast<double>(sd.tctx + A))),
+                                  1.0 + 0x1p-51);
+    return __dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0);
+  }
+  return policy != FB_POLICY_PREFILL_FIRST || A <= I->token_budget;
+}
+
+// The repeated plan's scalar bookkeeping (finalize_plan, the truth step time,
+// step log, digest, counters); the caller has written the entry log.
+__device__ __forceinline__ void steady_commit(const EngineParams& P, Inst& w, Steady& sd,
+                                              int64_t now, int A, double init_ms,
+                                              int64_t min_dec, bool log_ok) {
+  const DevInst* I = w.I;
+  const int64_t tn = A;
+  const int64_t tctx = sd.tctx + A;
+  const double predicted = predict_ms(I->sa, I->sb, I->sc, tn, tctx);
+  double actual = predict_ms(I->ta, I->tb, I->tc, tn, tctx);
+  const double amp = I->noise_amp;
+  if (amp != 0.0) actual = apply_noise(actual, amp, I->noise_seed, w.S.step_counter);
+  int64_t dur = ms_to_us(actual);
+  if (dur < 1) dur = 1;
+  if (P.log_on) {
+    if (log_ok) {
+      if (tile_lane() == 0) {
+        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
+        sl.t_us = now;
+        sl.duration_us = dur;
+        sl.predicted_ms = predicted;
+        sl.actual_ms = actual;
+        sl.total_new = tn;
+        sl.total_ctx = tctx;
+        sl.init_budget_ms = init_ms;
+        sl.entry_off = w.S.log_entries;
+        sl.n_entries = A;
+      }
+      w.S.log_steps++;
+      w.S.log_entries += A;
+    } else {
+      w.S.log_trunc = 1;
+    }
+  }
+  w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(A), sd.esum, predicted,
+                              actual);
+  w.S.sum_visible += A;
+  w.S.sum_entries += A;
+  w.S.sum_new += tn;
+  w.S.busy = 1;
+  w.S.step_end = now + dur;
+  w.S.step_counter++;
+  sd.tctx = tctx;
+  sd.min_dec = min_dec;
+  sd.now = now;
+}
+
 // Node::begin_step, engine.cpp:153-202.  Returns false when there is nothing
 // to schedule (no step launched, no step ordinal consumed).
 static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
   const DevInst* I = w.I;
+  Steady& sd = w.sd;
   if (w.S.pulled < w.S.arr) {
+    sd.ok = false;
     if (w.policy == FB_POLICY_FAIRBATCH_PAB) {
       pull_pab(P, w, now);
     } else {
@@ -334,7 +458,25 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
     }
   }
   const int64_t A = visible_count(w);
-  if (A == 0) return false;
+  if (A == 0) {
+    sd.ok = false;
+    return false;
+  }
+#if FB_STEADY
+  // repeated plan: the in-flight takes in vlist are already the plan's
+  // (complete_step leaves them; every visible task is active), so only the
+  // scalar bookkeeping remains -- without the entry log, which needs the order
+  if (sd.ok && A == sd.E && !P.log_on) {
+    double init_ms;
+    int64_t min_dec;
+    if (steady_fits(w, sd, now, static_cast<int>(A), init_ms, min_dec)) {
+      steady_commit(P, w, sd, now, static_cast<int>(A), init_ms, min_dec, false);
+      w.S.paths |= kPathRepeatMemory;
+      return true;
+    }
+  }
+  sd.ok = false;
+#endif
   const Scratch s = scratch_for(P, w, A);
 
   // K1: views, envelope slack and the init_time_budget reductions.
@@ -453,6 +595,10 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
   w.S.busy = 1;
   w.S.step_end = now + dur;
   w.S.step_counter++;
+#if FB_STEADY
+  steady_record(sd, w, o.n_entries == Ai && o.total_new == A && acc.n_dec == Ai, Ai, esum,
+                o.total_ctx, acc.min_dec, now);
+#endif
   return true;
 }
 
@@ -468,7 +614,6 @@ namespace fbgpu {
 // Per-instance loop state of run_node's event loop.
 struct RunCtx {
   TaskReg tk;
-  Steady sd;         // repeated-plan state of the register path
   bool rr;           // live requests held in registers (fb_engine_rr.cuh)
   int64_t next_arr;  // arrival time of the next trace row
   int64_t ev;        // events processed in this launch
@@ -476,7 +621,6 @@ struct RunCtx {
 
 __device__ __forceinline__ void run_begin(const EngineParams& P, const Inst& w, RunCtx& c) {
   c.tk = TaskReg{};
-  c.sd.ok = false;
   c.rr = false;
   c.next_arr = w.S.arr < w.nreq ? P.arrival[w.toff + w.S.arr] : kInf;
   c.ev = 0;
@@ -521,7 +665,7 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   w.S.t_last = t;
   if (w.S.busy && t_step == t) {
     if (c.rr) {
-      complete_rr(P, w, c.tk, c.sd);
+      complete_rr(P, w, c.tk);
     } else {
       complete_step(P, w);
     }
@@ -544,15 +688,16 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
     }
     if (c.rr && upcoming > kTile) {
       rr_spill(P, w, c.tk);
+      w.sd.ok = false;
       c.rr = false;
     } else if (!c.rr && upcoming <= kTile) {
       rr_load(P, w, c.tk);
-      c.sd.ok = false;
+      w.sd.ok = false;
       c.rr = true;
       w.S.paths |= kPathRegister;
     }
     if (c.rr) {
-      if (begin_rr(P, w, c.tk, t, s, c.sd) < 0) {  // keys outside the packed range
+      if (begin_rr(P, w, c.tk, t, s) < 0) {  // keys outside the packed range
         rr_spill(P, w, c.tk);
         c.rr = false;
         begin_step(P, w, t);

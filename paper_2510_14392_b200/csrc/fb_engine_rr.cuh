@@ -21,21 +21,6 @@ namespace fbgpu {
 #define FB_RANK_UNROLL 4  // 8: 36.2 ms, 16: 37.8 ms on C2 (code size)
 #endif
 constexpr int kRankUnroll = FB_RANK_UNROLL;
-#ifndef FB_STEADY
-#define FB_STEADY FB_RANK_REUSE  // repeated-plan steps (needs the reused ranks)
-#endif
-
-// Warp-uniform record of the last register-path plan, for repeated-plan
-// steps: `ok` when that plan admitted every visible task as a one-token
-// decode (E == A == total_new) and nothing has entered or left the node since
-// (no arrival pulled, no request finished).  Then the visible set, their
-// sorted order and the plan entries repeat exactly -- see steady_rr.
-struct Steady {
-  bool ok;
-  int32_t E;      // plan size == visible count
-  uint64_t esum;  // XOR of the entries' digests (idx, request, 1)
-  int64_t tctx;   // the plan's total context
-};
 
 // One live request held by one lane.
 struct TaskReg {
@@ -157,8 +142,7 @@ __device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
 }
 
 // Node::complete_step (engine.cpp:204-254) on registers.
-__device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, TaskReg& t,
-                                            Steady& sd) {
+__device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, TaskReg& t) {
   const int64_t now = w.S.step_end;
   const int lane = tile_lane();
   const bool live = lane < w.S.n_live;
@@ -176,7 +160,7 @@ __device__ __forceinline__ void complete_rr(const EngineParams& P, Inst& w, Task
   if (P.lead_bucket > 0) lead_step(P, w, now, emit, fin, t.r, t.output);
   const unsigned finm = tile_ballot(fin);
   if (finm) {  // order-preserving removal from active_ (engine.cpp:228-229)
-    sd.ok = false;
+    w.sd.ok = false;
 #if FB_RANK_REUSE
     // previous-order ranks stay dense over the remaining tasks
     const unsigned gone = tile_or(fin && t.rk >= 0 ? 1u << t.rk : 0u);
@@ -295,91 +279,21 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
 }
 
 #if FB_STEADY
-// A repeated-plan step: begin_step when the previous register-path plan
-// admitted all A visible tasks as one-token decodes and no request has
-// entered or left the node since.  The plan is then the same one again:
-//  * order -- every task is a decode.  Sarathi / prefill-first order by seq
-//    alone.  Fair batching orders by (group, slack, seq) with group 0 iff
-//    slack < urgency, i.e. by (slack, seq); with one tpot every decode's
-//    slack moved by the same tpot - duration, so the order (and each task's
-//    rank t.rk) is unchanged;
-//  * admission -- sarathi admits every decode (sched.cpp:180-183);
-//    prefill-first does while A <= token_budget (sched.cpp:214-224); fair
-//    batching admits everything whole when the all-fit test of begin_rr holds,
-//    here evaluated on an upper bound of the cost sum: with b, c >= 0 and one
-//    new token per task, sum_i fl(b + fl(c ctx_i)) <= (1 + 2^-53)^2 (A b +
-//    c sum ctx) <= RU(RU(RU(A b) + RU(c sum ctx)) (1 + 2^-51)); if the bound
-//    fails the caller takes the full path;
-//  * totals -- total_new = A, total_ctx = previous + A (every decode's
-//    context grew by its one emitted token), the entry digests repeat.
-// Returns false (nothing modified) when the full path must decide.
+// A repeated-plan step on registers (steady_fits / steady_commit): every
+// visible lane's task is admitted again with one token, at its unchanged rank.
 __device__ __forceinline__ bool steady_rr(const EngineParams& P, Inst& w, TaskReg& t,
                                           int64_t now, Steady& sd, int A) {
-  const DevInst* I = w.I;
-  const int policy = w.policy;
-  const bool vis = tile_lane() < A;
-  const int64_t tctx = sd.tctx + A;
-  double init_ms = 0.0;
-  if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
-    // min decode slack = the rank-0 task's (sorted by (slack, seq))
-    const int l0 = __ffs(tile_ballot(vis && t.rk == 0)) - 1;
-    int64_t anchor = t.dl0;
-    if (t.first >= 0 && t.first < anchor) anchor = t.first;
-    const int64_t min_dec = tile_shfl(anchor + t.tpot * static_cast<int64_t>(t.nidx) - now, l0);
-    const int64_t tpot_u = I->tpot_uniform;
-    init_ms = us_to_ms(min_dec > tpot_u ? min_dec : tpot_u);
-    const double tb0 = dsub(init_ms, I->sa);
-    if (!(I->sb >= 0.0 && I->sc >= 0.0 && tb0 >= 0.0 && A <= I->token_budget)) return false;
-    const double s_up = __dmul_ru(__dadd_ru(__dmul_ru(static_cast<double>(A), I->sb),
-                                            __dmul_ru(I->sc, static_cast<double>(tctx))),
-                                  1.0 + 0x1p-51);
-    if (!(__dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0)))
-      return false;
-  } else if (policy == FB_POLICY_PREFILL_FIRST) {
-    if (A > I->token_budget) return false;
-  }
-  const int E = A;
-  const int64_t tn = A;
-  const double predicted = predict_ms(I->sa, I->sb, I->sc, tn, tctx);
+  double init_ms;
+  int64_t min_dec;
+  if (!steady_fits(w, sd, now, A, init_ms, min_dec)) return false;
   const bool log_ok = P.log_on && w.S.log_steps < P.log_step_cap &&
-                      w.S.log_entries + E <= P.log_entry_cap;
+                      w.S.log_entries + A <= P.log_entry_cap;
+  const bool vis = tile_lane() < A;
   if (log_ok && vis)
-    P.log_entries[I->log_entry_off + w.S.log_entries + t.rk] = fb_plan_entry{t.r, 1};
-  double actual = predict_ms(I->ta, I->tb, I->tc, tn, tctx);
-  const double amp = I->noise_amp;
-  if (amp != 0.0) actual = apply_noise(actual, amp, I->noise_seed, w.S.step_counter);
-  int64_t dur = ms_to_us(actual);
-  if (dur < 1) dur = 1;
+    P.log_entries[w.I->log_entry_off + w.S.log_entries + t.rk] = fb_plan_entry{t.r, 1};
   t.take = vis ? 1 : 0;
-  if (P.log_on) {
-    if (log_ok) {
-      if (tile_lane() == 0) {
-        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
-        sl.t_us = now;
-        sl.duration_us = dur;
-        sl.predicted_ms = predicted;
-        sl.actual_ms = actual;
-        sl.total_new = tn;
-        sl.total_ctx = tctx;
-        sl.init_budget_ms = init_ms;
-        sl.entry_off = w.S.log_entries;
-        sl.n_entries = E;
-      }
-      w.S.log_steps++;
-      w.S.log_entries += E;
-    } else {
-      w.S.log_trunc = 1;
-    }
-  }
-  w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(E), sd.esum, predicted,
-                              actual);
-  w.S.sum_visible += A;
-  w.S.sum_entries += E;
-  w.S.sum_new += tn;
-  w.S.busy = 1;
-  w.S.step_end = now + dur;
-  w.S.step_counter++;
-  sd.tctx = tctx;
+  steady_commit(P, w, sd, now, A, init_ms, min_dec, log_ok);
+  w.S.paths |= kPathRepeatRegister;
   return true;
 }
 #endif
@@ -389,8 +303,9 @@ __device__ __forceinline__ bool steady_rr(const EngineParams& P, Inst& w, TaskRe
 // keys do not fit the packed form (caller spills and takes the memory path;
 // nothing has been modified except the pulled arrivals, which are spilled).
 __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg& t,
-                                        int64_t now, const Scratch& s, Steady& sd) {
+                                        int64_t now, const Scratch& s) {
   const DevInst* I = w.I;
+  Steady& sd = w.sd;
   const int lane = tile_lane();
   if (w.S.pulled < w.S.arr) {
     sd.ok = false;
@@ -628,10 +543,7 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   // every visible task admitted as a one-token decode: the next step repeats
   // this plan while nothing enters or leaves (fair batching also needs one
   // tpot for the order to stay put)
-  sd.ok = E == A && tn == A && n_dec == A && (!fair || tpot_u >= 0);
-  sd.E = E;
-  sd.esum = esum;
-  sd.tctx = tctx;
+  steady_record(sd, w, E == A && tn == A && n_dec == A, E, esum, tctx, min_dec, now);
 #endif
   return 1;
 }

@@ -287,7 +287,30 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
     tile_sync();
   }
   if (fair) {
-    scan_fairbatch(s, A, out.init_ms, f, exits_ok);
+    // Everything fits whole (the register path's exact sufficient test, see
+    // begin_rr): tb0 - RU(sum of the rounded costs) >= A 2^-52 tb0 and the
+    // new tokens within token_budget imply every `consider` admits whole.
+    bool all_fit = false;
+    if (!kExact && exits_ok) {
+      const double tb0 = dsub(out.init_ms, f.a);
+      double part = 0.0;
+      int64_t nn = 0;
+      for (int k = tile_lane(); k < A; k += kTile) {
+        part = __dadd_ru(part, s.tcost[k]);
+        nn += static_cast<int64_t>(s.khi[k] & 0x7fffffffu);
+      }
+      const double s_up = tile_sum_ru(part);
+      const int64_t n_new = tile_sum_small(nn);
+      all_fit = tb0 >= 0.0 && n_new <= f.token_budget &&
+                __dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0);
+    }
+    if (all_fit) {
+      for (int k = tile_lane(); k < A; k += kTile)
+        s.take[k] = static_cast<int32_t>(s.khi[k] & 0x7fffffffu);
+      tile_sync();
+    } else {
+      scan_fairbatch(s, A, out.init_ms, f, exits_ok);
+    }
   } else if (f.policy == FB_POLICY_SARATHI) {
     scan_sarathi(s, A, acc.n_dec, f);
   } else {

@@ -190,9 +190,11 @@ def test_engine_logs_match_oracle(gpu, oracle, name):
     assert a.records.tobytes() == b.records.tobytes()
 
 
-@pytest.mark.parametrize("name,want", [("c2_subset", 1), ("large_live", 2), ("wide", 4)])
+@pytest.mark.parametrize("name,want", [("c2_subset", 1), ("large_live", 2), ("wide", 4),
+                                       ("c2_subset", 8), ("large_live", 16)])
 def test_engine_paths_exercised(fb, gpu, name, want):
-    """The scenarios really drive the register, memory and CTA-wide paths."""
+    """The scenarios really drive the register, memory and CTA-wide paths,
+    and the repeated-plan steps of the register and memory paths."""
     batch = SCENARIOS[name](gpu.generate_bursty)
     a = fb.Arena(0)
     a.load(batch)
