@@ -640,6 +640,20 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
     return true;
   }
   c.ev++;
+  int64_t t;
+#if FB_STEADY
+  // Repeated-plan lane: the in-flight step of a repeated-plan-eligible node
+  // ends before the next arrival with nothing pending -- the event is that
+  // step's end: complete it and, when nothing finished, begin the same plan
+  // again (the general code below would take the same branches).
+  if (c.rr && w.sd.ok && w.S.busy && c.next_arr > w.S.step_end && w.S.pulled == w.S.arr) {
+    t = w.S.step_end;
+    w.S.t_last = t;
+    complete_rr(P, w, c.tk);
+    if (w.sd.ok && t < w.horizon && steady_rr(P, w, c.tk, t, w.sd, w.sd.E)) return false;
+  } else
+#endif
+  {
   if (w.S.busy && c.next_arr < w.S.step_end) {
     // Arrivals strictly before the in-flight step's end only enqueue
     // (run_node's loop neither completes nor begins a step at those times):
@@ -654,7 +668,7 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
     c.next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
   }
   const int64_t t_step = w.S.busy ? w.S.step_end : kInf;
-  const int64_t t = t_step < c.next_arr ? t_step : c.next_arr;
+  t = t_step < c.next_arr ? t_step : c.next_arr;
   if (t == kInf || (!w.S.busy && t >= w.horizon)) {
     if (c.rr) rr_spill(P, w, c.tk);
     w.S.done = 1;
@@ -673,6 +687,7 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   while (c.next_arr == t) {  // Node::enqueue (visible at its arrival time)
     w.S.arr++;
     c.next_arr = w.S.arr < w.nreq ? arrival[w.S.arr] : kInf;
+  }
   }
   if (!w.S.busy && t < w.horizon) {
     const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
