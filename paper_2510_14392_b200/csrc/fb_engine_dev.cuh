@@ -639,14 +639,20 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
     if (c.rr) rr_spill(P, w, c.tk);
     return true;
   }
-  c.ev++;
   int64_t t;
 #if FB_STEADY
   // Repeated-plan lane: the in-flight step of a repeated-plan-eligible node
   // ends before the next arrival with nothing pending -- the event is that
   // step's end: complete it and, when nothing finished, begin the same plan
-  // again (the general code below would take the same branches).
-  if (c.rr && w.sd.ok && w.S.busy && c.next_arr > w.S.step_end && w.S.pulled == w.S.arr) {
+  // again (the general code below would take the same branches).  Without
+  // logs and lead series, a whole run of such events at once.
+  const bool lane_ok = c.rr && w.sd.ok && w.S.busy && c.next_arr > w.S.step_end &&
+                       w.S.pulled == w.S.arr;
+  if (lane_ok && !P.log_on && P.lead_bucket == 0) {
+    t = steady_burst(P, w, c.tk, c.ev, c.next_arr);
+    if (t < 0) return false;
+  } else if (lane_ok) {
+    c.ev++;
     t = w.S.step_end;
     w.S.t_last = t;
     complete_rr(P, w, c.tk);
@@ -654,6 +660,7 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   } else
 #endif
   {
+  c.ev++;
   if (w.S.busy && c.next_arr < w.S.step_end) {
     // Arrivals strictly before the in-flight step's end only enqueue
     // (run_node's loop neither completes nor begins a step at those times):
