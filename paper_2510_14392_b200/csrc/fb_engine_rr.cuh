@@ -122,7 +122,7 @@ __device__ __forceinline__ void rr_spill(const EngineParams& P, const Inst& w,
 // Token emission on registers (engine.cpp:211-232, metrics.cpp:42-60,196-214).
 __device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
   const int32_t idx = t.nidx;
-  if (idx == 0) {
+  if (FB_UNLIKELY(idx == 0)) {
     t.first = now;
     if (now <= t.dl0) t.flags |= FB_REC_MET_TTFT;  // emits[0] <= ttft_slo
   } else {
@@ -134,7 +134,7 @@ __device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
   }
   t.nidx = idx + 1;
   const bool fin = t.nidx >= t.output;
-  if (fin) {
+  if (FB_UNLIKELY(fin)) {
     t.flags |= FB_REC_FINISHED;
     if (!(t.flags & kTpotViolated)) t.flags |= FB_REC_MET_TPOT;
   }
@@ -341,10 +341,10 @@ __device__ __forceinline__ int64_t steady_burst(const EngineParams& P, Inst& w, 
     bool fin = false;
     if (t.take > 0) {
       fin = emit_reg(t, now);
-      if (fin) flush_task(P, w, t);
+      if (FB_UNLIKELY(fin)) flush_task(P, w, t);
     }
     const unsigned finm = tile_ballot(fin);
-    if (finm || now >= horizon || !budget_ok) {
+    if (FB_UNLIKELY(finm || now >= horizon || !budget_ok)) {
       t.take = 0;
       if (finm) remove_finished_rr(w, t, fin, tile_lane() < w.S.n_live, finm);
       owed = now;
@@ -359,7 +359,7 @@ __device__ __forceinline__ int64_t steady_burst(const EngineParams& P, Inst& w, 
       const double tb0 = dsub(init_ms, sa);
       const double s_up = __dmul_ru(__dadd_ru(s_b, __dmul_ru(sc, static_cast<double>(tctx + A))),
                                     1.0 + 0x1p-51);
-      if (!(tb0 >= 0.0 && __dsub_rd(tb0, s_up) >= __dmul_ru(slack_a, tb0))) {
+      if (FB_UNLIKELY(!(tb0 >= 0.0 && __dsub_rd(tb0, s_up) >= __dmul_ru(slack_a, tb0)))) {
         t.take = 0;
         owed = now;
         break;
@@ -368,7 +368,7 @@ __device__ __forceinline__ int64_t steady_burst(const EngineParams& P, Inst& w, 
     tctx += A;
     const double predicted = predict_ms(sa, sb, sc, A, tctx);
     double actual = predict_ms(ta, tb, tc, A, tctx);
-    if (amp != 0.0) actual = apply_noise(actual, amp, I->noise_seed, steps);
+    if (FB_UNLIKELY(amp != 0.0)) actual = apply_noise(actual, amp, I->noise_seed, steps);
     int64_t dur = ms_to_us(actual);
     if (dur < 1) dur = 1;
     digest = fb_digest_step(digest, now, static_cast<uint32_t>(A), esum, predicted, actual);
