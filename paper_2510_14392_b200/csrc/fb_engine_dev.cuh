@@ -444,6 +444,119 @@ __device__ __forceinline__ void steady_commit(const EngineParams& P, Inst& w, St
   sd.now = now;
 }
 
+// A run of repeated-plan steps back to back (run_event's repeated-plan lane,
+// without event logs or the envelope-lead series): each iteration is one
+// event of run_node's loop -- the in-flight step ends before the next arrival
+// with nothing pending: complete_step (`complete(now)`, true when a request
+// finished; it has then done the removal), then begin_step repeats the plan
+// (steady_fits / steady_commit, same arithmetic; `recommit()` re-arms the
+// path's in-flight takes).  The node's hot scalars stay in registers for the
+// whole run.  Returns -1 when the run stopped with a step in flight (the next
+// event is not a repeated-plan one), else the time t of an event whose step
+// completed but whose begin_step the general code still has to decide (a
+// request finished, the horizon, or the capacity bound failed).
+template <class CompleteFn, class RecommitFn>
+__device__ __forceinline__ int64_t steady_run(const EngineParams& P, Inst& w, int64_t& ev,
+                                              int64_t next_arr, CompleteFn&& complete,
+                                              RecommitFn&& recommit, uint32_t path_bit) {
+  const DevInst* I = w.I;
+  const bool fair = w.policy == FB_POLICY_FAIRBATCH || w.policy == FB_POLICY_FAIRBATCH_PAB;
+  const int A = w.sd.E;
+  const int64_t horizon = w.horizon, max_ev = P.max_events;
+  const int64_t tpot_u = I->tpot_uniform;
+  const double sa = I->sa, sb = I->sb, sc = I->sc, ta = I->ta, tb = I->tb, tc = I->tc;
+  const double amp = I->noise_amp;
+  const uint64_t esum = w.sd.esum;
+  const double slack_a = __dmul_ru(static_cast<double>(A), 0x1p-52);
+  const double s_b = __dmul_ru(static_cast<double>(A), sb);
+  const bool budget_ok = w.policy == FB_POLICY_SARATHI || A <= I->token_budget;
+  int64_t step_end = w.S.step_end, tctx = w.sd.tctx, min_dec = w.sd.min_dec, snow = w.sd.now;
+  uint64_t digest = w.S.digest, steps = w.S.step_counter;
+  int64_t n_steps = 0;
+  int64_t owed = -1;
+  while (ev < max_ev && next_arr > step_end) {
+    const int64_t now = step_end;
+    ++ev;
+    if (FB_UNLIKELY(complete(now) || now >= horizon || !budget_ok)) {
+      owed = now;
+      break;
+    }
+    // begin_step: the same plan again
+    double init_ms = 0.0;
+    int64_t md = 0;
+    if (fair) {
+      md = min_dec + tpot_u - (now - snow);
+      init_ms = us_to_ms(md > tpot_u ? md : tpot_u);
+      const double tb0 = dsub(init_ms, sa);
+      const double s_up = __dmul_ru(__dadd_ru(s_b, __dmul_ru(sc, static_cast<double>(tctx + A))),
+                                    1.0 + 0x1p-51);
+      if (FB_UNLIKELY(!(tb0 >= 0.0 && __dsub_rd(tb0, s_up) >= __dmul_ru(slack_a, tb0)))) {
+        owed = now;
+        break;
+      }
+    }
+    tctx += A;
+    const double predicted = predict_ms(sa, sb, sc, A, tctx);
+    double actual = predict_ms(ta, tb, tc, A, tctx);
+    if (FB_UNLIKELY(amp != 0.0)) actual = apply_noise(actual, amp, I->noise_seed, steps);
+    int64_t dur = ms_to_us(actual);
+    if (dur < 1) dur = 1;
+    digest = fb_digest_step(digest, now, static_cast<uint32_t>(A), esum, predicted, actual);
+    steps++;
+    n_steps++;
+    step_end = now + dur;
+    min_dec = md;
+    snow = now;
+    recommit();
+  }
+  w.S.digest = digest;
+  w.S.step_counter = steps;
+  w.S.sum_visible += n_steps * A;
+  w.S.sum_entries += n_steps * A;
+  w.S.sum_new += n_steps * A;
+  w.sd.tctx = tctx;
+  w.sd.min_dec = min_dec;
+  w.sd.now = snow;
+  w.S.step_end = step_end;
+  if (n_steps > 0) w.S.paths |= path_bit;
+  if (owed >= 0) {
+    w.S.t_last = owed;
+    w.S.busy = 0;
+  } else if (n_steps > 0) {
+    w.S.t_last = snow;
+  }
+  return owed;
+}
+
+// The memory path's run: every visible task is active with its one-token
+// take still in vlist (complete_step never clears takes) and is a decode.
+__device__ __forceinline__ int64_t steady_burst_mem(const EngineParams& P, Inst& w,
+                                                    int64_t& ev, int64_t next_arr) {
+  const int64_t A = w.sd.E;
+  return steady_run(
+      P, w, ev, next_arr,
+      [&](int64_t now) {  // complete_step (engine.cpp:204-254) for decodes
+        bool any_fin = false;
+        for (int64_t b = 0; b < A; b += kTile) {
+          const int64_t p = b + tile_lane();
+          bool fin = false;
+          if (p < A) {
+            const int32_t r = w.vl[p].x;
+            fin = emit_token(P, w.roff + r, w.toff + r, now);
+            if (FB_UNLIKELY(fin)) w.vl[p].x = -1;
+          }
+          any_fin |= tile_any(fin);
+        }
+        tile_sync();
+        if (FB_UNLIKELY(any_fin)) {
+          w.sd.ok = false;
+          compact_vlist(w);
+        }
+        return any_fin;
+      },
+      [] {}, kPathRepeatMemory);
+}
+
 // Node::begin_step, engine.cpp:153-202.  Returns false when there is nothing
 // to schedule (no step launched, no step ordinal consumed).
 static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, int64_t now) {
@@ -648,7 +761,11 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   // logs and lead series, a whole run of such events at once.
   const bool lane_ok = c.rr && w.sd.ok && w.S.busy && c.next_arr > w.S.step_end &&
                        w.S.pulled == w.S.arr;
-  if (lane_ok && !P.log_on && P.lead_bucket == 0) {
+  if (!c.rr && w.sd.ok && w.S.busy && c.next_arr > w.S.step_end && w.S.pulled == w.S.arr &&
+      !P.log_on && P.lead_bucket == 0) {
+    t = steady_burst_mem(P, w, c.ev, c.next_arr);
+    if (t < 0) return false;
+  } else if (lane_ok && !P.log_on && P.lead_bucket == 0) {
     t = steady_burst(P, w, c.tk, c.ev, c.next_arr);
     if (t < 0) return false;
   } else if (lane_ok) {

@@ -306,97 +306,26 @@ __device__ __forceinline__ bool steady_rr(const EngineParams& P, Inst& w, TaskRe
 
 
 #if FB_STEADY
-// A run of repeated-plan steps back to back (run_event's repeated-plan lane,
-// without event logs or the envelope-lead series): each iteration is one
-// event of run_node's loop -- the in-flight step ends before the next arrival
-// with nothing pending: complete_step, then begin_step repeats the plan
-// (steady_fits / steady_commit, same arithmetic).  The node's hot scalars stay
-// in registers for the whole run.  Returns -1 when the run stopped with a
-// step in flight (the next event is not a repeated-plan one), else the time t
-// of an event whose step completed but whose begin_step still has to be
-// decided by the general code (a request finished, the horizon, or the
-// capacity bound failed).
+// A run of repeated-plan steps on registers (steady_run): every visible lane's
+// task emits its token, and the plan gives it one token again.
 __device__ __forceinline__ int64_t steady_burst(const EngineParams& P, Inst& w, TaskReg& t,
                                                 int64_t& ev, int64_t next_arr) {
-  const DevInst* I = w.I;
-  const bool fair = w.policy == FB_POLICY_FAIRBATCH || w.policy == FB_POLICY_FAIRBATCH_PAB;
-  const int A = w.sd.E;
-  const bool vis = tile_lane() < A;
-  const int64_t horizon = w.horizon, max_ev = P.max_events;
-  const int64_t tpot_u = I->tpot_uniform;
-  const double sa = I->sa, sb = I->sb, sc = I->sc, ta = I->ta, tb = I->tb, tc = I->tc;
-  const double amp = I->noise_amp;
-  const uint64_t esum = w.sd.esum;
-  const double slack_a = __dmul_ru(static_cast<double>(A), 0x1p-52);
-  const double s_b = __dmul_ru(static_cast<double>(A), sb);
-  const bool budget_ok = w.policy == FB_POLICY_SARATHI || A <= I->token_budget;
-  int64_t step_end = w.S.step_end, tctx = w.sd.tctx, min_dec = w.sd.min_dec, snow = w.sd.now;
-  uint64_t digest = w.S.digest, steps = w.S.step_counter;
-  int64_t n_steps = 0;
-  int64_t owed = -1;
-  while (ev < max_ev && next_arr > step_end) {
-    const int64_t now = step_end;
-    ++ev;
-    // complete_step: every visible task emits one token
-    bool fin = false;
-    if (t.take > 0) {
-      fin = emit_reg(t, now);
-      if (FB_UNLIKELY(fin)) flush_task(P, w, t);
-    }
-    const unsigned finm = tile_ballot(fin);
-    if (FB_UNLIKELY(finm || now >= horizon || !budget_ok)) {
-      t.take = 0;
-      if (finm) remove_finished_rr(w, t, fin, tile_lane() < w.S.n_live, finm);
-      owed = now;
-      break;
-    }
-    // begin_step: the same plan again
-    double init_ms = 0.0;
-    int64_t md = 0;
-    if (fair) {
-      md = min_dec + tpot_u - (now - snow);
-      init_ms = us_to_ms(md > tpot_u ? md : tpot_u);
-      const double tb0 = dsub(init_ms, sa);
-      const double s_up = __dmul_ru(__dadd_ru(s_b, __dmul_ru(sc, static_cast<double>(tctx + A))),
-                                    1.0 + 0x1p-51);
-      if (FB_UNLIKELY(!(tb0 >= 0.0 && __dsub_rd(tb0, s_up) >= __dmul_ru(slack_a, tb0)))) {
+  const bool vis = tile_lane() < w.sd.E;
+  return steady_run(
+      P, w, ev, next_arr,
+      [&](int64_t now) {  // complete_step
+        bool fin = false;
+        if (t.take > 0) {
+          fin = emit_reg(t, now);
+          if (FB_UNLIKELY(fin)) flush_task(P, w, t);
+        }
         t.take = 0;
-        owed = now;
-        break;
-      }
-    }
-    tctx += A;
-    const double predicted = predict_ms(sa, sb, sc, A, tctx);
-    double actual = predict_ms(ta, tb, tc, A, tctx);
-    if (FB_UNLIKELY(amp != 0.0)) actual = apply_noise(actual, amp, I->noise_seed, steps);
-    int64_t dur = ms_to_us(actual);
-    if (dur < 1) dur = 1;
-    digest = fb_digest_step(digest, now, static_cast<uint32_t>(A), esum, predicted, actual);
-    steps++;
-    n_steps++;
-    step_end = now + dur;
-    min_dec = md;
-    snow = now;
-    t.take = vis ? 1 : 0;
-  }
-  w.S.digest = digest;
-  w.S.step_counter = steps;
-  w.S.sum_visible += n_steps * A;
-  w.S.sum_entries += n_steps * A;
-  w.S.sum_new += n_steps * A;
-  w.sd.tctx = tctx;
-  w.sd.min_dec = min_dec;
-  w.sd.now = snow;
-  if (n_steps > 0) w.S.paths |= kPathRepeatRegister;
-  if (owed >= 0) {
-    w.S.t_last = owed;
-    w.S.busy = 0;
-    w.S.step_end = step_end;
-  } else {
-    w.S.step_end = step_end;
-    if (n_steps > 0) w.S.t_last = snow;
-  }
-  return owed;
+        const unsigned finm = tile_ballot(fin);
+        if (FB_UNLIKELY(finm)) remove_finished_rr(w, t, fin, tile_lane() < w.S.n_live, finm);
+        return finm != 0;
+      },
+      [&]() { t.take = vis ? 1 : 0; },
+      kPathRepeatRegister);
 }
 #endif
 
