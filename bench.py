@@ -255,7 +255,7 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3, cpu: bool = True) -> di
     arena.close()
     ph = {k: statistics.median(p[k] for p in phases) for k in phases[0]}
     try:
-        with open(os.path.join(ROOT, "profiles", "r02_wide_wide_grid_kernel_ncu.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "wide_ncu_summary.json")) as f:
             wide_ncu = json.load(f)
     except (OSError, ValueError):
         wide_ncu = {}
@@ -278,8 +278,9 @@ def bench_c4(peak: float, peak_kind: str, reps: int = 3, cpu: bool = True) -> di
             "mean_visible": float(r["sum_visible"].sum()) / max(steps, 1),
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": wide_ncu.get("dram_bytes_per_launch"),
-                         "traffic_source": "profiles/r02_wide_wide_grid_kernel_ncu.json "
-                                           "(wide_grid_kernel, one C4 pass)",
+                         "traffic_source": "profiles/wide_ncu_summary.json (" +
+                                           str(wide_ncu.get("tag")) +
+                                           ": wide_grid_kernel, one C4 pass)",
                          "kernel": "engine_kernel+wide_grid_kernel (whole pass)",
                          "alg_bytes_per_launch": alg, "peak_source": peak_kind},
             "phases_ms": ph,
