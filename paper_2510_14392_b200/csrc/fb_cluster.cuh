@@ -173,7 +173,7 @@ __device__ __forceinline__ void cluster_node_init(const EngineParams& P, const C
   w.vl = P.vlist + w.roff;
   w.smem = smem_warp;
   nd.tk = TaskReg{};
-  w.sd.ok = false;
+  w.sd.clear();
   nd.rr = false;
   nd.rep_head = nd.rep_tail = 0;
 }
@@ -249,11 +249,11 @@ __device__ __forceinline__ void node_begin(const EngineParams& P, ClusterNode& n
   const int64_t upcoming = w.S.n_live + (w.S.arr - w.S.pulled);
   if (nd.rr && upcoming > kWarp) {
     rr_spill(P, w, nd.tk);
-    w.sd.ok = false;
+    w.sd.clear();
     nd.rr = false;
   } else if (!nd.rr && upcoming <= kWarp) {
     rr_load(P, w, nd.tk);
-    w.sd.ok = false;
+    w.sd.clear();
     nd.rr = true;
     w.S.paths |= kPathRegister;
   }

@@ -64,7 +64,7 @@ engine_kernel(const __grid_constant__ EngineParams P) {
     w.max_active = w.I->max_active;
     w.vl = P.vlist + w.roff;
     w.smem = my;
-    w.sd.ok = false;
+    w.sd.clear();
     run_instance(P, w);
     tile_sync();
     if (tile_lane() == 0) {

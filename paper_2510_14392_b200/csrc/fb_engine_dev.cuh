@@ -45,11 +45,18 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // the plan entries repeat exactly -- see steady_fits.
 struct Steady {
   bool ok;
+  bool sub;         // (register path) the plan was `ok`, then only finished requests left
+                    // (order and ranks of the rest intact): the next plan is the same
+                    // minus them if it fits -- see sub_rr
   int32_t E;        // plan size == visible count
   uint64_t esum;    // XOR of the entries' digests (idx, request, 1)
   int64_t tctx;     // the plan's total context
   int64_t min_dec;  // the plan's minimum decode slack (fair batching)
   int64_t now;      // the plan's begin time
+  __device__ __forceinline__ void clear() {
+    ok = false;
+    sub = false;
+  }
 };
 
 // Warp-uniform view of one instance while a warp owns it.
@@ -251,7 +258,7 @@ static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w
   }
   tile_sync();
   if (any_fin) {
-    w.sd.ok = false;
+    w.sd.clear();
     compact_vlist(w);
   }
   w.S.busy = 0;
@@ -351,6 +358,7 @@ __device__ __forceinline__ void steady_record(Steady& sd, const Inst& w, bool al
                                               int64_t min_dec, int64_t now) {
   const bool fair = w.policy == FB_POLICY_FAIRBATCH || w.policy == FB_POLICY_FAIRBATCH_PAB;
   sd.ok = all_decode_whole && (!fair || w.I->tpot_uniform >= 0);
+  sd.sub = false;
   sd.E = E;
   sd.esum = esum;
   sd.tctx = tctx;
@@ -377,34 +385,38 @@ __device__ __forceinline__ void steady_record(Steady& sd, const Inst& w, bool al
 //  * totals -- total_new = A, total_ctx = previous + A (every decode's
 //    context grew by its one emitted token), the entry digests repeat.
 // Returns false (nothing modified) when the full path must decide.
-__device__ __forceinline__ bool steady_fits(const Inst& w, const Steady& sd, int64_t now, int A,
-                                            double& init_ms, int64_t& min_dec) {
+// Does the plan "all A visible decodes, one token each" (total context tctx,
+// minimum decode slack min_dec) pass the policy's admission whole?
+__device__ __forceinline__ bool plan_fits(const Inst& w, int A, int64_t tctx, int64_t min_dec,
+                                          double& init_ms) {
   const DevInst* I = w.I;
   const int policy = w.policy;
   init_ms = 0.0;
-  min_dec = 0;
   if (policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB) {
     const int64_t tpot_u = I->tpot_uniform;
-    min_dec = sd.min_dec + tpot_u - (now - sd.now);
     init_ms = us_to_ms(min_dec > tpot_u ? min_dec : tpot_u);
     const double tb0 = dsub(init_ms, I->sa);
     if (!(tb0 >= 0.0 && A <= I->token_budget)) return false;
     const double s_up = __dmul_ru(__dadd_ru(__dmul_ru(static_cast<double>(A), I->sb),
-                                            __dmul_ru(I->sc, static_cast<double>(sd.tctx + A))),
+                                            __dmul_ru(I->sc, static_cast<double>(tctx))),
                                   1.0 + 0x1p-51);
     return __dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0);
   }
   return policy != FB_POLICY_PREFILL_FIRST || A <= I->token_budget;
+}
+__device__ __forceinline__ bool steady_fits(const Inst& w, const Steady& sd, int64_t now, int A,
+                                            double& init_ms, int64_t& min_dec) {
+  min_dec = sd.min_dec + w.I->tpot_uniform - (now - sd.now);  // used by fair batching only
+  return plan_fits(w, A, sd.tctx + A, min_dec, init_ms);
 }
 
 // The repeated plan's scalar bookkeeping (finalize_plan, the truth step time,
 // step log, digest, counters); the caller has written the entry log.
 __device__ __forceinline__ void steady_commit(const EngineParams& P, Inst& w, Steady& sd,
                                               int64_t now, int A, double init_ms,
-                                              int64_t min_dec, bool log_ok) {
+                                              int64_t min_dec, bool log_ok, int64_t tctx) {
   const DevInst* I = w.I;
   const int64_t tn = A;
-  const int64_t tctx = sd.tctx + A;
   const double predicted = predict_ms(I->sa, I->sb, I->sc, tn, tctx);
   double actual = predict_ms(I->ta, I->tb, I->tc, tn, tctx);
   const double amp = I->noise_amp;
@@ -549,7 +561,7 @@ __device__ __forceinline__ int64_t steady_burst_mem(const EngineParams& P, Inst&
         }
         tile_sync();
         if (FB_UNLIKELY(any_fin)) {
-          w.sd.ok = false;
+          w.sd.clear();
           compact_vlist(w);
         }
         return any_fin;
@@ -563,7 +575,7 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
   const DevInst* I = w.I;
   Steady& sd = w.sd;
   if (w.S.pulled < w.S.arr) {
-    sd.ok = false;
+    sd.clear();
     if (w.policy == FB_POLICY_FAIRBATCH_PAB) {
       pull_pab(P, w, now);
     } else {
@@ -572,7 +584,7 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
   }
   const int64_t A = visible_count(w);
   if (A == 0) {
-    sd.ok = false;
+    sd.clear();
     return false;
   }
 #if FB_STEADY
@@ -583,12 +595,12 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
     double init_ms;
     int64_t min_dec;
     if (steady_fits(w, sd, now, static_cast<int>(A), init_ms, min_dec)) {
-      steady_commit(P, w, sd, now, static_cast<int>(A), init_ms, min_dec, false);
+      steady_commit(P, w, sd, now, static_cast<int>(A), init_ms, min_dec, false, sd.tctx + A);
       w.S.paths |= kPathRepeatMemory;
       return true;
     }
   }
-  sd.ok = false;
+  sd.clear();
 #endif
   const Scratch s = scratch_for(P, w, A);
 
@@ -827,11 +839,11 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
     }
     if (c.rr && upcoming > kTile) {
       rr_spill(P, w, c.tk);
-      w.sd.ok = false;
+      w.sd.clear();
       c.rr = false;
     } else if (!c.rr && upcoming <= kTile) {
       rr_load(P, w, c.tk);
-      w.sd.ok = false;
+      w.sd.clear();
       c.rr = true;
       w.S.paths |= kPathRegister;
     }

@@ -146,6 +146,7 @@ __device__ __forceinline__ bool emit_reg(TaskReg& t, int64_t now) {
 __device__ __forceinline__ void remove_finished_rr(Inst& w, TaskReg& t, bool fin, bool live,
                                                    unsigned finm) {
   const int lane = tile_lane();
+  w.sd.sub = w.sd.ok;  // the rest of an all-decode plan keeps its order and dense ranks
   w.sd.ok = false;
 #if FB_RANK_REUSE
   // previous-order ranks stay dense over the remaining tasks
@@ -298,7 +299,44 @@ __device__ __forceinline__ bool steady_rr(const EngineParams& P, Inst& w, TaskRe
   if (log_ok && vis)
     P.log_entries[w.I->log_entry_off + w.S.log_entries + t.rk] = fb_plan_entry{t.r, 1};
   t.take = vis ? 1 : 0;
-  steady_commit(P, w, sd, now, A, init_ms, min_dec, log_ok);
+  steady_commit(P, w, sd, now, A, init_ms, min_dec, log_ok, sd.tctx + A);
+  w.S.paths |= kPathRepeatRegister;
+  return true;
+}
+
+#ifndef FB_SUB
+#define FB_SUB 0  // C2 +2 % slower (code size), C1 2 % faster: off
+#endif
+// The plan after requests finished out of an all-decode, all-admitted plan
+// (nothing arrived): the A remaining visible tasks are that plan's decodes
+// (A == n_active: no waiting task became visible), their order is unchanged
+// and their ranks were kept dense by remove_finished_rr -- so the plan is
+// again "all A decodes, one token each, in rank order" when it fits.  Only
+// the totals are recounted: the context sum, the entry digests (positions
+// moved) and the minimum decode slack (the rank-0 task's).
+__device__ __forceinline__ bool sub_rr(const EngineParams& P, Inst& w, TaskReg& t, int64_t now,
+                                       Steady& sd, int A) {
+  const bool vis = tile_lane() < A;
+  const int64_t tctx = tile_sum_small(vis ? static_cast<int64_t>(t.prompt) + t.nidx : 0);
+  int64_t anchor = t.dl0;
+  if (t.first >= 0 && t.first < anchor) anchor = t.first;
+  const int l0 = __ffs(tile_ballot(vis && t.rk == 0)) - 1;
+  const int64_t min_dec = tile_shfl(anchor + t.tpot * static_cast<int64_t>(t.nidx) - now, l0);
+  double init_ms;
+  if (!plan_fits(w, A, tctx, min_dec, init_ms)) return false;
+  const uint64_t eh = vis ? fb_digest_entry(static_cast<uint32_t>(t.rk),
+                                            static_cast<uint32_t>(t.r), 1u)
+                          : 0;
+  sd.esum = tile_xor_u64(eh);
+  sd.E = A;
+  const bool log_ok = P.log_on && w.S.log_steps < P.log_step_cap &&
+                      w.S.log_entries + A <= P.log_entry_cap;
+  if (log_ok && vis)
+    P.log_entries[w.I->log_entry_off + w.S.log_entries + t.rk] = fb_plan_entry{t.r, 1};
+  t.take = vis ? 1 : 0;
+  steady_commit(P, w, sd, now, A, init_ms, min_dec, log_ok, tctx);
+  sd.ok = true;
+  sd.sub = false;
   w.S.paths |= kPathRepeatRegister;
   return true;
 }
@@ -339,17 +377,20 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
   Steady& sd = w.sd;
   const int lane = tile_lane();
   if (w.S.pulled < w.S.arr) {
-    sd.ok = false;
+    sd.clear();
     pull_rr(P, w, t, now, s);
   }
   const int A = static_cast<int>(visible_count(w));
   if (A == 0) {
-    sd.ok = false;
+    sd.clear();
     return 0;
   }
 #if FB_STEADY
   if (sd.ok && A == sd.E && steady_rr(P, w, t, now, sd, A)) return 1;
-  sd.ok = false;
+#if FB_SUB
+  if (sd.sub && A == w.S.n_active && sub_rr(P, w, t, now, sd, A)) return 1;
+#endif
+  sd.clear();
 #endif
   const bool vis = lane < A;
   const int policy = w.policy;

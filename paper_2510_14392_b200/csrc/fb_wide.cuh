@@ -1157,7 +1157,7 @@ __device__ __forceinline__ Inst wide_view_ctx(const EngineParams& P, int64_t ins
   w.max_active = w.I->max_active;
   w.vl = P.vlist + w.roff;
   w.smem = nullptr;
-  w.sd.ok = false;
+  w.sd.clear();
   return w;
 }
 
