@@ -1,0 +1,60 @@
+"""Seeded random engine corpus: instances whose traces and configurations are
+drawn across the space the reference's `run_node` accepts (every policy,
+token budgets from 16 to 8192, chunk caps, scheduler and truth cost models of
+different magnitudes including c = 0, truth noise, max_active, per-request or
+uniform SLOs), so the engines' fast paths -- repeated plans, all-fit
+shortcuts, rank reuse, the memory path -- are checked against the oracle /
+reference on configurations no named scenario holds.  Test infrastructure.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2510_14392_b200.batch import Batch, CostModel, Rows, engine_config, ms_to_us
+
+POLICIES = ("prefill_first", "sarathi", "fairbatch", "fairbatch_pab")
+
+
+def random_rows(rng: np.random.Generator, uniform_slo: bool) -> Rows:
+    n = int(rng.integers(1, 400))
+    rate_per_ms = float(rng.choice([0.005, 0.02, 0.08, 0.3]))
+    gaps = rng.exponential(1.0 / rate_per_ms, size=n)
+    if rng.random() < 0.3:  # bursts: runs of simultaneous arrivals
+        gaps[rng.random(n) < 0.4] = 0.0
+    arrival = np.cumsum(np.round(gaps * 1000.0)).astype(np.int64)
+    prompt = rng.integers(1, int(rng.choice([64, 600, 3000])) + 1, size=n).astype(np.int32)
+    output = rng.integers(1, int(rng.choice([8, 120, 600])) + 1, size=n).astype(np.int32)
+    if uniform_slo:
+        ttft = np.full(n, ms_to_us(float(rng.choice([200.0, 500.0, 2000.0]))), np.int64)
+        tpot = np.full(n, ms_to_us(float(rng.choice([20.0, 50.0, 100.0]))), np.int64)
+    else:
+        ttft = rng.integers(ms_to_us(100.0), ms_to_us(3000.0), size=n).astype(np.int64)
+        tpot = rng.integers(ms_to_us(10.0), ms_to_us(200.0), size=n).astype(np.int64)
+    return Rows(arrival, prompt, output, ttft, tpot)
+
+
+def random_model(rng: np.random.Generator) -> CostModel:
+    return CostModel(float(rng.choice([0.5, 1.0, 5.0, 12.5])),
+                     float(rng.choice([0.001, 0.01, 0.05, 0.2])),
+                     float(rng.choice([0.0, 1e-6, 1e-4, 1e-3])))
+
+
+def random_batch(seed: int, n_inst: int) -> Batch:
+    rng = np.random.default_rng(seed)
+    b = Batch()
+    for _ in range(n_inst):
+        rows = random_rows(rng, uniform_slo=rng.random() < 0.75)
+        pol = POLICIES[int(rng.integers(0, 4))]
+        budget = int(rng.choice([16, 64, 512, 2048, 8192]))
+        max_chunk = int(rng.integers(1, budget + 1)) if rng.random() < 0.3 else None
+        model = random_model(rng)
+        truth = random_model(rng) if rng.random() < 0.3 else None
+        noisy = rng.random() < 0.3
+        cfg = engine_config(pol, budget, model, float(rng.choice([300.0, 500.0, 1000.0])),
+                            float(rng.choice([30.0, 50.0, 80.0])), max_chunk=max_chunk,
+                            noise_amplitude=0.1 if noisy else 0.0,
+                            noise_seed=int(rng.integers(0, 1 << 31)),
+                            max_active=int(rng.choice([0, 0, 0, 4, 16])), truth=truth)
+        horizon = ms_to_us(float(rng.choice([2_000.0, 20_000.0, 120_000.0])))
+        b.add(rows, cfg, horizon)
+    return b
