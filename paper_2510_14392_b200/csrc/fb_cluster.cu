@@ -180,6 +180,12 @@ extern "C" int fb_debug_cluster_prof(unsigned long long* out) {
   cudaMemcpyToSymbol(g_cluster_prof, z, sizeof(z));
   return static_cast<int>(cudaDeviceSynchronize());
 }
+extern "C" int fb_debug_epoch_max(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_epoch_max, sizeof(unsigned long long) * 16384);
+  static unsigned long long z[16384];
+  cudaMemcpyToSymbol(g_epoch_max, z, sizeof(z));
+  return static_cast<int>(cudaDeviceSynchronize());
+}
 #endif
 
 // ------------------------------------------------- pure scheduler kernels

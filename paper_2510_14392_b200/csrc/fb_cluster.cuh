@@ -47,6 +47,7 @@ struct __align__(16) NodeReport {
 
 #ifdef FB_CLUSTER_PROF
 __device__ unsigned long long g_cluster_prof[8];
+__device__ unsigned long long g_epoch_max[16384];  // per epoch: max over nodes of C(e-1) + A(e)
 #endif
 
 struct ClusterParams {
@@ -536,6 +537,7 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
   // [0] phase A (own node), [1] barrier wait, [2] report read + stop test,
   // [3] routing, [4] phase C (own node), [5] epochs
 #define CPT(k) { const uint64_t n_ = global_ns(); pacc[k] += n_ - pt0; pt0 = n_; }
+  uint64_t wt0 = pt0;  // this warp's node work since the previous routing
 #else
 #define CPT(k)
 #endif
@@ -543,6 +545,13 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     const int64_t t_a = C.epoch_t[e];
     int32_t cmp = 0;
     if (owner) node_phase_a(P, C, nd, rs, e, t_a, &cmp, &status);
+#ifdef FB_CLUSTER_PROF
+    if (owner && lane_id() == 0 && e < 16384) {
+      const unsigned long long busy = global_ns() - wt0;
+      atomicMax(&g_epoch_max[e], busy);
+      atomicAdd(&g_cluster_prof[7], busy);
+    }
+#endif
     CPT(0)
     if (C.hw_cluster) {
       // the grid is one thread-block cluster: the hardware cluster barrier
@@ -561,6 +570,9 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     if (warp == 0) cluster_route(P, C, rs, all, e, node_base);
     __syncthreads();
     CPT(3)
+#ifdef FB_CLUSTER_PROF
+    wt0 = global_ns();
+#endif
     if (owner && (rs.got[warp] || cmp)) {  // Node::enqueue (visible at t_a), begin_step(t_a)
       Inst& w = nd.w;
       w.S.arr = rs.n_routed[warp];

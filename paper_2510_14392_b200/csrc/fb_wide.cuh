@@ -1755,6 +1755,41 @@ __device__ __forceinline__ void wg_publish(const EngineParams& P, const Inst& w,
 
 // Owner: runs the node's event loop until it must form a batch (returns
 // true, slot published) or the slot has no node left (returns false).
+// Escalation records of every node the warp engine handed over (begin
+// pending): admitted-waiting marks all-zero and the 16-byte view record of
+// every request, built by the whole grid -- an equal share of all those
+// nodes' requests per CTA -- instead of by each node's owner alone (C4: 64
+// nodes x 120 k requests, 254 us when the 64 owners built their own).
+__device__ void wg_build_records(const EngineParams& P) {
+  const int64_t n_list = static_cast<int64_t>(P.work[3]);
+  auto pending = [&](int64_t i) { return P.state[i].pending_begin && !P.state[i].done; };
+  int64_t tot = 0;
+  for (int64_t j = 0; j < n_list; ++j) {
+    const int64_t i = P.wide_list[j];
+    if (pending(i)) tot += P.inst[i].n_req;
+  }
+  const int64_t lo = tot * blockIdx.x / gridDim.x, hi = tot * (blockIdx.x + 1) / gridDim.x;
+  int64_t base = 0;
+  for (int64_t j = 0; j < n_list && base < hi; ++j) {
+    const int64_t i = P.wide_list[j];
+    if (!pending(i)) continue;
+    const int64_t n = P.inst[i].n_req;
+    const int64_t a = lo > base ? lo - base : 0;
+    const int64_t z = hi - base < n ? hi - base : n;
+    if (a < z) {
+      const Inst w = wide_view_ctx(P, i);
+      const WideScratch ws = wide_scratch(P, w);
+      for (int64_t q = a + threadIdx.x; q < z; q += kWideThreads) {
+        ws.mark[q] = 0;
+        const int64_t g = w.roff + q, row = w.toff + q;
+        ws.rec[q] = make_wrec(P.arrival[row] + P.ttft[row], P.first[g], P.prompt[row],
+                              P.prefilled[g], P.nidx[g], P.seq[g]);
+      }
+    }
+    base += n;
+  }
+}
+
 __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& ev,
                            WideSlot* my, WideSmem& sm, WidePred& pred) {
   for (;;) {
@@ -1780,15 +1815,9 @@ __device__ bool wg_advance(const EngineParams& P, Inst& w, bool& have, int64_t& 
       if (threadIdx.x == 0) pred.valid = 0;  // a new node: no prediction yet
       __syncthreads();
       if (w.S.pending_begin) {
-        // escalation: admitted-waiting marks all-zero, in-flight takes cleared
+        // escalation (view records and admitted-waiting marks were built by
+        // the whole grid at launch, wg_build_records): in-flight takes cleared
         // (the warp engine's memory path leaves consumed takes behind)
-        const WideScratch ws = wide_scratch(P, w);
-        for (int64_t q = threadIdx.x; q < w.nreq; q += kWideThreads) {
-          ws.mark[q] = 0;
-          const int64_t g = w.roff + q, row = w.toff + q;
-          ws.rec[q] = make_wrec(P.arrival[row] + P.ttft[row], P.first[g], P.prompt[row],
-                                P.prefilled[g], P.nidx[g], P.seq[g]);
-        }
         for (int64_t q = threadIdx.x; q < w.S.n_active; q += kWideThreads) w.vl[q].y = 0;
         __syncthreads();
         w.S.pending_begin = 0;
@@ -2069,6 +2098,8 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
 #define CPROF(k)
 #define SPROF(k)
 #endif
+  wg_build_records(P);
+  wg_barrier(P.wg.bar, ++gen);
   for (;;) {
     // ---- owner: advance to the next begin_step
     {
@@ -2086,6 +2117,10 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
       CPROF(3)
     }
     wg_barrier(P.wg.bar, ++gen);
+#ifdef FB_WIDE_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_wide_prof[23] == 0)
+      g_wide_prof[23] = static_cast<unsigned long long>(clock64() - gp_t);  // first advance
+#endif
     GPROF(12)
     phase(0);
     // ---- work split (every CTA, from the published slots)

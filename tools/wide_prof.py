@@ -30,6 +30,7 @@ tot = sum(buf[i] for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 11))
 steps = buf[10]
 print(f"{n} instances, {ms:.3f} ms, {steps} wide steps")
 print(f"  windows per step {buf[20] / max(steps, 1):.3f}, fused window load {buf[21] / max(steps, 1) / 1965:.2f} us/step, sort: warp runs {buf[22] / max(steps, 1) / 1965:.2f} merges {buf[23] / max(steps, 1) / 1965:.2f} us/step")
+print(f"  first iteration's advance (escalation) wall: {buf[23] / 1965:.1f} us")
 print(f"  bin sort: {buf[16]} merge-sort fallbacks, mean rank work {buf[17] / max(steps, 1):.0f}, "
       f"mean window {buf[18] / max(steps, 1):.0f} keys, mean last bin {buf[19] / max(steps, 1):.0f}")
 gnames = {12: "advance+barrier", 13: "grid K1+barrier", 14: "grid hist+barrier",
