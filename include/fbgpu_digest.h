@@ -54,15 +54,19 @@ FB_HD uint64_t fb_digest_bits(double x) {
 }
 
 /* entry_sum = XOR over k of fb_digest_entry(k, req_k, new_k).  One chained
- * mix per step over the step's fields (time, entry sum, entry count,
- * predicted and ground-truth step-time bit patterns). */
+ * step per begin_step over the step's fields (time, entry sum, entry count,
+ * predicted and ground-truth step-time bit patterns): the fields are folded
+ * into the running state, then one odd multiply and one xorshift -- both
+ * bijections, so the new state changes whenever the folded word does.  (The
+ * per-step cost matters: the device engine's repeated-plan loop runs ~190
+ * warp instructions per step, and the round-1 splitmix chain took ~35.) */
 FB_HD uint64_t fb_digest_step(uint64_t h, int64_t t_us, uint32_t n_entries,
                               uint64_t entry_sum, double predicted_ms,
                               double actual_ms) {
-  uint64_t x = (uint64_t)t_us * 0x9e3779b97f4a7c15ULL;
-  x ^= entry_sum ^ fb_rotl64((uint64_t)n_entries | 0x5354455000000000ULL, 19);
-  x ^= fb_rotl64(fb_digest_bits(predicted_ms), 7) ^ fb_rotl64(fb_digest_bits(actual_ms), 37);
-  return fb_mix64(h ^ x);
+  uint64_t x = h ^ (uint64_t)t_us ^ entry_sum ^ ((uint64_t)n_entries << 44) ^
+               fb_rotl64(fb_digest_bits(predicted_ms), 21) ^ fb_digest_bits(actual_ms);
+  x *= 0x9e3779b97f4a7c15ULL;
+  return x ^ (x >> 31);
 }
 
 FB_HD uint64_t fb_digest_reject(uint64_t h, int64_t t_us, uint32_t req,
