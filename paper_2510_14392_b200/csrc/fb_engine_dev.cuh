@@ -459,8 +459,9 @@ __device__ __forceinline__ void steady_commit(const EngineParams& P, Inst& w, St
 // A run of repeated-plan steps back to back (run_event's repeated-plan lane,
 // without event logs or the envelope-lead series): each iteration is one
 // event of run_node's loop -- the in-flight step ends before the next arrival
-// with nothing pending: complete_step (`complete(now)`, true when a request
-// finished; it has then done the removal), then begin_step repeats the plan
+// with nothing pending: complete_step (`complete(now, steps started)`, true
+// when a request finished; it has then done the removal), then begin_step
+// repeats the plan
 // (steady_fits / steady_commit, same arithmetic; `recommit()` re-arms the
 // path's in-flight takes).  The node's hot scalars stay in registers for the
 // whole run.  Returns -1 when the run stopped with a step in flight (the next
@@ -489,7 +490,7 @@ __device__ __forceinline__ int64_t steady_run(const EngineParams& P, Inst& w, in
   while (ev < max_ev && next_arr > step_end) {
     const int64_t now = step_end;
     ++ev;
-    if (FB_UNLIKELY(complete(now) || now >= horizon || !budget_ok)) {
+    if (FB_UNLIKELY(complete(now, steps) || now >= horizon || !budget_ok)) {
       owed = now;
       break;
     }
@@ -547,7 +548,7 @@ __device__ __forceinline__ int64_t steady_burst_mem(const EngineParams& P, Inst&
   const int64_t A = w.sd.E;
   return steady_run(
       P, w, ev, next_arr,
-      [&](int64_t now) {  // complete_step (engine.cpp:204-254) for decodes
+      [&](int64_t now, uint64_t) {  // complete_step (engine.cpp:204-254) for decodes
         bool any_fin = false;
         for (int64_t b = 0; b < A; b += kTile) {
           const int64_t p = b + tile_lane();

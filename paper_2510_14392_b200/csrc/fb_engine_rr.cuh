@@ -351,7 +351,7 @@ __device__ __forceinline__ int64_t steady_burst(const EngineParams& P, Inst& w, 
   const bool vis = tile_lane() < w.sd.E;
   return steady_run(
       P, w, ev, next_arr,
-      [&](int64_t now) {  // complete_step
+      [&](int64_t now, uint64_t) {  // complete_step
         bool fin = false;
         if (t.take > 0) {
           fin = emit_reg(t, now);
