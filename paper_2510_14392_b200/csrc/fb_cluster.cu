@@ -182,8 +182,10 @@ extern "C" int fb_debug_cluster_prof(unsigned long long* out) {
 }
 extern "C" int fb_debug_epoch_max(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_epoch_max, sizeof(unsigned long long) * 16384);
+  cudaMemcpyFromSymbol(out + 16384, g_epoch_max_c, sizeof(unsigned long long) * 16384);
   static unsigned long long z[16384];
   cudaMemcpyToSymbol(g_epoch_max, z, sizeof(z));
+  cudaMemcpyToSymbol(g_epoch_max_c, z, sizeof(z));
   return static_cast<int>(cudaDeviceSynchronize());
 }
 #endif

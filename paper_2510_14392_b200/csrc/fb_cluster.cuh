@@ -48,6 +48,7 @@ struct __align__(16) NodeReport {
 #ifdef FB_CLUSTER_PROF
 __device__ unsigned long long g_cluster_prof[8];
 __device__ unsigned long long g_epoch_max[16384];  // per epoch: max over nodes of C(e-1) + A(e)
+__device__ unsigned long long g_epoch_max_c[16384];  // max over nodes of phase C(e-1) alone
 #endif
 
 struct ClusterParams {
@@ -294,15 +295,28 @@ __device__ void node_phase_a(const EngineParams& P, const ClusterParams& C, Clus
   nr.fresh = 0;
   nr.bz = bz;
   int64_t h = nd.rep_head;
-  while (h < nd.rep_tail) {  // newest report delivered by t_a
-    const int64_t* r = C.rep + (w.id * C.report_cap + h % C.report_cap) * 4;
-    if (r[0] + C.latency > t_a) break;
-    nr.t = r[0];
-    nr.pab = r[1];
-    nr.waiting = static_cast<int32_t>(r[2]);
-    nr.running = static_cast<int32_t>(r[3]);
-    nr.fresh = 1;
-    ++h;
+  if (h < nd.rep_tail) {  // newest report delivered by t_a
+    // emit times increase along the FIFO and the latency is constant, so the
+    // delivered reports are a prefix: when the newest is delivered (always
+    // with zero latency) they all are -- one read instead of a walk
+    const int64_t* r = C.rep + (w.id * C.report_cap + (nd.rep_tail - 1) % C.report_cap) * 4;
+    if (r[0] + C.latency <= t_a) {
+      h = nd.rep_tail;
+    } else {
+      while (h < nd.rep_tail) {
+        const int64_t* q = C.rep + (w.id * C.report_cap + h % C.report_cap) * 4;
+        if (q[0] + C.latency > t_a) break;
+        ++h;
+      }
+      r = C.rep + (w.id * C.report_cap + (h - 1) % C.report_cap) * 4;
+    }
+    if (h > nd.rep_head) {
+      nr.t = r[0];
+      nr.pab = r[1];
+      nr.waiting = static_cast<int32_t>(r[2]);
+      nr.running = static_cast<int32_t>(r[3]);
+      nr.fresh = 1;
+    }
   }
   nd.rep_head = h;
   if (C.hw_cluster) {
@@ -581,6 +595,10 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
     }
     __syncwarp();
     if (owner && lane_id() == 0) rs.got[warp] = 0;
+#ifdef FB_CLUSTER_PROF
+    if (owner && lane_id() == 0 && e + 1 < 16384)
+      atomicMax(&g_epoch_max_c[e + 1], global_ns() - wt0);
+#endif
     CPT(4)
   }
 #ifdef FB_CLUSTER_PROF

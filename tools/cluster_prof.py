@@ -18,13 +18,15 @@ for k, n in enumerate(names):
 # per epoch: the slowest node's work since the previous routing (phase C of
 # the previous epoch + phase A of this one), against the mean node's
 b7 = b[7]
-em = (C.c_ulonglong * 16384)()
+em = (C.c_ulonglong * 32768)()
 fbgpu.lib().fb_debug_epoch_max(em)   # first run's values: reset
 out = cluster.run_cluster(rows, cfgs, lb, hz)
 fbgpu.lib().fb_debug_cluster_prof(b)
 fbgpu.lib().fb_debug_epoch_max(em)
 import numpy as np
 m = np.array(em[:min(e, 16384)], dtype=np.float64)
+mc = np.array(em[16384:16384 + min(e, 16384)], dtype=np.float64)
+print(f"  slowest phase C per epoch: mean {mc.mean()/1000:6.2f} us, p50 {np.median(mc)/1000:6.2f}, p90 {np.percentile(mc, 90)/1000:6.2f}")
 print(f"  slowest node per epoch: mean {m.mean()/1000:6.2f} us, p50 {np.median(m)/1000:6.2f}, "
       f"p90 {np.percentile(m, 90)/1000:6.2f}, max {m.max()/1000:8.2f}; "
       f"mean node {b[7] / max(e, 1) / 64 / 1000:6.2f} us/epoch")
