@@ -430,7 +430,8 @@ class Arena:
         return int(self._lib.fb_arena_record_rows(self._h))
 
     def paths(self) -> np.ndarray:
-        """Per instance FB_PATH_* bits: 1 register-resident, 2 warp memory, 4 CTA-wide."""
+        """Per instance FB_PATH_* bits: 1 register-resident, 2 warp memory, 4 CTA-wide,
+        8 / 16 repeated-plan steps on the register / memory path."""
         out = np.zeros(max(1, self.n_instances), np.uint32)
         _check(self._lib.fb_arena_fetch_paths(self._h, _abi.vptr(out)), "fb_arena_fetch_paths")
         return out[:self.n_instances]
