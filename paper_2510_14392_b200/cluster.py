@@ -487,6 +487,11 @@ def run_cluster_host(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, device: in
     if dist is not None:
         import torch
         cap = max(partition(n, world, r)[1] for r in range(world))
+        # NCCL moves device tensors only: the per-epoch report all-gather
+        # and the clock all-reduce then run on this rank's GPU (over NVLink
+        # between GPUs); gloo (the CPU tests) takes host tensors
+        cdev = (torch.device("cuda", device) if dist.get_backend() == "nccl"
+                else torch.device("cpu"))
     try:
         view = HostRouter(n, lb)
         arrival = rows.arrival_us
@@ -502,11 +507,11 @@ def run_cluster_host(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, device: in
                 return local
             buf = np.zeros(cap, _abi.NODE_REPORT_DTYPE)
             buf[:nl] = local
-            t = torch.from_numpy(buf.view(np.int64).copy())
+            t = torch.from_numpy(buf.view(np.int64).copy()).to(cdev)
             parts = [torch.empty_like(t) for _ in range(world)]
             dist.all_gather(parts, t)
-            return np.concatenate([p.numpy().view(_abi.NODE_REPORT_DTYPE)[:partition(n, world, r)[1]]
-                                   for r, p in enumerate(parts)])
+            return np.concatenate([p.cpu().numpy().view(_abi.NODE_REPORT_DTYPE)
+                                   [:partition(n, world, r)[1]] for r, p in enumerate(parts)])
 
         def enqueue(t, targets, qrows):
             targets = np.asarray(targets, np.int64)
@@ -520,7 +525,7 @@ def run_cluster_host(rows: Rows, cfgs, lb: LbConfig, horizon_us: int, device: in
             busy = st["busy"] != 0
             m = int(st["step_end"][busy].min()) if busy.any() else kinf
             if dist is not None:
-                v = torch.tensor([m], dtype=torch.int64)
+                v = torch.tensor([m], dtype=torch.int64, device=cdev)
                 dist.all_reduce(v, op=dist.ReduceOp.MIN)
                 m = int(v.item())
             return m
