@@ -8,6 +8,18 @@
 //   * time is int64 microseconds (time.h:23-34).
 #pragma once
 
+// Loops off the repeated-plan hot path are kept rolled: the warp engine is
+// instruction-fetch bound, so code size costs more than loop overhead there
+// (FB_COLD_UNROLL=0 restores the compiler's default unrolling).
+#ifndef FB_COLD_UNROLL
+#define FB_COLD_UNROLL 1
+#endif
+#if FB_COLD_UNROLL
+#define FB_COLD_LOOP _Pragma("unroll 1")
+#else
+#define FB_COLD_LOOP
+#endif
+
 #ifndef FB_NOHINT
 #define FB_LIKELY(x) __builtin_expect(!!(x), 1)
 #define FB_UNLIKELY(x) __builtin_expect(!!(x), 0)

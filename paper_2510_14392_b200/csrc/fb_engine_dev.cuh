@@ -200,6 +200,7 @@ __device__ __forceinline__ void compact_vlist(Inst& w) {
   const int64_t n = w.S.n_live;
   int64_t out = 0;
   int64_t removed_active = 0;
+  FB_COLD_LOOP
   for (int64_t b = 0; b < n; b += kTile) {
     const int64_t p = b + tile_lane();
     int2 v = make_int2(-1, 0);
@@ -224,6 +225,7 @@ static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w
   bool any_fin = false;
   uint32_t lemit = 0;
   int64_t lfin = 0;
+  FB_COLD_LOOP
   for (int64_t b = 0; b < w.S.n_active; b += kTile) {
     const int64_t p = b + tile_lane();
     bool fin = false;
@@ -267,6 +269,7 @@ static __device__ __noinline__ void complete_step(const EngineParams& P, Inst& w
 // Node::pull_arrivals without admission control (engine.cpp:127-151).
 __device__ __forceinline__ void pull_plain(const EngineParams& P, Inst& w) {
   const int64_t k = w.S.arr - w.S.pulled;
+  FB_COLD_LOOP
   for (int64_t j = tile_lane(); j < k; j += kTile) {
     const int64_t r = arrival_row(w, w.S.pulled + j);
     P.seq[w.roff + r] = static_cast<int32_t>(w.S.seq_counter + j);
@@ -289,6 +292,7 @@ static __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
   int64_t A = visible_count(w);
   const Scratch s = scratch_for(P, w, A);
   int64_t lmin = kInf, lpf = 0;
+  FB_COLD_LOOP
   for (int64_t p = tile_lane(); p < A; p += kTile) {
     const View v = load_view(P, w, p, now);
     s.tcost[p] = pab_term(Wm, Tm, b, c, v.slack, v.ctx);
@@ -299,6 +303,7 @@ static __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
   int64_t min_slack = tile_min_i64(lmin);
   int64_t pf_tok = tile_sum_small(lpf);
   double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
+  FB_COLD_LOOP
   for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
     const int64_t r = arrival_row(w, q);
     const int64_t row = w.toff + r;
@@ -607,6 +612,7 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
 
   // K1: views, envelope slack and the init_time_budget reductions.
   ViewAcc acc;
+  FB_COLD_LOOP
   for (int64_t p = tile_lane(); p < A; p += kTile) {
     const View v = load_view(P, w, p, now);
     s.slack[p] = v.slack;
@@ -647,6 +653,7 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
   const int64_t entry_base = I->log_entry_off + w.S.log_entries;
   int run_all = 0, run_w = 0;
   uint64_t esum = 0;
+  FB_COLD_LOOP
   for (int k0 = 0; k0 < Ai; k0 += kTile) {
     const int k = k0 + tile_lane();
     int tk = 0, p = 0;
@@ -677,6 +684,7 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
   // unadmitted visible waiting keep their relative order after the movers
   int run_u = 0;
   const int64_t base_u = n_act + run_w;
+  FB_COLD_LOOP
   for (int64_t p0 = n_act; p0 < A; p0 += kTile) {
     const int64_t p = p0 + tile_lane();
     bool un = false;
@@ -686,6 +694,7 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
     run_u += __popc(mu);
   }
   tile_sync();
+  FB_COLD_LOOP
   for (int64_t p = tile_lane(); p < A; p += kTile) {
     const int64_t pk = s.slack[p];
     w.vl[pk >> 32] = make_int2(s.req[p], static_cast<int32_t>(pk & 0xffffffff));

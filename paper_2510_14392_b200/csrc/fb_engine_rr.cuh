@@ -18,7 +18,7 @@ namespace fbgpu {
 #define FB_RANK_REUSE 1  // C1 77.7 -> 74.9 ms, C2 35.55 -> 35.27 ms (tools/ab_time.py)
 #endif
 #ifndef FB_RANK_UNROLL
-#define FB_RANK_UNROLL 4  // 8: 36.2 ms, 16: 37.8 ms on C2 (code size)
+#define FB_RANK_UNROLL 1  // C2: 4 -> 1 20.3 -> 19.2 ms (code size: the pass is instruction-fetch bound)
 #endif
 constexpr int kRankUnroll = FB_RANK_UNROLL;
 
@@ -237,6 +237,7 @@ __device__ __forceinline__ void pull_rr(const EngineParams& P, Inst& w, TaskReg&
   int64_t min_slack = tile_min_i64(lmin);
   int64_t pf_tok = tile_sum_small(lpf);
   double r_tasks = ordered_fold(s.tcost, static_cast<int>(A));
+  FB_COLD_LOOP
   for (int64_t q = w.S.pulled; q < w.S.arr; ++q) {
     const int64_t r = arrival_row(w, q);
     const int64_t row = w.toff + r;

@@ -65,6 +65,7 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
   const bool fair = policy == FB_POLICY_FAIRBATCH || policy == FB_POLICY_FAIRBATCH_PAB;
   bool ok = seq_unique;
   if (ok) {
+    FB_COLD_LOOP
     for (int p = tile_lane(); p < A; p += kTile) {
       const int64_t sq = s.seq[p];
       bool f = sq >= 0 && sq < kPackSeq;
@@ -76,6 +77,7 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
     }
   }
   const bool packed = tile_all(ok);
+  FB_COLD_LOOP
   for (int p = tile_lane(); p < A; p += kTile) {
     const bool decode = (static_cast<uint32_t>(s.nw[p]) & kDecodeBit) != 0;
     uint64_t g, sl = 0;
@@ -102,17 +104,19 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
 // position so the result is always a permutation.
 __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed) {
   if (packed) {
+    FB_COLD_LOOP
     for (int p0 = 0; p0 < A; p0 += kTile) {
       const int p = p0 + tile_lane();
       const uint64_t kh = p < A ? s.khi[p] : 0;
       int rank = 0;
-#pragma unroll 4
+FB_COLD_LOOP
       for (int q = 0; q < A; ++q) rank += s.khi[q] < kh;
       if (p < A) s.order[rank] = p;
     }
     tile_sync();
     return;
   }
+  FB_COLD_LOOP
   for (int p0 = 0; p0 < A; p0 += kTile) {
     const int p = p0 + tile_lane();
     uint64_t kh = 0;
@@ -122,6 +126,7 @@ __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed)
       ks = s.seq[p];
     }
     int rank = 0;
+    FB_COLD_LOOP
     for (int q = 0; q < A; ++q) {
       const uint64_t qh = s.khi[q];
       const int64_t qs = s.seq[q];
@@ -137,6 +142,7 @@ __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed)
 __device__ __forceinline__ void gather_sorted(const Scratch& s, int A, double b,
                                               double c) {
   // khi / seq are free after rank_order (which ends in __syncwarp).
+  FB_COLD_LOOP
   for (int k = tile_lane(); k < A; k += kTile) {
     {
       const int p = s.order[k];
@@ -176,6 +182,7 @@ __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
     // the reference's implicit tb < 0 one).
     const bool bpos = f.b > 0.0;
     const double b_lo = bpos ? __dmul_rd(f.b, 1.0 - 0x1p-52) : 0.0;
+    FB_COLD_LOOP
     for (int k = 0; k < A; ++k) {
       if (exits_ok && (tok <= 0 || tb < 0.0 || tb < b_lo)) break;
       const double tc = s.tcost[k];
@@ -206,10 +213,12 @@ __device__ __forceinline__ void scan_fairbatch(const Scratch& s, int A,
 // K3b': form_batch_sarathi (sched.cpp:172-206); sorted decodes first.
 __device__ __forceinline__ void scan_sarathi(const Scratch& s, int A, int n_dec,
                                              const FormCfg& f) {
+  FB_COLD_LOOP
   for (int k = tile_lane(); k < n_dec; k += kTile) s.take[k] = 1;
   if (tile_lane() == 0) {
     int64_t remaining = f.token_budget - n_dec;
     if (remaining < 0) remaining = 0;
+    FB_COLD_LOOP
     for (int k = n_dec; k < A; ++k) {
       if (remaining <= 0) break;
       const int64_t nv = static_cast<uint32_t>(s.khi[k]) & 0x7fffffffu;
@@ -229,6 +238,7 @@ __device__ __forceinline__ void scan_prefill_first(const Scratch& s, int A,
                                                    const FormCfg& f) {
   if (tile_lane() == 0) {
     int64_t budget = f.token_budget;
+    FB_COLD_LOOP
     for (int k = 0; k < A; ++k) {
       if (budget <= 0) break;
       const uint32_t w = static_cast<uint32_t>(s.khi[k]);
@@ -283,6 +293,7 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
   rank_order(s, A, packed);
   gather_sorted(s, A, f.b, f.c);
   if (kExact) {
+    FB_COLD_LOOP
     for (int k = tile_lane(); k < A; k += kTile) s.take[k] = -1;
     tile_sync();
   }
@@ -295,6 +306,7 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
       const double tb0 = dsub(out.init_ms, f.a);
       double part = 0.0;
       int64_t nn = 0;
+      FB_COLD_LOOP
       for (int k = tile_lane(); k < A; k += kTile) {
         part = __dadd_ru(part, s.tcost[k]);
         nn += static_cast<int64_t>(s.khi[k] & 0x7fffffffu);
@@ -305,6 +317,7 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
                 __dsub_rd(tb0, s_up) >= __dmul_ru(__dmul_ru(static_cast<double>(A), 0x1p-52), tb0);
     }
     if (all_fit) {
+      FB_COLD_LOOP
       for (int k = tile_lane(); k < A; k += kTile)
         s.take[k] = static_cast<int32_t>(s.khi[k] & 0x7fffffffu);
       tile_sync();
@@ -319,6 +332,7 @@ __device__ __forceinline__ FormOut form_batch_warp(const Scratch& s, int A,
   // finalize_plan, sched.cpp:37-48 (integer sums: any order is exact)
   int32_t e = 0;
   int64_t tn = 0, tc = 0;
+  FB_COLD_LOOP
   for (int k = tile_lane(); k < A; k += kTile) {
     const int32_t tk = s.take[k];
     if (admitted_take<kExact>(tk)) {
@@ -372,6 +386,7 @@ __device__ __forceinline__ int64_t pab_close(double W, double T, double a, doubl
 __device__ __forceinline__ double ordered_fold(const double* v, int A) {
   double r = 0.0;
   if (tile_lane() == 0) {
+    FB_COLD_LOOP
     for (int p = 0; p < A; ++p) r = dadd(r, v[p]);
   }
   return tile_shfl(r, 0);
