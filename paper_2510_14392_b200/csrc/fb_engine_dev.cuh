@@ -555,6 +555,7 @@ __device__ __forceinline__ int64_t steady_burst_mem(const EngineParams& P, Inst&
       P, w, ev, next_arr,
       [&](int64_t now, uint64_t) {  // complete_step (engine.cpp:204-254) for decodes
         bool any_fin = false;
+        FB_COLD_LOOP
         for (int64_t b = 0; b < A; b += kTile) {
           const int64_t p = b + tile_lane();
           bool fin = false;
