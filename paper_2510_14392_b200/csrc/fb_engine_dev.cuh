@@ -776,6 +776,9 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
     return true;
   }
   int64_t t;
+#ifndef FB_EVENT_LANE
+#define FB_EVENT_LANE 0  // per-event repeated-plan lane (logs / lead series on): code size costs C2 3 %
+#endif
 #if FB_STEADY
   // Repeated-plan lane: the in-flight step of a repeated-plan-eligible node
   // ends before the next arrival with nothing pending -- the event is that
@@ -791,12 +794,14 @@ __device__ __forceinline__ bool run_event(const EngineParams& P, Inst& w, RunCtx
   } else if (lane_ok && !P.log_on && P.lead_bucket == 0) {
     t = steady_burst(P, w, c.tk, c.ev, c.next_arr);
     if (t < 0) return false;
+#if FB_EVENT_LANE
   } else if (lane_ok) {
     c.ev++;
     t = w.S.step_end;
     w.S.t_last = t;
     complete_rr(P, w, c.tk);
     if (w.sd.ok && t < w.horizon && steady_rr(P, w, c.tk, t, w.sd, w.sd.E)) return false;
+#endif
   } else
 #endif
   {
