@@ -358,6 +358,32 @@ static __device__ void pull_pab(const EngineParams& P, Inst& w, int64_t now) {
 }
 
 
+// The step's begin_step log row and counters (event logs on; out of line,
+// off the engines' hot code).
+static __device__ __noinline__ void log_step(const EngineParams& P, Inst& w, bool log_ok,
+                                             int64_t now, int64_t dur, double predicted,
+                                             double actual, int64_t tn, int64_t tctx,
+                                             double init_ms, int E) {
+  if (log_ok) {
+    if (tile_lane() == 0) {
+      fb_step_log& sl = P.log_steps[w.I->log_step_off + w.S.log_steps];
+      sl.t_us = now;
+      sl.duration_us = dur;
+      sl.predicted_ms = predicted;
+      sl.actual_ms = actual;
+      sl.total_new = tn;
+      sl.total_ctx = tctx;
+      sl.init_budget_ms = init_ms;
+      sl.entry_off = w.S.log_entries;
+      sl.n_entries = E;
+    }
+    w.S.log_steps++;
+    w.S.log_entries += E;
+  } else {
+    w.S.log_trunc = 1;
+  }
+}
+
 __device__ __forceinline__ void steady_record(Steady& sd, const Inst& w, bool all_decode_whole,
                                               int E, uint64_t esum, int64_t tctx,
                                               int64_t min_dec, int64_t now) {
@@ -428,26 +454,7 @@ __device__ __forceinline__ void steady_commit(const EngineParams& P, Inst& w, St
   if (amp != 0.0) actual = apply_noise(actual, amp, I->noise_seed, w.S.step_counter);
   int64_t dur = ms_to_us(actual);
   if (dur < 1) dur = 1;
-  if (P.log_on) {
-    if (log_ok) {
-      if (tile_lane() == 0) {
-        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
-        sl.t_us = now;
-        sl.duration_us = dur;
-        sl.predicted_ms = predicted;
-        sl.actual_ms = actual;
-        sl.total_new = tn;
-        sl.total_ctx = tctx;
-        sl.init_budget_ms = init_ms;
-        sl.entry_off = w.S.log_entries;
-        sl.n_entries = A;
-      }
-      w.S.log_steps++;
-      w.S.log_entries += A;
-    } else {
-      w.S.log_trunc = 1;
-    }
-  }
+  if (P.log_on) log_step(P, w, log_ok, now, dur, predicted, actual, tn, tctx, init_ms, A);
   w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(A), sd.esum, predicted,
                               actual);
   w.S.sum_visible += A;
@@ -702,26 +709,9 @@ static __device__ __noinline__ bool begin_step(const EngineParams& P, Inst& w, i
   }
   tile_sync();
 
-  if (P.log_on) {
-    if (log_ok) {
-      if (tile_lane() == 0) {
-        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
-        sl.t_us = now;
-        sl.duration_us = dur;
-        sl.predicted_ms = o.predicted_ms;
-        sl.actual_ms = actual;
-        sl.total_new = o.total_new;
-        sl.total_ctx = o.total_ctx;
-        sl.init_budget_ms = o.init_ms;
-        sl.entry_off = w.S.log_entries;
-        sl.n_entries = o.n_entries;
-      }
-      w.S.log_steps++;
-      w.S.log_entries += o.n_entries;
-    } else {
-      w.S.log_trunc = 1;
-    }
-  }
+  if (P.log_on)
+    log_step(P, w, log_ok, now, dur, o.predicted_ms, actual, o.total_new, o.total_ctx, o.init_ms,
+             o.n_entries);
   w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(o.n_entries), esum,
                               o.predicted_ms, actual);
   w.S.sum_visible += A;

@@ -584,26 +584,8 @@ __device__ __forceinline__ int begin_rr(const EngineParams& P, Inst& w, TaskReg&
     permute_task(t, src);
   }
 
-  if (P.log_on) {
-    if (log_ok) {
-      if (lane == 0) {
-        fb_step_log& sl = P.log_steps[I->log_step_off + w.S.log_steps];
-        sl.t_us = now;
-        sl.duration_us = dur;
-        sl.predicted_ms = predicted;
-        sl.actual_ms = actual;
-        sl.total_new = tn;
-        sl.total_ctx = tctx;
-        sl.init_budget_ms = init_ms;
-        sl.entry_off = w.S.log_entries;
-        sl.n_entries = E;
-      }
-      w.S.log_steps++;
-      w.S.log_entries += E;
-    } else {
-      w.S.log_trunc = 1;
-    }
-  }
+  if (P.log_on) log_step(P, w, log_ok, now, dur, predicted, actual, tn, tctx, init_ms, E);
+
   w.S.digest = fb_digest_step(w.S.digest, now, static_cast<uint32_t>(E), esum, predicted, actual);
   w.S.sum_visible += A;
   w.S.sum_entries += E;
