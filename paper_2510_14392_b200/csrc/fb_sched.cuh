@@ -103,6 +103,25 @@ __device__ __forceinline__ bool make_keys(const Scratch& s, int A, int policy,
 // compare per pair suffices; the general form breaks exact ties by view
 // position so the result is always a permutation.
 __device__ __forceinline__ void rank_order(const Scratch& s, int A, bool packed) {
+  if (packed && A <= 2 * kTile) {
+    // at most two keys per lane, compared over shuffles (no shared-memory
+    // round trip per compare; absent slots hold ~0, above every packed key)
+    const int l = tile_lane();
+    const uint64_t k0 = l < A ? s.khi[l] : ~uint64_t(0);
+    const uint64_t k1 = l + kTile < A ? s.khi[l + kTile] : ~uint64_t(0);
+    int r0 = 0, r1 = 0;
+    FB_COLD_LOOP
+    for (int q = 0; q < kTile; ++q) {
+      const uint64_t b0 = tile_shfl(k0, q), b1 = tile_shfl(k1, q);
+      r0 += (b0 < k0) + (b1 < k0);
+      r1 += (b0 < k1) + (b1 < k1);
+    }
+    tile_sync();
+    if (l < A) s.order[r0] = l;
+    if (l + kTile < A) s.order[r1] = l + kTile;
+    tile_sync();
+    return;
+  }
   if (packed) {
     FB_COLD_LOOP
     for (int p0 = 0; p0 < A; p0 += kTile) {
