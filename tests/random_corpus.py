@@ -15,9 +15,11 @@ from paper_2510_14392_b200.batch import Batch, CostModel, Rows, engine_config, m
 POLICIES = ("prefill_first", "sarathi", "fairbatch", "fairbatch_pab")
 
 
-def random_rows(rng: np.random.Generator, uniform_slo: bool) -> Rows:
-    n = int(rng.integers(1, 400))
-    rate_per_ms = float(rng.choice([0.005, 0.02, 0.08, 0.3]))
+def random_rows(rng: np.random.Generator, uniform_slo: bool, wide: bool = False) -> Rows:
+    # wide: thousands of requests arriving faster than they drain, so more
+    # than 512 are live at once (the grid-wide engine)
+    n = int(rng.integers(600, 4000)) if wide else int(rng.integers(1, 400))
+    rate_per_ms = float(rng.choice([2.0, 8.0])) if wide else float(rng.choice([0.005, 0.02, 0.08, 0.3]))
     gaps = rng.exponential(1.0 / rate_per_ms, size=n)
     if rng.random() < 0.3:  # bursts: runs of simultaneous arrivals
         gaps[rng.random(n) < 0.4] = 0.0
@@ -39,11 +41,11 @@ def random_model(rng: np.random.Generator) -> CostModel:
                      float(rng.choice([0.0, 1e-6, 1e-4, 1e-3])))
 
 
-def random_batch(seed: int, n_inst: int) -> Batch:
+def random_batch(seed: int, n_inst: int, wide: bool = False) -> Batch:
     rng = np.random.default_rng(seed)
     b = Batch()
     for _ in range(n_inst):
-        rows = random_rows(rng, uniform_slo=rng.random() < 0.75)
+        rows = random_rows(rng, uniform_slo=rng.random() < 0.75, wide=wide)
         pol = POLICIES[int(rng.integers(0, 4))]
         budget = int(rng.choice([16, 64, 512, 2048, 8192]))
         max_chunk = int(rng.integers(1, budget + 1)) if rng.random() < 0.3 else None

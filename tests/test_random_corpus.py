@@ -60,3 +60,20 @@ def test_gpu_logs_match_oracle_on_random_corpus(fb, oracle, seed):
         assert rejects[i][: c["rejects"]].tobytes() == want.rejects[i][: c["rejects"]].tobytes(), i
     assert res.tobytes() == want.results.tobytes()
     assert rec.tobytes() == want.records.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [7, 8])
+def test_gpu_wide_random_corpus_matches_oracle(fb, oracle, seed):
+    """Thousands of live requests per instance: the grid-wide engine."""
+    batch = random_batch(seed, 8, wide=True)
+    arena = fb.Arena(0)
+    arena.load(batch)
+    arena.run()
+    res, rec, paths = arena.results(), arena.records(), arena.paths()
+    arena.close()
+    want = oracle.run(batch, nthreads=8)
+    for i in range(batch.n_instances):
+        assert res[i].tobytes() == want.results[i].tobytes(), i
+    assert rec.tobytes() == want.records.tobytes()
+    assert (paths & 4).any()  # FB_PATH_WIDE
