@@ -60,3 +60,23 @@ def random_batch(seed: int, n_inst: int, wide: bool = False) -> Batch:
         horizon = ms_to_us(float(rng.choice([2_000.0, 20_000.0, 120_000.0])))
         b.add(rows, cfg, horizon)
     return b
+
+
+def random_cluster(seed: int):
+    """(rows, node configs, LbConfig, horizon_us) of a random run_cluster case:
+    1-64 nodes of one random policy, pab / count balancing, report interval
+    1-3, report latency 0-50 ms, a quarter with retry_reroute."""
+    from paper_2510_14392_b200 import cluster
+    rng = np.random.default_rng(seed)
+    rows = random_rows(rng, uniform_slo=rng.random() < 0.7)
+    nodes = int(rng.choice([1, 2, 3, 5, 8, 16, 33, 64]))
+    pol = POLICIES[int(rng.integers(0, 4))]
+    cfgs = [engine_config(pol, int(rng.choice([64, 512, 2048])), random_model(rng),
+                          float(rng.choice([300.0, 500.0])), float(rng.choice([30.0, 50.0])),
+                          max_active=int(rng.choice([0, 0, 4])))
+            for _ in range(nodes)]
+    lb = cluster.LbConfig(str(rng.choice(["pab_lb", "count_lb"])), int(rng.choice([1, 1, 2, 3])),
+                          float(rng.choice([0.0, 0.0, 5.0, 50.0])),
+                          retry_reroute=bool(rng.random() < 0.25))
+    hz = ms_to_us(float(rng.choice([5_000.0, 60_000.0])))
+    return rows, cfgs, lb, hz

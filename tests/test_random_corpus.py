@@ -7,8 +7,9 @@ from __future__ import annotations
 
 import pytest
 
+from backends import cluster_summary
 from full_size import canonical_results
-from random_corpus import random_batch
+from random_corpus import random_batch, random_cluster
 from paper_2510_14392_b200 import _abi
 
 
@@ -77,3 +78,19 @@ def test_gpu_wide_random_corpus_matches_oracle(fb, oracle, seed):
         assert res[i].tobytes() == want.results[i].tobytes(), i
     assert rec.tobytes() == want.records.tobytes()
     assert (paths & 4).any()  # FB_PATH_WIDE
+
+
+@pytest.mark.parametrize("seed", [300, 301, 302, 303, 305, 306])
+def test_oracle_cluster_matches_reference_on_random_cases(oracle, ref, seed):
+    rows, cfgs, lb, hz = random_cluster(seed)
+    assert cluster_summary(oracle.run_cluster(rows, cfgs, lb, hz)) == \
+        cluster_summary(ref.run_cluster(rows, cfgs, lb, hz, check=True))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(300, 312))
+def test_gpu_cluster_matches_oracle_on_random_cases(oracle, seed):
+    from paper_2510_14392_b200 import cluster
+    rows, cfgs, lb, hz = random_cluster(seed)
+    assert cluster_summary(cluster.run_cluster(rows, cfgs, lb, hz)) == \
+        cluster_summary(oracle.run_cluster(rows, cfgs, lb, hz))
