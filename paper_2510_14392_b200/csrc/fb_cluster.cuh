@@ -464,8 +464,12 @@ __device__ __forceinline__ int cluster_pick(const ClusterParams& C, RouterSmem& 
 }
 
 // Phase B (warp 0 of each CTA): reports -> view, route the epoch's arrivals.
+// q_lo / q_hi / prompt0: the epoch's request range and its first prompt,
+// loaded by the caller before phase A so their latency is off the critical
+// path (the router runs between the barrier and phase C of every epoch).
 __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, RouterSmem& rs,
-                              const NodeReport* all, int64_t e, int node_base) {
+                              const NodeReport* all, int64_t e, int node_base, int64_t q_lo,
+                              int64_t q_hi, int64_t prompt0) {
   const int n = C.n_nodes;
   for (int i = lane_id(); i < n; i += kWarp) {
     // the whole 32-byte report in two 16-byte loads (one round trip)
@@ -485,8 +489,9 @@ __device__ void cluster_route(const EngineParams& P, const ClusterParams& C, Rou
     }
   }
   __syncwarp();
-  for (int64_t q = C.epoch_lo[e]; q < C.epoch_lo[e + 1]; ++q) {
-    const int chosen = cluster_pick(C, rs, P.prompt[q], blockIdx.x == 0 ? q : -1, C.epoch_t[e], q);
+  for (int64_t q = q_lo; q < q_hi; ++q) {
+    const int64_t prompt = q == q_lo ? prompt0 : P.prompt[q];
+    const int chosen = cluster_pick(C, rs, prompt, blockIdx.x == 0 ? q : -1, C.epoch_t[e], q);
     if (lane_id() == 0) {
       if (blockIdx.x == 0) C.route_node[q] = chosen;
       const int k = chosen - node_base;  // Node::enqueue, on the owning CTA
@@ -557,6 +562,13 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
 #endif
   for (; e < C.n_epochs; ++e) {
     const int64_t t_a = C.epoch_t[e];
+    // the router's inputs for this epoch, fetched ahead of phase A
+    int64_t q_lo = 0, q_hi = 0, prompt0 = 0;
+    if (warp == 0) {
+      q_lo = C.epoch_lo[e];
+      q_hi = C.epoch_lo[e + 1];
+      prompt0 = q_lo < q_hi ? P.prompt[q_lo] : 0;
+    }
     int32_t cmp = 0;
     if (owner) node_phase_a(P, C, nd, rs, e, t_a, &cmp, &status);
 #ifdef FB_CLUSTER_PROF
@@ -581,7 +593,7 @@ cluster_kernel(const __grid_constant__ EngineParams P, const __grid_constant__ C
         C.hw_cluster ? rs.xrep[e & 1] : xchg_reports(C.xbuf[C.rank], C.n_nodes, e);
     if (cluster_stopped(C, all, t_a)) break;
     CPT(2)
-    if (warp == 0) cluster_route(P, C, rs, all, e, node_base);
+    if (warp == 0) cluster_route(P, C, rs, all, e, node_base, q_lo, q_hi, prompt0);
     __syncthreads();
     CPT(3)
 #ifdef FB_CLUSTER_PROF
