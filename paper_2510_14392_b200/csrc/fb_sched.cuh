@@ -405,7 +405,9 @@ __device__ __forceinline__ int64_t pab_close(double W, double T, double a, doubl
 __device__ __forceinline__ double ordered_fold(const double* v, int A) {
   double r = 0.0;
   if (tile_lane() == 0) {
-    FB_COLD_LOOP
+    // a serial chain: unrolled so the shared-memory loads run ahead of it
+    // (the cluster's per-step PAB report sits on the epoch's critical path)
+#pragma unroll 4
     for (int p = 0; p < A; ++p) r = dadd(r, v[p]);
   }
   return tile_shfl(r, 0);
