@@ -491,6 +491,10 @@ __device__ __forceinline__ int64_t steady_run(const EngineParams& P, Inst& w, in
   const int64_t tpot_u = I->tpot_uniform;
   const double sa = I->sa, sb = I->sb, sc = I->sc, ta = I->ta, tb = I->tb, tc = I->tc;
   const double amp = I->noise_amp;
+  // truth model == scheduler model bit for bit (C1-C3): one evaluation per step
+  const bool same_model = __double_as_longlong(sa) == __double_as_longlong(ta) &&
+                          __double_as_longlong(sb) == __double_as_longlong(tb) &&
+                          __double_as_longlong(sc) == __double_as_longlong(tc);
   const uint64_t esum = w.sd.esum;
   const double slack_a = __dmul_ru(static_cast<double>(A), 0x1p-52);
   const double s_b = __dmul_ru(static_cast<double>(A), sb);
@@ -522,7 +526,8 @@ __device__ __forceinline__ int64_t steady_run(const EngineParams& P, Inst& w, in
     }
     tctx += A;
     const double predicted = predict_ms(sa, sb, sc, A, tctx);
-    double actual = predict_ms(ta, tb, tc, A, tctx);
+    double actual = predicted;
+    if (!same_model) actual = predict_ms(ta, tb, tc, A, tctx);
     if (FB_UNLIKELY(amp != 0.0)) actual = apply_noise(actual, amp, I->noise_seed, steps);
     int64_t dur = ms_to_us(actual);
     if (dur < 1) dur = 1;
