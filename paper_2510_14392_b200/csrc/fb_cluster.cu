@@ -294,7 +294,6 @@ __global__ void init_time_budget_kernel(const fb_task_view* __restrict__ tasks,
     const int64_t off = set_off[set];
     const int64_t n = set_off[set + 1] - off;
     ViewAcc acc;
-    bool unusual = false;
     for (int64_t p = lane_id(); p < n; p += kWarp) {
       const fb_task_view t = tasks[off + p];
       acc.add(t.phase == FB_PHASE_DECODE, t.slack_us, t.tpot_us);

@@ -1999,7 +1999,6 @@ __device__ void wg_bin_sort(const EngineParams& P, int t, int K, int bmax, int p
   WPROF_COUNT(17, rank_work)
   WPROF_COUNT(18, K)
   WPROF_COUNT(19, bmax)
-  const uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
   const int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
   if (rank_work > kBinRankWork) {
     for (int k = threadIdx.x; k < K; k += kWideThreads) {
@@ -2326,7 +2325,6 @@ wide_grid_kernel(const __grid_constant__ EngineParams P) {
         const Inst wv = wide_view_ctx(P, sv.inst);
         const WideScratch ws = wide_scratch(P, wv);
         const int64_t p_lo = a - s_v0[t], p_hi = z - s_v0[t];
-        uint64_t* ck = P.wg.ckey + static_cast<size_t>(t) * kWideWin;
         int32_t* cp = P.wg.cpos + static_cast<size_t>(t) * kWideWin;
         int32_t* ncand = &slots[t].ncand;
         // the bins K2a left in shared memory: only the selected views' stems
