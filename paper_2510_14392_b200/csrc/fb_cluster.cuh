@@ -156,6 +156,10 @@ struct ClusterNode {
   TaskReg tk;
   bool rr;
   int64_t rep_head, rep_tail;
+  // the newest report of the FIFO (rep_tail - 1), kept in registers so phase A
+  // reads it without a global-memory round trip when it is delivered
+  int64_t nt, npab;
+  int32_t nwait, nrun;
 };
 
 __device__ __forceinline__ void cluster_node_init(const EngineParams& P, const ClusterParams& C,
@@ -178,6 +182,9 @@ __device__ __forceinline__ void cluster_node_init(const EngineParams& P, const C
   w.sd.clear();
   nd.rr = false;
   nd.rep_head = nd.rep_tail = 0;
+  nd.nt = -1;
+  nd.npab = 0;
+  nd.nwait = nd.nrun = 0;
 }
 
 // Node::current_pab (engine.cpp:123-125): pab over the node's views at now.
@@ -225,6 +232,10 @@ __device__ void node_report(const EngineParams& P, const ClusterParams& C, Clust
       r[2] = w.S.n_live - w.S.n_active;  // waiting_count (engine.h:133-135)
       r[3] = w.S.n_active;                // running_count
     }
+    nd.nt = now;
+    nd.npab = pab;
+    nd.nwait = w.S.n_live - w.S.n_active;
+    nd.nrun = w.S.n_active;
     nd.rep_tail++;
   }
   __syncwarp();
@@ -299,23 +310,29 @@ __device__ void node_phase_a(const EngineParams& P, const ClusterParams& C, Clus
     // emit times increase along the FIFO and the latency is constant, so the
     // delivered reports are a prefix: when the newest is delivered (always
     // with zero latency) they all are -- one read instead of a walk
-    const int64_t* r = C.rep + (w.id * C.report_cap + (nd.rep_tail - 1) % C.report_cap) * 4;
-    if (r[0] + C.latency <= t_a) {
+    if (nd.nt + C.latency <= t_a) {  // from the register copy
       h = nd.rep_tail;
+      if (h > nd.rep_head) {
+        nr.t = nd.nt;
+        nr.pab = nd.npab;
+        nr.waiting = nd.nwait;
+        nr.running = nd.nrun;
+        nr.fresh = 1;
+      }
     } else {
       while (h < nd.rep_tail) {
         const int64_t* q = C.rep + (w.id * C.report_cap + h % C.report_cap) * 4;
         if (q[0] + C.latency > t_a) break;
         ++h;
       }
-      r = C.rep + (w.id * C.report_cap + (h - 1) % C.report_cap) * 4;
-    }
-    if (h > nd.rep_head) {
-      nr.t = r[0];
-      nr.pab = r[1];
-      nr.waiting = static_cast<int32_t>(r[2]);
-      nr.running = static_cast<int32_t>(r[3]);
-      nr.fresh = 1;
+      if (h > nd.rep_head) {
+        const int64_t* r = C.rep + (w.id * C.report_cap + (h - 1) % C.report_cap) * 4;
+        nr.t = r[0];
+        nr.pab = r[1];
+        nr.waiting = static_cast<int32_t>(r[2]);
+        nr.running = static_cast<int32_t>(r[3]);
+        nr.fresh = 1;
+      }
     }
   }
   nd.rep_head = h;
