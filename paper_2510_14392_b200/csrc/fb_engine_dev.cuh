@@ -16,13 +16,17 @@
 
 namespace fbgpu {
 
+// One 16-warp block per SM (the same 16 resident warps as two 8-warp blocks,
+// at most 128 registers each): C2 15.4 -> 15.25 ms, C3 sample 32.6 -> 31.8 ms
+// (profiles/r02u_engine_blocks_ab.txt); 8 or 12 warps per SM with more
+// registers are slower (19.1 / 16.5 ms on C2).
 #ifndef FB_WARPS_PER_BLOCK
-#define FB_WARPS_PER_BLOCK 8
+#define FB_WARPS_PER_BLOCK 16
 #endif
 constexpr int kWarpsPerBlock = FB_WARPS_PER_BLOCK;
 constexpr int kSmemSlots = 64;  // visible tasks held in shared-memory scratch
 #ifndef FB_ENGINE_BLOCKS_PER_SM
-#define FB_ENGINE_BLOCKS_PER_SM 2
+#define FB_ENGINE_BLOCKS_PER_SM 1
 #endif
 constexpr int kEngineBlocksPerSm = FB_ENGINE_BLOCKS_PER_SM;  // register cap for occupancy
 constexpr int64_t kEscalateLive = 512;  // live requests beyond which a node goes CTA-wide
