@@ -182,6 +182,10 @@ EngineGeometry engine_geometry(int device) {
   g.sms = sms;
   cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(g.smem));
+#ifdef FB_ENGINE_CARVEOUT
+  cudaFuncSetAttribute(engine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       FB_ENGINE_CARVEOUT);
+#endif
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, engine_kernel, g.threads, g.smem);
   if (per_sm < 1) per_sm = 1;
   g.blocks = sms * per_sm;

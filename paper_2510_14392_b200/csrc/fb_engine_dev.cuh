@@ -24,7 +24,12 @@ namespace fbgpu {
 #define FB_WARPS_PER_BLOCK 16
 #endif
 constexpr int kWarpsPerBlock = FB_WARPS_PER_BLOCK;
-constexpr int kSmemSlots = 64;  // visible tasks held in shared-memory scratch
+#ifndef FB_SMEM_SLOTS
+#define FB_SMEM_SLOTS 64
+#endif
+// visible tasks held in shared-memory scratch (>= 32: the register path's)
+constexpr int kSmemSlots = FB_SMEM_SLOTS;
+static_assert(kSmemSlots >= 32, "register-path scratch");
 #ifndef FB_ENGINE_BLOCKS_PER_SM
 #define FB_ENGINE_BLOCKS_PER_SM 1
 #endif
